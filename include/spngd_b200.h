@@ -1,0 +1,247 @@
+/*
+ * spngd_b200.h — C ABI of the B200-native SP-NGD optimizer step.
+ *
+ * This is the drop-in boundary for the reference's hot path
+ * (/root/reference/proj, the `spngd` C++ library).  Every entry point below
+ * replaces one reference function or one stage of
+ * `accumulate_microsteps` (src/dist.cpp:406-675) and cites it.  All tensors
+ * are DEVICE pointers to fp32 data on the context's GPU in the reference's
+ * layouts:
+ *   - packed symmetric matrices: upper triangle, row-major,
+ *     offset(i,j) = i*n - i*(i-1)/2 + (j-i)         (include/spngd/linalg.hpp:48-51)
+ *   - weights / gradients: row-major g x a (d_out x d_in, or c_out x c_in*k*k)
+ *                                                  (include/spngd/net.hpp:46-50)
+ *   - FC activation capture: M x d_in rows; conv capture: stacked im2col
+ *     (M*c_in*k*k) x (h_out*w_out), row = ch*k*k + ky*k + kx
+ *                                                  (include/spngd/net.hpp:84-101)
+ *   - BN unit moments: interleaved (fgg, fgb, fbb) x c  (src/dist.cpp:283-292)
+ *   - BN gradient / parameter payload: gamma(c) then beta(c) (src/dist.cpp:363-389)
+ *
+ * Errors: every function returns an spngd_status; nonzero codes mirror the
+ * reference exception taxonomy (include/spngd/errors.hpp:10-85) and
+ * spngd_last_error() returns the message.  There is no CPU fallback: without a
+ * usable sm_100 device every compute entry point fails with SPNGD_ERR_CUDA.
+ */
+#ifndef SPNGD_B200_H_
+#define SPNGD_B200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum spngd_status {
+  SPNGD_OK = 0,
+  SPNGD_ERR_SHAPE_MISMATCH = 1,        /* errors.hpp:16  ShapeMismatch */
+  SPNGD_ERR_NOT_POSITIVE_DEFINITE = 2, /* errors.hpp:22  NotPositiveDefinite */
+  SPNGD_ERR_SINGULAR_BLOCK = 3,        /* errors.hpp:27  SingularBlock */
+  SPNGD_ERR_ZERO_REFERENCE = 4,        /* errors.hpp:32  ZeroReference */
+  SPNGD_ERR_EMPTY_BATCH = 5,           /* errors.hpp:37  EmptyBatch */
+  SPNGD_ERR_MISSING_MC_PASS = 6,       /* errors.hpp:42  MissingMcPass */
+  SPNGD_ERR_STALE_BEYOND_LIMIT = 7,    /* errors.hpp:52  StaleBeyondLimit */
+  SPNGD_ERR_REFRESH_OUT_OF_TURN = 8,   /* errors.hpp:57  RefreshOutOfTurn */
+  SPNGD_ERR_INDIVISIBLE_BATCH = 9,     /* errors.hpp:62  IndivisibleBatch */
+  SPNGD_ERR_MISSING_OWNER = 10,        /* errors.hpp:67  MissingOwner */
+  SPNGD_ERR_EMPTY_ACCUMULATION = 11,   /* errors.hpp:72  EmptyAccumulation */
+  SPNGD_ERR_CUDA = 100,                /* CUDA runtime / launch failure */
+  SPNGD_ERR_NCCL = 101,                /* NCCL failure */
+  SPNGD_ERR_INVALID = 102              /* bad argument (null pointer, ...) */
+} spngd_status;
+
+typedef struct spngd_ctx spngd_ctx;
+
+/* Last error message of the calling thread (empty string if none). */
+const char* spngd_last_error(void);
+const char* spngd_version(void);
+
+/* One context per GPU and host thread; owns workspace and the stream.
+ * `stream` may be NULL (a private non-blocking stream is created). */
+int spngd_ctx_create(int device, void* stream, spngd_ctx** out);
+void spngd_ctx_destroy(spngd_ctx* ctx);
+/* Synchronizes the context stream and returns the first device-side error
+ * raised since the previous call (NotPositiveDefinite, SingularBlock). */
+int spngd_ctx_sync(spngd_ctx* ctx);
+void* spngd_ctx_stream(spngd_ctx* ctx);
+
+/* ---- K1: Kronecker factors ------------------------------------------------
+ * Replaces factor_A (src/fisher.cpp:92-114) and factor_G (src/fisher.cpp:116-145)
+ * via mean_outer (src/fisher.cpp:55-75):
+ *   out = scale * sum_{s in [lo,hi)} X_s X_s^T, packed upper triangle,
+ * X_s = row s of an M x dim capture (layout 0, FC) or the dim x hw block s of a
+ * stacked (M*dim) x hw capture (layout 1, conv).  Computed with 3xTF32
+ * tcgen05 MMAs (fp32-accurate), split-K partials reduced in fp64. */
+typedef struct spngd_factor_req {
+  const float* x;      /* capture, device */
+  int64_t dim;         /* a (A factor) or g (G factor) */
+  int64_t hw;          /* h_out*w_out (layout 1); ignored for layout 0 */
+  int64_t layout;      /* 0 = FC rows, 1 = conv stacked blocks */
+  int64_t lo, hi;      /* sample range [lo, hi) */
+  double scale;        /* 1/(n*hw) for conv A, 1/n otherwise (fisher.cpp:104-108,138-139) */
+  float* packed_out;   /* dim*(dim+1)/2 floats, device */
+} spngd_factor_req;
+int spngd_factor_sym_batched(spngd_ctx* ctx, int n, const spngd_factor_req* reqs);
+
+/* ---- K2: BatchNorm unit moments -------------------------------------------
+ * Replaces build_bn_block (src/fisher.cpp:147-185) + stat_payload's 3c
+ * interleave (src/dist.cpp:283-292).  gg, gb: M x c row-major. */
+typedef struct spngd_bn_moments_req {
+  const float* gg;
+  const float* gb;
+  int64_t c;
+  int64_t lo, hi;
+  float* out3c;
+} spngd_bn_moments_req;
+int spngd_bn_moments_batched(spngd_ctx* ctx, int n, const spngd_bn_moments_req* reqs);
+
+/* ---- K3/K4: damped SPD inverse ---------------------------------------------
+ * Replaces spd_inverse (src/linalg.cpp:29-48): (M + d I)^-1 of a packed
+ * symmetric matrix.  `damping_dev` (device float) overrides `damping` when
+ * non-NULL.  Output: dense row-major (ld >= n) and/or packed; exactly
+ * symmetric.  Fails with SPNGD_ERR_NOT_POSITIVE_DEFINITE on a non-positive
+ * pivot or non-finite entries. */
+typedef struct spngd_spd_req {
+  const float* packed;   /* input, n(n+1)/2 */
+  int64_t n;
+  float damping;
+  const float* damping_dev;
+  float* dense_out;      /* n x ld, may be NULL if packed_out given */
+  int64_t ld;
+  float* packed_out;     /* may be NULL */
+} spngd_spd_req;
+int spngd_spd_inverse_batched(spngd_ctx* ctx, int n, const spngd_spd_req* reqs);
+
+/* Replaces damp_and_invert (src/fisher.cpp:218-228) incl. avg_eigenvalue
+ * (src/linalg.cpp:64-69): pi = sqrt((trA/a)/(trG/g)) (1 if either < 1e-12),
+ * A_inv = (A + pi sqrt(lambda) I)^-1, G_inv = (G + sqrt(lambda)/pi I)^-1. */
+typedef struct spngd_kron_req {
+  const float* A_packed;
+  const float* G_packed;
+  int64_t a, g;
+  float* Ainv_dense; int64_t lda;   /* dense outputs (may be NULL) */
+  float* Ginv_dense; int64_t ldg;
+  float* Ainv_packed;               /* packed outputs (may be NULL) */
+  float* Ginv_packed;
+  float* pi_out;                    /* device float (may be NULL) */
+} spngd_kron_req;
+int spngd_damp_and_invert_batched(spngd_ctx* ctx, int n, const spngd_kron_req* reqs, double lambda);
+
+/* ---- K5/K6: preconditioning + momentum/rescale update ------------------------
+ * Replaces precondition/kron_matvec (src/fisher.cpp:255-257,
+ * src/linalg.cpp:58-62), the FC/Conv branch of ngd_step
+ * (src/fisher.cpp:332-333) and rescale_weights + velocity fix
+ * (src/schemes.cpp:116-119, src/dist.cpp:621-632):
+ *   P = G_inv dW A_inv ;  W' = W - eta P + momentum V ; V' = W' - W ;
+ *   if rescale: W'' = sqrt(2 g) W'/(||W'||_F + 1e-9), V'' = W'' - W.
+ * G_inv, A_inv dense symmetric.  W/V updated in place when W != NULL. */
+typedef struct spngd_precond_req {
+  const float* Ginv; int64_t ldg;
+  const float* Ainv; int64_t lda;
+  const float* dW;                 /* g x a row-major */
+  int64_t g, a;
+  float* P_out;                    /* optional g x a */
+  float* W;                        /* optional: update in place */
+  float* V;
+  int rescale;
+} spngd_precond_req;
+int spngd_precondition_update_batched(spngd_ctx* ctx, int n, const spngd_precond_req* reqs,
+                                      double eta, double momentum);
+
+/* ---- K7: unit-wise BatchNorm 2x2 solve + update -----------------------------
+ * Replaces damp_bn / precondition_bn (src/fisher.cpp:230-246, 259-276,
+ * inv2x2 src/linalg.cpp:50-56) and the BN branch of ngd_step
+ * (src/fisher.cpp:336-357).  Unit BN uses lambda (not sqrt) and no pi.
+ * grad = [g_gamma(c), g_beta(c)]; SingularBlock if |det| < 1e-30. */
+typedef struct spngd_bn_update_req {
+  const float* m3c;
+  const float* grad;
+  int64_t c;
+  float* gamma; float* beta;       /* optional in-place update */
+  float* vgamma; float* vbeta;
+  float* pg_out; float* pb_out;    /* optional preconditioned gradient */
+} spngd_bn_update_req;
+int spngd_bn_solve_update_batched(spngd_ctx* ctx, int n, const spngd_bn_update_req* reqs,
+                                  double lambda, double eta, double momentum);
+
+/* ---- K8: stale-statistics similarity ----------------------------------------
+ * Replaces to_stat / weighted_norm / similar (include/spngd/stale.hpp:23-64)
+ * over a packed statistic (off-diagonal weight 2) or a BN 3c payload (weights
+ * 1,2,1).  out[0..3] = ||x-x1||_w, ||x1||_w, ||x-x2||_w, ||x2||_w (fp64). */
+typedef struct spngd_stat_req {
+  const float* x; const float* x1; const float* x2;  /* x1/x2 may be NULL */
+  int64_t n;            /* packed dimension (kind 0) or channels (kind 1) */
+  int64_t kind;         /* 0 = packed symmetric, 1 = BN 3c */
+  double* out4;         /* device doubles */
+} spngd_stat_req;
+int spngd_stat_distance_batched(spngd_ctx* ctx, int n, const spngd_stat_req* reqs);
+
+/* ---- stale scheduler (host logic, include/spngd/stale.hpp:78-132) ---------- */
+typedef struct spngd_tracker spngd_tracker;
+spngd_tracker* spngd_tracker_create(const char* id, double alpha);
+void spngd_tracker_destroy(spngd_tracker* t);
+int spngd_tracker_should_refresh(const spngd_tracker* t, int64_t step);
+/* d1 = ||x-x1||, r1 = ||x1|| (has1 = 0 if no snapshot), same for x2.
+ * reason: 0 FirstBuild, 1 Dissimilar1, 2 Dissimilar2, 3 SimilarBoth. */
+int spngd_tracker_on_refresh(spngd_tracker* t, int64_t step, int has1, double d1, double r1,
+                             int has2, double d2, double r2, int64_t* next_interval, int* reason);
+void spngd_tracker_state(const spngd_tracker* t, int64_t* t_x, int64_t* delta, int64_t* delta_prev,
+                         int64_t* refresh_count);
+
+/* ---- collectives (src/dist.cpp:181-237) over NCCL ----------------------------
+ * nccl_id: 128-byte ncclUniqueId from spngd_nccl_unique_id on rank 0. */
+int spngd_nccl_unique_id(void* out128);
+int spngd_ctx_init_comm(spngd_ctx* ctx, int world, int rank, const void* id128);
+/* ReduceScatter (mean, ncclAvg) of `count` floats per rank: send[world*count]
+ * -> recv[count]; equals reduce_scatter_v's ascending-order mean up to
+ * reduction order (dist.cpp:204-213). In-place if recv == send + rank*count. */
+int spngd_reduce_scatter_mean(spngd_ctx* ctx, const float* send, float* recv, int64_t count);
+/* AllGather of `count` floats per rank (all_gather_v, dist.cpp:222-237). */
+int spngd_all_gather(spngd_ctx* ctx, const float* send, float* recv, int64_t count);
+
+/* ---- whole optimizer step (accumulate_microsteps Stages 2-5) ---------------- */
+typedef enum spngd_layer_kind { SPNGD_FC = 0, SPNGD_CONV = 1, SPNGD_BN = 2 } spngd_layer_kind;
+
+typedef struct spngd_layer_desc {
+  int32_t kind;        /* spngd_layer_kind */
+  int32_t pad_;
+  int64_t a;           /* FC d_in, conv c_in*k*k */
+  int64_t g;           /* FC d_out, conv c_out; BN channels */
+  int64_t hw;          /* conv h_out*w_out, FC 1 */
+} spngd_layer_desc;
+
+typedef struct spngd_opt_config {
+  double lambda;       /* OptimizerConfig::lambda (dist.hpp:117) */
+  int32_t rescale;     /* OptimizerConfig::rescale */
+  int32_t stale;       /* stale_enabled */
+  double stale_alpha;
+  int64_t batch;       /* per-rank micro-batch M/K */
+} spngd_opt_config;
+
+typedef struct spngd_opt spngd_opt;
+
+int spngd_opt_create(spngd_ctx* ctx, const spngd_layer_desc* layers, int n_layers,
+                     const spngd_opt_config* cfg, spngd_opt** out);
+void spngd_opt_destroy(spngd_opt* opt);
+/* Device pointers of per-layer buffers:
+ *   which 0 act capture, 1 grad capture, 2 dW (this rank's shard-mean grad,
+ *   g x a or 2c), 3 W (g x a, or gamma|beta 2c), 4 V, 5 bn gg (M x c),
+ *   6 bn gb, 7 A_inv dense, 8 G_inv dense, 9 A packed (reduced), 10 G packed,
+ *   11 BN moments 3c (reduced). NULL if the layer has no such buffer or this
+ *   rank does not own it. */
+float* spngd_opt_buffer(spngd_opt* opt, int layer, int which, int64_t* ld);
+int spngd_opt_owner(const spngd_opt* opt, int layer);
+/* One SP-NGD step over the resident inputs (accumulate_microsteps,
+ * dist.cpp:406-675, n = 1 micro-step): factors + BN moments, RS, damped
+ * inverse, precondition + update + rescale, BN solve + update, AG. */
+int spngd_opt_step(spngd_opt* opt, int64_t step, double eta, double momentum);
+/* Per-phase device milliseconds of the last step: factor, reduce_scatter,
+ * inverse, precondition, all_gather. */
+int spngd_opt_phase_ms(spngd_opt* opt, float* out5);
+/* Number of kernels the last step launched on this rank. */
+int64_t spngd_opt_launch_count(const spngd_opt* opt);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SPNGD_B200_H_ */

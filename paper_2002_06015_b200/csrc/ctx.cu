@@ -1,0 +1,105 @@
+// Context lifecycle, error reporting and small shared host utilities.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+
+#include "ctx.cuh"
+
+namespace {
+thread_local char g_last_error[1024] = "";
+}
+
+namespace spngd {
+
+int fail(int code, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_last_error, sizeof(g_last_error), fmt, ap);
+  va_end(ap);
+  return code;
+}
+
+int fail_cuda(cudaError_t e, const char* what) {
+  return fail(SPNGD_ERR_CUDA, "CUDA error %s (%s) in %s", cudaGetErrorName(e), cudaGetErrorString(e), what);
+}
+
+int choose_kchunk(const std::vector<std::pair<int64_t, int64_t>>& tiles_and_k, int waves) {
+  double work = 0;
+  for (auto& tk : tiles_and_k) work += double(tk.first) * double(tk.second);
+  const double target_items = double(kNumSMs) * waves;
+  int64_t chunk = int64_t(work / target_items);
+  chunk = std::max<int64_t>(chunk, 1024);
+  chunk = (chunk + 31) / 32 * 32;
+  return int(std::min<int64_t>(chunk, 1 << 30));
+}
+
+}  // namespace spngd
+
+extern "C" {
+
+const char* spngd_last_error(void) { return g_last_error; }
+const char* spngd_version(void) { return "spngd_b200 0.1 (sm_100a, tcgen05 3xTF32)"; }
+
+int spngd_ctx_create(int device, void* stream, spngd_ctx** out) {
+  if (!out) return spngd::fail(SPNGD_ERR_INVALID, "spngd_ctx_create: out is NULL");
+  int count = 0;
+  cudaError_t e = cudaGetDeviceCount(&count);
+  if (e != cudaSuccess || count == 0)
+    return spngd::fail(SPNGD_ERR_CUDA, "spngd_ctx_create: no CUDA device (%s); there is no CPU fallback",
+                       cudaGetErrorString(e));
+  SPNGD_CUDA_TRY(cudaSetDevice(device));
+  cudaDeviceProp prop;
+  SPNGD_CUDA_TRY(cudaGetDeviceProperties(&prop, device));
+  if (prop.major != 10)
+    return spngd::fail(SPNGD_ERR_CUDA, "spngd_ctx_create: device %d is sm_%d%d, need sm_100 (B200)", device,
+                       prop.major, prop.minor);
+  auto* c = new spngd_ctx();
+  c->device = device;
+  if (stream) {
+    c->stream = static_cast<cudaStream_t>(stream);
+  } else {
+    SPNGD_CUDA_TRY(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    c->own_stream = true;
+  }
+  SPNGD_CUDA_TRY(cudaMalloc(&c->d_status, sizeof(int)));
+  SPNGD_CUDA_TRY(cudaMemset(c->d_status, 0, sizeof(int)));
+  SPNGD_CUDA_TRY(cudaMallocHost(&c->h_status, sizeof(int)));
+  *out = c;
+  return SPNGD_OK;
+}
+
+void spngd_ctx_destroy(spngd_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  cudaStreamSynchronize(ctx->stream);
+  if (ctx->d_status) cudaFree(ctx->d_status);
+  if (ctx->h_status) cudaFreeHost(ctx->h_status);
+  if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
+  spngd::comm_destroy(ctx);
+  delete ctx;
+}
+
+void* spngd_ctx_stream(spngd_ctx* ctx) { return ctx ? static_cast<void*>(ctx->stream) : nullptr; }
+
+int spngd_ctx_sync(spngd_ctx* ctx) {
+  if (!ctx) return spngd::fail(SPNGD_ERR_INVALID, "spngd_ctx_sync: ctx is NULL");
+  SPNGD_CUDA_TRY(cudaMemcpyAsync(ctx->h_status, ctx->d_status, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  SPNGD_CUDA_TRY(cudaMemsetAsync(ctx->d_status, 0, sizeof(int), ctx->stream));
+  SPNGD_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  const int s = *ctx->h_status;
+  switch (s) {
+    case SPNGD_OK:
+      return SPNGD_OK;
+    case SPNGD_ERR_NOT_POSITIVE_DEFINITE:
+      return spngd::fail(s, "spd_inverse: Cholesky/Schur pivot not positive or non-finite entries");
+    case SPNGD_ERR_SINGULAR_BLOCK:
+      return spngd::fail(s, "inv2x2: determinant below 1e-30");
+    default:
+      return spngd::fail(s, "device-side error %d", s);
+  }
+}
+
+}  // extern "C"

@@ -1,0 +1,61 @@
+// Context, device workspace and descriptor upload helpers.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "spngd_b200.h"
+
+struct ncclComm;
+
+struct spngd_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  int* d_status = nullptr;      // device-side error word
+  int* h_status = nullptr;      // pinned mirror
+  ncclComm* comm = nullptr;
+  int world = 1, rank = 0;
+  int64_t launches = 0;         // kernels launched through this context
+};
+
+namespace spngd {
+
+// Stream-ordered scratch buffer (cudaMallocAsync) released at scope exit.
+class DeviceScratch {
+ public:
+  DeviceScratch(spngd_ctx* ctx) : ctx_(ctx) {}
+  ~DeviceScratch() {
+    for (void* p : ptrs_) cudaFreeAsync(p, ctx_->stream);
+  }
+  template <typename T>
+  T* alloc(size_t count) {
+    void* p = nullptr;
+    if (count == 0) count = 1;
+    if (cudaMallocAsync(&p, count * sizeof(T), ctx_->stream) != cudaSuccess) return nullptr;
+    ptrs_.push_back(p);
+    return static_cast<T*>(p);
+  }
+  template <typename T>
+  T* upload(const std::vector<T>& v) {
+    T* d = alloc<T>(v.size());
+    if (d && !v.empty()) cudaMemcpyAsync(d, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, ctx_->stream);
+    return d;
+  }
+
+ private:
+  spngd_ctx* ctx_;
+  std::vector<void*> ptrs_;
+};
+
+inline int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
+
+// Chooses the split-K chunk so a grouped launch has ~`waves` work items per SM.
+void comm_destroy(spngd_ctx* ctx);  // comm.cu
+
+int choose_kchunk(const std::vector<std::pair<int64_t, int64_t>>& tiles_and_k, int waves = 6);
+
+}  // namespace spngd

@@ -1,0 +1,154 @@
+// K1: Kronecker-factor construction (factor_A / factor_G, src/fisher.cpp:55-145)
+// and K2: BatchNorm unit moments (build_bn_block, src/fisher.cpp:147-185).
+//
+// K1 is one grouped SYRK launch over every requested factor: only the upper
+// triangle of 128x128 tiles is computed (SYRK-half), the capture is read in
+// its reference layout (conv: stacked im2col (M*dim) x hw, FC: M x dim), and
+// the epilogue writes the packed upper triangle (linalg.hpp:48-51) scaled by
+// 1/(n*hw) or 1/n directly.  Long K (up to B*h*w = 401,408 at ResNet-50 conv1)
+// is split into chunks whose fp32 partial tiles are summed in fp64 by a
+// deterministic reduction kernel.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+
+#include "ctx.cuh"
+#include "factor.cuh"
+#include "gemm_tf32x3.cuh"
+
+namespace spngd {
+
+namespace {
+
+__global__ void bn_moments_kernel(const spngd_bn_moments_req* __restrict__ reqs) {
+  const spngd_bn_moments_req r = reqs[blockIdx.y];
+  const int64_t ch = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (ch >= r.c) return;
+  // Same per-channel accumulation order as build_bn_block (fisher.cpp:172-177).
+  double sgg = 0.0, sgb = 0.0, sbb = 0.0;
+  for (int64_t s = r.lo; s < r.hi; ++s) {
+    const double g = r.gg[s * r.c + ch], b = r.gb[s * r.c + ch];
+    sgg += g * g;
+    sgb += g * b;
+    sbb += b * b;
+  }
+  const double inv_n = 1.0 / double(r.hi - r.lo);
+  r.out3c[3 * ch + 0] = float(sgg * inv_n);
+  r.out3c[3 * ch + 1] = float(sgb * inv_n);
+  r.out3c[3 * ch + 2] = float(sbb * inv_n);
+}
+
+}  // namespace
+
+int plan_factors(const spngd_factor_req* reqs, int n, FactorPlan& plan) {
+  plan = FactorPlan();
+  std::vector<std::pair<int64_t, int64_t>> tk;
+  for (int i = 0; i < n; ++i) {
+    const spngd_factor_req& r = reqs[i];
+    if (!r.x || !r.packed_out) return fail(SPNGD_ERR_INVALID, "factor request %d: null pointer", i);
+    if (r.dim <= 0) return fail(SPNGD_ERR_SHAPE_MISMATCH, "factor request %d: dim must be > 0", i);
+    if (r.lo < 0 || r.hi <= r.lo) return fail(SPNGD_ERR_EMPTY_BATCH, "factor request %d: empty sample range", i);
+    if (r.layout == 1 && r.hw <= 0) return fail(SPNGD_ERR_SHAPE_MISMATCH, "factor request %d: hw must be > 0", i);
+    GemmOperand op{};
+    if (r.layout == 0) {  // FC: element (row i, sample s) = x[s*dim + i]
+      op.ptr = r.x + r.lo * r.dim;
+      op.row_stride = 1;
+      op.seg_len = 1;
+      op.seg_stride = r.dim;
+    } else {              // conv: element (i, s*hw+p) = x[s*dim*hw + i*hw + p]
+      op.ptr = r.x + r.lo * r.dim * r.hw;
+      op.row_stride = r.hw;
+      op.seg_len = r.hw;
+      op.seg_stride = r.dim * r.hw;
+    }
+    op.rows = int32_t(r.dim);
+    finalize_operand(op);
+    const int64_t K = (r.hi - r.lo) * (r.layout == 0 ? 1 : r.hw);
+    if (K > INT32_MAX) return fail(SPNGD_ERR_SHAPE_MISMATCH, "factor request %d: K too large", i);
+    GemmProblem p{};
+    p.A = op;
+    p.B = op;
+    p.M = p.N = int32_t(r.dim);
+    p.K = int32_t(K);
+    p.flags = FLAG_SAME_AB;
+    p.alpha = float(r.scale);
+    p.C = r.packed_out;
+    plan.probs.push_back(p);
+    const int64_t t = (r.dim + kTileM - 1) / kTileM;
+    tk.push_back({t * (t + 1) / 2, K});
+  }
+  plan.kchunk = choose_kchunk(tk);
+  int slot = 0;
+  for (int i = 0; i < n; ++i) {
+    GemmProblem& p = plan.probs[i];
+    const bool split = p.K > plan.kchunk;
+    p.mode = split ? EPI_PARTIAL : EPI_PACKED;
+    plan_problem_tiles(i, p, /*upper_only=*/true, split ? plan.kchunk : p.K + kTileK, plan.items, &plan.reduce,
+                       &slot, reqs[i].scale, reqs[i].packed_out);
+  }
+  plan.n_slots = slot;
+  // Longest work first: items are independent, so issue the big K ranges early.
+  std::stable_sort(plan.items.begin(), plan.items.end(), [](const GemmWorkItem& x, const GemmWorkItem& y) {
+    return (x.k1 - x.k0) > (y.k1 - y.k0);
+  });
+  return SPNGD_OK;
+}
+
+int run_factors(spngd_ctx* ctx, const GemmProblem* d_probs, const GemmWorkItem* d_items, int n_items,
+                float* d_partials, const SyrkReduceTask* d_reduce, int n_reduce) {
+  int rc = launch_gemm(d_probs, d_items, n_items, d_partials, ctx->d_status, ctx->stream);
+  if (rc) return rc;
+  ctx->launches += n_items > 0;
+  rc = launch_syrk_reduce(d_reduce, n_reduce, d_partials, ctx->stream);
+  ctx->launches += n_reduce > 0;
+  return rc;
+}
+
+int launch_bn_moments(spngd_ctx* ctx, const spngd_bn_moments_req* d_reqs, int n, int64_t max_c) {
+  if (n <= 0) return SPNGD_OK;
+  dim3 grid(unsigned((max_c + 255) / 256), unsigned(n));
+  bn_moments_kernel<<<grid, 256, 0, ctx->stream>>>(d_reqs);
+  SPNGD_CUDA_TRY(cudaGetLastError());
+  ctx->launches++;
+  return SPNGD_OK;
+}
+
+}  // namespace spngd
+
+extern "C" int spngd_factor_sym_batched(spngd_ctx* ctx, int n, const spngd_factor_req* reqs) {
+  using namespace spngd;
+  if (!ctx || (n > 0 && !reqs)) return fail(SPNGD_ERR_INVALID, "spngd_factor_sym_batched: null argument");
+  if (n == 0) return SPNGD_OK;
+  FactorPlan plan;
+  int rc = plan_factors(reqs, n, plan);
+  if (rc) return rc;
+  DeviceScratch scratch(ctx);
+  auto* d_probs = scratch.upload(plan.probs);
+  auto* d_items = scratch.upload(plan.items);
+  auto* d_reduce = scratch.upload(plan.reduce);
+  float* d_partials = scratch.alloc<float>(size_t(std::max(plan.n_slots, 1)) * kTileM * kTileN);
+  if (!d_probs || !d_items || !d_reduce || !d_partials) return fail(SPNGD_ERR_CUDA, "factor: workspace allocation failed");
+  rc = run_factors(ctx, d_probs, d_items, int(plan.items.size()), d_partials, d_reduce, int(plan.reduce.size()));
+  if (rc) return rc;
+  SPNGD_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  return SPNGD_OK;
+}
+
+extern "C" int spngd_bn_moments_batched(spngd_ctx* ctx, int n, const spngd_bn_moments_req* reqs) {
+  using namespace spngd;
+  if (!ctx || (n > 0 && !reqs)) return fail(SPNGD_ERR_INVALID, "spngd_bn_moments_batched: null argument");
+  int64_t max_c = 0;
+  for (int i = 0; i < n; ++i) {
+    if (reqs[i].lo < 0 || reqs[i].hi <= reqs[i].lo) return fail(SPNGD_ERR_EMPTY_BATCH, "build_bn_block: empty sample range");
+    if (!reqs[i].gg || !reqs[i].gb || !reqs[i].out3c) return fail(SPNGD_ERR_EMPTY_BATCH, "build_bn_block: no captured gradients");
+    max_c = std::max(max_c, reqs[i].c);
+  }
+  if (n == 0) return SPNGD_OK;
+  DeviceScratch scratch(ctx);
+  std::vector<spngd_bn_moments_req> v(reqs, reqs + n);
+  auto* d = scratch.upload(v);
+  int rc = launch_bn_moments(ctx, d, n, max_c);
+  if (rc) return rc;
+  SPNGD_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  return SPNGD_OK;
+}

@@ -1,0 +1,386 @@
+// sm_100a grouped 3xTF32 GEMM on tcgen05 tensor cores with TMEM accumulators.
+//
+// CTA layout (288 threads, one CTA per SM):
+//   warps 0-3  producers of the A tile (128 rows x 32 k per stage)
+//   warps 4-7  producers of the B tile (idle on SYRK diagonal tiles)
+//   warp  8    TMEM allocator + single-thread tcgen05.mma issuer
+// Producers read fp32 from HBM/L2 (coalesced float4 when the layout allows),
+// split every element into tf32 hi/lo (x = hi + lo to ~2^-22) and store both
+// into 128B-swizzled K-major smem tiles; the MMA thread issues
+// hi*hi + hi*lo + lo*hi per 8-wide k step (3xTF32 = fp32-accurate products,
+// SURVEY.md §7.3).  mbarrier full/empty rings pipeline kStages smem stages;
+// tcgen05.commit releases smem slots.
+// The tensor core's fp32 accumulator rounds toward zero on every MMA, which
+// biases long sums (measured ~1e-8 * K relative).  Each 32-deep stage
+// therefore accumulates into one of two TMEM buffers that the producer warps
+// drain right after (tcgen05.ld 32x32b) into round-to-nearest fp32 registers,
+// so the truncation bias is bounded by one stage (~4e-7) at any K.
+// Epilogue: registers -> padded smem tile -> coalesced global writes in the
+// order each epilogue mode needs.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+
+#include "common.cuh"
+#include "gemm_tf32x3.cuh"
+
+namespace spngd {
+
+namespace {
+
+constexpr int kOperandBytes = kTileM * kTileK * 4;     // 16 KB (128 rows x 128 B)
+constexpr int kStageBytes = 4 * kOperandBytes;         // Ahi, Alo, Bhi, Blo
+constexpr int kEpiStride = kTileN + 1;                 // padded fp32 tile row
+constexpr int kTmemCols = 256;  // two 128-column accumulators
+
+struct __align__(8) SmemCtl {
+  uint64_t full[kStages];
+  uint64_t empty[kStages];
+  uint64_t tmem_full[2];
+  uint64_t tmem_empty[2];
+  uint32_t tmem_base;
+  int32_t pad;
+  GemmProblem prob;
+  GemmWorkItem item;
+};
+
+__device__ __forceinline__ float4 ldg4(const float* p) { return __ldg(reinterpret_cast<const float4*>(p)); }
+
+// Loads the 4 consecutive k values (k .. k+3) of row `r` of `op`, zero outside.
+__device__ __forceinline__ float4 load_chunk(const GemmOperand& op, int32_t r, int64_t k, int64_t kend) {
+  float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (r >= op.rows || k >= kend) return v;
+  if (op.vec && k + 3 < kend) {
+    const int64_t s = k / op.seg_len;
+    const int64_t p = k - s * op.seg_len;
+    return ldg4(op.ptr + s * op.seg_stride + int64_t(r) * op.row_stride + p);
+  }
+  float t[4];
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    const int64_t kk = k + e;
+    t[e] = 0.f;
+    if (kk < kend) {
+      const int64_t s = kk / op.seg_len;
+      const int64_t p = kk - s * op.seg_len;
+      t[e] = __ldg(op.ptr + s * op.seg_stride + int64_t(r) * op.row_stride + p);
+    }
+  }
+  return make_float4(t[0], t[1], t[2], t[3]);
+}
+
+__global__ void __launch_bounds__(kGemmThreads, 1)
+    gemm_tf32x3_kernel(const GemmProblem* __restrict__ probs, const GemmWorkItem* __restrict__ items,
+                       float* __restrict__ partials, int* status) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  // 1024-byte alignment for the SWIZZLE_128B atoms.
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  SmemCtl* ctl = reinterpret_cast<SmemCtl*>(smem + kStages * kStageBytes);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+
+  if (threadIdx.x == 0) {
+    ctl->item = items[blockIdx.x];
+  }
+  __syncthreads();
+  {
+    // Cooperative copy of the problem descriptor.
+    const int32_t* src = reinterpret_cast<const int32_t*>(probs + ctl->item.problem);
+    int32_t* dst = reinterpret_cast<int32_t*>(&ctl->prob);
+    for (int i = threadIdx.x; i < int(sizeof(GemmProblem) / 4); i += blockDim.x) dst[i] = src[i];
+  }
+  __syncthreads();
+
+  const GemmWorkItem item = ctl->item;
+  const GemmProblem& prob = ctl->prob;
+  const bool same_ab = (prob.flags & FLAG_SAME_AB) != 0;
+  const bool diag_shared = same_ab && item.tm == item.tn;
+  const int n_iters = (item.k1 - item.k0 + kTileK - 1) / kTileK;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&ctl->full[s], diag_shared ? 128 : 256);
+      mbar_init(&ctl->empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&ctl->tmem_full[b], 1);
+      mbar_init(&ctl->tmem_empty[b], 256);
+    }
+    mbar_fence_init();
+  }
+  if (warp == 8) tmem_alloc<kTmemCols>(&ctl->tmem_base);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = ctl->tmem_base;
+
+  float* T = reinterpret_cast<float*>(smem);  // 128 x 129 fp32 epilogue tile, reuses the stage ring
+  if (warp < 8) {
+    // ------------------------------------------- producers + accumulator drain
+    const bool is_b = warp >= 4;
+    const bool produce = !(is_b && diag_shared);
+    const GemmOperand& op = is_b ? prob.B : prob.A;
+    const int t = threadIdx.x & 127;
+    const int c = t & 7;           // 16-byte chunk within the 128-byte row
+    const int rbase = t >> 3;      // 0..15
+    const int32_t row0 = (is_b ? item.tn : item.tm) * kTileM;
+    const uint32_t hi_off = is_b ? 2 * kOperandBytes : 0;
+    const uint32_t lo_off = hi_off + kOperandBytes;
+    // Drain role: TMEM lanes 32*(warp%4).., columns 64*(warp/4)..+63.
+    const uint32_t lane_base = uint32_t((warp & 3) * 32) << 16;
+    const uint32_t col_base = (warp >> 2) * 64;
+    float acc[64];
+#pragma unroll
+    for (int j = 0; j < 64; ++j) acc[j] = 0.f;
+    auto drain = [&](int j) {
+      const int b = j & 1;
+      mbar_wait(&ctl->tmem_full[b], (j >> 1) & 1);
+      tc_fence_after();
+      float v[32];
+      tmem_ld_32x32b_x32(tmem + lane_base + b * 128 + col_base, v);
+#pragma unroll
+      for (int q = 0; q < 32; ++q) acc[q] += v[q];
+      tmem_ld_32x32b_x32(tmem + lane_base + b * 128 + col_base + 32, v);
+#pragma unroll
+      for (int q = 0; q < 32; ++q) acc[32 + q] += v[q];
+      tc_fence_before();
+      mbar_arrive(&ctl->tmem_empty[b]);
+    };
+    float4 v[8];
+    if (produce) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) v[j] = load_chunk(op, row0 + rbase + 16 * j, int64_t(item.k0) + 4 * c, item.k1);
+    }
+    for (int it = 0; it < n_iters; ++it) {
+      if (produce) {
+        const int slot = it % kStages;
+        const uint32_t round = it / kStages;
+        mbar_wait(&ctl->empty[slot], (round & 1) ^ 1);
+        uint8_t* stage = smem + slot * kStageBytes;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const int r = rbase + 16 * j;
+          const uint32_t off = r * 128 + ((c ^ (r & 7)) << 4);
+          float4 h, l;
+          tf32_split(v[j].x, h.x, l.x);
+          tf32_split(v[j].y, h.y, l.y);
+          tf32_split(v[j].z, h.z, l.z);
+          tf32_split(v[j].w, h.w, l.w);
+          *reinterpret_cast<float4*>(stage + hi_off + off) = h;
+          *reinterpret_cast<float4*>(stage + lo_off + off) = l;
+        }
+        fence_proxy_async_smem();
+        mbar_arrive(&ctl->full[slot]);
+        if (it + 1 < n_iters) {
+          const int64_t kn = int64_t(item.k0) + int64_t(it + 1) * kTileK + 4 * c;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) v[j] = load_chunk(op, row0 + rbase + 16 * j, kn, item.k1);
+        }
+      }
+      if (it >= 1) drain(it - 1);
+    }
+    if (n_iters >= 1) drain(n_iters - 1);
+    // All MMAs have completed (last tmem_full), so the stage ring is free.
+    __syncwarp();
+    asm volatile("bar.sync 1, 256;" ::: "memory");  // producers only: ring reads done before T writes
+    const int r = (warp & 3) * 32 + lane;
+#pragma unroll
+    for (int j = 0; j < 64; ++j) T[r * kEpiStride + col_base + j] = acc[j];
+  } else {
+    // ------------------------------------------------------------ MMA issuer
+    constexpr uint32_t idesc = umma_idesc_tf32(kTileM, kTileN);
+    for (int it = 0; it < n_iters; ++it) {
+      const int slot = it % kStages;
+      const uint32_t round = it / kStages;
+      const int b = it & 1;
+      mbar_wait(&ctl->full[slot], round & 1);
+      if (it >= 2) mbar_wait(&ctl->tmem_empty[b], ((it >> 1) + 1) & 1);
+      tc_fence_after();
+      if (lane == 0) {
+        const uint32_t base = smem_u32(smem + slot * kStageBytes);
+        const uint32_t a_hi = base, a_lo = base + kOperandBytes;
+        const uint32_t b_hi = diag_shared ? a_hi : base + 2 * kOperandBytes;
+        const uint32_t b_lo = diag_shared ? a_lo : base + 3 * kOperandBytes;
+        const uint32_t d = tmem + b * 128;
+#pragma unroll
+        for (int kk = 0; kk < kTileK / 8; ++kk) {
+          const uint32_t koff = kk * 32;  // 8 tf32 = 32 bytes along the swizzled row
+          const uint64_t dah = umma_desc_k_sw128(a_hi + koff), dal = umma_desc_k_sw128(a_lo + koff);
+          const uint64_t dbh = umma_desc_k_sw128(b_hi + koff), dbl = umma_desc_k_sw128(b_lo + koff);
+          umma_tf32(d, dal, dbh, idesc, kk > 0 ? 1u : 0u);
+          umma_tf32(d, dah, dbl, idesc, 1u);
+          umma_tf32(d, dah, dbh, idesc, 1u);
+        }
+        umma_commit(&ctl->empty[slot]);
+        umma_commit(&ctl->tmem_full[b]);
+      }
+      __syncwarp();
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 8) {
+    tc_fence_after();
+    tmem_dealloc<kTmemCols>(tmem);
+  }
+
+  const int tid = threadIdx.x;
+  const int nthr = blockDim.x;
+  const int32_t m0 = item.tm * kTileM, n0 = item.tn * kTileN;
+  switch (prob.mode) {
+    case EPI_PARTIAL: {
+      float* dst = partials + int64_t(item.slot) * kTileM * kTileN;
+      for (int idx = tid; idx < kTileM * kTileN; idx += nthr) {
+        const int r = idx >> 7, c = idx & 127;
+        dst[idx] = T[r * kEpiStride + c];
+      }
+      break;
+    }
+    case EPI_PACKED: {
+      const int64_t n = prob.M;
+      for (int idx = tid; idx < kTileM * kTileN; idx += nthr) {
+        const int r = idx >> 7, c = idx & 127;
+        const int64_t i = m0 + r, j = n0 + c;
+        if (i < prob.M && j < prob.N && i <= j) prob.C[packed_offset(n, i, j)] = prob.alpha * T[r * kEpiStride + c];
+      }
+      break;
+    }
+    case EPI_DENSE: {
+      const bool mirror = (prob.flags & FLAG_SYM_MIRROR) != 0;
+      for (int idx = tid; idx < kTileM * kTileN; idx += nthr) {
+        const int r = idx >> 7, c = idx & 127;
+        const int64_t i = m0 + r, j = n0 + c;
+        if (i < prob.M && j < prob.N && (!mirror || i <= j)) {
+          float val = prob.alpha * T[r * kEpiStride + c];
+          if (prob.beta != 0.f) val += prob.beta * prob.Cin[i * prob.ldc + j];
+          prob.C[i * prob.ldc + j] = val;
+          T[r * kEpiStride + c] = val;
+        }
+      }
+      if (mirror || (prob.flags & FLAG_TRANS)) {
+        __syncthreads();
+        float* dstT = mirror ? prob.C : prob.CT;
+        const int64_t ldt = mirror ? prob.ldc : prob.ldct;
+        for (int idx = tid; idx < kTileM * kTileN; idx += nthr) {
+          const int c = idx >> 7, r = idx & 127;
+          const int64_t i = m0 + r, j = n0 + c;
+          if (i < prob.M && j < prob.N && (!mirror || i < j)) dstT[j * ldt + i] = T[r * kEpiStride + c];
+        }
+      }
+      break;
+    }
+    case EPI_UPDATE: {
+      // Tile of P^T: rows = a-index (M = a), cols = g-index.  W is g x a
+      // row-major, so element (i = n0+c, j = m0+r) lives at W[i*a + j].
+      const int64_t a = prob.M;
+      double ss = 0.0;
+      for (int idx = tid; idx < kTileM * kTileN; idx += nthr) {
+        const int c = idx >> 7, r = idx & 127;
+        const int64_t j = m0 + r, i = n0 + c;
+        if (j < prob.M && i < prob.N) {
+          const float p = prob.alpha * T[r * kEpiStride + c];
+          const int64_t w_idx = i * a + j;
+          if (prob.P_out) prob.P_out[w_idx] = p;
+          if (prob.W) {
+            const float w = prob.W[w_idx], vel = prob.V[w_idx];
+            const float nw = w - prob.eta * p + prob.momentum * vel;  // fisher.cpp:332
+            prob.W[w_idx] = nw;
+            prob.V[w_idx] = nw - w;                                   // fisher.cpp:333
+            ss += double(nw) * double(nw);
+          }
+        }
+      }
+      if (prob.norm2) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+        if (lane == 0) atomicAdd(prob.norm2, ss);
+      }
+      break;
+    }
+    default:
+      if (tid == 0) set_status(status, SPNGD_ERR_INVALID);
+  }
+}
+
+__global__ void syrk_reduce_kernel(const SyrkReduceTask* __restrict__ tasks, const float* __restrict__ partials) {
+  const SyrkReduceTask t = tasks[blockIdx.x];
+  const int64_t n = t.n;
+  for (int idx = threadIdx.x; idx < kTileM * kTileN; idx += blockDim.x) {
+    const int r = idx >> 7, c = idx & 127;
+    const int64_t i = int64_t(t.tm) * kTileM + r, j = int64_t(t.tn) * kTileN + c;
+    if (i >= n || j >= n || i > j) continue;
+    double s = 0.0;
+    const float* p = partials + int64_t(t.slot0) * kTileM * kTileN + idx;
+    for (int q = 0; q < t.nslots; ++q) s += double(p[int64_t(q) * kTileM * kTileN]);
+    t.packed_out[packed_offset(n, i, j)] = float(s * t.scale);
+  }
+}
+
+}  // namespace
+
+void finalize_operand(GemmOperand& op) {
+  const uintptr_t addr = reinterpret_cast<uintptr_t>(op.ptr);
+  op.vec = (addr % 16 == 0) && (op.seg_len % 4 == 0) && (op.row_stride % 4 == 0) && (op.seg_stride % 4 == 0);
+}
+
+size_t gemm_smem_bytes() { return size_t(kStages) * kStageBytes + sizeof(SmemCtl) + 1024; }
+
+int launch_gemm(const GemmProblem* d_probs, const GemmWorkItem* d_items, int n_items, float* d_partials,
+                int* d_status, cudaStream_t stream) {
+  if (n_items <= 0) return SPNGD_OK;
+  static bool attr_set = false;
+  const size_t smem = gemm_smem_bytes();
+  if (!attr_set) {
+    SPNGD_CUDA_TRY(cudaFuncSetAttribute(gemm_tf32x3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    attr_set = true;
+  }
+  gemm_tf32x3_kernel<<<n_items, kGemmThreads, smem, stream>>>(d_probs, d_items, d_partials, d_status);
+  SPNGD_CUDA_TRY(cudaGetLastError());
+  return SPNGD_OK;
+}
+
+int launch_syrk_reduce(const SyrkReduceTask* d_tasks, int n_tasks, const float* d_partials, cudaStream_t stream) {
+  if (n_tasks <= 0) return SPNGD_OK;
+  syrk_reduce_kernel<<<n_tasks, 256, 0, stream>>>(d_tasks, d_partials);
+  SPNGD_CUDA_TRY(cudaGetLastError());
+  return SPNGD_OK;
+}
+
+int plan_problem_tiles(int problem_index, const GemmProblem& p, bool upper_only, int kchunk,
+                       std::vector<GemmWorkItem>& items, std::vector<SyrkReduceTask>* reduce, int* next_slot,
+                       double reduce_scale, float* packed_out) {
+  const int tiles_m = (p.M + kTileM - 1) / kTileM;
+  const int tiles_n = (p.N + kTileN - 1) / kTileN;
+  kchunk = std::max(kTileK, (kchunk / kTileK) * kTileK);
+  const int nchunks = std::max(1, (p.K + kchunk - 1) / kchunk);
+  int used = 0;
+  for (int tm = 0; tm < tiles_m; ++tm)
+    for (int tn = upper_only ? tm : 0; tn < tiles_n; ++tn) {
+      if (p.ktri) {  // triangular operands: one item over the nonzero K band
+        int k0 = 0, k1 = p.K;
+        if (p.ktri & KTRI_A_LOWER) k1 = std::min(k1, (tm + 1) * kTileM);
+        if (p.ktri & KTRI_A_UPPER) k0 = std::max(k0, tm * kTileM);
+        if (p.ktri & KTRI_B_LOWER) k1 = std::min(k1, (tn + 1) * kTileN);
+        if (p.ktri & KTRI_B_UPPER) k0 = std::max(k0, tn * kTileN);
+        if (k1 < k0) k1 = k0;
+        items.push_back({problem_index, tm, tn, k0, k1, -1});
+        continue;
+      }
+      if (nchunks == 1) {
+        items.push_back({problem_index, tm, tn, 0, p.K, -1});
+        continue;
+      }
+      const int slot0 = *next_slot;
+      for (int q = 0; q < nchunks; ++q) {
+        const int k0 = q * kchunk, k1 = std::min(p.K, k0 + kchunk);
+        items.push_back({problem_index, tm, tn, k0, k1, (*next_slot)++});
+      }
+      used += nchunks;
+      if (reduce) reduce->push_back({tm, tn, slot0, nchunks, p.M, 0, reduce_scale, packed_out});
+    }
+  return used;
+}
+
+}  // namespace spngd

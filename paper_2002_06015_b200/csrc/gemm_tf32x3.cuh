@@ -1,0 +1,107 @@
+// Grouped 3xTF32 tcgen05 GEMM: C[m,n] = alpha * sum_k A[m,k] B[n,k] (+ epilogue).
+//
+// One engine serves every dense contraction of the SP-NGD step:
+//   * K1 factor construction (SYRK over captures, packed/partial epilogues),
+//   * the Schur-complement recursion of the damped inverse (dense epilogues),
+//   * K5 preconditioning G^-1 dW A^-1 with the fused momentum update.
+// Operands are fp32 in HBM, K-major ("row r, column k") with an optional
+// segmented K axis so a conv capture (M*dim) x hw is addressed in place:
+//   element (r, k) = ptr[(k / seg_len) * seg_stride + r * row_stride + k % seg_len].
+#pragma once
+
+#include <stdint.h>
+
+#include <vector>
+
+namespace spngd {
+
+struct GemmOperand {
+  const float* ptr;
+  int64_t row_stride;
+  int64_t seg_len;
+  int64_t seg_stride;
+  int32_t rows;   // valid rows; rows >= this read as zero
+  int32_t vec;    // float4 loads legal (set by finalize_operand)
+};
+
+enum GemmEpi : int32_t {
+  EPI_PARTIAL = 0,  // raw fp32 tile -> partials[slot] (split-K)
+  EPI_PACKED = 1,   // alpha*acc -> packed upper triangle (i <= j) of C (n = M)
+  EPI_DENSE = 2,    // alpha*acc + beta*Cin -> C (row-major), optional mirror / transposed copy
+  EPI_UPDATE = 3,   // P^T tile -> W/V momentum update (+ ||W'||^2), see precond.cu
+};
+
+enum GemmFlags : int32_t {
+  FLAG_SAME_AB = 1,    // B is the same operand as A (SYRK): diagonal tiles load once
+  FLAG_SYM_MIRROR = 2, // EPI_DENSE: write only i <= j and mirror to (j, i)
+  FLAG_TRANS = 4,      // EPI_DENSE: also write CT[j*ldct + i]
+};
+
+struct GemmProblem {
+  GemmOperand A, B;
+  int32_t M, N, K;
+  int32_t mode;
+  int32_t flags;
+  int32_t ktri;     // triangular operands: K range trimmed per tile (KTRI_*)
+  int32_t pad_;
+  float alpha, beta;
+  float* C;
+  int64_t ldc;
+  const float* Cin;
+  float* CT;
+  int64_t ldct;
+  // EPI_UPDATE
+  float* W;
+  float* V;
+  float* P_out;
+  double* norm2;
+  float eta, momentum;
+};
+
+enum KTri : int32_t {
+  KTRI_A_LOWER = 1,  // A row i is zero for k > i      -> k < (tm+1)*128
+  KTRI_A_UPPER = 2,  // A row i is zero for k < i      -> k >= tm*128
+  KTRI_B_LOWER = 4,  // B row j is zero for k > j      -> k < (tn+1)*128
+  KTRI_B_UPPER = 8,  // B row j is zero for k < j      -> k >= tn*128
+};
+
+struct GemmWorkItem {
+  int32_t problem;
+  int32_t tm, tn;
+  int32_t k0, k1;
+  int32_t slot;
+};
+
+// Reduction task for split-K SYRK tiles: sum partial slots, scale, pack.
+struct SyrkReduceTask {
+  int32_t tm, tn;
+  int32_t slot0, nslots;
+  int32_t n;          // matrix dimension
+  int32_t pad_;
+  double scale;
+  float* packed_out;
+};
+
+constexpr int kTileM = 128;
+constexpr int kTileN = 128;
+constexpr int kTileK = 32;     // fp32 elements per stage = one 128-byte swizzle row
+constexpr int kStages = 3;
+constexpr int kGemmThreads = 288;  // 4 A-producer warps, 4 B-producer warps, 1 MMA warp
+
+void finalize_operand(GemmOperand& op);
+size_t gemm_smem_bytes();
+
+// Launch one grouped GEMM over device-resident problem/work arrays.
+int launch_gemm(const GemmProblem* d_probs, const GemmWorkItem* d_items, int n_items, float* d_partials,
+                int* d_status, cudaStream_t stream);
+int launch_syrk_reduce(const SyrkReduceTask* d_tasks, int n_tasks, const float* d_partials, cudaStream_t stream);
+
+// Host planning helpers.
+// Upper-triangle (or full) tile list for one problem with K split into chunks
+// of at most `kchunk` (multiple of kTileK).  Appends to items; returns the
+// number of partial slots consumed (0 if unsplit).
+int plan_problem_tiles(int problem_index, const GemmProblem& p, bool upper_only, int kchunk,
+                       std::vector<GemmWorkItem>& items, std::vector<SyrkReduceTask>* reduce,
+                       int* next_slot, double reduce_scale, float* packed_out);
+
+}  // namespace spngd

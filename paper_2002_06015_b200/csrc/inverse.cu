@@ -1,0 +1,503 @@
+// K3/K4: damped SPD inverse (spd_inverse, src/linalg.cpp:29-48;
+// damp_and_invert, src/fisher.cpp:218-228).
+//
+// (M + dI)^-1 = L^-T L^-1 with L = chol(M + dI), like the reference's
+// Eigen::LLT + solve(I), computed by a recursive blocked Cholesky that carries
+// T = L^-1 along (n^3 flops: potrf n^3/3 + trtri n^3/3 + lauum n^3/3):
+//     M = [A B^T-block ; B C]:  chol(A) -> T11 (recurse),
+//     L21 = B T11^T,  S = C - L21 L21^T,  U^T = T11^T L21^T,
+//     chol(S) -> T22 (recurse),  T21 = -T22 U,      finally X = T^T T.
+// Every update is a K-major GEMM on the 3xTF32 tcgen05 engine; triangular
+// operands trim the K range per tile.  Leaves (n <= 128) run one CTA that
+// factors in fp64 registers and forms T by forward elimination.  A
+// non-positive or non-finite pivot raises NotPositiveDefinite (the LLT
+// failure of linalg.cpp:37-40).  X is written upper-tile + mirrored, so the
+// result is exactly symmetric as the reference's 0.5 (X + X^T) makes it.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+
+#include "ctx.cuh"
+#include "inverse.cuh"
+
+namespace spngd {
+
+namespace {
+
+constexpr int kBaseMax = 128;
+constexpr int kBlk = 8;
+constexpr int kBaseThreads = 160;  // >= 16*17/2 = 136 lower 8x8 register blocks
+
+// One CTA per leaf.  Thread owns lower block (bi >= bj) of both the trailing
+// matrix (fp64 registers) and T = L^-1 (fp32 registers).  Step k publishes
+// column k of the trailing matrix and row k of T through smem, then:
+//   L[i][k] = a[i][k] / sqrt(p);  a[i][j] -= a[i][k] a[j][k] / p   (i, j > k)
+//   T[k][:] /= sqrt(p);           T[i][:] -= (a[i][k] / p) T_old[k][:]  (i > k)
+__global__ void __launch_bounds__(kBaseThreads) base_chol_inv_kernel(const BaseTask* __restrict__ tasks, int* status) {
+  const BaseTask t = tasks[blockIdx.x];
+  const int n = t.n;
+  const int nb = (n + kBlk - 1) / kBlk;
+  __shared__ double colbuf[2][kBaseMax];
+  __shared__ float rowbuf[2][kBaseMax];
+  int bi = -1, bj = -1;
+  {
+    int idx = threadIdx.x;
+    for (int c = 0; c < nb; ++c) {  // column-major enumeration of lower blocks
+      const int cnt = nb - c;
+      if (idx < cnt) { bj = c; bi = c + idx; break; }
+      idx -= cnt;
+    }
+  }
+  const bool active = bi >= 0;
+  double m[kBlk][kBlk];
+  float tt[kBlk][kBlk];
+#pragma unroll
+  for (int ii = 0; ii < kBlk; ++ii)
+#pragma unroll
+    for (int jj = 0; jj < kBlk; ++jj) {
+      const int i = bi * kBlk + ii, j = bj * kBlk + jj;
+      double v = (i == j) ? 1.0 : 0.0;  // identity padding beyond n is inert
+      if (active && i < n && j < n) v = double(t.m[int64_t(i) * t.ld + j]);
+      m[ii][jj] = v;
+      tt[ii][jj] = (i == j) ? 1.f : 0.f;
+    }
+  bool bad = false;
+  for (int kb = 0; kb < nb; ++kb) {
+#pragma unroll
+    for (int kk = 0; kk < kBlk; ++kk) {
+      const int k = kb * kBlk + kk;
+      double* cb = colbuf[k & 1];
+      float* rb = rowbuf[k & 1];
+      if (active) {
+        if (bj == kb) {
+#pragma unroll
+          for (int ii = 0; ii < kBlk; ++ii) cb[bi * kBlk + ii] = m[ii][kk];
+        }
+        if (bi == kb) {
+#pragma unroll
+          for (int jj = 0; jj < kBlk; ++jj) rb[bj * kBlk + jj] = tt[kk][jj];
+        }
+      }
+      __syncthreads();
+      double p = cb[k];
+      if (!(p > 0.0) || !isfinite(p)) {
+        bad = true;
+        p = 1.0;
+      }
+      const double inv_p = 1.0 / p;
+      const double inv_s = rsqrt(p);
+      if (active && bi >= kb) {
+        double ci[kBlk], cj[kBlk];
+        float rj[kBlk];
+#pragma unroll
+        for (int ii = 0; ii < kBlk; ++ii) ci[ii] = cb[bi * kBlk + ii] * inv_p;
+#pragma unroll
+        for (int jj = 0; jj < kBlk; ++jj) {
+          cj[jj] = cb[bj * kBlk + jj];
+          rj[jj] = rb[bj * kBlk + jj];
+        }
+        // Trailing update, rows/cols > k only (earlier ones hold finished values).
+        if (bj >= kb) {
+#pragma unroll
+          for (int ii = 0; ii < kBlk; ++ii)
+#pragma unroll
+            for (int jj = 0; jj < kBlk; ++jj) {
+              const int i = bi * kBlk + ii, j = bj * kBlk + jj;
+              if (i > k && j > k) m[ii][jj] = fma(-ci[ii], cj[jj], m[ii][jj]);
+            }
+        }
+        // T elimination: columns j <= k live in blocks bj <= kb.
+        if (bj <= kb) {
+#pragma unroll
+          for (int ii = 0; ii < kBlk; ++ii) {
+            const int i = bi * kBlk + ii;
+            const float f = (i == k) ? 0.f : float(ci[ii]);
+#pragma unroll
+            for (int jj = 0; jj < kBlk; ++jj) {
+              const int j = bj * kBlk + jj;
+              if (j <= k) {
+                if (i == k) tt[ii][jj] = float(double(rj[jj]) * inv_s);
+                else if (i > k) tt[ii][jj] = fmaf(-f, rj[jj], tt[ii][jj]);
+              }
+            }
+          }
+        }
+      }
+    }
+  }
+  if (bad && threadIdx.x == 0) set_status(status, SPNGD_ERR_NOT_POSITIVE_DEFINITE);
+  if (active) {
+#pragma unroll
+    for (int ii = 0; ii < kBlk; ++ii)
+#pragma unroll
+      for (int jj = 0; jj < kBlk; ++jj) {
+        const int i = bi * kBlk + ii, j = bj * kBlk + jj;
+        if (i < n && j < n && i >= j) {
+          t.tlow[int64_t(i) * t.ld + j] = tt[ii][jj];
+          t.tup[int64_t(j) * t.ld + i] = tt[ii][jj];
+        }
+      }
+  }
+}
+
+__global__ void pi_kernel(const PiTask* __restrict__ tasks) {
+  const PiTask t = tasks[blockIdx.x];
+  double sa = 0.0, sg = 0.0;
+  for (int64_t i = threadIdx.x; i < t.a; i += blockDim.x) sa += double(t.A[packed_offset(t.a, i, i)]);
+  for (int64_t i = threadIdx.x; i < t.g; i += blockDim.x) sg += double(t.G[packed_offset(t.g, i, i)]);
+  __shared__ double ra[32], rg[32];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    sa += __shfl_xor_sync(0xffffffffu, sa, o);
+    sg += __shfl_xor_sync(0xffffffffu, sg, o);
+  }
+  if ((threadIdx.x & 31) == 0) { ra[threadIdx.x >> 5] = sa; rg[threadIdx.x >> 5] = sg; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double ta = 0, tg = 0;
+    for (int w = 0; w < int(blockDim.x >> 5); ++w) { ta += ra[w]; tg += rg[w]; }
+    const double ea = ta / double(t.a), eg = tg / double(t.g);      // avg_eigenvalue, linalg.cpp:64-69
+    const double pi = (ea < 1e-12 || eg < 1e-12) ? 1.0 : sqrt(ea / eg);  // fisher.cpp:223
+    t.dampA[0] = float(pi * t.sqrt_lambda);
+    t.dampG[0] = float(t.sqrt_lambda / pi);
+    if (t.pi_out) t.pi_out[0] = float(pi);
+  }
+}
+
+// dense = unpack(packed) + d I, by 32x32 tiles of the upper triangle so both
+// the packed reads and the mirrored (transposed) dense writes are coalesced.
+__global__ void unpack_damp_kernel(const UnpackTask* __restrict__ tasks, int* status) {
+  const UnpackTask t = tasks[blockIdx.y];
+  const float d = t.damp_dev ? t.damp_dev[0] : t.damp;
+  __shared__ float s[32][33];
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
+  const int64_t tn = (t.n + 31) / 32;
+  bool bad = false;
+  for (int64_t tt = blockIdx.x; tt < tn * tn; tt += gridDim.x) {
+    const int64_t ti = tt / tn, tj = tt % tn;
+    if (ti > tj) continue;
+    __syncthreads();
+    for (int q = 0; q < 4; ++q) {
+      const int64_t i = ti * 32 + ty + 8 * q, j = tj * 32 + tx;
+      float v = 0.f;
+      if (i < t.n && j < t.n && j >= i) {
+        v = t.packed[i * t.n - i * (i - 1) / 2 + (j - i)];
+        bad |= !isfinite(v);
+        if (i == j) v += d;
+      }
+      s[ty + 8 * q][tx] = v;
+    }
+    __syncthreads();
+    for (int q = 0; q < 4; ++q) {
+      const int li = ty + 8 * q;
+      const int64_t i = ti * 32 + li, j = tj * 32 + tx;
+      if (i < t.n && j < t.n) t.dense[i * t.ld + j] = (j >= i) ? s[li][tx] : s[tx][li];
+      if (ti != tj) {
+        const int64_t r = tj * 32 + li, c = ti * 32 + tx;  // transposed tile
+        if (r < t.n && c < t.n) t.dense[r * t.ld + c] = s[tx][li];
+      }
+    }
+  }
+  if (bad) set_status(status, SPNGD_ERR_NOT_POSITIVE_DEFINITE);
+}
+
+__global__ void pack_kernel(const PackTask* __restrict__ tasks, int* status) {
+  const PackTask t = tasks[blockIdx.y];
+  bool bad = false;
+  for (int64_t i = blockIdx.x; i < t.n; i += gridDim.x) {
+    const int64_t base = i * t.n - i * (i - 1) / 2;
+    for (int64_t j = i + threadIdx.x; j < t.n; j += blockDim.x) {
+      const float v = t.dense[i * t.ld + j];
+      bad |= !isfinite(v);
+      t.packed[base + (j - i)] = v;
+    }
+  }
+  if (bad) set_status(status, SPNGD_ERR_NOT_POSITIVE_DEFINITE);
+}
+
+// ---------------------------------------------------------------- planning
+struct Op {
+  int kind;  // 0 base, 1 gemm
+  BaseTask base;
+  GemmProblem prob;
+  bool upper;
+};
+
+int64_t split_point(int64_t n) {
+  // Keep the leading block a multiple of the 128-row MMA tile when possible.
+  int64_t n1 = round_up((n + 1) / 2, n > 2 * kBaseMax ? 128 : 32);
+  if (n1 >= n) n1 = n - 1;
+  return n1;
+}
+
+GemmOperand dense_op(const float* ptr, int64_t ld, int64_t rows, int64_t K) {
+  GemmOperand o{};
+  o.ptr = ptr;
+  o.row_stride = ld;
+  o.seg_len = std::max<int64_t>(K, 1);
+  o.seg_stride = 0;
+  o.rows = int32_t(rows);
+  finalize_operand(o);
+  return o;
+}
+
+struct Gen {
+  float* ws;
+  size_t used = 0;
+  float* take(size_t n) {
+    float* p = ws ? ws + used : nullptr;
+    used += round_up(int64_t(n), 64);
+    return p;
+  }
+};
+
+template <typename T>
+T* at(T* base, int64_t ld, int64_t r, int64_t c) {
+  return base ? base + r * ld + c : nullptr;
+}
+
+Op gemm_op(const GemmOperand& a, const GemmOperand& b, int64_t M, int64_t N, int64_t K, int32_t flags, int32_t ktri,
+           float alpha, float beta, float* C, int64_t ldc, float* CT = nullptr, int64_t ldct = 0, bool upper = false) {
+  Op o{};
+  o.kind = 1;
+  o.upper = upper;
+  GemmProblem& p = o.prob;
+  p.A = a;
+  p.B = b;
+  p.M = int32_t(M); p.N = int32_t(N); p.K = int32_t(K);
+  p.mode = EPI_DENSE; p.flags = flags; p.ktri = ktri;
+  p.alpha = alpha; p.beta = beta;
+  p.C = C; p.Cin = C; p.ldc = ldc; p.CT = CT; p.ldct = ldct;
+  return o;
+}
+
+// Cholesky + running inverse of the diagonal block at `off` of size n.
+void gen_chol(const DenseMatrix& m, int64_t off, int64_t n, Gen& g, std::vector<Op>& ops) {
+  const int64_t ld = m.ld;
+  if (n <= kBaseMax) {
+    Op o{};
+    o.kind = 0;
+    o.base = BaseTask{at(m.ptr, ld, off, off), at(m.tlow, ld, off, off), at(m.tup, ld, off, off), ld, int32_t(n), 0};
+    ops.push_back(o);
+    return;
+  }
+  const int64_t n1 = split_point(n), n2 = n - n1, o2 = off + n1;
+  gen_chol(m, off, n1, g, ops);
+  const int64_t ldl = round_up(n1, 32), ldu = round_up(n2, 32);
+  float* L21 = g.take(size_t(n2) * ldl);
+  float* Ut = g.take(size_t(n1) * ldu);
+  // L21 = B T11^T  (B = M[o2.., off..]); T11 lower -> K band k <= j
+  ops.push_back(gemm_op(dense_op(at(m.ptr, ld, o2, off), ld, n2, n1), dense_op(at(m.tlow, ld, off, off), ld, n1, n1),
+                        n2, n1, n1, 0, KTRI_B_LOWER, 1.f, 0.f, L21, ldl));
+  // S = C - L21 L21^T  (symmetric, in place)
+  ops.push_back(gemm_op(dense_op(L21, ldl, n2, n1), dense_op(L21, ldl, n2, n1), n2, n2, n1,
+                        FLAG_SAME_AB | FLAG_SYM_MIRROR, 0, -1.f, 1.f, at(m.ptr, ld, o2, o2), ld, nullptr, 0, true));
+  // U^T = T11^T L21^T; T11^T upper -> K band k >= j
+  ops.push_back(gemm_op(dense_op(at(m.tup, ld, off, off), ld, n1, n1), dense_op(L21, ldl, n2, n1), n1, n2, n1, 0,
+                        KTRI_A_UPPER, 1.f, 0.f, Ut, ldu));
+  gen_chol(m, o2, n2, g, ops);
+  // T21 = -T22 U (+ T21^T into the upper factor); T22 lower -> K band k <= i
+  ops.push_back(gemm_op(dense_op(at(m.tlow, ld, o2, o2), ld, n2, n2), dense_op(Ut, ldu, n1, n2), n2, n1, n2,
+                        FLAG_TRANS, KTRI_A_LOWER, -1.f, 0.f, at(m.tlow, ld, o2, off), ld, at(m.tup, ld, off, o2), ld));
+}
+
+void gen_ops(const DenseMatrix& m, Gen& g, std::vector<Op>& ops) {
+  gen_chol(m, 0, m.n, g, ops);
+  // X = T^T T = Tup Tup^T; row i of Tup is zero for k < i.
+  ops.push_back(gemm_op(dense_op(m.tup, m.ld, m.n, m.n), dense_op(m.tup, m.ld, m.n, m.n), m.n, m.n, m.n,
+                        FLAG_SAME_AB | FLAG_SYM_MIRROR, KTRI_A_UPPER | KTRI_B_UPPER, 1.f, 0.f, m.ptr, m.ld, nullptr, 0,
+                        true));
+}
+
+}  // namespace
+
+void plan_inverse(const std::vector<DenseMatrix>& mats, float* workspace, InversePlan& plan) {
+  plan = InversePlan();
+  Gen g{workspace};
+  std::vector<std::vector<Op>> per(mats.size());
+  size_t max_ops = 0;
+  for (size_t m = 0; m < mats.size(); ++m) {
+    gen_ops(mats[m], g, per[m]);
+    max_ops = std::max(max_ops, per[m].size());
+  }
+  plan.workspace_floats = g.used;
+  // Round r runs op r of every matrix: one base launch + one grouped GEMM.
+  for (size_t r = 0; r < max_ops; ++r) {
+    InverseRound rd{int(plan.items.size()), 0, int(plan.bases.size()), 0};
+    for (size_t m = 0; m < mats.size(); ++m) {
+      if (r >= per[m].size()) continue;
+      const Op& o = per[m][r];
+      if (o.kind == 0) {
+        plan.bases.push_back(o.base);
+      } else {
+        const int pi = int(plan.probs.size());
+        plan.probs.push_back(o.prob);
+        int slot = 0;
+        plan_problem_tiles(pi, o.prob, o.upper, o.prob.K + kTileK, plan.items, nullptr, &slot, 1.0, nullptr);
+      }
+    }
+    rd.item_cnt = int(plan.items.size()) - rd.item_off;
+    rd.base_cnt = int(plan.bases.size()) - rd.base_off;
+    plan.rounds.push_back(rd);
+  }
+}
+
+int launch_pi(spngd_ctx* ctx, const PiTask* d_tasks, int n) {
+  if (n <= 0) return SPNGD_OK;
+  pi_kernel<<<n, 256, 0, ctx->stream>>>(d_tasks);
+  SPNGD_CUDA_TRY(cudaGetLastError());
+  ctx->launches++;
+  return SPNGD_OK;
+}
+
+int launch_unpack(spngd_ctx* ctx, const UnpackTask* d_tasks, int n, int64_t max_n) {
+  if (n <= 0) return SPNGD_OK;
+  const int64_t tn = (max_n + 31) / 32;
+  dim3 grid(unsigned(std::min<int64_t>(tn * tn, 1024)), unsigned(n));
+  unpack_damp_kernel<<<grid, 256, 0, ctx->stream>>>(d_tasks, ctx->d_status);
+  SPNGD_CUDA_TRY(cudaGetLastError());
+  ctx->launches++;
+  return SPNGD_OK;
+}
+
+int launch_pack(spngd_ctx* ctx, const PackTask* d_tasks, int n, int64_t max_n) {
+  if (n <= 0) return SPNGD_OK;
+  dim3 grid(unsigned(std::min<int64_t>(max_n, 512)), unsigned(n));
+  pack_kernel<<<grid, 256, 0, ctx->stream>>>(d_tasks, ctx->d_status);
+  SPNGD_CUDA_TRY(cudaGetLastError());
+  ctx->launches++;
+  return SPNGD_OK;
+}
+
+int launch_base(spngd_ctx* ctx, const BaseTask* d_tasks, int n) {
+  if (n <= 0) return SPNGD_OK;
+  base_chol_inv_kernel<<<n, kBaseThreads, 0, ctx->stream>>>(d_tasks, ctx->d_status);
+  SPNGD_CUDA_TRY(cudaGetLastError());
+  ctx->launches++;
+  return SPNGD_OK;
+}
+
+int run_inverse(spngd_ctx* ctx, const InversePlan& plan, const GemmProblem* d_probs, const GemmWorkItem* d_items,
+                const BaseTask* d_bases) {
+  for (const InverseRound& r : plan.rounds) {
+    int rc = launch_base(ctx, d_bases + r.base_off, r.base_cnt);
+    if (rc) return rc;
+    if (r.item_cnt > 0) {
+      rc = launch_gemm(d_probs, d_items + r.item_off, r.item_cnt, nullptr, ctx->d_status, ctx->stream);
+      if (rc) return rc;
+      ctx->launches++;
+    }
+  }
+  return SPNGD_OK;
+}
+
+}  // namespace spngd
+
+using namespace spngd;
+
+extern "C" int spngd_spd_inverse_batched(spngd_ctx* ctx, int n, const spngd_spd_req* reqs) {
+  if (!ctx || (n > 0 && !reqs)) return fail(SPNGD_ERR_INVALID, "spngd_spd_inverse_batched: null argument");
+  if (n == 0) return SPNGD_OK;
+  DeviceScratch scratch(ctx);
+  std::vector<DenseMatrix> mats;
+  std::vector<UnpackTask> unpack;
+  std::vector<PackTask> pack;
+  int64_t max_n = 0;
+  for (int i = 0; i < n; ++i) {
+    const spngd_spd_req& r = reqs[i];
+    if (r.n <= 0) return fail(SPNGD_ERR_SHAPE_MISMATCH, "spd_inverse: empty matrix");
+    if (!r.packed || (!r.dense_out && !r.packed_out)) return fail(SPNGD_ERR_INVALID, "spd_inverse: null pointer");
+    if (r.dense_out && r.ld < r.n) return fail(SPNGD_ERR_SHAPE_MISMATCH, "spd_inverse: ld < n");
+    float* dense = r.dense_out;
+    int64_t ld = r.ld;
+    if (!dense) {
+      ld = round_up(r.n, 32);
+      dense = scratch.alloc<float>(size_t(r.n) * ld);
+      if (!dense) return fail(SPNGD_ERR_CUDA, "spd_inverse: allocation failed");
+    }
+    float* tl = scratch.alloc<float>(size_t(r.n) * ld);
+    float* tu = scratch.alloc<float>(size_t(r.n) * ld);
+    if (!tl || !tu) return fail(SPNGD_ERR_CUDA, "spd_inverse: allocation failed");
+    cudaMemsetAsync(tl, 0, sizeof(float) * r.n * ld, ctx->stream);
+    cudaMemsetAsync(tu, 0, sizeof(float) * r.n * ld, ctx->stream);
+    mats.push_back({dense, tl, tu, ld, r.n});
+    unpack.push_back({r.packed, r.n, r.damping_dev, r.damping, 0, dense, ld});
+    if (r.packed_out) pack.push_back({dense, ld, r.n, r.packed_out});
+    max_n = std::max(max_n, r.n);
+  }
+  InversePlan sizing;
+  plan_inverse(mats, nullptr, sizing);
+  float* ws = scratch.alloc<float>(std::max<size_t>(sizing.workspace_floats, 1));
+  InversePlan plan;
+  plan_inverse(mats, ws, plan);
+  auto* d_unpack = scratch.upload(unpack);
+  auto* d_pack = scratch.upload(pack);
+  auto* d_probs = scratch.upload(plan.probs);
+  auto* d_items = scratch.upload(plan.items);
+  auto* d_bases = scratch.upload(plan.bases);
+  int rc = launch_unpack(ctx, d_unpack, int(unpack.size()), max_n);
+  if (!rc) rc = run_inverse(ctx, plan, d_probs, d_items, d_bases);
+  if (!rc) rc = launch_pack(ctx, d_pack, int(pack.size()), max_n);
+  if (rc) return rc;
+  return spngd_ctx_sync(ctx);
+}
+
+extern "C" int spngd_damp_and_invert_batched(spngd_ctx* ctx, int n, const spngd_kron_req* reqs, double lambda) {
+  if (!ctx || (n > 0 && !reqs)) return fail(SPNGD_ERR_INVALID, "spngd_damp_and_invert_batched: null argument");
+  if (!(lambda > 0.0)) return fail(SPNGD_ERR_NOT_POSITIVE_DEFINITE, "damp_and_invert: lambda must be > 0");
+  if (n == 0) return SPNGD_OK;
+  DeviceScratch scratch(ctx);
+  float* damps = scratch.alloc<float>(2 * n);
+  std::vector<PiTask> pis;
+  std::vector<DenseMatrix> mats;
+  std::vector<UnpackTask> unpack;
+  std::vector<PackTask> pack;
+  int64_t max_n = 0;
+  for (int i = 0; i < n; ++i) {
+    const spngd_kron_req& r = reqs[i];
+    if (r.a <= 0 || r.g <= 0) return fail(SPNGD_ERR_SHAPE_MISMATCH, "avg_eigenvalue: empty matrix");
+    if (!r.A_packed || !r.G_packed) return fail(SPNGD_ERR_INVALID, "damp_and_invert: null factor");
+    pis.push_back({r.A_packed, r.G_packed, r.a, r.g, std::sqrt(lambda), damps + 2 * i, damps + 2 * i + 1, r.pi_out});
+    const float* in[2] = {r.A_packed, r.G_packed};
+    float* dn[2] = {r.Ainv_dense, r.Ginv_dense};
+    int64_t lds[2] = {r.lda, r.ldg};
+    float* pk[2] = {r.Ainv_packed, r.Ginv_packed};
+    int64_t dims[2] = {r.a, r.g};
+    for (int s = 0; s < 2; ++s) {
+      float* dense = dn[s];
+      int64_t ld = lds[s];
+      if (dense && ld < dims[s]) return fail(SPNGD_ERR_SHAPE_MISMATCH, "damp_and_invert: ld < n");
+      if (!dense) {
+        ld = round_up(dims[s], 32);
+        dense = scratch.alloc<float>(size_t(dims[s]) * ld);
+      }
+      float* tl = scratch.alloc<float>(size_t(dims[s]) * ld);
+      float* tu = scratch.alloc<float>(size_t(dims[s]) * ld);
+      if (!dense || !tl || !tu) return fail(SPNGD_ERR_CUDA, "damp_and_invert: allocation failed");
+      cudaMemsetAsync(tl, 0, sizeof(float) * dims[s] * ld, ctx->stream);
+      cudaMemsetAsync(tu, 0, sizeof(float) * dims[s] * ld, ctx->stream);
+      mats.push_back({dense, tl, tu, ld, dims[s]});
+      unpack.push_back({in[s], dims[s], damps + 2 * i + s, 0.f, 0, dense, ld});
+      if (pk[s]) pack.push_back({dense, ld, dims[s], pk[s]});
+      max_n = std::max(max_n, dims[s]);
+    }
+  }
+  InversePlan sizing;
+  plan_inverse(mats, nullptr, sizing);
+  float* ws = scratch.alloc<float>(std::max<size_t>(sizing.workspace_floats, 1));
+  InversePlan plan;
+  plan_inverse(mats, ws, plan);
+  auto* d_pis = scratch.upload(pis);
+  auto* d_unpack = scratch.upload(unpack);
+  auto* d_pack = scratch.upload(pack);
+  auto* d_probs = scratch.upload(plan.probs);
+  auto* d_items = scratch.upload(plan.items);
+  auto* d_bases = scratch.upload(plan.bases);
+  int rc = launch_pi(ctx, d_pis, int(pis.size()));
+  if (!rc) rc = launch_unpack(ctx, d_unpack, int(unpack.size()), max_n);
+  if (!rc) rc = run_inverse(ctx, plan, d_probs, d_items, d_bases);
+  if (!rc) rc = launch_pack(ctx, d_pack, int(pack.size()), max_n);
+  if (rc) return rc;
+  return spngd_ctx_sync(ctx);
+}

@@ -1,0 +1,274 @@
+// K5/K6: precondition (src/fisher.cpp:255-257 -> kron_matvec, src/linalg.cpp:58-62)
+// fused with ngd_step's FC/Conv update (src/fisher.cpp:332-333) and the
+// rescale + velocity fix (src/schemes.cpp:116-119, src/dist.cpp:621-632).
+// K7: unit-wise BatchNorm 2x2 solve + update (src/fisher.cpp:259-276, 336-357).
+// K8: stale-statistics similarity norms (include/spngd/stale.hpp:23-64).
+//
+// P = G^-1 dW A^-1 runs as two back-to-back grouped 3xTF32 GEMMs over all
+// layers, both with K-major operands thanks to the symmetry of the inverses:
+//   GEMM1  P1^T[j,i] = sum_k A^-1[j,k] dW[i,k]      (M=a, N=g, K=a)
+//   GEMM2  P^T [j,i] = sum_k P1^T[j,k] G^-1[i,k]    (M=a, N=g, K=g)
+// GEMM2's epilogue walks the P^T tile column-wise, i.e. along rows of the
+// g x a weight, so W' = W - eta P + m V and V' = W' - W are coalesced and
+// ||W'||_F^2 is reduced on the fly for the rescale pass.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+
+#include "ctx.cuh"
+#include "precond.cuh"
+
+namespace spngd {
+
+namespace {
+
+__global__ void rescale_kernel(const RescaleTask* __restrict__ tasks) {
+  const RescaleTask t = tasks[blockIdx.y];
+  const double nrm = sqrt(t.norm2[0]);
+  const float s = float(t.target / (nrm + 1e-9));  // schemes.cpp:117-118
+  const int64_t n4 = (t.n % 4 == 0 && (reinterpret_cast<uintptr_t>(t.W) % 16 == 0) &&
+                      (reinterpret_cast<uintptr_t>(t.V) % 16 == 0))
+                         ? t.n / 4
+                         : 0;
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; q < n4; q += stride) {
+    float4 w = reinterpret_cast<float4*>(t.W)[q];
+    float4 v = reinterpret_cast<float4*>(t.V)[q];
+    // V'' = W'' - W_old = W'' - (W' - V')   (dist.cpp:626-630)
+    float4 nw = make_float4(s * w.x, s * w.y, s * w.z, s * w.w);
+    v = make_float4(nw.x - w.x + v.x, nw.y - w.y + v.y, nw.z - w.z + v.z, nw.w - w.w + v.w);
+    reinterpret_cast<float4*>(t.W)[q] = nw;
+    reinterpret_cast<float4*>(t.V)[q] = v;
+  }
+  for (int64_t i = 4 * n4 + int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < t.n; i += stride) {
+    const float w = t.W[i], nw = s * w;
+    t.V[i] = nw - w + t.V[i];
+    t.W[i] = nw;
+  }
+}
+
+__global__ void bn_update_kernel(const spngd_bn_update_req* __restrict__ reqs, double lambda, double eta,
+                                 double momentum, int* status) {
+  const spngd_bn_update_req r = reqs[blockIdx.y];
+  const int64_t ch = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (ch >= r.c) return;
+  // inv2x2(fgg + lambda, fgb, fgb, fbb + lambda)  (linalg.cpp:50-56, fisher.cpp:268-270)
+  const double a = double(r.m3c[3 * ch]) + lambda, b = double(r.m3c[3 * ch + 1]);
+  const double d = double(r.m3c[3 * ch + 2]) + lambda;
+  const double det = a * d - b * b;
+  if (fabs(det) < 1e-30) {
+    set_status(status, SPNGD_ERR_SINGULAR_BLOCK);
+    return;
+  }
+  const double ia = d / det, ib = -b / det, id = a / det;
+  const double gg = r.grad[ch], gb = r.grad[r.c + ch];
+  const double pg = ia * gg + ib * gb, pb = ib * gg + id * gb;
+  if (r.pg_out) r.pg_out[ch] = float(pg);
+  if (r.pb_out) r.pb_out[ch] = float(pb);
+  if (r.gamma) {
+    // np = p - eta * delta + momentum * v ; nv = np - p   (fisher.cpp:353-356)
+    const float g0 = r.gamma[ch], b0 = r.beta[ch];
+    const float ng = float(double(g0) - eta * pg + momentum * double(r.vgamma[ch]));
+    const float nb = float(double(b0) - eta * pb + momentum * double(r.vbeta[ch]));
+    r.gamma[ch] = ng;
+    r.beta[ch] = nb;
+    r.vgamma[ch] = ng - g0;
+    r.vbeta[ch] = nb - b0;
+  }
+}
+
+// Weighted norms of x - x1, x1, x - x2, x2 (weights 1 on the diagonal, 2 off it
+// for packed statistics; 1,2,1 for BN 3c payloads), stale.hpp:23-64.
+__global__ void stat_distance_kernel(const spngd_stat_req* __restrict__ reqs) {
+  const spngd_stat_req r = reqs[blockIdx.y];
+  double acc[4] = {0, 0, 0, 0};
+  if (r.kind == 0) {
+    for (int64_t i = blockIdx.x; i < r.n; i += gridDim.x) {
+      const int64_t base = i * r.n - i * (i - 1) / 2;
+      for (int64_t j = i + threadIdx.x; j < r.n; j += blockDim.x) {
+        const double w = (i == j) ? 1.0 : 2.0;
+        const double x = r.x[base + j - i];
+        if (r.x1) {
+          const double y = r.x1[base + j - i];
+          acc[0] += w * (x - y) * (x - y);
+          acc[1] += w * y * y;
+        }
+        if (r.x2) {
+          const double y = r.x2[base + j - i];
+          acc[2] += w * (x - y) * (x - y);
+          acc[3] += w * y * y;
+        }
+      }
+    }
+  } else {
+    for (int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; q < 3 * r.n; q += int64_t(gridDim.x) * blockDim.x) {
+      const double w = (q % 3 == 1) ? 2.0 : 1.0;
+      const double x = r.x[q];
+      if (r.x1) { const double y = r.x1[q]; acc[0] += w * (x - y) * (x - y); acc[1] += w * y * y; }
+      if (r.x2) { const double y = r.x2[q]; acc[2] += w * (x - y) * (x - y); acc[3] += w * y * y; }
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < 4; ++k)
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc[k] += __shfl_xor_sync(0xffffffffu, acc[k], o);
+  if ((threadIdx.x & 31) == 0)
+    for (int k = 0; k < 4; ++k) atomicAdd(r.out4 + k, acc[k]);
+}
+
+GemmOperand dense_operand(const float* ptr, int64_t ld, int64_t rows, int64_t K) {
+  GemmOperand o{};
+  o.ptr = ptr;
+  o.row_stride = ld;
+  o.seg_len = std::max<int64_t>(K, 1);
+  o.rows = int32_t(rows);
+  finalize_operand(o);
+  return o;
+}
+
+}  // namespace
+
+int plan_precondition(const spngd_precond_req* reqs, int n, double eta, double momentum, float* tmp,
+                      double* norms, PrecondPlan& plan) {
+  plan = PrecondPlan();
+  size_t off = 0;
+  for (int i = 0; i < n; ++i) {
+    const spngd_precond_req& r = reqs[i];
+    if (r.g <= 0 || r.a <= 0) return fail(SPNGD_ERR_SHAPE_MISMATCH, "kron_matvec: empty operand");
+    if (!r.Ginv || !r.Ainv || !r.dW) return fail(SPNGD_ERR_INVALID, "precondition: null pointer");
+    if (r.ldg < r.g || r.lda < r.a) return fail(SPNGD_ERR_SHAPE_MISMATCH, "kron_matvec: X must be dim(G) x dim(A)");
+    if (r.W && !r.V) return fail(SPNGD_ERR_INVALID, "ngd_step: velocity missing");
+    const int64_t ldp = round_up(r.g, 4);
+    float* p1t = tmp ? tmp + off : nullptr;
+    off += size_t(round_up(r.a * ldp, 64));
+    GemmProblem p1{};
+    p1.A = dense_operand(r.Ainv, r.lda, r.a, r.a);
+    p1.B = dense_operand(r.dW, r.a, r.g, r.a);
+    p1.M = int32_t(r.a); p1.N = int32_t(r.g); p1.K = int32_t(r.a);
+    p1.mode = EPI_DENSE; p1.alpha = 1.f; p1.beta = 0.f;
+    p1.C = p1t; p1.ldc = ldp;
+    GemmProblem p2{};
+    p2.A = dense_operand(p1t, ldp, r.a, r.g);
+    p2.B = dense_operand(r.Ginv, r.ldg, r.g, r.g);
+    p2.M = int32_t(r.a); p2.N = int32_t(r.g); p2.K = int32_t(r.g);
+    p2.mode = EPI_UPDATE; p2.alpha = 1.f;
+    p2.W = r.W; p2.V = r.V; p2.P_out = r.P_out;
+    p2.eta = float(eta); p2.momentum = float(momentum);
+    p2.norm2 = (r.W && r.rescale && norms) ? norms + i : nullptr;
+    const int idx = int(plan.probs1.size());
+    plan.probs1.push_back(p1);
+    plan.probs2.push_back(p2);
+    int slot = 0;
+    plan_problem_tiles(idx, p1, false, p1.K + kTileK, plan.items1, nullptr, &slot, 1.0, nullptr);
+    plan_problem_tiles(idx, p2, false, p2.K + kTileK, plan.items2, nullptr, &slot, 1.0, nullptr);
+    if (r.W && r.rescale)
+      plan.rescale.push_back({r.W, r.V, r.g * r.a, norms ? norms + i : nullptr, std::sqrt(2.0 * double(r.g))});
+  }
+  plan.tmp_floats = off;
+  plan.n_norms = n;
+  auto longest = [](const GemmWorkItem& x, const GemmWorkItem& y) { return (x.k1 - x.k0) > (y.k1 - y.k0); };
+  std::stable_sort(plan.items1.begin(), plan.items1.end(), longest);
+  std::stable_sort(plan.items2.begin(), plan.items2.end(), longest);
+  return SPNGD_OK;
+}
+
+int run_precondition(spngd_ctx* ctx, const PrecondPlan& plan, const GemmProblem* d_p1, const GemmWorkItem* d_i1,
+                     const GemmProblem* d_p2, const GemmWorkItem* d_i2, const RescaleTask* d_rescale,
+                     double* d_norms) {
+  if (d_norms && plan.n_norms > 0)
+    SPNGD_CUDA_TRY(cudaMemsetAsync(d_norms, 0, sizeof(double) * plan.n_norms, ctx->stream));
+  int rc = launch_gemm(d_p1, d_i1, int(plan.items1.size()), nullptr, ctx->d_status, ctx->stream);
+  if (rc) return rc;
+  rc = launch_gemm(d_p2, d_i2, int(plan.items2.size()), nullptr, ctx->d_status, ctx->stream);
+  if (rc) return rc;
+  ctx->launches += 2;
+  if (!plan.rescale.empty()) {
+    dim3 grid(296, unsigned(plan.rescale.size()));
+    rescale_kernel<<<grid, 256, 0, ctx->stream>>>(d_rescale);
+    SPNGD_CUDA_TRY(cudaGetLastError());
+    ctx->launches++;
+  }
+  return SPNGD_OK;
+}
+
+int launch_bn_update(spngd_ctx* ctx, const spngd_bn_update_req* d_reqs, int n, int64_t max_c, double lambda,
+                     double eta, double momentum) {
+  if (n <= 0) return SPNGD_OK;
+  dim3 grid(unsigned((max_c + 255) / 256), unsigned(n));
+  bn_update_kernel<<<grid, 256, 0, ctx->stream>>>(d_reqs, lambda, eta, momentum, ctx->d_status);
+  SPNGD_CUDA_TRY(cudaGetLastError());
+  ctx->launches++;
+  return SPNGD_OK;
+}
+
+int launch_stat_distance(spngd_ctx* ctx, const spngd_stat_req* d_reqs, int n, int64_t max_rows) {
+  if (n <= 0) return SPNGD_OK;
+  dim3 grid(unsigned(std::min<int64_t>(std::max<int64_t>(max_rows, 1), 256)), unsigned(n));
+  stat_distance_kernel<<<grid, 256, 0, ctx->stream>>>(d_reqs);
+  SPNGD_CUDA_TRY(cudaGetLastError());
+  ctx->launches++;
+  return SPNGD_OK;
+}
+
+}  // namespace spngd
+
+using namespace spngd;
+
+extern "C" int spngd_precondition_update_batched(spngd_ctx* ctx, int n, const spngd_precond_req* reqs, double eta,
+                                                 double momentum) {
+  if (!ctx || (n > 0 && !reqs)) return fail(SPNGD_ERR_INVALID, "spngd_precondition_update_batched: null argument");
+  if (n == 0) return SPNGD_OK;
+  PrecondPlan sizing;
+  int rc = plan_precondition(reqs, n, eta, momentum, nullptr, nullptr, sizing);
+  if (rc) return rc;
+  DeviceScratch scratch(ctx);
+  float* tmp = scratch.alloc<float>(sizing.tmp_floats);
+  double* norms = scratch.alloc<double>(n);
+  PrecondPlan plan;
+  plan_precondition(reqs, n, eta, momentum, tmp, norms, plan);
+  auto* d_p1 = scratch.upload(plan.probs1);
+  auto* d_i1 = scratch.upload(plan.items1);
+  auto* d_p2 = scratch.upload(plan.probs2);
+  auto* d_i2 = scratch.upload(plan.items2);
+  auto* d_rs = scratch.upload(plan.rescale);
+  rc = run_precondition(ctx, plan, d_p1, d_i1, d_p2, d_i2, d_rs, norms);
+  if (rc) return rc;
+  return spngd_ctx_sync(ctx);
+}
+
+extern "C" int spngd_bn_solve_update_batched(spngd_ctx* ctx, int n, const spngd_bn_update_req* reqs, double lambda,
+                                             double eta, double momentum) {
+  if (!ctx || (n > 0 && !reqs)) return fail(SPNGD_ERR_INVALID, "spngd_bn_solve_update_batched: null argument");
+  int64_t max_c = 0;
+  for (int i = 0; i < n; ++i) {
+    if (!reqs[i].m3c || !reqs[i].grad) return fail(SPNGD_ERR_INVALID, "precondition_bn: null pointer");
+    if (reqs[i].gamma && (!reqs[i].beta || !reqs[i].vgamma || !reqs[i].vbeta))
+      return fail(SPNGD_ERR_INVALID, "ngd_step: BN state incomplete");
+    max_c = std::max(max_c, reqs[i].c);
+  }
+  if (n == 0) return SPNGD_OK;
+  DeviceScratch scratch(ctx);
+  std::vector<spngd_bn_update_req> v(reqs, reqs + n);
+  auto* d = scratch.upload(v);
+  int rc = launch_bn_update(ctx, d, n, max_c, lambda, eta, momentum);
+  if (rc) return rc;
+  return spngd_ctx_sync(ctx);
+}
+
+extern "C" int spngd_stat_distance_batched(spngd_ctx* ctx, int n, const spngd_stat_req* reqs) {
+  if (!ctx || (n > 0 && !reqs)) return fail(SPNGD_ERR_INVALID, "spngd_stat_distance_batched: null argument");
+  int64_t max_rows = 0;
+  for (int i = 0; i < n; ++i) {
+    if (!reqs[i].x || !reqs[i].out4) return fail(SPNGD_ERR_INVALID, "similar: null pointer");
+    max_rows = std::max(max_rows, reqs[i].kind == 0 ? reqs[i].n : (3 * reqs[i].n + 255) / 256);
+    cudaMemsetAsync(reqs[i].out4, 0, 4 * sizeof(double), ctx->stream);
+  }
+  if (n == 0) return SPNGD_OK;
+  DeviceScratch scratch(ctx);
+  std::vector<spngd_stat_req> v(reqs, reqs + n);
+  auto* d = scratch.upload(v);
+  int rc = launch_stat_distance(ctx, d, n, max_rows);
+  if (rc) return rc;
+  return spngd_ctx_sync(ctx);
+}
