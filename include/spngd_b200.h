@@ -64,6 +64,15 @@ void spngd_ctx_destroy(spngd_ctx* ctx);
  * raised since the previous call (NotPositiveDefinite, SingularBlock). */
 int spngd_ctx_sync(spngd_ctx* ctx);
 void* spngd_ctx_stream(spngd_ctx* ctx);
+/* Stream-ordered copy (any direction, cudaMemcpyDefault) on the context stream. */
+int spngd_copy(spngd_ctx* ctx, void* dst, const void* src, size_t bytes);
+/* Pinned host buffers for host-resident inputs (the e2e drop-in path). */
+int spngd_host_alloc(void** out, size_t bytes);
+void spngd_host_free(void* p);
+/* CUDA-event timing on the context stream: call with record_second = 0 to
+ * start, 1 to stop, synchronize and read `ms`.  ev_pair: two NULL-initialised
+ * opaque slots owned by the caller. */
+int spngd_event_time(spngd_ctx* ctx, void** ev_pair, int record_second, float* ms);
 
 /* ---- K1: Kronecker factors ------------------------------------------------
  * Replaces factor_A (src/fisher.cpp:92-114) and factor_G (src/fisher.cpp:116-145)
@@ -227,7 +236,8 @@ void spngd_opt_destroy(spngd_opt* opt);
  *   which 0 act capture, 1 grad capture, 2 dW (this rank's shard-mean grad,
  *   g x a or 2c), 3 W (g x a, or gamma|beta 2c), 4 V, 5 bn gg (M x c),
  *   6 bn gb, 7 A_inv dense, 8 G_inv dense, 9 A packed (reduced), 10 G packed,
- *   11 BN moments 3c (reduced). NULL if the layer has no such buffer or this
+ *   11 BN moments 3c (reduced), 12 the whole weight all-gather buffer
+ *   (ld = its float count). NULL if the layer has no such buffer or this
  *   rank does not own it. */
 float* spngd_opt_buffer(spngd_opt* opt, int layer, int which, int64_t* ld);
 int spngd_opt_owner(const spngd_opt* opt, int layer);
@@ -235,9 +245,10 @@ int spngd_opt_owner(const spngd_opt* opt, int layer);
  * dist.cpp:406-675, n = 1 micro-step): factors + BN moments, RS, damped
  * inverse, precondition + update + rescale, BN solve + update, AG. */
 int spngd_opt_step(spngd_opt* opt, int64_t step, double eta, double momentum);
-/* Per-phase device milliseconds of the last step: factor, reduce_scatter,
- * inverse, precondition, all_gather. */
-int spngd_opt_phase_ms(spngd_opt* opt, float* out5);
+/* Per-phase device milliseconds of the last step: factor GEMM, factor
+ * reduction + BN moments, reduce_scatter, inverse, precondition + BN update,
+ * all_gather. */
+int spngd_opt_phase_ms(spngd_opt* opt, float* out6);
 /* Number of kernels the last step launched on this rank. */
 int64_t spngd_opt_launch_count(const spngd_opt* opt);
 

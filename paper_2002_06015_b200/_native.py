@@ -71,7 +71,8 @@ STATUS_NAMES = {
 
 EXPORTS = [
     "spngd_last_error", "spngd_version", "spngd_ctx_create", "spngd_ctx_destroy", "spngd_ctx_sync",
-    "spngd_ctx_stream", "spngd_factor_sym_batched", "spngd_bn_moments_batched",
+    "spngd_ctx_stream", "spngd_copy", "spngd_host_alloc", "spngd_host_free", "spngd_event_time",
+    "spngd_factor_sym_batched", "spngd_bn_moments_batched",
     "spngd_spd_inverse_batched", "spngd_damp_and_invert_batched",
     "spngd_precondition_update_batched", "spngd_bn_solve_update_batched",
     "spngd_stat_distance_batched", "spngd_tracker_create", "spngd_tracker_destroy",
@@ -110,6 +111,10 @@ def _declare(L):
         "spngd_ctx_destroy": (None, [P]),
         "spngd_ctx_sync": (C.c_int, [P]),
         "spngd_ctx_stream": (P, [P]),
+        "spngd_copy": (C.c_int, [P, P, P, C.c_size_t]),
+        "spngd_host_alloc": (C.c_int, [C.POINTER(P), C.c_size_t]),
+        "spngd_host_free": (None, [P]),
+        "spngd_event_time": (C.c_int, [P, C.POINTER(P), C.c_int, C.POINTER(C.c_float)]),
         "spngd_factor_sym_batched": (C.c_int, [P, C.c_int, C.POINTER(FactorReq)]),
         "spngd_bn_moments_batched": (C.c_int, [P, C.c_int, C.POINTER(BnMomentsReq)]),
         "spngd_spd_inverse_batched": (C.c_int, [P, C.c_int, C.POINTER(SpdReq)]),

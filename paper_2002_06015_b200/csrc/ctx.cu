@@ -82,6 +82,35 @@ void spngd_ctx_destroy(spngd_ctx* ctx) {
   delete ctx;
 }
 
+int spngd_copy(spngd_ctx* ctx, void* dst, const void* src, size_t bytes) {
+  if (!ctx) return spngd::fail(SPNGD_ERR_INVALID, "spngd_copy: ctx is NULL");
+  SPNGD_CUDA_TRY(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, ctx->stream));
+  return SPNGD_OK;
+}
+
+int spngd_host_alloc(void** out, size_t bytes) {
+  SPNGD_CUDA_TRY(cudaMallocHost(out, bytes));
+  return SPNGD_OK;
+}
+
+void spngd_host_free(void* p) { cudaFreeHost(p); }
+
+int spngd_event_time(spngd_ctx* ctx, void** ev_pair, int record_second, float* ms) {
+  // Harness helper: ev_pair[0] created+recorded on first call, ev_pair[1] on second.
+  if (!ctx || !ev_pair) return spngd::fail(SPNGD_ERR_INVALID, "spngd_event_time: bad argument");
+  cudaEvent_t* e = reinterpret_cast<cudaEvent_t*>(ev_pair);
+  if (!e[0]) SPNGD_CUDA_TRY(cudaEventCreate(&e[0]));
+  if (!e[1]) SPNGD_CUDA_TRY(cudaEventCreate(&e[1]));
+  if (!record_second) {
+    SPNGD_CUDA_TRY(cudaEventRecord(e[0], ctx->stream));
+    return SPNGD_OK;
+  }
+  SPNGD_CUDA_TRY(cudaEventRecord(e[1], ctx->stream));
+  SPNGD_CUDA_TRY(cudaEventSynchronize(e[1]));
+  SPNGD_CUDA_TRY(cudaEventElapsedTime(ms, e[0], e[1]));
+  return SPNGD_OK;
+}
+
 void* spngd_ctx_stream(spngd_ctx* ctx) { return ctx ? static_cast<void*>(ctx->stream) : nullptr; }
 
 int spngd_ctx_sync(spngd_ctx* ctx) {

@@ -1,0 +1,180 @@
+"""Whole-step optimizer over the C ABI (spngd_opt_*), the drop-in for
+`accumulate_microsteps` / `run_step` (src/dist.cpp:406-682) at n = 1 micro-step.
+
+One `Optimizer` per rank (one process per GPU).  Inputs (captures, BN per-sample
+gradient pairs, this rank's shard-mean weight gradient) and state (weights,
+velocity) are device buffers owned by the library; `buffer()` exposes them.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from typing import List, Optional
+
+import torch
+
+from . import _native as N
+from .spngd import check
+from .workloads import Layer
+
+ACT, GRAD, DW, W, V, BN_GG, BN_GB, AINV, GINV, A_PACKED, G_PACKED, BN_M3C, ALL_WEIGHTS = range(13)
+PHASES = ["factor_gemm", "factor_reduce_bn", "reduce_scatter", "inverse", "precondition_update", "all_gather"]
+
+
+def _mix(*xs) -> int:
+    h = 0x9E3779B97F4A7C15
+    for x in xs:
+        h = (h ^ (int(x) & 0xFFFFFFFFFFFFFFFF)) * 0xBF58476D1CE4E5B9 & 0xFFFFFFFFFFFFFFFF
+        h ^= h >> 31
+    return h
+
+
+class Comm:
+    """NCCL communicator bootstrap: rank 0's unique id is shared by the caller
+    (torch.distributed object broadcast), then spngd_ctx_init_comm."""
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = C.create_string_buffer(128)
+        check(N.lib().spngd_nccl_unique_id(buf))
+        return buf.raw
+
+
+class Optimizer:
+    def __init__(self, layers: List[Layer], batch: int, lam: float = 2.5e-4, rescale: bool = True,
+                 device: int = 0, world: int = 1, rank: int = 0, nccl_id: Optional[bytes] = None,
+                 stream=None):
+        self.layers, self.batch, self.lam = layers, batch, lam
+        self.world, self.rank, self.device = world, rank, device
+        L = N.lib()
+        self.ctx = C.c_void_p()
+        check(L.spngd_ctx_create(device, stream, C.byref(self.ctx)))
+        if world > 1:
+            check(L.spngd_ctx_init_comm(self.ctx, world, rank, C.create_string_buffer(nccl_id, 128)))
+        descs = []
+        for l in layers:
+            kind = {"fc": 0, "conv": 1, "bn": 2}[l.kind]
+            descs.append(N.LayerDesc(kind, 0, l.a if l.kind != "bn" else 0, l.g, l.hw if l.kind == "conv" else 1))
+        arr = (N.LayerDesc * len(descs))(*descs)
+        cfg = N.OptConfig(lam, int(rescale), 0, 0.1, batch)
+        self.h = C.c_void_p()
+        check(L.spngd_opt_create(self.ctx, arr, len(descs), C.byref(cfg), C.byref(self.h)))
+
+    def close(self):
+        L = N.lib()
+        if getattr(self, "h", None):
+            L.spngd_opt_destroy(self.h)
+            self.h = None
+        if getattr(self, "ctx", None):
+            L.spngd_ctx_destroy(self.ctx)
+            self.ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ---- buffers --------------------------------------------------------------
+    def numel(self, li: int, which: int) -> int:
+        l, B = self.layers[li], self.batch
+        if which == ACT:
+            return B * l.a * l.hw
+        if which == GRAD:
+            return B * l.g * l.hw
+        if which in (DW, W, V):
+            return 2 * l.g if l.kind == "bn" else l.g * l.a
+        if which in (BN_GG, BN_GB):
+            return B * l.g
+        if which == A_PACKED:
+            return l.a * (l.a + 1) // 2
+        if which == G_PACKED:
+            return l.g * (l.g + 1) // 2
+        if which == BN_M3C:
+            return 3 * l.g
+        raise ValueError(which)
+
+    def ptr(self, li: int, which: int):
+        ld = C.c_int64()
+        p = N.lib().spngd_opt_buffer(self.h, li, which, C.byref(ld))
+        return p, ld.value
+
+    def owner(self, li: int) -> int:
+        return N.lib().spngd_opt_owner(self.h, li)
+
+    def download(self, li: int, which: int) -> torch.Tensor:
+        """Copies a buffer to a CPU float32 tensor (synchronizes)."""
+        p, ld = self.ptr(li, which)
+        if not p:
+            raise ValueError(f"layer {li} buffer {which} not available on rank {self.rank}")
+        if which in (AINV, GINV):
+            n = self.layers[li].a if which == AINV else self.layers[li].g
+            t = torch.empty(n, ld, dtype=torch.float32).pin_memory()
+            check(N.lib().spngd_copy(self.ctx, C.c_void_p(t.data_ptr()), C.c_void_p(p), t.numel() * 4))
+            self.sync()
+            return t[:, :n].clone()
+        n = self.numel(li, which)
+        t = torch.empty(n, dtype=torch.float32).pin_memory()
+        check(N.lib().spngd_copy(self.ctx, C.c_void_p(t.data_ptr()), C.c_void_p(p), n * 4))
+        self.sync()
+        return t.clone()
+
+    def upload(self, li: int, which: int, host: torch.Tensor):
+        p, _ = self.ptr(li, which)
+        h = host.contiguous().float()
+        if h.numel() != self.numel(li, which):
+            raise ValueError("size mismatch")
+        h = h.pin_memory()
+        check(N.lib().spngd_copy(self.ctx, C.c_void_p(p), C.c_void_p(h.data_ptr()), h.numel() * 4))
+        self.sync()
+
+    def sync(self):
+        check(N.lib().spngd_ctx_sync(self.ctx))
+
+    # ---- synthetic inputs -------------------------
+    def synth(self, seed: int = 42):
+        """Per-layer synthetic inputs generated in place on the device:
+        conv/FC inputs ReLU(N(0,1)) laid out as the reference im2col capture,
+        output grads N(0,1)/sqrt(B hw), BN pairs g ~ N, b = 0.6 g + 0.8 N,
+        dW ~ N(0,1)/sqrt(a), W He-normal (identical on every rank), V = 0.01 N,
+        gamma = 1, beta = 0.  Captures and dW differ per rank (distinct shards)."""
+        L, B, r = N.lib(), self.batch, self.rank
+        for li, l in enumerate(self.layers):
+            if l.kind == "bn":
+                gg, _ = self.ptr(li, BN_GG)
+                gb, _ = self.ptr(li, BN_GB)
+                check(L.spngd_synth_bn_pairs(self.ctx, gg, gb, B * l.g, _mix(seed, li, 5, r)))
+                dw, _ = self.ptr(li, DW)
+                check(L.spngd_synth_normal(self.ctx, dw, 2 * l.g, _mix(seed, li, 2, r), 0.1, 0.0, 0))
+                w, _ = self.ptr(li, W)
+                check(L.spngd_synth_normal(self.ctx, w, l.g, 0, 0.0, 1.0, 0))  # gamma = 1
+                check(L.spngd_synth_normal(self.ctx, C.c_void_p(w + 4 * l.g), l.g, 0, 0.0, 0.0, 0))  # beta = 0
+                continue
+            act, _ = self.ptr(li, ACT)
+            if l.kind == "conv":
+                check(L.spngd_synth_conv_capture(self.ctx, act, B, l.c_in, l.h_in, l.w_in, l.k, l.stride, l.pad,
+                                                 _mix(seed, li, 0, r), 1, 1.0, 0.0))
+            else:
+                check(L.spngd_synth_normal(self.ctx, act, B * l.a, _mix(seed, li, 0, r), 1.0, 0.0, 1))
+            grad, _ = self.ptr(li, GRAD)
+            check(L.spngd_synth_normal(self.ctx, grad, B * l.g * l.hw, _mix(seed, li, 1, r),
+                                       float((B * l.hw) ** -0.5), 0.0, 0))
+            dw, _ = self.ptr(li, DW)
+            check(L.spngd_synth_normal(self.ctx, dw, l.g * l.a, _mix(seed, li, 2, r), float(l.a ** -0.5), 0.0, 0))
+            w, _ = self.ptr(li, W)
+            check(L.spngd_synth_normal(self.ctx, w, l.g * l.a, _mix(seed, li, 3), float((2.0 / l.a) ** 0.5), 0.0, 0))
+            v, _ = self.ptr(li, V)
+            if v:
+                check(L.spngd_synth_normal(self.ctx, v, l.g * l.a, _mix(seed, li, 4), 0.01, 0.0, 0))
+        self.sync()
+
+    # ---- the step -----------------------------------------------------------------
+    def step(self, step: int, eta: float = 1.25e-2, momentum: float = 0.993):
+        check(N.lib().spngd_opt_step(self.h, step, eta, momentum))
+
+    def phase_ms(self):
+        out = (C.c_float * 6)()
+        check(N.lib().spngd_opt_phase_ms(self.h, out))
+        return dict(zip(PHASES, list(out)))
+
+    def launch_count(self) -> int:
+        return N.lib().spngd_opt_launch_count(self.h)

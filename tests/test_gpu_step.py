@@ -1,0 +1,93 @@
+"""Whole-step parity (accumulate_microsteps Stages 2-5 at K = 1) against the
+fp64 oracle on identical device-generated inputs, rel. Frobenius <= 1e-4 on the
+updated weights / velocities (north_star gate).  Full-size MLP (config 1);
+ResNet-18/50 checked on a layer sample (the fp64 oracle needs minutes per
+4608^2 inverse)."""
+import ctypes as C
+
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+from paper_2002_06015_b200 import workloads as W  # noqa: E402
+from paper_2002_06015_b200.step import ACT, BN_GB, BN_GG, DW, GRAD, V, Optimizer  # noqa: E402
+from paper_2002_06015_b200.step import W as WB  # noqa: E402
+
+ETA, MOM, LAM = 1.25e-2, 0.993, 2.5e-4
+
+
+def rel(a, b):
+    return float(np.linalg.norm(np.asarray(a, np.float64) - b) / np.linalg.norm(b))
+
+
+def oracle_layer(l, batch, before):
+    act, grad, dW, W0, V0 = (before[k] for k in (ACT, GRAD, DW, WB, V))
+    rec = O.OrLayer()
+    wo, vo = np.empty(l.g * l.a), np.empty(l.g * l.a)
+    rec.is_conv, rec.a, rec.g, rec.hw, rec.batch = int(l.kind == "conv"), l.a, l.g, l.hw, batch
+    rec.act, rec.grad, rec.dW, rec.W, rec.V = [b.ctypes.data_as(C.POINTER(C.c_float)) for b in (act, grad, dW, W0, V0)]
+    rec.W_out = wo.ctypes.data_as(C.POINTER(C.c_double))
+    rec.V_out = vo.ctypes.data_as(C.POINTER(C.c_double))
+    O.kfac_layers([rec], LAM, ETA, MOM, rescale=True, fast_inverse=True, threads=1)
+    return wo, vo
+
+
+def oracle_bn(l, batch, before):
+    c = l.g
+    m3 = O.build_bn_block(before[BN_GG].reshape(batch, c), before[BN_GB].reshape(batch, c), 0, batch)
+    g2 = before[DW].astype(np.float64)
+    pg, pb = O.precondition_bn(m3, g2[:c], g2[c:], LAM)
+    return O.ngd_update(before[WB], np.concatenate([pg, pb]), before[V], ETA, MOM)
+
+
+def run_and_check(layers, batch, check_layers):
+    opt = Optimizer(layers, batch, lam=LAM)
+    opt.synth(seed=3)
+    before = {}
+    for li in check_layers:
+        l = layers[li]
+        ws = [BN_GG, BN_GB, DW, WB, V] if l.kind == "bn" else [ACT, GRAD, DW, WB, V]
+        before[li] = {w: opt.download(li, w).numpy() for w in ws}
+    opt.step(1, ETA, MOM)
+    opt.sync()
+    worst = 0.0
+    for li in check_layers:
+        l = layers[li]
+        wo, vo = (oracle_bn if l.kind == "bn" else oracle_layer)(l, batch, before[li])
+        ew = rel(opt.download(li, WB).numpy(), wo)
+        ev = rel(opt.download(li, V).numpy(), vo)
+        assert ew <= 1e-4 and ev <= 1e-4, f"layer {li} {l}: W {ew:.2e} V {ev:.2e}"
+        worst = max(worst, ew, ev)
+    ph = opt.phase_ms()
+    assert all(v >= 0 for v in ph.values())
+    opt.close()
+    return worst
+
+
+def test_mlp_full_step(cuda_dev):
+    layers, batch, _ = W.CONFIGS["mlp"]
+    run_and_check(layers(), batch, range(3))
+
+
+def test_small_convnet_full_step(cuda_dev):
+    layers = [W.conv(3, 16, 3, 1, 16), W.bn(16), W.conv(16, 32, 3, 2, 16), W.bn(32), W.conv(32, 32, 1, 1, 8),
+              W.bn(32), W.fc(32 * 4, 10)]
+    run_and_check(layers, 16, range(len(layers)))
+
+
+def test_resnet18_sampled_layers(cuda_dev):
+    layers = W.resnet18_cifar()
+    pick = [0, 1, 2, 5, 8, len(layers) - 1]
+    run_and_check(layers, 128, pick)
+
+
+def test_resnet50_sampled_layers(cuda_dev):
+    layers = W.resnet50()
+    # conv1 (147x64, K = 401,408 split-K), a 576 3x3, a 1152 3x3, BN, the FC.
+    idx = {(l.a, l.g, l.hw): i for i, l in reversed(list(enumerate(layers)))}
+    pick = [0, 1, idx[(576, 64, 3136)], idx[(1152, 128, 784)], len(layers) - 1]
+    run_and_check(layers, 32, pick)
