@@ -47,27 +47,91 @@ struct __align__(8) SmemCtl {
 
 __device__ __forceinline__ float4 ldg4(const float* p) { return __ldg(reinterpret_cast<const float4*>(p)); }
 
-// Loads the 4 consecutive k values (k .. k+3) of row `r` of `op`, zero outside.
-__device__ __forceinline__ float4 load_chunk(const GemmOperand& op, int32_t r, int64_t k, int64_t kend) {
-  float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-  if (r >= op.rows || k >= kend) return v;
-  if (op.vec && k + 3 < kend) {
-    const int64_t s = k / op.seg_len;
-    const int64_t p = k - s * op.seg_len;
-    return ldg4(op.ptr + s * op.seg_stride + int64_t(r) * op.row_stride + p);
+// Per-thread cursor over the segmented K axis: k = s * seg_len + p.  Advanced
+// incrementally (no 64-bit division in the main loop).
+struct KCursor {
+  int64_t s;
+  int32_t p;
+  int32_t k;  // absolute k of the chunk start
+};
+
+__device__ __forceinline__ KCursor cursor_at(const GemmOperand& op, int32_t k) {
+  KCursor c;
+  c.k = k;
+  if (op.seg_len == 1) {
+    c.s = k;
+    c.p = 0;
+  } else {
+    c.s = k / op.seg_len;
+    c.p = int32_t(k - c.s * op.seg_len);
   }
-  float t[4];
+  return c;
+}
+
+__device__ __forceinline__ void cursor_advance(const GemmOperand& op, KCursor& c, int32_t dk) {
+  c.k += dk;
+  if (op.seg_len == 1) {
+    c.s += dk;
+    return;
+  }
+  c.p += dk;
+  while (c.p >= op.seg_len) {
+    c.p -= int32_t(op.seg_len);
+    ++c.s;
+  }
+}
+
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, uint32_t src_bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(src_bytes) : "memory");
+}
+__device__ __forceinline__ void cp_async4(uint32_t dst, const void* src, uint32_t src_bytes) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(dst), "l"(src), "r"(src_bytes) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+// Issues the async copies of k .. k+3 for the 8 rows (r0 + 16 j) this thread
+// feeds into the swizzled fp32 plane at `plane` (zero-filled outside).
+__device__ __forceinline__ void issue_stage(const GemmOperand& op, int32_t r0, int rbase, int c, const KCursor& cur,
+                                           int32_t kend, uint32_t plane) {
+  if (op.vec && cur.k + 3 < kend) {
+    const float* base = op.ptr + cur.s * op.seg_stride + cur.p;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int32_t r = r0 + 16 * j;
+      const int rl = rbase + 16 * j;
+      const uint32_t dst = plane + rl * 128 + ((c ^ (rl & 7)) << 4);
+      const bool ok = r < op.rows;
+      cp_async16(dst, ok ? base + int64_t(r) * op.row_stride : op.ptr, ok ? 16u : 0u);
+    }
+    return;
+  }
+  int64_t off[4];
+  bool ok[4];
 #pragma unroll
   for (int e = 0; e < 4; ++e) {
-    const int64_t kk = k + e;
-    t[e] = 0.f;
-    if (kk < kend) {
-      const int64_t s = kk / op.seg_len;
-      const int64_t p = kk - s * op.seg_len;
-      t[e] = __ldg(op.ptr + s * op.seg_stride + int64_t(r) * op.row_stride + p);
+    ok[e] = cur.k + e < kend;
+    if (op.seg_len == 1) {
+      off[e] = (cur.s + e) * op.seg_stride;
+    } else {
+      int64_t ss = cur.s;
+      int32_t pp = cur.p + e;
+      if (pp >= op.seg_len) { pp -= int32_t(op.seg_len); ++ss; }
+      off[e] = ss * op.seg_stride + pp;
     }
   }
-  return make_float4(t[0], t[1], t[2], t[3]);
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const int32_t r = r0 + 16 * j;
+    const int rl = rbase + 16 * j;
+    const uint32_t dst = plane + rl * 128 + ((c ^ (rl & 7)) << 4);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const bool v = r < op.rows && ok[e];
+      cp_async4(dst + 4 * e, v ? op.ptr + off[e] + int64_t(r) * op.row_stride : op.ptr, v ? 4u : 0u);
+    }
+  }
 }
 
 __global__ void __launch_bounds__(kGemmThreads, 1)
@@ -148,36 +212,53 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       tc_fence_before();
       mbar_arrive(&ctl->tmem_empty[b]);
     };
-    float4 v[8];
-    if (produce) {
+    // cp.async pipeline, two stages ahead: raw fp32 lands in the hi plane of
+    // its slot; the same thread then rewrites it in place as tf32 hi and
+    // writes tf32 lo (it converts exactly the bytes it copied, so its own
+    // cp.async.wait_group is the only synchronisation needed).
+    const int32_t r0 = row0 + rbase;
+    KCursor cur{};
+    auto issue = [&](int it) {
+      const uint32_t plane = smem_u32(smem + (it % kStages) * kStageBytes + hi_off);
+      issue_stage(op, r0, rbase, c, cur, item.k1, plane);
+      cursor_advance(op, cur, kTileK);
+    };
+    auto convert = [&](int it) {
+      const int slot = it % kStages;
+      uint8_t* stage = smem + slot * kStageBytes;
 #pragma unroll
-      for (int j = 0; j < 8; ++j) v[j] = load_chunk(op, row0 + rbase + 16 * j, int64_t(item.k0) + 4 * c, item.k1);
+      for (int j = 0; j < 8; ++j) {
+        const int r = rbase + 16 * j;
+        const uint32_t off = r * 128 + ((c ^ (r & 7)) << 4);
+        const float4 x = *reinterpret_cast<const float4*>(stage + hi_off + off);
+        float4 h, l;
+        tf32_split(x.x, h.x, l.x);
+        tf32_split(x.y, h.y, l.y);
+        tf32_split(x.z, h.z, l.z);
+        tf32_split(x.w, h.w, l.w);
+        *reinterpret_cast<float4*>(stage + hi_off + off) = h;
+        *reinterpret_cast<float4*>(stage + lo_off + off) = l;
+      }
+      fence_proxy_async_smem();
+      mbar_arrive(&ctl->full[slot]);
+    };
+    if (produce) {
+      cur = cursor_at(op, item.k0 + 4 * c);
+      issue(0);
+      cp_async_commit();
+      if (n_iters > 1) issue(1);
+      cp_async_commit();
     }
     for (int it = 0; it < n_iters; ++it) {
       if (produce) {
-        const int slot = it % kStages;
-        const uint32_t round = it / kStages;
-        mbar_wait(&ctl->empty[slot], (round & 1) ^ 1);
-        uint8_t* stage = smem + slot * kStageBytes;
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const int r = rbase + 16 * j;
-          const uint32_t off = r * 128 + ((c ^ (r & 7)) << 4);
-          float4 h, l;
-          tf32_split(v[j].x, h.x, l.x);
-          tf32_split(v[j].y, h.y, l.y);
-          tf32_split(v[j].z, h.z, l.z);
-          tf32_split(v[j].w, h.w, l.w);
-          *reinterpret_cast<float4*>(stage + hi_off + off) = h;
-          *reinterpret_cast<float4*>(stage + lo_off + off) = l;
+        cp_async_wait<1>();
+        convert(it);
+        if (it + 2 < n_iters) {
+          const uint32_t round = (it + 2) / kStages;
+          mbar_wait(&ctl->empty[(it + 2) % kStages], (round & 1) ^ 1);
+          issue(it + 2);
         }
-        fence_proxy_async_smem();
-        mbar_arrive(&ctl->full[slot]);
-        if (it + 1 < n_iters) {
-          const int64_t kn = int64_t(item.k0) + int64_t(it + 1) * kTileK + 4 * c;
-#pragma unroll
-          for (int j = 0; j < 8; ++j) v[j] = load_chunk(op, row0 + rbase + 16 * j, kn, item.k1);
-        }
+        cp_async_commit();
       }
       if (it >= 1) drain(it - 1);
     }
@@ -337,7 +418,13 @@ int launch_gemm(const GemmProblem* d_probs, const GemmWorkItem* d_items, int n_i
     attr_set = true;
   }
   gemm_tf32x3_kernel<<<n_items, kGemmThreads, smem, stream>>>(d_probs, d_items, d_partials, d_status);
-  SPNGD_CUDA_TRY(cudaGetLastError());
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    cudaFuncAttributes fa{};
+    cudaFuncGetAttributes(&fa, gemm_tf32x3_kernel);
+    return fail(SPNGD_ERR_CUDA, "gemm launch failed: %s (regs %d, maxThreads %d, static smem %zu, dyn smem %zu)",
+                cudaGetErrorString(e), fa.numRegs, fa.maxThreadsPerBlock, fa.sharedSizeBytes, smem);
+  }
   return SPNGD_OK;
 }
 

@@ -26,118 +26,150 @@ namespace spngd {
 namespace {
 
 constexpr int kBaseMax = 128;
-constexpr int kBlk = 8;
-constexpr int kBaseThreads = 160;  // >= 16*17/2 = 136 lower 8x8 register blocks
+constexpr int kPB = 16;                 // panel width
+constexpr int kBaseThreads = 256;
+constexpr int kLd = kBaseMax + 1;       // padded smem row (floats)
+constexpr size_t kBaseSmem = 2 * size_t(kBaseMax) * kLd * sizeof(float) + kPB * (kPB + 1) * sizeof(double) +
+                             (kBaseMax / kPB) * kPB * kPB * sizeof(float);
 
-// One CTA per leaf.  Thread owns lower block (bi >= bj) of both the trailing
-// matrix (fp64 registers) and T = L^-1 (fp32 registers).  Step k publishes
-// column k of the trailing matrix and row k of T through smem, then:
-//   L[i][k] = a[i][k] / sqrt(p);  a[i][j] -= a[i][k] a[j][k] / p   (i, j > k)
-//   T[k][:] /= sqrt(p);           T[i][:] -= (a[i][k] / p) T_old[k][:]  (i > k)
+// One CTA per leaf (n <= 128): blocked right-looking Cholesky with 16-column
+// panels (fp64 diagonal blocks, fp32 FMA panel solves and register-tiled SYRK
+// trailing updates), then T = L^-1 by blocked forward substitution.
 __global__ void __launch_bounds__(kBaseThreads) base_chol_inv_kernel(const BaseTask* __restrict__ tasks, int* status) {
+  extern __shared__ __align__(16) uint8_t base_smem[];
+  float* A = reinterpret_cast<float*>(base_smem);               // [128][129], lower = M -> L
+  float* T = A + kBaseMax * kLd;                                // [128][129], T = L^-1
+  double* D = reinterpret_cast<double*>(T + kBaseMax * kLd);    // [16][17] diagonal block (fp64)
+  float* R = reinterpret_cast<float*>(D + kPB * (kPB + 1));     // [8][16][16] scratch
   const BaseTask t = tasks[blockIdx.x];
   const int n = t.n;
-  const int nb = (n + kBlk - 1) / kBlk;
-  __shared__ double colbuf[2][kBaseMax];
-  __shared__ float rowbuf[2][kBaseMax];
-  int bi = -1, bj = -1;
-  {
-    int idx = threadIdx.x;
-    for (int c = 0; c < nb; ++c) {  // column-major enumeration of lower blocks
-      const int cnt = nb - c;
-      if (idx < cnt) { bj = c; bi = c + idx; break; }
-      idx -= cnt;
-    }
+  const int np = (n + kPB - 1) / kPB * kPB;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int idx = tid; idx < np * np; idx += kBaseThreads) {
+    const int i = idx / np, j = idx % np;
+    float v = (i == j) ? 1.f : 0.f;  // identity padding beyond n is inert
+    if (i < n && j < n && j <= i) v = t.m[int64_t(i) * t.ld + j];
+    A[i * kLd + j] = v;
+    T[i * kLd + j] = 0.f;
   }
-  const bool active = bi >= 0;
-  double m[kBlk][kBlk];
-  float tt[kBlk][kBlk];
-#pragma unroll
-  for (int ii = 0; ii < kBlk; ++ii)
-#pragma unroll
-    for (int jj = 0; jj < kBlk; ++jj) {
-      const int i = bi * kBlk + ii, j = bj * kBlk + jj;
-      double v = (i == j) ? 1.0 : 0.0;  // identity padding beyond n is inert
-      if (active && i < n && j < n) v = double(t.m[int64_t(i) * t.ld + j]);
-      m[ii][jj] = v;
-      tt[ii][jj] = (i == j) ? 1.f : 0.f;
-    }
+  __syncthreads();
   bool bad = false;
-  for (int kb = 0; kb < nb; ++kb) {
-#pragma unroll
-    for (int kk = 0; kk < kBlk; ++kk) {
-      const int k = kb * kBlk + kk;
-      double* cb = colbuf[k & 1];
-      float* rb = rowbuf[k & 1];
-      if (active) {
-        if (bj == kb) {
-#pragma unroll
-          for (int ii = 0; ii < kBlk; ++ii) cb[bi * kBlk + ii] = m[ii][kk];
+  const int nblk = np / kPB;
+  for (int kb = 0; kb < nblk; ++kb) {
+    const int k0 = kb * kPB;
+    // (1) diagonal block: fp64 Cholesky + inverse by warp 0.
+    if (warp == 0) {
+      if (lane < kPB)
+        for (int j = 0; j <= lane; ++j) D[lane * (kPB + 1) + j] = double(A[(k0 + lane) * kLd + k0 + j]);
+      __syncwarp();
+      for (int k = 0; k < kPB; ++k) {
+        double p = D[k * (kPB + 1) + k];
+        if (!(p > 0.0) || !isfinite(p)) {
+          bad = true;
+          p = 1.0;
         }
-        if (bi == kb) {
-#pragma unroll
-          for (int jj = 0; jj < kBlk; ++jj) rb[bj * kBlk + jj] = tt[kk][jj];
+        const double s = sqrt(p);
+        __syncwarp();
+        if (lane > k && lane < kPB) D[lane * (kPB + 1) + k] /= s;
+        if (lane == k) D[k * (kPB + 1) + k] = s;
+        __syncwarp();
+        if (lane > k && lane < kPB) {
+          const double lik = D[lane * (kPB + 1) + k];
+          for (int j = k + 1; j <= lane; ++j) D[lane * (kPB + 1) + j] -= lik * D[j * (kPB + 1) + k];
         }
+        __syncwarp();
+      }
+      // Column `lane` of L_dd^-1 by forward substitution (fp64), into T's diagonal block.
+      if (lane < kPB) {
+        double col[kPB];
+#pragma unroll
+        for (int i = 0; i < kPB; ++i) {
+          double acc = (i == lane) ? 1.0 : 0.0;
+#pragma unroll
+          for (int p = 0; p < i; ++p) acc -= D[i * (kPB + 1) + p] * col[p];
+          col[i] = (i < lane) ? 0.0 : acc / D[i * (kPB + 1) + i];
+        }
+#pragma unroll
+        for (int i = 0; i < kPB; ++i) T[(k0 + i) * kLd + k0 + lane] = float(col[i]);
+        for (int i = lane; i < kPB; ++i) A[(k0 + i) * kLd + k0 + lane] = float(D[i * (kPB + 1) + lane]);
+      }
+    }
+    __syncthreads();
+    const int m = np - k0 - kPB;  // trailing size
+    if (m > 0) {
+      // (2) panel: L[i][k0+j] = sum_{p<=j} A[i][k0+p] * Dinv[j][p], i >= k0+16.
+      float res[(kBaseMax - kPB) / kPB];
+      const int j = tid & (kPB - 1);
+      int cnt = 0;
+      for (int i = k0 + kPB + (tid >> 4); i < np; i += kBaseThreads / kPB, ++cnt) {
+        float acc = 0.f;
+#pragma unroll
+        for (int p = 0; p < kPB; ++p)
+          if (p <= j) acc = fmaf(A[i * kLd + k0 + p], T[(k0 + j) * kLd + k0 + p], acc);
+        res[cnt] = acc;
       }
       __syncthreads();
-      double p = cb[k];
-      if (!(p > 0.0) || !isfinite(p)) {
-        bad = true;
-        p = 1.0;
-      }
-      const double inv_p = 1.0 / p;
-      const double inv_s = rsqrt(p);
-      if (active && bi >= kb) {
-        double ci[kBlk], cj[kBlk];
-        float rj[kBlk];
+      cnt = 0;
+      for (int i = k0 + kPB + (tid >> 4); i < np; i += kBaseThreads / kPB, ++cnt) A[i * kLd + k0 + j] = res[cnt];
+      __syncthreads();
+      // (3) trailing SYRK on 4x4 register tiles of the lower triangle.
+      const int mt = m / 4;
+      const int ntiles = mt * (mt + 1) / 2;
+      for (int tt = tid; tt < ntiles; tt += kBaseThreads) {
+        int ti = int((sqrtf(8.f * tt + 1.f) - 1.f) * 0.5f);
+        while ((ti + 1) * (ti + 2) / 2 <= tt) ++ti;
+        while (ti * (ti + 1) / 2 > tt) --ti;
+        const int tj = tt - ti * (ti + 1) / 2;
+        const int i0 = k0 + kPB + 4 * ti, j0 = k0 + kPB + 4 * tj;
+        float acc[4][4] = {};
 #pragma unroll
-        for (int ii = 0; ii < kBlk; ++ii) ci[ii] = cb[bi * kBlk + ii] * inv_p;
+        for (int p = 0; p < kPB; ++p) {
+          float a[4], b[4];
 #pragma unroll
-        for (int jj = 0; jj < kBlk; ++jj) {
-          cj[jj] = cb[bj * kBlk + jj];
-          rj[jj] = rb[bj * kBlk + jj];
-        }
-        // Trailing update, rows/cols > k only (earlier ones hold finished values).
-        if (bj >= kb) {
-#pragma unroll
-          for (int ii = 0; ii < kBlk; ++ii)
-#pragma unroll
-            for (int jj = 0; jj < kBlk; ++jj) {
-              const int i = bi * kBlk + ii, j = bj * kBlk + jj;
-              if (i > k && j > k) m[ii][jj] = fma(-ci[ii], cj[jj], m[ii][jj]);
-            }
-        }
-        // T elimination: columns j <= k live in blocks bj <= kb.
-        if (bj <= kb) {
-#pragma unroll
-          for (int ii = 0; ii < kBlk; ++ii) {
-            const int i = bi * kBlk + ii;
-            const float f = (i == k) ? 0.f : float(ci[ii]);
-#pragma unroll
-            for (int jj = 0; jj < kBlk; ++jj) {
-              const int j = bj * kBlk + jj;
-              if (j <= k) {
-                if (i == k) tt[ii][jj] = float(double(rj[jj]) * inv_s);
-                else if (i > k) tt[ii][jj] = fmaf(-f, rj[jj], tt[ii][jj]);
-              }
-            }
+          for (int q = 0; q < 4; ++q) {
+            a[q] = A[(i0 + q) * kLd + k0 + p];
+            b[q] = A[(j0 + q) * kLd + k0 + p];
           }
+#pragma unroll
+          for (int x = 0; x < 4; ++x)
+#pragma unroll
+            for (int y = 0; y < 4; ++y) acc[x][y] = fmaf(a[x], b[y], acc[x][y]);
         }
+#pragma unroll
+        for (int x = 0; x < 4; ++x)
+#pragma unroll
+          for (int y = 0; y < 4; ++y)
+            if (j0 + y <= i0 + x) A[(i0 + x) * kLd + j0 + y] -= acc[x][y];
       }
+      __syncthreads();
     }
   }
-  if (bad && threadIdx.x == 0) set_status(status, SPNGD_ERR_NOT_POSITIVE_DEFINITE);
-  if (active) {
+  // (4) off-diagonal blocks of T = L^-1: T[ib][jb] = -T[ib][ib] * sum_{kb=jb}^{ib-1} L[ib][kb] T[kb][jb].
+  const int r = tid >> 4, c = tid & 15;
+  for (int ib = 1; ib < nblk; ++ib) {
+    for (int jb = 0; jb < ib; ++jb) {
+      float acc = 0.f;
+      for (int p = jb * kPB; p < ib * kPB; ++p) acc = fmaf(A[(ib * kPB + r) * kLd + p], T[p * kLd + jb * kPB + c], acc);
+      R[(jb * kPB + r) * kPB + c] = acc;
+    }
+    __syncthreads();
+    for (int jb = 0; jb < ib; ++jb) {
+      float acc = 0.f;
 #pragma unroll
-    for (int ii = 0; ii < kBlk; ++ii)
-#pragma unroll
-      for (int jj = 0; jj < kBlk; ++jj) {
-        const int i = bi * kBlk + ii, j = bj * kBlk + jj;
-        if (i < n && j < n && i >= j) {
-          t.tlow[int64_t(i) * t.ld + j] = tt[ii][jj];
-          t.tup[int64_t(j) * t.ld + i] = tt[ii][jj];
-        }
-      }
+      for (int q = 0; q < kPB; ++q)
+        if (q <= r) acc = fmaf(T[(ib * kPB + r) * kLd + ib * kPB + q], R[(jb * kPB + q) * kPB + c], acc);
+      T[(ib * kPB + r) * kLd + jb * kPB + c] = -acc;
+    }
+    __syncthreads();
+  }
+  if (bad) set_status(status, SPNGD_ERR_NOT_POSITIVE_DEFINITE);
+  for (int idx = tid; idx < n * n; idx += kBaseThreads) {
+    const int i = idx / n, j = idx % n;
+    if (j <= i) {
+      const float v = T[i * kLd + j];
+      t.tlow[int64_t(i) * t.ld + j] = v;
+      t.tup[int64_t(j) * t.ld + i] = v;
+    }
   }
 }
 
@@ -372,7 +404,13 @@ int launch_pack(spngd_ctx* ctx, const PackTask* d_tasks, int n, int64_t max_n) {
 
 int launch_base(spngd_ctx* ctx, const BaseTask* d_tasks, int n) {
   if (n <= 0) return SPNGD_OK;
-  base_chol_inv_kernel<<<n, kBaseThreads, 0, ctx->stream>>>(d_tasks, ctx->d_status);
+  static bool attr = false;
+  if (!attr) {
+    SPNGD_CUDA_TRY(cudaFuncSetAttribute(base_chol_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        int(kBaseSmem)));
+    attr = true;
+  }
+  base_chol_inv_kernel<<<n, kBaseThreads, kBaseSmem, ctx->stream>>>(d_tasks, ctx->d_status);
   SPNGD_CUDA_TRY(cudaGetLastError());
   ctx->launches++;
   return SPNGD_OK;
