@@ -26,91 +26,126 @@ namespace spngd {
 namespace {
 
 constexpr int kBaseMax = 128;
-constexpr int kPB = 16;                 // panel width
+constexpr int kPB = 32;                 // panel width = one warp of rows
 constexpr int kBaseThreads = 256;
 constexpr int kLd = kBaseMax + 1;       // padded smem row (floats)
-constexpr size_t kBaseSmem = 2 * size_t(kBaseMax) * kLd * sizeof(float) + kPB * (kPB + 1) * sizeof(double) +
-                             (kBaseMax / kPB) * kPB * kPB * sizeof(float);
+constexpr int kNb = kBaseMax / kPB;
+constexpr size_t kBaseSmem = (2 * size_t(kBaseMax) * kLd + size_t(kNb) * kPB * kPB + kBaseMax) * sizeof(float);
 
-// One CTA per leaf (n <= 128): blocked right-looking Cholesky with 16-column
-// panels (fp64 diagonal blocks, fp32 FMA panel solves and register-tiled SYRK
-// trailing updates), then T = L^-1 by blocked forward substitution.
-__global__ void __launch_bounds__(kBaseThreads) base_chol_inv_kernel(const BaseTask* __restrict__ tasks, int* status) {
+// Compile-time-unrolled steps of the 32x32 diagonal factorization (rows in
+// lanes) and of the column substitution, so `row`/`col` stay in registers.
+template <int K>
+__device__ __forceinline__ void diag_chol_step(float (&row)[32], int lane, float* rdiag, bool& bad) {
+  float p = __shfl_sync(0xffffffffu, row[K], K);
+  if (!(p > 0.f) || !isfinite(p)) {
+    bad = true;
+    p = 1.f;
+  }
+  float inv = rsqrtf(p);
+  inv = inv * fmaf(-0.5f * p, inv * inv, 1.5f);  // MUFU rsqrt + one Newton step
+  if (lane == K) rdiag[K] = inv;
+  row[K] = (lane == K) ? p * inv : (lane > K ? row[K] * inv : row[K]);
+#pragma unroll
+  for (int j = K + 1; j < 32; ++j) {
+    const float ljk = __shfl_sync(0xffffffffu, row[K], j);
+    row[j] = (lane >= j) ? fmaf(-row[K], ljk, row[j]) : row[j];
+  }
+  if constexpr (K + 1 < 32) diag_chol_step<K + 1>(row, lane, rdiag, bad);
+}
+
+template <int I>
+__device__ __forceinline__ void diag_subst_step(float (&col)[32], const float* Ld, int ld, const float* rdiag,
+                                                int lane) {
+  float a0 = (I == lane) ? 1.f : 0.f, a1 = 0.f;
+#pragma unroll
+  for (int p = 0; p < I; ++p) {
+    if (p & 1) a1 = fmaf(-Ld[I * ld + p], col[p], a1);
+    else a0 = fmaf(-Ld[I * ld + p], col[p], a0);
+  }
+  col[I] = (I < lane) ? 0.f : (a0 + a1) * rdiag[I];
+  if constexpr (I + 1 < 32) diag_subst_step<I + 1>(col, Ld, ld, rdiag, lane);
+}
+
+// One CTA per leaf (n <= 128): blocked right-looking Cholesky with 32-column
+// panels.  Warp 0 factors each 32x32 diagonal block with rows in lanes and
+// columns broadcast by shuffle, then inverts it by forward substitution; all
+// warps solve the panel and apply the SYRK trailing update on 4x4 register
+// tiles; finally T = L^-1 by blocked forward substitution.  fp32 storage and
+// FMA (LAPACK spotrf class).
+__global__ void __launch_bounds__(kBaseThreads, 1) base_chol_inv_kernel(const BaseTask* __restrict__ tasks, int* status) {
   extern __shared__ __align__(16) uint8_t base_smem[];
-  float* A = reinterpret_cast<float*>(base_smem);               // [128][129], lower = M -> L
-  float* T = A + kBaseMax * kLd;                                // [128][129], T = L^-1
-  double* D = reinterpret_cast<double*>(T + kBaseMax * kLd);    // [16][17] diagonal block (fp64)
-  float* R = reinterpret_cast<float*>(D + kPB * (kPB + 1));     // [8][16][16] scratch
+  float* A = reinterpret_cast<float*>(base_smem);   // [128][129], lower = M -> L
+  float* T = A + kBaseMax * kLd;                    // [128][129], T = L^-1
+  float* R = T + kBaseMax * kLd;                    // [4][32][32] scratch
+  float* rdiag = R + kNb * kPB * kPB;               // [128] 1 / L_ii
   const BaseTask t = tasks[blockIdx.x];
   const int n = t.n;
   const int np = (n + kPB - 1) / kPB * kPB;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  for (int idx = tid; idx < np * np; idx += kBaseThreads) {
-    const int i = idx / np, j = idx % np;
-    float v = (i == j) ? 1.f : 0.f;  // identity padding beyond n is inert
-    if (i < n && j < n && j <= i) v = t.m[int64_t(i) * t.ld + j];
-    A[i * kLd + j] = v;
-    T[i * kLd + j] = 0.f;
+  // Load M's lower triangle: each warp owns rows warp + 8 q; all loads of a
+  // row batch are issued before any smem store.
+  for (int jc = 0; jc < np; jc += 32) {
+    const int j = jc + lane;
+    float v[kBaseMax / 8];
+#pragma unroll
+    for (int q = 0; q < kBaseMax / 8; ++q) {
+      const int i = warp + 8 * q;
+      v[q] = (i == j) ? 1.f : 0.f;  // identity padding beyond n is inert
+      if (i < n && j < n && j <= i) v[q] = __ldg(t.m + int64_t(i) * t.ld + j);
+    }
+#pragma unroll
+    for (int q = 0; q < kBaseMax / 8; ++q) {
+      const int i = warp + 8 * q;
+      if (i < np) {
+        A[i * kLd + j] = v[q];
+        T[i * kLd + j] = 0.f;
+      }
+    }
   }
   __syncthreads();
   bool bad = false;
   const int nblk = np / kPB;
   for (int kb = 0; kb < nblk; ++kb) {
     const int k0 = kb * kPB;
-    // (1) diagonal block: fp64 Cholesky + inverse by warp 0.
     if (warp == 0) {
-      if (lane < kPB)
-        for (int j = 0; j <= lane; ++j) D[lane * (kPB + 1) + j] = double(A[(k0 + lane) * kLd + k0 + j]);
+      // (1) 32x32 diagonal block: lane i owns row i in registers; column k is
+      //     broadcast by shuffle.
+      float row[kPB];
+#pragma unroll
+      for (int j = 0; j < kPB; ++j) row[j] = (j <= lane) ? A[(k0 + lane) * kLd + k0 + j] : 0.f;
+      diag_chol_step<0>(row, lane, rdiag + k0, bad);
+#pragma unroll
+      for (int j = 0; j < kPB; ++j)
+        if (j <= lane) A[(k0 + lane) * kLd + k0 + j] = row[j];
       __syncwarp();
-      for (int k = 0; k < kPB; ++k) {
-        double p = D[k * (kPB + 1) + k];
-        if (!(p > 0.0) || !isfinite(p)) {
-          bad = true;
-          p = 1.0;
-        }
-        const double s = sqrt(p);
-        __syncwarp();
-        if (lane > k && lane < kPB) D[lane * (kPB + 1) + k] /= s;
-        if (lane == k) D[k * (kPB + 1) + k] = s;
-        __syncwarp();
-        if (lane > k && lane < kPB) {
-          const double lik = D[lane * (kPB + 1) + k];
-          for (int j = k + 1; j <= lane; ++j) D[lane * (kPB + 1) + j] -= lik * D[j * (kPB + 1) + k];
-        }
-        __syncwarp();
-      }
-      // Column `lane` of L_dd^-1 by forward substitution (fp64), into T's diagonal block.
-      if (lane < kPB) {
-        double col[kPB];
+      // Column `lane` of L_dd^-1 (forward substitution), into T's diagonal block.
+      float col[kPB];
+      diag_subst_step<0>(col, A + k0 * kLd + k0, kLd, rdiag + k0, lane);
 #pragma unroll
-        for (int i = 0; i < kPB; ++i) {
-          double acc = (i == lane) ? 1.0 : 0.0;
-#pragma unroll
-          for (int p = 0; p < i; ++p) acc -= D[i * (kPB + 1) + p] * col[p];
-          col[i] = (i < lane) ? 0.0 : acc / D[i * (kPB + 1) + i];
-        }
-#pragma unroll
-        for (int i = 0; i < kPB; ++i) T[(k0 + i) * kLd + k0 + lane] = float(col[i]);
-        for (int i = lane; i < kPB; ++i) A[(k0 + i) * kLd + k0 + lane] = float(D[i * (kPB + 1) + lane]);
-      }
+      for (int i = 0; i < kPB; ++i) T[(k0 + i) * kLd + k0 + lane] = col[i];
     }
     __syncthreads();
     const int m = np - k0 - kPB;  // trailing size
     if (m > 0) {
-      // (2) panel: L[i][k0+j] = sum_{p<=j} A[i][k0+p] * Dinv[j][p], i >= k0+16.
-      float res[(kBaseMax - kPB) / kPB];
+      // (2) panel: L[i][k0+j] = sum_{p<=j} A[i][k0+p] Dinv[j][p]; thread = (row group, column j).
+      constexpr int kRows = (kBaseMax - kPB) / (kBaseThreads / kPB);  // 12 rows per thread max
       const int j = tid & (kPB - 1);
-      int cnt = 0;
-      for (int i = k0 + kPB + (tid >> 4); i < np; i += kBaseThreads / kPB, ++cnt) {
-        float acc = 0.f;
+      const int ibase = k0 + kPB + (tid >> 5);
+      const int stride = kBaseThreads / kPB;
+      float res[kRows];
 #pragma unroll
-        for (int p = 0; p < kPB; ++p)
-          if (p <= j) acc = fmaf(A[i * kLd + k0 + p], T[(k0 + j) * kLd + k0 + p], acc);
-        res[cnt] = acc;
+      for (int q = 0; q < kRows; ++q) res[q] = 0.f;
+#pragma unroll 8
+      for (int p = 0; p < kPB; ++p) {
+        const float d = (p <= j) ? T[(k0 + j) * kLd + k0 + p] : 0.f;
+#pragma unroll
+        for (int q = 0; q < kRows; ++q)
+          if (ibase + q * stride < np) res[q] = fmaf(A[(ibase + q * stride) * kLd + k0 + p], d, res[q]);
       }
       __syncthreads();
-      cnt = 0;
-      for (int i = k0 + kPB + (tid >> 4); i < np; i += kBaseThreads / kPB, ++cnt) A[i * kLd + k0 + j] = res[cnt];
+#pragma unroll
+      for (int q = 0; q < kRows; ++q)
+        if (ibase + q * stride < np) A[(ibase + q * stride) * kLd + k0 + j] = res[q];
       __syncthreads();
       // (3) trailing SYRK on 4x4 register tiles of the lower triangle.
       const int mt = m / 4;
@@ -122,7 +157,7 @@ __global__ void __launch_bounds__(kBaseThreads) base_chol_inv_kernel(const BaseT
         const int tj = tt - ti * (ti + 1) / 2;
         const int i0 = k0 + kPB + 4 * ti, j0 = k0 + kPB + 4 * tj;
         float acc[4][4] = {};
-#pragma unroll
+#pragma unroll 8
         for (int p = 0; p < kPB; ++p) {
           float a[4], b[4];
 #pragma unroll
@@ -144,33 +179,68 @@ __global__ void __launch_bounds__(kBaseThreads) base_chol_inv_kernel(const BaseT
       __syncthreads();
     }
   }
-  // (4) off-diagonal blocks of T = L^-1: T[ib][jb] = -T[ib][ib] * sum_{kb=jb}^{ib-1} L[ib][kb] T[kb][jb].
-  const int r = tid >> 4, c = tid & 15;
+  // (4) T = L^-1 off-diagonal 32x32 blocks, block row by block row:
+  //     R[jb] = sum_{p in [32 jb, 32 ib)} L[ib][p] T[p][jb],  T[ib][jb] = -T[ib][ib] R[jb].
+  //     Thread owns 4 rows (r0 + 8 q) of column c for every jb: independent chains.
+  const int c = tid & 31, r0 = tid >> 5;
   for (int ib = 1; ib < nblk; ++ib) {
-    for (int jb = 0; jb < ib; ++jb) {
-      float acc = 0.f;
-      for (int p = jb * kPB; p < ib * kPB; ++p) acc = fmaf(A[(ib * kPB + r) * kLd + p], T[p * kLd + jb * kPB + c], acc);
-      R[(jb * kPB + r) * kPB + c] = acc;
-    }
-    __syncthreads();
-    for (int jb = 0; jb < ib; ++jb) {
-      float acc = 0.f;
+    float acc[kNb - 1][4];
 #pragma unroll
-      for (int q = 0; q < kPB; ++q)
-        if (q <= r) acc = fmaf(T[(ib * kPB + r) * kLd + ib * kPB + q], R[(jb * kPB + q) * kPB + c], acc);
-      T[(ib * kPB + r) * kLd + jb * kPB + c] = -acc;
+    for (int jb = 0; jb < kNb - 1; ++jb)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) acc[jb][q] = 0.f;
+    for (int p = 0; p < ib * kPB; ++p) {
+      float l[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) l[q] = A[(ib * kPB + r0 + 8 * q) * kLd + p];
+#pragma unroll
+      for (int jb = 0; jb < kNb - 1; ++jb)
+        if (jb < ib && jb * kPB <= p) {
+          const float tv = T[p * kLd + jb * kPB + c];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) acc[jb][q] = fmaf(l[q], tv, acc[jb][q]);
+        }
     }
+#pragma unroll
+    for (int jb = 0; jb < kNb - 1; ++jb)
+      if (jb < ib)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) R[(jb * kPB + r0 + 8 * q) * kPB + c] = acc[jb][q];
+    __syncthreads();
+#pragma unroll
+    for (int jb = 0; jb < kNb - 1; ++jb)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) acc[jb][q] = 0.f;
+#pragma unroll 8
+    for (int qq = 0; qq < kPB; ++qq) {
+      float d[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int r = r0 + 8 * q;
+        d[q] = (qq <= r) ? T[(ib * kPB + r) * kLd + ib * kPB + qq] : 0.f;
+      }
+#pragma unroll
+      for (int jb = 0; jb < kNb - 1; ++jb)
+        if (jb < ib) {
+          const float rv = R[(jb * kPB + qq) * kPB + c];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) acc[jb][q] = fmaf(d[q], rv, acc[jb][q]);
+        }
+    }
+#pragma unroll
+    for (int jb = 0; jb < kNb - 1; ++jb)
+      if (jb < ib)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) T[(ib * kPB + r0 + 8 * q) * kLd + jb * kPB + c] = -acc[jb][q];
     __syncthreads();
   }
   if (bad) set_status(status, SPNGD_ERR_NOT_POSITIVE_DEFINITE);
-  for (int idx = tid; idx < n * n; idx += kBaseThreads) {
-    const int i = idx / n, j = idx % n;
-    if (j <= i) {
-      const float v = T[i * kLd + j];
-      t.tlow[int64_t(i) * t.ld + j] = v;
-      t.tup[int64_t(j) * t.ld + i] = v;
+  // Coalesced stores: T rows (lower) and T^T rows (upper, read transposed from smem).
+  for (int i = warp; i < n; i += kBaseThreads / 32)
+    for (int j = lane; j < n; j += 32) {
+      if (j <= i) t.tlow[int64_t(i) * t.ld + j] = T[i * kLd + j];
+      if (j >= i) t.tup[int64_t(i) * t.ld + j] = T[j * kLd + i];
     }
-  }
 }
 
 __global__ void pi_kernel(const PiTask* __restrict__ tasks) {
@@ -254,6 +324,9 @@ struct Op {
   BaseTask base;
   GemmProblem prob;
   bool upper;
+  GemmProblem prob2;  // optional independent GEMM in the same round
+  bool upper2;
+  bool has2;
 };
 
 int64_t split_point(int64_t n) {
@@ -322,12 +395,16 @@ void gen_chol(const DenseMatrix& m, int64_t off, int64_t n, Gen& g, std::vector<
   // L21 = B T11^T  (B = M[o2.., off..]); T11 lower -> K band k <= j
   ops.push_back(gemm_op(dense_op(at(m.ptr, ld, o2, off), ld, n2, n1), dense_op(at(m.tlow, ld, off, off), ld, n1, n1),
                         n2, n1, n1, 0, KTRI_B_LOWER, 1.f, 0.f, L21, ldl));
-  // S = C - L21 L21^T  (symmetric, in place)
-  ops.push_back(gemm_op(dense_op(L21, ldl, n2, n1), dense_op(L21, ldl, n2, n1), n2, n2, n1,
-                        FLAG_SAME_AB | FLAG_SYM_MIRROR, 0, -1.f, 1.f, at(m.ptr, ld, o2, o2), ld, nullptr, 0, true));
-  // U^T = T11^T L21^T; T11^T upper -> K band k >= j
-  ops.push_back(gemm_op(dense_op(at(m.tup, ld, off, off), ld, n1, n1), dense_op(L21, ldl, n2, n1), n1, n2, n1, 0,
-                        KTRI_A_UPPER, 1.f, 0.f, Ut, ldu));
+  // S = C - L21 L21^T (symmetric, in place) and, independent of it in the
+  // same round, U^T = T11^T L21^T (T11^T upper -> K band k >= j).
+  Op s = gemm_op(dense_op(L21, ldl, n2, n1), dense_op(L21, ldl, n2, n1), n2, n2, n1, FLAG_SAME_AB | FLAG_SYM_MIRROR, 0,
+                 -1.f, 1.f, at(m.ptr, ld, o2, o2), ld, nullptr, 0, true);
+  const Op u = gemm_op(dense_op(at(m.tup, ld, off, off), ld, n1, n1), dense_op(L21, ldl, n2, n1), n1, n2, n1, 0,
+                       KTRI_A_UPPER, 1.f, 0.f, Ut, ldu);
+  s.prob2 = u.prob;
+  s.upper2 = false;
+  s.has2 = true;
+  ops.push_back(s);
   gen_chol(m, o2, n2, g, ops);
   // T21 = -T22 U (+ T21^T into the upper factor); T22 lower -> K band k <= i
   ops.push_back(gemm_op(dense_op(at(m.tlow, ld, o2, o2), ld, n2, n2), dense_op(Ut, ldu, n1, n2), n2, n1, n2,
@@ -367,6 +444,11 @@ void plan_inverse(const std::vector<DenseMatrix>& mats, float* workspace, Invers
         plan.probs.push_back(o.prob);
         int slot = 0;
         plan_problem_tiles(pi, o.prob, o.upper, o.prob.K + kTileK, plan.items, nullptr, &slot, 1.0, nullptr);
+        if (o.has2) {
+          const int pj = int(plan.probs.size());
+          plan.probs.push_back(o.prob2);
+          plan_problem_tiles(pj, o.prob2, o.upper2, o.prob2.K + kTileK, plan.items, nullptr, &slot, 1.0, nullptr);
+        }
       }
     }
     rd.item_cnt = int(plan.items.size()) - rd.item_off;
