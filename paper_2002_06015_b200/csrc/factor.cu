@@ -62,8 +62,11 @@ int plan_factors(const spngd_factor_req* reqs, int n, FactorPlan& plan) {
       op.seg_stride = r.dim * r.hw;
     }
     op.rows = int32_t(r.dim);
-    finalize_operand(op);
-    const int64_t K = (r.hi - r.lo) * (r.layout == 0 ? 1 : r.hw);
+    op.nseg = r.layout == 0 ? (r.hi - r.lo) : (r.hi - r.lo);
+    const int64_t K_true = (r.hi - r.lo) * (r.layout == 0 ? 1 : r.hw);
+    finalize_operand(op, K_true);
+    // TMA-3D iterates zero-padded 32-wide chunks per sample (padded_k).
+    const int64_t K = padded_k(op, K_true);
     if (K > INT32_MAX) return fail(SPNGD_ERR_SHAPE_MISMATCH, "factor request %d: K too large", i);
     GemmProblem p{};
     p.A = op;

@@ -19,8 +19,11 @@
 // order each epilogue mode needs.
 #include <cuda_runtime.h>
 
+#include <cudaTypedefs.h>
+
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "gemm_tf32x3.cuh"
@@ -39,6 +42,7 @@ struct __align__(8) SmemCtl {
   uint64_t empty[kStages];
   uint64_t tmem_full[2];
   uint64_t tmem_empty[2];
+  uint64_t raw[2][kStages];  // TMA raw-tile arrival per operand (A, B)
   uint32_t tmem_base;
   int32_t pad;
   GemmProblem prob;
@@ -90,6 +94,24 @@ __device__ __forceinline__ void cp_async4(uint32_t dst, const void* src, uint32_
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, int32_t c0, int32_t c1, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map, int32_t c0, int32_t c1, int32_t c2,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(
+          dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+      : "memory");
+}
 
 // Issues the async copies of k .. k+3 for the 8 rows (r0 + 16 j) this thread
 // feeds into the swizzled fp32 plane at `plane` (zero-filled outside).
@@ -171,6 +193,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     for (int b = 0; b < 2; ++b) {
       mbar_init(&ctl->tmem_full[b], 1);
       mbar_init(&ctl->tmem_empty[b], 256);
+      for (int q = 0; q < kStages; ++q) mbar_init(&ctl->raw[b][q], 1);
     }
     mbar_fence_init();
   }
@@ -212,16 +235,34 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       tc_fence_before();
       mbar_arrive(&ctl->tmem_empty[b]);
     };
-    // cp.async pipeline, two stages ahead: raw fp32 lands in the hi plane of
-    // its slot; the same thread then rewrites it in place as tf32 hi and
-    // writes tf32 lo (it converts exactly the bytes it copied, so its own
-    // cp.async.wait_group is the only synchronisation needed).
+    // Raw fp32 tiles land in the hi plane of their slot two stages ahead --
+    // by TMA (one elected thread, mbarrier complete_tx) when the layout allows,
+    // else by per-thread cp.async.  Every producer thread then rewrites its
+    // 8 16-byte chunks in place as tf32 hi and writes tf32 lo.
     const int32_t r0 = row0 + rbase;
+    const bool tma = op.mode != OP_ASYNC;
+    const CUtensorMap* tmap = is_b ? &probs[item.problem].B.tmap : &probs[item.problem].A.tmap;
+    uint64_t* raw = ctl->raw[is_b ? 1 : 0];
     KCursor cur{};
+    int32_t tq = 0;  // TMA: 32-wide chunk index of the next stage
     auto issue = [&](int it) {
-      const uint32_t plane = smem_u32(smem + (it % kStages) * kStageBytes + hi_off);
-      issue_stage(op, r0, rbase, c, cur, item.k1, plane);
-      cursor_advance(op, cur, kTileK);
+      const int slot = it % kStages;
+      const uint32_t plane = smem_u32(smem + slot * kStageBytes + hi_off);
+      if (tma) {
+        if (t == 0) {
+          mbar_expect_tx(&raw[slot], kOperandBytes);
+          if (op.mode == OP_TMA2D) {
+            tma_load_2d(plane, tmap, tq * kTileK, row0, &raw[slot]);
+          } else {
+            const int32_t seg = tq / op.cps, ch = tq - seg * op.cps;
+            tma_load_3d(plane, tmap, ch * kTileK, row0, seg, &raw[slot]);
+          }
+        }
+        ++tq;
+      } else {
+        issue_stage(op, r0, rbase, c, cur, item.k1, plane);
+        cursor_advance(op, cur, kTileK);
+      }
     };
     auto convert = [&](int it) {
       const int slot = it % kStages;
@@ -243,7 +284,12 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       mbar_arrive(&ctl->full[slot]);
     };
     if (produce) {
-      cur = cursor_at(op, item.k0 + 4 * c);
+      if (tma) {
+        tq = item.k0 / kTileK;
+        if (t == 0) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(tmap)) : "memory");
+      } else {
+        cur = cursor_at(op, item.k0 + 4 * c);
+      }
       issue(0);
       cp_async_commit();
       if (n_iters > 1) issue(1);
@@ -251,11 +297,17 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     }
     for (int it = 0; it < n_iters; ++it) {
       if (produce) {
-        cp_async_wait<1>();
+        if (tma) {
+          mbar_wait(&raw[it % kStages], (it / kStages) & 1);
+        } else {
+          cp_async_wait<1>();
+        }
         convert(it);
         if (it + 2 < n_iters) {
-          const uint32_t round = (it + 2) / kStages;
-          mbar_wait(&ctl->empty[(it + 2) % kStages], (round & 1) ^ 1);
+          if (!tma || t == 0) {
+            const uint32_t round = (it + 2) / kStages;
+            mbar_wait(&ctl->empty[(it + 2) % kStages], (round & 1) ^ 1);
+          }
           issue(it + 2);
         }
         cp_async_commit();
@@ -401,9 +453,55 @@ __global__ void syrk_reduce_kernel(const SyrkReduceTask* __restrict__ tasks, con
 
 }  // namespace
 
-void finalize_operand(GemmOperand& op) {
+namespace {
+PFN_cuTensorMapEncodeTiled_v12000 tma_encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+}  // namespace
+
+void finalize_operand(GemmOperand& op, int64_t K, bool allow_tma) {
   const uintptr_t addr = reinterpret_cast<uintptr_t>(op.ptr);
   op.vec = (addr % 16 == 0) && (op.seg_len % 4 == 0) && (op.row_stride % 4 == 0) && (op.seg_stride % 4 == 0);
+  op.mode = OP_ASYNC;
+  op.cps = 0;
+  static const bool no_tma = getenv("SPNGD_NO_TMA") != nullptr;
+  if (no_tma || !allow_tma || !op.ptr || addr % 16 != 0 || op.rows <= 0) return;
+  auto encode = tma_encode_fn();
+  if (!encode) return;
+  const bool dense = (K < 0) || (op.seg_len >= K && op.seg_stride == 0);
+  cuuint32_t box[3] = {32, 128, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r;
+  if (dense) {
+    if (op.row_stride % 4 != 0 || K <= 0) return;
+    cuuint64_t dims[2] = {cuuint64_t(K), cuuint64_t(op.rows)};
+    cuuint64_t strides[1] = {cuuint64_t(op.row_stride) * 4};
+    r = encode(&op.tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(op.ptr), dims, strides, box, estr,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r == CUDA_SUCCESS) op.mode = OP_TMA2D;
+  } else {
+    if (op.seg_len % 4 != 0 || op.row_stride % 4 != 0 || op.seg_stride % 4 != 0 || op.nseg <= 0) return;
+    cuuint64_t dims[3] = {cuuint64_t(op.seg_len), cuuint64_t(op.rows), cuuint64_t(op.nseg)};
+    cuuint64_t strides[2] = {cuuint64_t(op.row_stride) * 4, cuuint64_t(op.seg_stride) * 4};
+    r = encode(&op.tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(op.ptr), dims, strides, box, estr,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r == CUDA_SUCCESS) {
+      op.mode = OP_TMA3D;
+      op.cps = int32_t((op.seg_len + 31) / 32);
+    }
+  }
 }
 
 size_t gemm_smem_bytes() { return size_t(kStages) * kStageBytes + sizeof(SmemCtl) + 1024; }

@@ -9,19 +9,30 @@
 //   element (r, k) = ptr[(k / seg_len) * seg_stride + r * row_stride + k % seg_len].
 #pragma once
 
+#include <cuda.h>
 #include <stdint.h>
 
 #include <vector>
 
 namespace spngd {
 
-struct GemmOperand {
+enum OperandMode : int32_t {
+  OP_ASYNC = 0,   // cp.async (LDGSTS) from any layout (fallback)
+  OP_TMA2D = 1,   // TMA 2D box {32 k, 128 rows} of a K-contiguous matrix
+  OP_TMA3D = 2,   // TMA 3D box {32 p, 128 rows, 1 segment}; K = nseg * cps * 32 (zero-padded chunks)
+};
+
+struct alignas(64) GemmOperand {
+  CUtensorMap tmap;   // valid for OP_TMA2D / OP_TMA3D (encoded by finalize_operand)
   const float* ptr;
   int64_t row_stride;
   int64_t seg_len;
   int64_t seg_stride;
-  int32_t rows;   // valid rows; rows >= this read as zero
-  int32_t vec;    // float4 loads legal (set by finalize_operand)
+  int64_t nseg;       // number of segments (OP_TMA3D)
+  int32_t rows;       // valid rows; rows >= this read as zero
+  int32_t vec;        // float4 loads legal (OP_ASYNC)
+  int32_t mode;       // OperandMode
+  int32_t cps;        // 32-wide chunks per segment (OP_TMA3D)
 };
 
 enum GemmEpi : int32_t {
@@ -37,7 +48,7 @@ enum GemmFlags : int32_t {
   FLAG_TRANS = 4,      // EPI_DENSE: also write CT[j*ldct + i]
 };
 
-struct GemmProblem {
+struct alignas(64) GemmProblem {
   GemmOperand A, B;
   int32_t M, N, K;
   int32_t mode;
@@ -88,7 +99,13 @@ constexpr int kTileK = 32;     // fp32 elements per stage = one 128-byte swizzle
 constexpr int kStages = 3;
 constexpr int kGemmThreads = 288;  // 4 A-producer warps, 4 B-producer warps, 1 MMA warp
 
-void finalize_operand(GemmOperand& op);
+// Chooses the operand mode and encodes its TMA descriptor.  `K` is the true
+// K extent; for OP_TMA3D the GEMM must iterate the padded K returned by
+// padded_k().  allow_tma = false forces the cp.async path.
+void finalize_operand(GemmOperand& op, int64_t K = -1, bool allow_tma = true);
+inline int64_t padded_k(const GemmOperand& op, int64_t K) {
+  return op.mode == OP_TMA3D ? op.nseg * op.cps * 32 : K;
+}
 size_t gemm_smem_bytes();
 
 // Launch one grouped GEMM over device-resident problem/work arrays.

@@ -343,7 +343,7 @@ GemmOperand dense_op(const float* ptr, int64_t ld, int64_t rows, int64_t K) {
   o.seg_len = std::max<int64_t>(K, 1);
   o.seg_stride = 0;
   o.rows = int32_t(rows);
-  finalize_operand(o);
+  finalize_operand(o, K);
   return o;
 }
 

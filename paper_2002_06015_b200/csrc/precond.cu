@@ -123,7 +123,7 @@ GemmOperand dense_operand(const float* ptr, int64_t ld, int64_t rows, int64_t K)
   o.row_stride = ld;
   o.seg_len = std::max<int64_t>(K, 1);
   o.rows = int32_t(rows);
-  finalize_operand(o);
+  finalize_operand(o, K);
   return o;
 }
 
