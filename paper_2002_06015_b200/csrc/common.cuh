@@ -142,6 +142,14 @@ __device__ __forceinline__ void tf32_split(float x, float& hi, float& lo) {
   lo = __uint_as_float(l);
 }
 
+// Residual of the hardware's fp32 -> tf32 truncation, rounded to tf32.
+__device__ __forceinline__ float tf32_lo(float x) {
+  const float r = x - __uint_as_float(__float_as_uint(x) & 0xffffe000u);
+  uint32_t l;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(l) : "f"(r));
+  return __uint_as_float(l);
+}
+
 __device__ __forceinline__ int64_t packed_offset(int64_t n, int64_t i, int64_t j) {
   // linalg.hpp:48-51, requires i <= j
   return i * n - i * (i - 1) / 2 + (j - i);

@@ -38,9 +38,29 @@ __global__ void bn_moments_kernel(const spngd_bn_moments_req* __restrict__ reqs)
   r.out3c[3 * ch + 2] = float(sbb * inv_n);
 }
 
+// X'[i][s*hw + p] = X[(s*dim + i)*hw + p]: coalesced reads, runs of hw writes.
+__global__ void repack_kernel(const RepackTask* __restrict__ tasks) {
+  const RepackTask t = tasks[blockIdx.y];
+  const int64_t total = t.n * t.dim * t.hw;
+  for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < total; e += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t p = e % t.hw, row = e / t.hw;
+    const int64_t i = row % t.dim, s = row / t.dim;
+    t.dst[i * (t.n * t.hw) + s * t.hw + p] = t.src[e];
+  }
+}
+
 }  // namespace
 
-int plan_factors(const spngd_factor_req* reqs, int n, FactorPlan& plan) {
+int launch_repack(spngd_ctx* ctx, const RepackTask* d_tasks, int n, int64_t max_elems) {
+  if (n <= 0) return SPNGD_OK;
+  dim3 grid(unsigned(std::min<int64_t>((max_elems + 255) / 256, 2048)), unsigned(n));
+  repack_kernel<<<grid, 256, 0, ctx->stream>>>(d_tasks);
+  SPNGD_CUDA_TRY(cudaGetLastError());
+  ctx->launches++;
+  return SPNGD_OK;
+}
+
+int plan_factors(const spngd_factor_req* reqs, int n, FactorPlan& plan, float* ws) {
   plan = FactorPlan();
   std::vector<std::pair<int64_t, int64_t>> tk;
   for (int i = 0; i < n; ++i) {
@@ -62,8 +82,21 @@ int plan_factors(const spngd_factor_req* reqs, int n, FactorPlan& plan) {
       op.seg_stride = r.dim * r.hw;
     }
     op.rows = int32_t(r.dim);
-    op.nseg = r.layout == 0 ? (r.hi - r.lo) : (r.hi - r.lo);
+    op.nseg = r.hi - r.lo;
     const int64_t K_true = (r.hi - r.lo) * (r.layout == 0 ? 1 : r.hw);
+    const int64_t hw = r.layout == 0 ? 1 : r.hw;
+    if (hw % 4 != 0 && K_true % 4 == 0) {
+      // Row strides of 4*hw bytes defeat TMA (16-byte strides): repack this
+      // capture K-contiguous first and read it as a dense 2D operand.
+      float* dst = ws ? ws + plan.repack_floats : nullptr;
+      plan.repacks.push_back({op.ptr, dst, r.hi - r.lo, r.dim, hw});
+      plan.repack_floats += size_t(round_up(r.dim * K_true, 64));
+      plan.repack_max = std::max(plan.repack_max, r.dim * K_true);
+      op.ptr = dst;
+      op.row_stride = K_true;
+      op.seg_len = K_true;
+      op.seg_stride = 0;
+    }
     finalize_operand(op, K_true);
     // TMA-3D iterates zero-padded 32-wide chunks per sample (padded_k).
     const int64_t K = padded_k(op, K_true);
@@ -122,10 +155,16 @@ extern "C" int spngd_factor_sym_batched(spngd_ctx* ctx, int n, const spngd_facto
   using namespace spngd;
   if (!ctx || (n > 0 && !reqs)) return fail(SPNGD_ERR_INVALID, "spngd_factor_sym_batched: null argument");
   if (n == 0) return SPNGD_OK;
-  FactorPlan plan;
-  int rc = plan_factors(reqs, n, plan);
+  FactorPlan sizing;
+  int rc = plan_factors(reqs, n, sizing);
   if (rc) return rc;
   DeviceScratch scratch(ctx);
+  float* ws = scratch.alloc<float>(std::max<size_t>(sizing.repack_floats, 1));
+  FactorPlan plan;
+  plan_factors(reqs, n, plan, ws);
+  auto* d_repack = scratch.upload(plan.repacks);
+  rc = launch_repack(ctx, d_repack, int(plan.repacks.size()), plan.repack_max);
+  if (rc) return rc;
   auto* d_probs = scratch.upload(plan.probs);
   auto* d_items = scratch.upload(plan.items);
   auto* d_reduce = scratch.upload(plan.reduce);

@@ -7,7 +7,16 @@
 
 namespace spngd {
 
+struct RepackTask {  // conv/FC capture -> K-contiguous dim x (n*hw) matrix
+  const float* src;
+  float* dst;
+  int64_t n, dim, hw;
+};
+
 struct FactorPlan {
+  std::vector<RepackTask> repacks;
+  size_t repack_floats = 0;
+  int64_t repack_max = 0;  // largest element count of one repack
   std::vector<GemmProblem> probs;
   std::vector<GemmWorkItem> items;
   std::vector<SyrkReduceTask> reduce;
@@ -15,7 +24,10 @@ struct FactorPlan {
   int kchunk = 0;
 };
 
-int plan_factors(const spngd_factor_req* reqs, int n, FactorPlan& plan);
+// `ws` receives the repacked captures (sizing pass when null: only
+// repack_floats is meaningful).
+int plan_factors(const spngd_factor_req* reqs, int n, FactorPlan& plan, float* ws = nullptr);
+int launch_repack(spngd_ctx* ctx, const RepackTask* d_tasks, int n, int64_t max_elems);
 int run_factors(spngd_ctx* ctx, const GemmProblem* d_probs, const GemmWorkItem* d_items, int n_items,
                 float* d_partials, const SyrkReduceTask* d_reduce, int n_reduce);
 int launch_bn_moments(spngd_ctx* ctx, const spngd_bn_moments_req* d_reqs, int n, int64_t max_c);

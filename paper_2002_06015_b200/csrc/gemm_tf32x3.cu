@@ -5,8 +5,9 @@
 //   warps 4-7  producers of the B tile (idle on SYRK diagonal tiles)
 //   warp  8    TMEM allocator + single-thread tcgen05.mma issuer
 // Producers read fp32 from HBM/L2 (coalesced float4 when the layout allows),
-// split every element into tf32 hi/lo (x = hi + lo to ~2^-22) and store both
-// into 128B-swizzled K-major smem tiles; the MMA thread issues
+// derive the tf32 lo plane (the raw fp32 tile doubles as the hi operand since
+// the tensor core truncates to tf32) into 128B-swizzled K-major smem tiles;
+// the MMA thread issues
 // hi*hi + hi*lo + lo*hi per 8-wide k step (3xTF32 = fp32-accurate products,
 // SURVEY.md §7.3).  mbarrier full/empty rings pipeline kStages smem stages;
 // tcgen05.commit releases smem slots.
@@ -158,7 +159,7 @@ __device__ __forceinline__ void issue_stage(const GemmOperand& op, int32_t r0, i
 
 __global__ void __launch_bounds__(kGemmThreads, 1)
     gemm_tf32x3_kernel(const GemmProblem* __restrict__ probs, const GemmWorkItem* __restrict__ items,
-                       float* __restrict__ partials, int* status) {
+                       float* __restrict__ partials, int* status, int dbg) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 1024-byte alignment for the SWIZZLE_128B atoms.
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -225,6 +226,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       const int b = j & 1;
       mbar_wait(&ctl->tmem_full[b], (j >> 1) & 1);
       tc_fence_after();
+      if (dbg & 2) {
+        tc_fence_before();
+        mbar_arrive(&ctl->tmem_empty[b]);
+        return;
+      }
       float v[32];
       tmem_ld_32x32b_x32(tmem + lane_base + b * 128 + col_base, v);
 #pragma unroll
@@ -237,8 +243,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     };
     // Raw fp32 tiles land in the hi plane of their slot two stages ahead --
     // by TMA (one elected thread, mbarrier complete_tx) when the layout allows,
-    // else by per-thread cp.async.  Every producer thread then rewrites its
-    // 8 16-byte chunks in place as tf32 hi and writes tf32 lo.
+    // else by per-thread cp.async.  Every producer thread then derives the
+    // tf32 lo plane for its 8 16-byte chunks (the raw plane is the hi operand).
     const int32_t r0 = row0 + rbase;
     const bool tma = op.mode != OP_ASYNC;
     const CUtensorMap* tmap = is_b ? &probs[item.problem].B.tmap : &probs[item.problem].A.tmap;
@@ -267,18 +273,23 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     auto convert = [&](int it) {
       const int slot = it % kStages;
       uint8_t* stage = smem + slot * kStageBytes;
+      // The tensor core reads the top 19 bits of each fp32 word (truncation to
+      // tf32, verified against the fp64 oracle), so the raw tile IS the hi
+      // operand; only lo = rna_tf32(x - trunc_tf32(x)) is written.  Then
+      // x = hi + lo to 2^-22 relative and 3xTF32 products are fp32-accurate.
+      if (!(dbg & 1)) {
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const int r = rbase + 16 * j;
-        const uint32_t off = r * 128 + ((c ^ (r & 7)) << 4);
-        const float4 x = *reinterpret_cast<const float4*>(stage + hi_off + off);
-        float4 h, l;
-        tf32_split(x.x, h.x, l.x);
-        tf32_split(x.y, h.y, l.y);
-        tf32_split(x.z, h.z, l.z);
-        tf32_split(x.w, h.w, l.w);
-        *reinterpret_cast<float4*>(stage + hi_off + off) = h;
-        *reinterpret_cast<float4*>(stage + lo_off + off) = l;
+        for (int j = 0; j < 8; ++j) {
+          const int r = rbase + 16 * j;
+          const uint32_t off = r * 128 + ((c ^ (r & 7)) << 4);
+          const float4 x = *reinterpret_cast<const float4*>(stage + hi_off + off);
+          float4 l;
+          l.x = tf32_lo(x.x);
+          l.y = tf32_lo(x.y);
+          l.z = tf32_lo(x.z);
+          l.w = tf32_lo(x.w);
+          *reinterpret_cast<float4*>(stage + lo_off + off) = l;
+        }
       }
       fence_proxy_async_smem();
       mbar_arrive(&ctl->full[slot]);
@@ -342,9 +353,13 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           const uint32_t koff = kk * 32;  // 8 tf32 = 32 bytes along the swizzled row
           const uint64_t dah = umma_desc_k_sw128(a_hi + koff), dal = umma_desc_k_sw128(a_lo + koff);
           const uint64_t dbh = umma_desc_k_sw128(b_hi + koff), dbl = umma_desc_k_sw128(b_lo + koff);
-          umma_tf32(d, dal, dbh, idesc, kk > 0 ? 1u : 0u);
-          umma_tf32(d, dah, dbl, idesc, 1u);
-          umma_tf32(d, dah, dbh, idesc, 1u);
+          if (!(dbg & 4)) {
+            umma_tf32(d, dal, dbh, idesc, kk > 0 ? 1u : 0u);
+            umma_tf32(d, dah, dbl, idesc, 1u);
+            umma_tf32(d, dah, dbh, idesc, 1u);
+          } else {
+            umma_tf32(d, dah, dbh, idesc, kk > 0 ? 1u : 0u);
+          }
         }
         umma_commit(&ctl->empty[slot]);
         umma_commit(&ctl->tmem_full[b]);
@@ -515,7 +530,8 @@ int launch_gemm(const GemmProblem* d_probs, const GemmWorkItem* d_items, int n_i
     SPNGD_CUDA_TRY(cudaFuncSetAttribute(gemm_tf32x3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     attr_set = true;
   }
-  gemm_tf32x3_kernel<<<n_items, kGemmThreads, smem, stream>>>(d_probs, d_items, d_partials, d_status);
+  static const int dbg = getenv("SPNGD_GEMM_DEBUG") ? atoi(getenv("SPNGD_GEMM_DEBUG")) : 0;
+  gemm_tf32x3_kernel<<<n_items, kGemmThreads, smem, stream>>>(d_probs, d_items, d_partials, d_status, dbg);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     cudaFuncAttributes fa{};

@@ -72,6 +72,7 @@ struct spngd_opt {
   // plans
   FactorPlan fplan;
   GemmProblem* d_fprobs = nullptr; GemmWorkItem* d_fitems = nullptr; SyrkReduceTask* d_freduce = nullptr;
+  RepackTask* d_repack = nullptr;
   float* d_partials = nullptr;
   std::vector<spngd_bn_moments_req> bnm;
   spngd_bn_moments_req* d_bnm = nullptr; int64_t bnm_maxc = 0;
@@ -234,8 +235,13 @@ int build(spngd_opt* o, const spngd_layer_desc* descs, int n) {
   }
   std::vector<void*>& own = o->owned;
   // factor plan (all layers, local shard)
-  int rc = plan_factors(freqs.data(), int(freqs.size()), o->fplan);
+  FactorPlan fsz;
+  int rc = plan_factors(freqs.data(), int(freqs.size()), fsz);
   if (rc) return rc;
+  float* fws = o->alloc(fsz.repack_floats);
+  rc = plan_factors(freqs.data(), int(freqs.size()), o->fplan, fws);
+  if (rc) return rc;
+  o->d_repack = dev_upload(o->fplan.repacks, own);
   o->d_fprobs = dev_upload(o->fplan.probs, own);
   o->d_fitems = dev_upload(o->fplan.items, own);
   o->d_freduce = dev_upload(o->fplan.reduce, own);
@@ -355,6 +361,8 @@ int spngd_opt_step(spngd_opt* o, int64_t step, double eta, double momentum) {
   if (rc) return rc;
   SPNGD_CUDA_TRY(cudaEventRecord(o->ev[0], s));
   // Stages 1-3 local part: factors + BN moments into the RS send buffer.
+  rc = launch_repack(ctx, o->d_repack, int(o->fplan.repacks.size()), o->fplan.repack_max);
+  if (rc) return rc;
   rc = launch_gemm(o->d_fprobs, o->d_fitems, int(o->fplan.items.size()), o->d_partials, ctx->d_status, s);
   if (rc) return rc;
   ctx->launches++;
