@@ -227,6 +227,22 @@ typedef struct spngd_opt_config {
   int64_t batch;       /* per-rank micro-batch M/K */
 } spngd_opt_config;
 
+/* Host-only planning of the hybrid schedule (no GPU needed): layer owners
+ * (LPT on a^3 + g^3 + 2 g^2 a + 2 g a^2; the reference uses li % K,
+ * dist.cpp:147-153 -- ownership never changes numerics) and the owner-major
+ * segment offsets (floats) of every payload in the reduce-scatter buffer
+ * (A, G packed; BN 3c moments; dW g*a or 2c) and the all-gather buffer
+ * (W g*a or gamma|beta 2c).  -1 marks payloads a layer does not have.
+ * seg_rs / seg_ag: padded per-owner segment sizes. */
+typedef struct spngd_layout_entry {
+  int32_t owner;
+  int32_t pad_;
+  int64_t off_A, off_G, off_M, off_dW;
+  int64_t off_W;
+} spngd_layout_entry;
+int spngd_plan_layout(const spngd_layer_desc* layers, int n_layers, int world, spngd_layout_entry* out,
+                      int64_t* seg_rs, int64_t* seg_ag);
+
 typedef struct spngd_opt spngd_opt;
 
 int spngd_opt_create(spngd_ctx* ctx, const spngd_layer_desc* layers, int n_layers,

@@ -56,6 +56,11 @@ class LayerDesc(C.Structure):
     _fields_ = [("kind", C.c_int32), ("pad_", C.c_int32), ("a", _i64), ("g", _i64), ("hw", _i64)]
 
 
+class LayoutEntry(C.Structure):
+    _fields_ = [("owner", C.c_int32), ("pad_", C.c_int32), ("off_A", _i64), ("off_G", _i64),
+                ("off_M", _i64), ("off_dW", _i64), ("off_W", _i64)]
+
+
 class OptConfig(C.Structure):
     _fields_ = [("lambda_", C.c_double), ("rescale", C.c_int32), ("stale", C.c_int32),
                 ("stale_alpha", C.c_double), ("batch", _i64)]
@@ -78,7 +83,7 @@ EXPORTS = [
     "spngd_stat_distance_batched", "spngd_tracker_create", "spngd_tracker_destroy",
     "spngd_tracker_should_refresh", "spngd_tracker_on_refresh", "spngd_tracker_state",
     "spngd_nccl_unique_id", "spngd_ctx_init_comm", "spngd_reduce_scatter_mean", "spngd_all_gather",
-    "spngd_opt_create", "spngd_opt_destroy", "spngd_opt_buffer", "spngd_opt_owner", "spngd_opt_step",
+    "spngd_plan_layout", "spngd_opt_create", "spngd_opt_destroy", "spngd_opt_buffer", "spngd_opt_owner", "spngd_opt_step",
     "spngd_opt_phase_ms", "spngd_opt_launch_count",
 ]
 
@@ -135,6 +140,8 @@ def _declare(L):
         "spngd_ctx_init_comm": (C.c_int, [P, C.c_int, C.c_int, P]),
         "spngd_reduce_scatter_mean": (C.c_int, [P, P, P, _i64]),
         "spngd_all_gather": (C.c_int, [P, P, P, _i64]),
+        "spngd_plan_layout": (C.c_int, [C.POINTER(LayerDesc), C.c_int, C.c_int, C.POINTER(LayoutEntry),
+                                        C.POINTER(_i64), C.POINTER(_i64)]),
         "spngd_opt_create": (C.c_int, [P, C.POINTER(LayerDesc), C.c_int, C.POINTER(OptConfig),
                                        C.POINTER(P)]),
         "spngd_opt_destroy": (None, [P]),

@@ -114,42 +114,20 @@ double layer_cost(const spngd_layer_desc& d) {
 
 int build(spngd_opt* o, const spngd_layer_desc* descs, int n) {
   const int W = o->world;
-  // ---- ownership: LPT on inverse + precondition cost
-  std::vector<int> order(n);
-  std::iota(order.begin(), order.end(), 0);
-  std::stable_sort(order.begin(), order.end(),
-                   [&](int x, int y) { return layer_cost(descs[x]) > layer_cost(descs[y]); });
-  std::vector<double> load(W, 0.0);
+  std::vector<spngd_layout_entry> lay(n);
+  int rc0 = spngd_plan_layout(descs, n, W, lay.data(), &o->seg_rs, &o->seg_ag);
+  if (rc0) return rc0;
   o->layers.resize(n);
-  for (int li : order) {
-    const int r = int(std::min_element(load.begin(), load.end()) - load.begin());
-    o->layers[li].owner = r;
-    load[r] += layer_cost(descs[li]);
-  }
-  // ---- owner-major segment layout (64-float aligned entries)
-  std::vector<int64_t> rs_fill(W, 0), ag_fill(W, 0);
-  auto place = [](int64_t& fill, int64_t n) {
-    const int64_t off = fill;
-    fill += round_up(n, 64);
-    return off;
-  };
   for (int li = 0; li < n; ++li) {
     LayerState& L = o->layers[li];
     L.d = descs[li];
-    const int r = L.owner;
-    if (L.d.kind == SPNGD_BN) {
-      L.off_M = place(rs_fill[r], 3 * L.d.g);
-      L.off_dW = place(rs_fill[r], 2 * L.d.g);
-      L.off_W = place(ag_fill[r], 2 * L.d.g);
-    } else {
-      L.off_A = place(rs_fill[r], L.d.a * (L.d.a + 1) / 2);
-      L.off_G = place(rs_fill[r], L.d.g * (L.d.g + 1) / 2);
-      L.off_dW = place(rs_fill[r], L.d.g * L.d.a);
-      L.off_W = place(ag_fill[r], L.d.g * L.d.a);
-    }
+    L.owner = lay[li].owner;
+    L.off_A = lay[li].off_A;
+    L.off_G = lay[li].off_G;
+    L.off_M = lay[li].off_M;
+    L.off_dW = lay[li].off_dW;
+    L.off_W = lay[li].off_W;
   }
-  o->seg_rs = std::max<int64_t>(64, *std::max_element(rs_fill.begin(), rs_fill.end()));
-  o->seg_ag = std::max<int64_t>(64, *std::max_element(ag_fill.begin(), ag_fill.end()));
   o->rs_send = o->alloc(size_t(W) * o->seg_rs, true);
   o->rs_recv = (W == 1) ? o->rs_send : o->alloc(o->seg_rs, true);
   o->ag = o->alloc(size_t(W) * o->seg_ag, true);
@@ -294,6 +272,49 @@ int set_update_scalars(spngd_opt* o, double eta, double momentum) {
 }  // namespace
 
 extern "C" {
+
+int spngd_plan_layout(const spngd_layer_desc* descs, int n, int W, spngd_layout_entry* out, int64_t* seg_rs,
+                      int64_t* seg_ag) {
+  if (!descs || !out || n <= 0 || W < 1) return fail(SPNGD_ERR_INVALID, "spngd_plan_layout: bad argument");
+  // ownership: LPT on inverse + precondition cost, deterministic tie-break
+  std::vector<int> order(n);
+  std::iota(order.begin(), order.end(), 0);
+  std::stable_sort(order.begin(), order.end(),
+                   [&](int x, int y) { return layer_cost(descs[x]) > layer_cost(descs[y]); });
+  std::vector<double> load(W, 0.0);
+  for (int li : order) {
+    const int r = int(std::min_element(load.begin(), load.end()) - load.begin());
+    out[li].owner = r;
+    load[r] += layer_cost(descs[li]);
+  }
+  // owner-major segment layout, 64-float aligned entries, in layer order
+  std::vector<int64_t> rs_fill(W, 0), ag_fill(W, 0);
+  auto place = [](int64_t& fill, int64_t cnt) {
+    const int64_t off = fill;
+    fill += round_up(cnt, 64);
+    return off;
+  };
+  for (int li = 0; li < n; ++li) {
+    spngd_layout_entry& e = out[li];
+    const spngd_layer_desc& d = descs[li];
+    const int r = e.owner;
+    e.pad_ = 0;
+    e.off_A = e.off_G = e.off_M = -1;
+    if (d.kind == SPNGD_BN) {
+      e.off_M = place(rs_fill[r], 3 * d.g);
+      e.off_dW = place(rs_fill[r], 2 * d.g);
+      e.off_W = place(ag_fill[r], 2 * d.g);
+    } else {
+      e.off_A = place(rs_fill[r], d.a * (d.a + 1) / 2);
+      e.off_G = place(rs_fill[r], d.g * (d.g + 1) / 2);
+      e.off_dW = place(rs_fill[r], d.g * d.a);
+      e.off_W = place(ag_fill[r], d.g * d.a);
+    }
+  }
+  if (seg_rs) *seg_rs = std::max<int64_t>(64, *std::max_element(rs_fill.begin(), rs_fill.end()));
+  if (seg_ag) *seg_ag = std::max<int64_t>(64, *std::max_element(ag_fill.begin(), ag_fill.end()));
+  return SPNGD_OK;
+}
 
 int spngd_opt_create(spngd_ctx* ctx, const spngd_layer_desc* layers, int n_layers, const spngd_opt_config* cfg,
                      spngd_opt** out) {

@@ -28,6 +28,24 @@ def _mix(*xs) -> int:
     return h
 
 
+def layer_descs(layers: List[Layer]):
+    descs = []
+    for l in layers:
+        kind = {"fc": 0, "conv": 1, "bn": 2}[l.kind]
+        descs.append(N.LayerDesc(kind, 0, l.a if l.kind != "bn" else 0, l.g, l.hw if l.kind == "conv" else 1))
+    return (N.LayerDesc * len(descs))(*descs)
+
+
+def plan_layout(layers: List[Layer], world: int):
+    """Owners and owner-major RS/AG offsets (spngd_plan_layout, host only)."""
+    arr = layer_descs(layers)
+    out = (N.LayoutEntry * len(layers))()
+    seg_rs, seg_ag = C.c_int64(), C.c_int64()
+    check(N.lib().spngd_plan_layout(arr, len(layers), world, out, C.byref(seg_rs), C.byref(seg_ag)))
+    return [dict(owner=e.owner, A=e.off_A, G=e.off_G, M=e.off_M, dW=e.off_dW, W=e.off_W) for e in out], \
+        seg_rs.value, seg_ag.value
+
+
 class Comm:
     """NCCL communicator bootstrap: rank 0's unique id is shared by the caller
     (torch.distributed object broadcast), then spngd_ctx_init_comm."""
@@ -50,14 +68,10 @@ class Optimizer:
         check(L.spngd_ctx_create(device, stream, C.byref(self.ctx)))
         if world > 1:
             check(L.spngd_ctx_init_comm(self.ctx, world, rank, C.create_string_buffer(nccl_id, 128)))
-        descs = []
-        for l in layers:
-            kind = {"fc": 0, "conv": 1, "bn": 2}[l.kind]
-            descs.append(N.LayerDesc(kind, 0, l.a if l.kind != "bn" else 0, l.g, l.hw if l.kind == "conv" else 1))
-        arr = (N.LayerDesc * len(descs))(*descs)
+        arr = layer_descs(layers)
         cfg = N.OptConfig(lam, int(rescale), 0, 0.1, batch)
         self.h = C.c_void_p()
-        check(L.spngd_opt_create(self.ctx, arr, len(descs), C.byref(cfg), C.byref(self.h)))
+        check(L.spngd_opt_create(self.ctx, arr, len(layers), C.byref(cfg), C.byref(self.h)))
 
     def close(self):
         L = N.lib()

@@ -1,0 +1,84 @@
+"""K-invariance of the NCCL path (tests/test_dist.cpp:363-387 analogue).
+
+torchrun --nproc-per-node 2 scripts/multi_gpu_check.py
+Every rank runs one step at P = 2 on its own shard; rank 0 then replays the
+same step at P = 1 over the concatenated batch (mean dW) and compares all
+updated weights.  Replicas must be bit-identical across ranks.  Exit 0 on pass.
+"""
+import os
+import sys
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2002_06015_b200 import workloads as W  # noqa: E402
+from paper_2002_06015_b200.step import ACT, BN_GB, BN_GG, DW, GRAD, V, Comm, Optimizer  # noqa: E402
+from paper_2002_06015_b200.step import W as WB  # noqa: E402
+
+LAYERS = [W.conv(16, 32, 3, 1, 16), W.bn(32), W.conv(32, 64, 3, 2, 16), W.bn(64), W.conv(64, 128, 3, 1, 8),
+          W.bn(128), W.conv(128, 256, 3, 2, 8), W.bn(256), W.fc(1024, 10)]
+B = 8
+
+
+def main():
+    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    dist.init_process_group("gloo")
+    obj = [Comm.unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0)
+    opt = Optimizer(LAYERS, B, device=local, world=world, rank=rank, nccl_id=obj[0])
+    opt.synth(seed=11)
+    inputs = {}
+    for li, l in enumerate(LAYERS):
+        ws = [BN_GG, BN_GB, DW] if l.kind == "bn" else [ACT, GRAD, DW]
+        inputs[li] = {w: opt.download(li, w).numpy() for w in ws}
+        inputs[li][WB] = opt.download(li, WB).numpy()
+        if opt.owner(li) == rank:
+            inputs[li][V] = opt.download(li, V).numpy()
+    opt.step(1)
+    opt.sync()
+    after = [opt.download(li, WB).numpy() for li in range(len(LAYERS))]
+    owners = [opt.owner(li) for li in range(len(LAYERS))]
+    gathered = [None] * world
+    dist.all_gather_object(gathered, (inputs, after))
+    ok = True
+    if rank == 0:
+        for r in range(1, world):
+            for li in range(len(LAYERS)):
+                if not np.array_equal(gathered[r][1][li], after[li]):
+                    print(f"replica mismatch rank {r} layer {li}")
+                    ok = False
+        ref = Optimizer(LAYERS, B * world, device=local)
+        for li, l in enumerate(LAYERS):
+            ws = [BN_GG, BN_GB] if l.kind == "bn" else [ACT, GRAD]
+            for w in ws:
+                ref.upload(li, w, torch.from_numpy(np.concatenate([gathered[r][0][li][w] for r in range(world)])))
+            ref.upload(li, DW, torch.from_numpy(np.mean([gathered[r][0][li][DW] for r in range(world)], axis=0)))
+            ref.upload(li, WB, torch.from_numpy(inputs[li][WB]))
+            vown = gathered[owners[li]][0][li][V]
+            ref.upload(li, V, torch.from_numpy(vown))
+        ref.step(1)
+        ref.sync()
+        worst = 0.0
+        for li in range(len(LAYERS)):
+            want = ref.download(li, WB).numpy().astype(np.float64)
+            err = np.linalg.norm(after[li] - want) / np.linalg.norm(want)
+            worst = max(worst, err)
+            print(f"layer {li} {LAYERS[li].kind} owner {owners[li]} rel {err:.2e}")
+        ok = ok and worst <= 1e-4
+        ph = opt.phase_ms()
+        print("phases", {k: round(v, 3) for k, v in ph.items()})
+        print("PASS" if ok else "FAIL", f"worst {worst:.2e}")
+        ref.close()
+    opt.close()
+    t = torch.tensor([1 if ok else 0])
+    dist.broadcast(t, 0)
+    dist.destroy_process_group()
+    sys.exit(0 if t.item() else 1)
+
+
+if __name__ == "__main__":
+    main()
