@@ -423,6 +423,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       // Tile of P^T: rows = a-index (M = a), cols = g-index.  W is g x a
       // row-major, so element (i = n0+c, j = m0+r) lives at W[i*a + j].
       const int64_t a = prob.M;
+      const float eta = prob.scal ? prob.scal[0] : prob.eta;
+      const float mom = prob.scal ? prob.scal[1] : prob.momentum;
       double ss = 0.0;
       for (int idx = tid; idx < kTileM * kTileN; idx += nthr) {
         const int c = idx >> 7, r = idx & 127;
@@ -433,7 +435,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           if (prob.P_out) prob.P_out[w_idx] = p;
           if (prob.W) {
             const float w = prob.W[w_idx], vel = prob.V[w_idx];
-            const float nw = w - prob.eta * p + prob.momentum * vel;  // fisher.cpp:332
+            const float nw = w - eta * p + mom * vel;  // fisher.cpp:332
             prob.W[w_idx] = nw;
             prob.V[w_idx] = nw - w;                                   // fisher.cpp:333
             ss += double(nw) * double(nw);

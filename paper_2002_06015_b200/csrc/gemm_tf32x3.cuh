@@ -67,6 +67,7 @@ struct alignas(64) GemmProblem {
   float* P_out;
   double* norm2;
   float eta, momentum;
+  const float* scal;   // optional device {eta, momentum}, overrides the fields above
 };
 
 enum KTri : int32_t {

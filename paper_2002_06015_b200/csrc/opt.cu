@@ -78,8 +78,21 @@ struct spngd_opt {
   spngd_bn_moments_req* d_bnm = nullptr; int64_t bnm_maxc = 0;
   std::vector<PiTask> pis; PiTask* d_pis = nullptr;
   std::vector<UnpackTask> unpacks; UnpackTask* d_unpacks = nullptr; int64_t max_n = 0;
-  InversePlan iplan;
-  GemmProblem* d_iprobs = nullptr; GemmWorkItem* d_iitems = nullptr; BaseTask* d_ibases = nullptr;
+  struct InvClass {  // one recursion schedule per matrix size class, on its own stream
+    InversePlan plan;
+    GemmProblem* d_probs = nullptr;
+    GemmWorkItem* d_items = nullptr;
+    BaseTask* d_bases = nullptr;
+    cudaStream_t stream = nullptr;
+    cudaEvent_t done = nullptr;
+  };
+  std::vector<InvClass> inv;
+  cudaEvent_t inv_fork = nullptr;
+  float* d_scal = nullptr;         // {eta, momentum} read by the update kernels
+  cudaGraph_t graphs[6] = {};
+  cudaGraphExec_t graph_exec[6] = {};
+  bool use_graph = true;
+  bool graphs_ready = false;
   PrecondPlan pplan;
   GemmProblem *d_p1 = nullptr, *d_p2 = nullptr; GemmWorkItem *d_i1 = nullptr, *d_i2 = nullptr;
   RescaleTask* d_rescale = nullptr; double* d_norms = nullptr;
@@ -98,6 +111,15 @@ struct spngd_opt {
     return static_cast<float*>(p);
   }
   ~spngd_opt() {
+    for (int i = 0; i < 6; ++i) {
+      if (graph_exec[i]) cudaGraphExecDestroy(graph_exec[i]);
+      if (graphs[i]) cudaGraphDestroy(graphs[i]);
+    }
+    for (auto& c : inv) {
+      if (c.done) cudaEventDestroy(c.done);
+      if (c.stream) cudaStreamDestroy(c.stream);
+    }
+    if (inv_fork) cudaEventDestroy(inv_fork);
     for (auto& e : ev)
       if (e) cudaEventDestroy(e);
     for (void* p : owned) cudaFree(p);
@@ -227,20 +249,41 @@ int build(spngd_opt* o, const spngd_layer_desc* descs, int n) {
   o->d_bnm = dev_upload(o->bnm, own);
   o->d_pis = dev_upload(o->pis, own);
   o->d_unpacks = dev_upload(o->unpacks, own);
-  // inverse plan
-  InversePlan sizing;
-  plan_inverse(mats, nullptr, sizing);
-  float* ws = o->alloc(sizing.workspace_floats);
-  plan_inverse(mats, ws, o->iplan);
-  o->d_iprobs = dev_upload(o->iplan.probs, own);
-  o->d_iitems = dev_upload(o->iplan.items, own);
-  o->d_ibases = dev_upload(o->iplan.bases, own);
+  // inverse plans: one per matrix size class (owned matrices of equal n share
+  // identical recursion schedules and batch into the same launches); classes
+  // run concurrently on their own streams.
+  {
+    std::vector<int64_t> sizes;
+    for (const auto& m : mats) sizes.push_back(m.n);
+    std::sort(sizes.begin(), sizes.end());
+    sizes.erase(std::unique(sizes.begin(), sizes.end()), sizes.end());
+    std::reverse(sizes.begin(), sizes.end());  // largest (critical path) first
+    for (int64_t n : sizes) {
+      std::vector<DenseMatrix> cls;
+      for (const auto& m : mats)
+        if (m.n == n) cls.push_back(m);
+      o->inv.emplace_back();
+      spngd_opt::InvClass& c = o->inv.back();
+      InversePlan sizing;
+      plan_inverse(cls, nullptr, sizing);
+      float* ws = o->alloc(sizing.workspace_floats);
+      plan_inverse(cls, ws, c.plan);
+      c.d_probs = dev_upload(c.plan.probs, own);
+      c.d_items = dev_upload(c.plan.items, own);
+      c.d_bases = dev_upload(c.plan.bases, own);
+      SPNGD_CUDA_TRY(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
+      SPNGD_CUDA_TRY(cudaEventCreateWithFlags(&c.done, cudaEventDisableTiming));
+    }
+    SPNGD_CUDA_TRY(cudaEventCreateWithFlags(&o->inv_fork, cudaEventDisableTiming));
+  }
+  o->d_scal = o->alloc(2);
+  o->use_graph = getenv("SPNGD_NO_GRAPH") == nullptr;
   // precondition plan
   PrecondPlan psz;
   rc = plan_precondition(preqs.data(), int(preqs.size()), 0.0, 0.0, nullptr, nullptr, psz);
   if (rc) return rc;
   float* ptmp = o->alloc(psz.tmp_floats);
-  rc = plan_precondition(preqs.data(), int(preqs.size()), 0.0, 0.0, ptmp, o->d_norms, o->pplan);
+  rc = plan_precondition(preqs.data(), int(preqs.size()), 0.0, 0.0, ptmp, o->d_norms, o->pplan, o->d_scal);
   if (rc) return rc;
   o->d_p1 = dev_upload(o->pplan.probs1, own);
   o->d_i1 = dev_upload(o->pplan.items1, own);
@@ -250,22 +293,6 @@ int build(spngd_opt* o, const spngd_layer_desc* descs, int n) {
   o->d_bnu = dev_upload(o->bnu, own);
   for (auto& e : o->ev) SPNGD_CUDA_TRY(cudaEventCreate(&e));
   SPNGD_CUDA_TRY(cudaDeviceSynchronize());
-  return SPNGD_OK;
-}
-
-// Rewrites eta/momentum into the device-resident EPI_UPDATE problems.
-int set_update_scalars(spngd_opt* o, double eta, double momentum) {
-  bool changed = false;
-  for (auto& p : o->pplan.probs2) {
-    if (p.eta != float(eta) || p.momentum != float(momentum)) {
-      p.eta = float(eta);
-      p.momentum = float(momentum);
-      changed = true;
-    }
-  }
-  if (changed && o->d_p2)
-    SPNGD_CUDA_TRY(cudaMemcpyAsync(o->d_p2, o->pplan.probs2.data(), o->pplan.probs2.size() * sizeof(GemmProblem),
-                                   cudaMemcpyHostToDevice, o->ctx->stream));
   return SPNGD_OK;
 }
 
@@ -372,51 +399,100 @@ float* spngd_opt_buffer(spngd_opt* o, int layer, int which, int64_t* ld) {
   }
 }
 
+}  // extern "C"
+
+namespace {
+
+// The six phases of one step.  Each phase is captured once into its own CUDA
+// graph; phase events are recorded between graph launches.
+int issue_phase(spngd_opt* o, int phase) {
+  spngd_ctx* ctx = o->ctx;
+  cudaStream_t s = ctx->stream;
+  int rc = SPNGD_OK;
+  switch (phase) {
+    case 0:  // Stages 1-3 local part: factor SYRK into the RS send buffer.
+      rc = launch_repack(ctx, o->d_repack, int(o->fplan.repacks.size()), o->fplan.repack_max);
+      if (rc) return rc;
+      rc = launch_gemm(o->d_fprobs, o->d_fitems, int(o->fplan.items.size()), o->d_partials, ctx->d_status, s);
+      ctx->launches++;
+      return rc;
+    case 1:  // split-K reduction + BN moments.
+      rc = launch_syrk_reduce(o->d_freduce, int(o->fplan.reduce.size()), o->d_partials, s);
+      ctx->launches += !o->fplan.reduce.empty();
+      if (!rc) rc = launch_bn_moments(ctx, o->d_bnm, int(o->bnm.size()), o->bnm_maxc);
+      return rc;
+    case 2:  // Stages 2-3: ReduceScatterV of A, G/F and grads (dist.cpp:510-537).
+      if (o->world > 1) rc = spngd_reduce_scatter_mean(ctx, o->rs_send, o->rs_recv, o->seg_rs);
+      return rc;
+    case 3: {  // Stage 4a: pi, damping, inverse (dist.cpp:539-602); size classes
+               // fork onto their own streams and join.
+      rc = launch_pi(ctx, o->d_pis, int(o->pis.size()));
+      if (!rc) rc = launch_unpack(ctx, o->d_unpacks, int(o->unpacks.size()), o->max_n);
+      if (rc) return rc;
+      SPNGD_CUDA_TRY(cudaEventRecord(o->inv_fork, s));
+      for (auto& c : o->inv) {
+        SPNGD_CUDA_TRY(cudaStreamWaitEvent(c.stream, o->inv_fork, 0));
+        ctx->stream = c.stream;
+        rc = run_inverse(ctx, c.plan, c.d_probs, c.d_items, c.d_bases);
+        ctx->stream = s;
+        if (rc) return rc;
+        SPNGD_CUDA_TRY(cudaEventRecord(c.done, c.stream));
+        SPNGD_CUDA_TRY(cudaStreamWaitEvent(s, c.done, 0));
+      }
+      return SPNGD_OK;
+    }
+    case 4:  // Stage 4b: precondition + update + rescale, BN solve + update (dist.cpp:604-633).
+      rc = run_precondition(ctx, o->pplan, o->d_p1, o->d_i1, o->d_p2, o->d_i2, o->d_rescale, o->d_norms);
+      if (!rc)
+        rc = launch_bn_update(ctx, o->d_bnu, int(o->bnu.size()), o->bnu_maxc, o->cfg.lambda, 0.0, 0.0, o->d_scal);
+      return rc;
+    case 5:  // Stage 5: AllGatherV of the updated weights (dist.cpp:646-663), in place.
+      if (o->world > 1) rc = spngd_all_gather(ctx, o->ag + int64_t(o->rank) * o->seg_ag, o->ag, o->seg_ag);
+      return rc;
+  }
+  return SPNGD_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
 int spngd_opt_step(spngd_opt* o, int64_t step, double eta, double momentum) {
   if (!o) return fail(SPNGD_ERR_INVALID, "spngd_opt_step: opt is NULL");
   (void)step;
   spngd_ctx* ctx = o->ctx;
   cudaStream_t s = ctx->stream;
+  // Host scalars of this step -> device (outside the graphs).  Pageable
+  // source: staged before cudaMemcpyAsync returns, so no host sync.
+  const float scal[2] = {float(eta), float(momentum)};
+  SPNGD_CUDA_TRY(cudaMemcpyAsync(o->d_scal, scal, sizeof(scal), cudaMemcpyHostToDevice, s));
+  const bool capture = o->use_graph && !o->graphs_ready;
   const int64_t l0 = ctx->launches;
-  int rc = set_update_scalars(o, eta, momentum);
-  if (rc) return rc;
-  SPNGD_CUDA_TRY(cudaEventRecord(o->ev[0], s));
-  // Stages 1-3 local part: factors + BN moments into the RS send buffer.
-  rc = launch_repack(ctx, o->d_repack, int(o->fplan.repacks.size()), o->fplan.repack_max);
-  if (rc) return rc;
-  rc = launch_gemm(o->d_fprobs, o->d_fitems, int(o->fplan.items.size()), o->d_partials, ctx->d_status, s);
-  if (rc) return rc;
-  ctx->launches++;
-  SPNGD_CUDA_TRY(cudaEventRecord(o->ev[1], s));
-  rc = launch_syrk_reduce(o->d_freduce, int(o->fplan.reduce.size()), o->d_partials, s);
-  ctx->launches += !o->fplan.reduce.empty();
-  if (!rc) rc = launch_bn_moments(ctx, o->d_bnm, int(o->bnm.size()), o->bnm_maxc);
-  if (rc) return rc;
-  SPNGD_CUDA_TRY(cudaEventRecord(o->ev[2], s));
-  // Stages 2-3: ReduceScatterV of A, G/F and grads (dist.cpp:510-537).
-  if (o->world > 1) {
-    rc = spngd_reduce_scatter_mean(ctx, o->rs_send, o->rs_recv, o->seg_rs);
-    if (rc) return rc;
-  }
-  SPNGD_CUDA_TRY(cudaEventRecord(o->ev[3], s));
-  // Stage 4a: pi, damping, inverse (dist.cpp:539-602).
-  rc = launch_pi(ctx, o->d_pis, int(o->pis.size()));
-  if (!rc) rc = launch_unpack(ctx, o->d_unpacks, int(o->unpacks.size()), o->max_n);
-  if (!rc) rc = run_inverse(ctx, o->iplan, o->d_iprobs, o->d_iitems, o->d_ibases);
-  if (rc) return rc;
-  SPNGD_CUDA_TRY(cudaEventRecord(o->ev[4], s));
-  // Stage 4b: precondition + update + rescale, BN solve + update (dist.cpp:604-633).
-  rc = run_precondition(ctx, o->pplan, o->d_p1, o->d_i1, o->d_p2, o->d_i2, o->d_rescale, o->d_norms);
-  if (!rc) rc = launch_bn_update(ctx, o->d_bnu, int(o->bnu.size()), o->bnu_maxc, o->cfg.lambda, eta, momentum);
-  if (rc) return rc;
-  SPNGD_CUDA_TRY(cudaEventRecord(o->ev[5], s));
-  // Stage 5: AllGatherV of the updated weights (dist.cpp:646-663), in place.
-  if (o->world > 1) {
-    rc = spngd_all_gather(ctx, o->ag + int64_t(o->rank) * o->seg_ag, o->ag, o->seg_ag);
-    if (rc) return rc;
+  for (int ph = 0; ph < 6; ++ph) {
+    SPNGD_CUDA_TRY(cudaEventRecord(o->ev[ph], s));
+    if (!o->use_graph) {
+      int rc = issue_phase(o, ph);
+      if (rc) return rc;
+      continue;
+    }
+    if (capture) {
+      SPNGD_CUDA_TRY(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+      int rc = issue_phase(o, ph);
+      cudaGraph_t g = nullptr;
+      cudaError_t e = cudaStreamEndCapture(s, &g);
+      if (rc) {
+        if (g) cudaGraphDestroy(g);
+        return rc;
+      }
+      if (e != cudaSuccess) return fail_cuda(e, "cudaStreamEndCapture");
+      o->graphs[ph] = g;
+      SPNGD_CUDA_TRY(cudaGraphInstantiate(&o->graph_exec[ph], g, 0));
+    }
+    SPNGD_CUDA_TRY(cudaGraphLaunch(o->graph_exec[ph], s));
   }
   SPNGD_CUDA_TRY(cudaEventRecord(o->ev[6], s));
-  o->launches = ctx->launches - l0;
+  if (capture || !o->use_graph) o->launches = ctx->launches - l0;
+  o->graphs_ready = o->use_graph;
   o->timed = true;
   return SPNGD_OK;
 }

@@ -49,7 +49,11 @@ __global__ void rescale_kernel(const RescaleTask* __restrict__ tasks) {
 }
 
 __global__ void bn_update_kernel(const spngd_bn_update_req* __restrict__ reqs, double lambda, double eta,
-                                 double momentum, int* status) {
+                                 double momentum, const float* scal, int* status) {
+  if (scal) {
+    eta = scal[0];
+    momentum = scal[1];
+  }
   const spngd_bn_update_req r = reqs[blockIdx.y];
   const int64_t ch = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (ch >= r.c) return;
@@ -130,7 +134,7 @@ GemmOperand dense_operand(const float* ptr, int64_t ld, int64_t rows, int64_t K)
 }  // namespace
 
 int plan_precondition(const spngd_precond_req* reqs, int n, double eta, double momentum, float* tmp,
-                      double* norms, PrecondPlan& plan) {
+                      double* norms, PrecondPlan& plan, const float* scal) {
   plan = PrecondPlan();
   size_t off = 0;
   for (int i = 0; i < n; ++i) {
@@ -155,6 +159,7 @@ int plan_precondition(const spngd_precond_req* reqs, int n, double eta, double m
     p2.mode = EPI_UPDATE; p2.alpha = 1.f;
     p2.W = r.W; p2.V = r.V; p2.P_out = r.P_out;
     p2.eta = float(eta); p2.momentum = float(momentum);
+    p2.scal = scal;
     p2.norm2 = (r.W && r.rescale && norms) ? norms + i : nullptr;
     const int idx = int(plan.probs1.size());
     plan.probs1.push_back(p1);
@@ -193,10 +198,10 @@ int run_precondition(spngd_ctx* ctx, const PrecondPlan& plan, const GemmProblem*
 }
 
 int launch_bn_update(spngd_ctx* ctx, const spngd_bn_update_req* d_reqs, int n, int64_t max_c, double lambda,
-                     double eta, double momentum) {
+                     double eta, double momentum, const float* scal) {
   if (n <= 0) return SPNGD_OK;
   dim3 grid(unsigned((max_c + 255) / 256), unsigned(n));
-  bn_update_kernel<<<grid, 256, 0, ctx->stream>>>(d_reqs, lambda, eta, momentum, ctx->d_status);
+  bn_update_kernel<<<grid, 256, 0, ctx->stream>>>(d_reqs, lambda, eta, momentum, scal, ctx->d_status);
   SPNGD_CUDA_TRY(cudaGetLastError());
   ctx->launches++;
   return SPNGD_OK;
