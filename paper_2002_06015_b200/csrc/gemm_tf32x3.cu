@@ -1,9 +1,10 @@
 // sm_100a grouped 3xTF32 GEMM on tcgen05 tensor cores with TMEM accumulators.
 //
-// CTA layout (288 threads, one CTA per SM):
-//   warps 0-3  producers of the A tile (128 rows x 32 k per stage)
-//   warps 4-7  producers of the B tile (idle on SYRK diagonal tiles)
-//   warp  8    TMEM allocator + single-thread tcgen05.mma issuer
+// CTA layout (512 threads, one CTA per SM):
+//   warps 0-3   producers of the A tile (128 rows x 32 k per stage)
+//   warps 4-7   producers of the B tile (idle on SYRK diagonal tiles)
+//   warps 8-15  accumulator drain (TMEM -> round-to-nearest fp32 registers);
+//               warp 8 also allocates TMEM and issues tcgen05.mma (one lane)
 // Producers read fp32 from HBM/L2 (coalesced float4 when the layout allows),
 // derive the tf32 lo plane (the raw fp32 tile doubles as the hi operand since
 // the tensor core truncates to tf32) into 128B-swizzled K-major smem tiles;
@@ -34,9 +35,10 @@ namespace spngd {
 namespace {
 
 constexpr int kOperandBytes = kTileM * kTileK * 4;     // 16 KB (128 rows x 128 B)
-constexpr int kStageBytes = 4 * kOperandBytes;         // Ahi, Alo, Bhi, Blo
+constexpr int kStageBytes = 3 * kOperandBytes;         // A raw, B raw (= B hi), B lo
 constexpr int kEpiStride = kTileN + 1;                 // padded fp32 tile row
-constexpr int kTmemCols = 256;  // two 128-column accumulators
+constexpr int kTmemCols = 512;  // 2 x 128 accumulator columns + kStages x (A hi | A lo) x 32
+constexpr uint32_t kTmemA = 256;                       // first A-operand column
 
 struct __align__(8) SmemCtl {
   uint64_t full[kStages];
@@ -159,7 +161,10 @@ __device__ __forceinline__ void issue_stage(const GemmOperand& op, int32_t r0, i
 
 __global__ void __launch_bounds__(kGemmThreads, 1)
     gemm_tf32x3_kernel(const GemmProblem* __restrict__ probs, const GemmWorkItem* __restrict__ items,
-                       float* __restrict__ partials, int* status, int dbg) {
+                       float* __restrict__ partials, int* status, int dbg, long long* trace) {
+  // trace (debug): for CTAs < 4, stages < 64: [cta][stage][4] clock64 stamps
+  // {A TMA issued, A raw landed, MMA saw full, drain saw MMA done}.
+  long long* tr = (trace && blockIdx.x < 4) ? trace + blockIdx.x * 64 * 4 : nullptr;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 1024-byte alignment for the SWIZZLE_128B atoms.
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -205,20 +210,13 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   const uint32_t tmem = ctl->tmem_base;
 
   float* T = reinterpret_cast<float*>(smem);  // 128 x 129 fp32 epilogue tile, reuses the stage ring
-  if (warp < 8) {
-    // ------------------------------------------- producers + accumulator drain
-    const bool is_b = warp >= 4;
-    const bool produce = !(is_b && diag_shared);
-    const GemmOperand& op = is_b ? prob.B : prob.A;
-    const int t = threadIdx.x & 127;
-    const int c = t & 7;           // 16-byte chunk within the 128-byte row
-    const int rbase = t >> 3;      // 0..15
-    const int32_t row0 = (is_b ? item.tn : item.tm) * kTileM;
-    const uint32_t hi_off = is_b ? 2 * kOperandBytes : 0;
-    const uint32_t lo_off = hi_off + kOperandBytes;
-    // Drain role: TMEM lanes 32*(warp%4).., columns 64*(warp/4)..+63.
+  if (warp >= 8) {
+    // ---------------------------------------- MMA issue (warp 8) + drain (8-15)
+    // Drain warp w reads TMEM lanes 32*(w%4).. (the tcgen05 lane-access rule),
+    // columns 64*((w-8)/4)..+63 of each stage's accumulator buffer into
+    // round-to-nearest fp32 registers.
     const uint32_t lane_base = uint32_t((warp & 3) * 32) << 16;
-    const uint32_t col_base = (warp >> 2) * 64;
+    const uint32_t col_base = ((warp - 8) >> 2) * 64;
     float acc[64];
 #pragma unroll
     for (int j = 0; j < 64; ++j) acc[j] = 0.f;
@@ -226,25 +224,82 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       const int b = j & 1;
       mbar_wait(&ctl->tmem_full[b], (j >> 1) & 1);
       tc_fence_after();
-      if (dbg & 2) {
-        tc_fence_before();
-        mbar_arrive(&ctl->tmem_empty[b]);
-        return;
+      if (warp == 8 && lane == 0 && tr && j < 64) tr[j * 4 + 3] = clock64();
+      if (!(dbg & 2)) {
+        float v[32];
+        tmem_ld_32x32b_x32(tmem + lane_base + b * 128 + col_base, v);
+#pragma unroll
+        for (int q = 0; q < 32; ++q) acc[q] += v[q];
+        tmem_ld_32x32b_x32(tmem + lane_base + b * 128 + col_base + 32, v);
+#pragma unroll
+        for (int q = 0; q < 32; ++q) acc[32 + q] += v[q];
       }
-      float v[32];
-      tmem_ld_32x32b_x32(tmem + lane_base + b * 128 + col_base, v);
-#pragma unroll
-      for (int q = 0; q < 32; ++q) acc[q] += v[q];
-      tmem_ld_32x32b_x32(tmem + lane_base + b * 128 + col_base + 32, v);
-#pragma unroll
-      for (int q = 0; q < 32; ++q) acc[32 + q] += v[q];
       tc_fence_before();
       mbar_arrive(&ctl->tmem_empty[b]);
     };
-    // Raw fp32 tiles land in the hi plane of their slot two stages ahead --
-    // by TMA (one elected thread, mbarrier complete_tx) when the layout allows,
-    // else by per-thread cp.async.  Every producer thread then derives the
-    // tf32 lo plane for its 8 16-byte chunks (the raw plane is the hi operand).
+    constexpr uint32_t idesc = umma_idesc_tf32(kTileM, kTileN);
+    auto issue_mma = [&](int it) {
+      const int slot = it % kStages;
+      const uint32_t round = it / kStages;
+      const int b = it & 1;
+      mbar_wait(&ctl->full[slot], round & 1);
+      if (it >= 2) mbar_wait(&ctl->tmem_empty[b], ((it >> 1) + 1) & 1);
+      tc_fence_after();
+      if (lane == 0 && tr && it < 64) tr[it * 4 + 2] = clock64();
+      if (lane == 0) {
+        const uint32_t base = smem_u32(smem + slot * kStageBytes);
+        const uint32_t b_hi = diag_shared ? base : base + kOperandBytes;
+        const uint32_t b_lo = base + 2 * kOperandBytes;
+        const uint32_t a_hi = tmem + kTmemA + slot * 64, a_lo = a_hi + 32;
+        const uint32_t dt = tmem + b * 128;
+#pragma unroll
+        for (int kk = 0; kk < kTileK / 8; ++kk) {
+          const uint32_t koff = kk * 32;  // 8 tf32 = 32 bytes along the swizzled row
+          const uint64_t dbh = umma_desc_k_sw128(b_hi + koff), dbl = umma_desc_k_sw128(b_lo + koff);
+          if (!(dbg & 4)) {
+            umma_tf32_ts(dt, a_lo + kk * 8, dbh, idesc, kk > 0 ? 1u : 0u);
+            umma_tf32_ts(dt, a_hi + kk * 8, dbl, idesc, 1u);
+            umma_tf32_ts(dt, a_hi + kk * 8, dbh, idesc, 1u);
+          } else {
+            umma_tf32_ts(dt, a_hi + kk * 8, dbh, idesc, kk > 0 ? 1u : 0u);
+          }
+        }
+        umma_commit(&ctl->empty[slot]);
+        umma_commit(&ctl->tmem_full[b]);
+      }
+      __syncwarp();
+    };
+    if (warp == 8) {
+      for (int it = 0; it < n_iters; ++it) {
+        issue_mma(it);
+        if (it >= 1) drain(it - 1);
+      }
+      if (n_iters >= 1) drain(n_iters - 1);
+    } else {
+      for (int j = 0; j < n_iters; ++j) drain(j);
+    }
+    // All MMAs have completed (last tmem_full), so the stage ring is free.
+    asm volatile("bar.sync 1, 256;" ::: "memory");
+    const int r = (warp & 3) * 32 + lane;
+#pragma unroll
+    for (int j = 0; j < 64; ++j) T[r * kEpiStride + col_base + j] = acc[j];
+  } else if (warp < 8) {
+    // --------------------------------------------------------------- producers
+    const bool is_b = warp >= 4;
+    const bool produce = !(is_b && diag_shared);
+    const GemmOperand& op = is_b ? prob.B : prob.A;
+    const int t = threadIdx.x & 127;
+    const int c = t & 7;           // cp.async: 16-byte chunk within the 128-byte row
+    const int rbase = t >> 3;      // cp.async: 0..15
+    const int32_t row0 = (is_b ? item.tn : item.tm) * kTileM;
+    const uint32_t raw_off = is_b ? kOperandBytes : 0;
+    const uint32_t blo_off = 2 * kOperandBytes;
+    // Raw fp32 tiles land three stages ahead -- by TMA (one elected thread,
+    // mbarrier complete_tx) when the layout allows, else by per-thread
+    // cp.async.  A: each thread takes one row, writes tf32 hi/lo into TMEM
+    // (lane = row) for the TS-form MMA.  B: the raw tile is the hi operand (the
+    // tensor core truncates fp32 to tf32), each thread derives the lo plane
+    // for its 8 16-byte chunks.
     const int32_t r0 = row0 + rbase;
     const bool tma = op.mode != OP_ASYNC;
     const CUtensorMap* tmap = is_b ? &probs[item.problem].B.tmap : &probs[item.problem].A.tmap;
@@ -253,9 +308,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     int32_t tq = 0;  // TMA: 32-wide chunk index of the next stage
     auto issue = [&](int it) {
       const int slot = it % kStages;
-      const uint32_t plane = smem_u32(smem + slot * kStageBytes + hi_off);
+      const uint32_t plane = smem_u32(smem + slot * kStageBytes + raw_off);
       if (tma) {
         if (t == 0) {
+          if (tr && !is_b && it < 64) tr[it * 4 + 0] = clock64();
           mbar_expect_tx(&raw[slot], kOperandBytes);
           if (op.mode == OP_TMA2D) {
             tma_load_2d(plane, tmap, tq * kTileK, row0, &raw[slot]);
@@ -270,26 +326,57 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         cursor_advance(op, cur, kTileK);
       }
     };
-    auto convert = [&](int it) {
+    auto convert_a = [&](int it) {
       const int slot = it % kStages;
       uint8_t* stage = smem + slot * kStageBytes;
-      // The tensor core reads the top 19 bits of each fp32 word (truncation to
-      // tf32, verified against the fp64 oracle), so the raw tile IS the hi
-      // operand; only lo = rna_tf32(x - trunc_tf32(x)) is written.  Then
-      // x = hi + lo to 2^-22 relative and 3xTF32 products are fp32-accurate.
-      if (!(dbg & 1)) {
+      if (dbg & 1) {
+        mbar_arrive(&ctl->full[slot]);
+        return;
+      }
+      const int r = t;  // row of the tile == TMEM lane
+      float x[32], h[32];
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const int r = rbase + 16 * j;
-          const uint32_t off = r * 128 + ((c ^ (r & 7)) << 4);
-          const float4 x = *reinterpret_cast<const float4*>(stage + hi_off + off);
-          float4 l;
-          l.x = tf32_lo(x.x);
-          l.y = tf32_lo(x.y);
-          l.z = tf32_lo(x.z);
-          l.w = tf32_lo(x.w);
-          *reinterpret_cast<float4*>(stage + lo_off + off) = l;
-        }
+      for (int q = 0; q < 8; ++q) {
+        const float4 v = *reinterpret_cast<const float4*>(stage + raw_off + r * 128 + ((q ^ (r & 7)) << 4));
+        x[4 * q] = v.x; x[4 * q + 1] = v.y; x[4 * q + 2] = v.z; x[4 * q + 3] = v.w;
+      }
+#pragma unroll
+      for (int q = 0; q < 32; ++q) h[q] = __uint_as_float(__float_as_uint(x[q]) & 0xffffe000u);
+      const uint32_t ta = tmem + (uint32_t(warp * 32) << 16) + kTmemA + slot * 64;
+      tmem_st_32x32b_x32(ta, h);
+#pragma unroll
+      for (int q = 0; q < 32; ++q) {
+        uint32_t l;
+        asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(l) : "f"(x[q] - h[q]));
+        x[q] = __uint_as_float(l);
+      }
+      tmem_st_32x32b_x32(ta + 32, x);
+      if (diag_shared) {  // the same rows are the B operand: lo plane in smem too
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          *reinterpret_cast<float4*>(stage + blo_off + r * 128 + ((q ^ (r & 7)) << 4)) =
+              make_float4(x[4 * q], x[4 * q + 1], x[4 * q + 2], x[4 * q + 3]);
+        fence_proxy_async_smem();
+      }
+      tmem_wait_st();
+      tc_fence_before();
+      mbar_arrive(&ctl->full[slot]);
+    };
+    auto convert_b = [&](int it) {
+      const int slot = it % kStages;
+      uint8_t* stage = smem + slot * kStageBytes;
+      if (!(dbg & 1))
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int r = rbase + 16 * j;
+        const uint32_t off = r * 128 + ((c ^ (r & 7)) << 4);
+        const float4 x = *reinterpret_cast<const float4*>(stage + raw_off + off);
+        float4 l;
+        l.x = tf32_lo(x.x);
+        l.y = tf32_lo(x.y);
+        l.z = tf32_lo(x.z);
+        l.w = tf32_lo(x.w);
+        *reinterpret_cast<float4*>(stage + blo_off + off) = l;
       }
       fence_proxy_async_smem();
       mbar_arrive(&ctl->full[slot]);
@@ -301,70 +388,30 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       } else {
         cur = cursor_at(op, item.k0 + 4 * c);
       }
-      issue(0);
-      cp_async_commit();
-      if (n_iters > 1) issue(1);
-      cp_async_commit();
+#pragma unroll
+      for (int q = 0; q < kStages - 1; ++q) {
+        if (q < n_iters) issue(q);
+        cp_async_commit();
+      }
     }
     for (int it = 0; it < n_iters; ++it) {
       if (produce) {
         if (tma) {
           mbar_wait(&raw[it % kStages], (it / kStages) & 1);
+          if (tr && !is_b && t == 0 && it < 64) tr[it * 4 + 1] = clock64();
         } else {
-          cp_async_wait<1>();
+          cp_async_wait<kStages - 2>();
+          if (!is_b) asm volatile("bar.sync 2, 128;" ::: "memory");  // rows span other threads' copies
         }
-        convert(it);
-        if (it + 2 < n_iters) {
-          if (!tma || t == 0) {
-            const uint32_t round = (it + 2) / kStages;
-            mbar_wait(&ctl->empty[(it + 2) % kStages], (round & 1) ^ 1);
-          }
-          issue(it + 2);
+        if (is_b) convert_b(it);
+        else convert_a(it);
+        const int nx = it + kStages - 1;
+        if (nx < n_iters) {
+          if (!tma || t == 0) mbar_wait(&ctl->empty[nx % kStages], ((nx / kStages) & 1) ^ 1);
+          issue(nx);
         }
         cp_async_commit();
       }
-      if (it >= 1) drain(it - 1);
-    }
-    if (n_iters >= 1) drain(n_iters - 1);
-    // All MMAs have completed (last tmem_full), so the stage ring is free.
-    __syncwarp();
-    asm volatile("bar.sync 1, 256;" ::: "memory");  // producers only: ring reads done before T writes
-    const int r = (warp & 3) * 32 + lane;
-#pragma unroll
-    for (int j = 0; j < 64; ++j) T[r * kEpiStride + col_base + j] = acc[j];
-  } else {
-    // ------------------------------------------------------------ MMA issuer
-    constexpr uint32_t idesc = umma_idesc_tf32(kTileM, kTileN);
-    for (int it = 0; it < n_iters; ++it) {
-      const int slot = it % kStages;
-      const uint32_t round = it / kStages;
-      const int b = it & 1;
-      mbar_wait(&ctl->full[slot], round & 1);
-      if (it >= 2) mbar_wait(&ctl->tmem_empty[b], ((it >> 1) + 1) & 1);
-      tc_fence_after();
-      if (lane == 0) {
-        const uint32_t base = smem_u32(smem + slot * kStageBytes);
-        const uint32_t a_hi = base, a_lo = base + kOperandBytes;
-        const uint32_t b_hi = diag_shared ? a_hi : base + 2 * kOperandBytes;
-        const uint32_t b_lo = diag_shared ? a_lo : base + 3 * kOperandBytes;
-        const uint32_t d = tmem + b * 128;
-#pragma unroll
-        for (int kk = 0; kk < kTileK / 8; ++kk) {
-          const uint32_t koff = kk * 32;  // 8 tf32 = 32 bytes along the swizzled row
-          const uint64_t dah = umma_desc_k_sw128(a_hi + koff), dal = umma_desc_k_sw128(a_lo + koff);
-          const uint64_t dbh = umma_desc_k_sw128(b_hi + koff), dbl = umma_desc_k_sw128(b_lo + koff);
-          if (!(dbg & 4)) {
-            umma_tf32(d, dal, dbh, idesc, kk > 0 ? 1u : 0u);
-            umma_tf32(d, dah, dbl, idesc, 1u);
-            umma_tf32(d, dah, dbh, idesc, 1u);
-          } else {
-            umma_tf32(d, dah, dbh, idesc, kk > 0 ? 1u : 0u);
-          }
-        }
-        umma_commit(&ctl->empty[slot]);
-        umma_commit(&ctl->tmem_full[b]);
-      }
-      __syncwarp();
     }
   }
   tc_fence_before();
@@ -533,7 +580,32 @@ int launch_gemm(const GemmProblem* d_probs, const GemmWorkItem* d_items, int n_i
     attr_set = true;
   }
   static const int dbg = getenv("SPNGD_GEMM_DEBUG") ? atoi(getenv("SPNGD_GEMM_DEBUG")) : 0;
-  gemm_tf32x3_kernel<<<n_items, kGemmThreads, smem, stream>>>(d_probs, d_items, d_partials, d_status, dbg);
+  static long long* trace = nullptr;
+  static const bool want_trace = getenv("SPNGD_GEMM_TRACE") != nullptr;
+  if (want_trace && !trace) {
+    cudaMalloc(&trace, 4 * 64 * 4 * sizeof(long long));
+    cudaMemset(trace, 0, 4 * 64 * 4 * sizeof(long long));
+  }
+  gemm_tf32x3_kernel<<<n_items, kGemmThreads, smem, stream>>>(d_probs, d_items, d_partials, d_status, dbg, trace);
+  if (want_trace && n_items >= 4) {
+    static int printed = 0;
+    if (printed++ < 2) {
+      long long h[4 * 64 * 4];
+      cudaStreamSynchronize(stream);
+      cudaMemcpy(h, trace, sizeof(h), cudaMemcpyDeviceToHost);
+      for (int b = 0; b < 2; ++b) {
+        const long long t0 = h[b * 256];
+        printf("trace cta %d (cycles rel. to first TMA issue): stage issue raw full mma_done\n", b);
+        for (int q = 0; q < 24; ++q) {
+          const long long* e = h + b * 256 + q * 4;
+          if (!e[0] && !e[2]) break;
+          printf("  %2d %8lld %8lld %8lld %8lld\n", q, e[0] ? e[0] - t0 : -1, e[1] ? e[1] - t0 : -1,
+                 e[2] ? e[2] - t0 : -1, e[3] ? e[3] - t0 : -1);
+        }
+      }
+      cudaMemset(trace, 0, 4 * 64 * 4 * sizeof(long long));
+    }
+  }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     cudaFuncAttributes fa{};

@@ -97,8 +97,8 @@ struct SyrkReduceTask {
 constexpr int kTileM = 128;
 constexpr int kTileN = 128;
 constexpr int kTileK = 32;     // fp32 elements per stage = one 128-byte swizzle row
-constexpr int kStages = 3;
-constexpr int kGemmThreads = 288;  // 4 A-producer warps, 4 B-producer warps, 1 MMA warp
+constexpr int kStages = 4;
+constexpr int kGemmThreads = 512;  // 4 A-producer, 4 B-producer, 8 drain warps (warp 8 also issues MMAs)
 
 // Chooses the operand mode and encodes its TMA descriptor.  `K` is the true
 // K extent; for OP_TMA3D the GEMM must iterate the padded K returned by
