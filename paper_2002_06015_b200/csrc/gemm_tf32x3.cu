@@ -36,11 +36,14 @@ namespace {
 
 constexpr int kOperandBytes = kTileM * kTileK * 4;     // 16 KB (128 rows x 128 B)
 constexpr int kStageBytes = 3 * kOperandBytes;         // A raw, B raw (= B hi), B lo
-constexpr int kEpiStride = kTileN + 1;                 // padded fp32 tile row
+// Epilogue tile row stride: 132 floats keeps rows 16-byte aligned (float4
+// row access is conflict-free) and makes the (16 columns x 2 row-quads) column
+// access of the transposed/update stores conflict-free too (528 = 16 mod 32).
+constexpr int kEpiStride = kTileN + 4;
 constexpr int kTmemCols = 512;  // 2 x 128 accumulator columns + kStages x (A hi | A lo) x 32
 constexpr uint32_t kTmemA = 256;                       // first A-operand column
 
-struct __align__(8) SmemCtl {
+struct __align__(64) SmemCtl {
   uint64_t full[kStages];
   uint64_t empty[kStages];
   uint64_t tmem_full[2];
@@ -164,10 +167,25 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                        float* __restrict__ partials, int* status, int dbg, long long* trace) {
   // trace (debug): for CTAs < 4, stages < 64: [cta][stage][4] clock64 stamps
   // {A TMA issued, A raw landed, MMA saw full, drain saw MMA done}.
-  long long* tr = (trace && blockIdx.x < 4) ? trace + blockIdx.x * 64 * 4 : nullptr;
+#ifdef SPNGD_GEMM_TRACE_BUILD
+  long long* tr = (trace && blockIdx.x < 4) ? trace + blockIdx.x * 264 : nullptr;
+  long long* meta = tr ? tr + 256 : nullptr;  // entry, setup, tmem, mma-end, prod-end, epi-start, epi-end, epi-mid
+#define TRACE_STAMP(cond, slot) \
+  do {                          \
+    if (cond) slot = clock64(); \
+  } while (0)
+#else
+#define TRACE_STAMP(cond, slot) \
+  do {                          \
+  } while (0)
+#endif
+  TRACE_STAMP(meta && threadIdx.x == 0, meta[0]);
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 1024-byte alignment for the SWIZZLE_128B atoms.
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // Offset from the __shared__ array itself (not via uintptr_t) so every
+  // derived pointer keeps the shared address space: LDS/STS, not generic
+  // LD/ST (which cost ~10k cycles per epilogue tile and slowed `prob` reads).
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   SmemCtl* ctl = reinterpret_cast<SmemCtl*>(smem + kStages * kStageBytes);
 
   const int warp = threadIdx.x >> 5;
@@ -203,11 +221,13 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     }
     mbar_fence_init();
   }
+  TRACE_STAMP(meta && threadIdx.x == 0, meta[1]);
   if (warp == 8) tmem_alloc<kTmemCols>(&ctl->tmem_base);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = ctl->tmem_base;
+  TRACE_STAMP(meta && threadIdx.x == 0, meta[2]);
 
   float* T = reinterpret_cast<float*>(smem);  // 128 x 129 fp32 epilogue tile, reuses the stage ring
   if (warp >= 8) {
@@ -224,7 +244,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       const int b = j & 1;
       mbar_wait(&ctl->tmem_full[b], (j >> 1) & 1);
       tc_fence_after();
-      if (warp == 8 && lane == 0 && tr && j < 64) tr[j * 4 + 3] = clock64();
+      TRACE_STAMP(warp == 8 && lane == 0 && tr && j < 64, tr[j * 4 + 3]);
       if (!(dbg & 2)) {
         float v[32];
         tmem_ld_32x32b_x32(tmem + lane_base + b * 128 + col_base, v);
@@ -245,7 +265,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       mbar_wait(&ctl->full[slot], round & 1);
       if (it >= 2) mbar_wait(&ctl->tmem_empty[b], ((it >> 1) + 1) & 1);
       tc_fence_after();
-      if (lane == 0 && tr && it < 64) tr[it * 4 + 2] = clock64();
+      TRACE_STAMP(lane == 0 && tr && it < 64, tr[it * 4 + 2]);
       if (lane == 0) {
         const uint32_t base = smem_u32(smem + slot * kStageBytes);
         const uint32_t b_hi = diag_shared ? base : base + kOperandBytes;
@@ -275,14 +295,16 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         if (it >= 1) drain(it - 1);
       }
       if (n_iters >= 1) drain(n_iters - 1);
+      TRACE_STAMP(meta && lane == 0, meta[3]);
     } else {
       for (int j = 0; j < n_iters; ++j) drain(j);
     }
     // All MMAs have completed (last tmem_full), so the stage ring is free.
     asm volatile("bar.sync 1, 256;" ::: "memory");
     const int r = (warp & 3) * 32 + lane;
+    float4* trow = reinterpret_cast<float4*>(T + r * kEpiStride + col_base);
 #pragma unroll
-    for (int j = 0; j < 64; ++j) T[r * kEpiStride + col_base + j] = acc[j];
+    for (int j = 0; j < 16; ++j) trow[j] = make_float4(acc[4 * j], acc[4 * j + 1], acc[4 * j + 2], acc[4 * j + 3]);
   } else if (warp < 8) {
     // --------------------------------------------------------------- producers
     const bool is_b = warp >= 4;
@@ -311,7 +333,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       const uint32_t plane = smem_u32(smem + slot * kStageBytes + raw_off);
       if (tma) {
         if (t == 0) {
-          if (tr && !is_b && it < 64) tr[it * 4 + 0] = clock64();
+          TRACE_STAMP(tr && !is_b && it < 64, tr[it * 4 + 0]);
           mbar_expect_tx(&raw[slot], kOperandBytes);
           if (op.mode == OP_TMA2D) {
             tma_load_2d(plane, tmap, tq * kTileK, row0, &raw[slot]);
@@ -398,7 +420,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       if (produce) {
         if (tma) {
           mbar_wait(&raw[it % kStages], (it / kStages) & 1);
-          if (tr && !is_b && t == 0 && it < 64) tr[it * 4 + 1] = clock64();
+          TRACE_STAMP(tr && !is_b && t == 0 && it < 64, tr[it * 4 + 1]);
         } else {
           cp_async_wait<kStages - 2>();
           if (!is_b) asm volatile("bar.sync 2, 128;" ::: "memory");  // rows span other threads' copies
@@ -413,6 +435,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         cp_async_commit();
       }
     }
+    TRACE_STAMP(meta && threadIdx.x == 0, meta[4]);
   }
   tc_fence_before();
   __syncthreads();
@@ -420,85 +443,246 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     tc_fence_after();
     tmem_dealloc<kTmemCols>(tmem);
   }
+  TRACE_STAMP(meta && threadIdx.x == 0, meta[5]);
 
   const int tid = threadIdx.x;
   const int nthr = blockDim.x;
   const int32_t m0 = item.tm * kTileM, n0 = item.tn * kTileN;
-  switch (prob.mode) {
+  // Epilogue arguments live in registers: `prob` sits in shared memory and
+  // every generic global store could alias it, which made the compiler reload
+  // prob fields after each store (measured 10-16k cycles per tile).
+  struct {
+    int32_t mode, flags, M, N;
+    float alpha, beta, eta, momentum;
+    float* C;
+    const float* Cin;
+    int64_t ldc;
+    float* CT;
+    int64_t ldct;
+    float* W;
+    float* V;
+    float* P_out;
+    double* norm2;
+    const float* scal;
+  } e{prob.mode, prob.flags, prob.M, prob.N, prob.alpha, prob.beta, prob.eta, prob.momentum, prob.C, prob.Cin,
+      prob.ldc, prob.CT, prob.ldct, prob.W, prob.V, prob.P_out, prob.norm2, prob.scal};
+  // Work is split in float4 chunks, 8 per thread (4096 per tile).  Row chunks
+  // (r, c4) read T rows; column chunks (c, r4) read 4 rows of one column in
+  // the (16 columns x 2 row-quads) lane layout.  In-bounds, aligned chunks use
+  // 16-byte global accesses; ragged or masked chunks fall back to scalars.
+  auto row_chunk = [&](int k, int& r, int& c) {
+    const int p = tid + k * kGemmThreads;
+    r = p >> 5;
+    c = (p & 31) * 4;
+  };
+  auto col_chunk = [&](int k, int& c, int& r) {
+    const int p = tid + k * kGemmThreads;
+    const int wk = p >> 5, ln = p & 31;
+    c = (wk & 7) * 16 + (ln & 15);
+    r = ((wk >> 3) * 2 + (ln >> 4)) * 4;
+  };
+  auto t_col4 = [&](int r, int c) {
+    return make_float4(T[r * kEpiStride + c], T[(r + 1) * kEpiStride + c], T[(r + 2) * kEpiStride + c],
+                       T[(r + 3) * kEpiStride + c]);
+  };
+  auto aligned16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+  switch (e.mode) {
     case EPI_PARTIAL: {
-      float* dst = partials + int64_t(item.slot) * kTileM * kTileN;
-      for (int idx = tid; idx < kTileM * kTileN; idx += nthr) {
-        const int r = idx >> 7, c = idx & 127;
-        dst[idx] = T[r * kEpiStride + c];
+      float4* dst = reinterpret_cast<float4*>(partials + int64_t(item.slot) * kTileM * kTileN);
+#pragma unroll 4
+      for (int k = 0; k < 8; ++k) {
+        int r, c;
+        row_chunk(k, r, c);
+        dst[r * 32 + (c >> 2)] = *reinterpret_cast<const float4*>(T + r * kEpiStride + c);
       }
       break;
     }
     case EPI_PACKED: {
-      const int64_t n = prob.M;
-      for (int idx = tid; idx < kTileM * kTileN; idx += nthr) {
-        const int r = idx >> 7, c = idx & 127;
-        const int64_t i = m0 + r, j = n0 + c;
-        if (i < prob.M && j < prob.N && i <= j) prob.C[packed_offset(n, i, j)] = prob.alpha * T[r * kEpiStride + c];
+      const int64_t n = e.M;
+#pragma unroll 2
+      for (int k = 0; k < 8; ++k) {
+        int r, c;
+        row_chunk(k, r, c);
+        const int64_t i = m0 + r;
+        if (i >= e.M) continue;
+        const int64_t rb = packed_offset(n, i, i) - i;  // offset of (i, j) = rb + j
+        const float4 v = *reinterpret_cast<const float4*>(T + r * kEpiStride + c);
+        const float vv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int64_t jj = n0 + c + q;
+          if (jj < e.N && i <= jj) e.C[rb + jj] = e.alpha * vv[q];
+        }
       }
       break;
     }
     case EPI_DENSE: {
-      const bool mirror = (prob.flags & FLAG_SYM_MIRROR) != 0;
-      for (int idx = tid; idx < kTileM * kTileN; idx += nthr) {
-        const int r = idx >> 7, c = idx & 127;
-        const int64_t i = m0 + r, j = n0 + c;
-        if (i < prob.M && j < prob.N && (!mirror || i <= j)) {
-          float val = prob.alpha * T[r * kEpiStride + c];
-          if (prob.beta != 0.f) val += prob.beta * prob.Cin[i * prob.ldc + j];
-          prob.C[i * prob.ldc + j] = val;
-          T[r * kEpiStride + c] = val;
+      const bool mirror = (e.flags & FLAG_SYM_MIRROR) != 0;
+      const bool has_cin = e.beta != 0.f;
+      const bool vec = aligned16(e.C) && (!has_cin || aligned16(e.Cin)) && (e.ldc & 3) == 0;
+#pragma unroll 1
+      for (int k0 = 0; k0 < 8; k0 += 4) {
+        float4 cin[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {  // Cin loads first: C and Cin may alias
+          int r, c;
+          row_chunk(k0 + u, r, c);
+          const int64_t i = m0 + r, j = n0 + c;
+          cin[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (!has_cin || i >= e.M) continue;
+          const float* src = e.Cin + i * e.ldc + j;
+          if (vec && j + 3 < e.N) {
+            cin[u] = __ldg(reinterpret_cast<const float4*>(src));
+          } else {
+            if (j < e.N) cin[u].x = src[0];
+            if (j + 1 < e.N) cin[u].y = src[1];
+            if (j + 2 < e.N) cin[u].z = src[2];
+            if (j + 3 < e.N) cin[u].w = src[3];
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          int r, c;
+          row_chunk(k0 + u, r, c);
+          const int64_t i = m0 + r, j = n0 + c;
+          if (i >= e.M) continue;
+          float4* tp = reinterpret_cast<float4*>(T + r * kEpiStride + c);
+          float4 v = *tp;
+          v.x = e.alpha * v.x + e.beta * cin[u].x;
+          v.y = e.alpha * v.y + e.beta * cin[u].y;
+          v.z = e.alpha * v.z + e.beta * cin[u].z;
+          v.w = e.alpha * v.w + e.beta * cin[u].w;
+          *tp = v;
+          if (dbg & 8) continue;
+          float* dst = e.C + i * e.ldc + j;
+          if (vec && j + 3 < e.N && (!mirror || i <= j)) {
+            *reinterpret_cast<float4*>(dst) = v;
+          } else {
+            const float vv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+              if (j + q < e.N && (!mirror || i <= j + q)) dst[q] = vv[q];
+          }
         }
       }
-      if (mirror || (prob.flags & FLAG_TRANS)) {
+      TRACE_STAMP(meta && tid == 0, meta[7]);
+      if (mirror || (e.flags & FLAG_TRANS)) {
         __syncthreads();
-        float* dstT = mirror ? prob.C : prob.CT;
-        const int64_t ldt = mirror ? prob.ldc : prob.ldct;
-        for (int idx = tid; idx < kTileM * kTileN; idx += nthr) {
-          const int c = idx >> 7, r = idx & 127;
-          const int64_t i = m0 + r, j = n0 + c;
-          if (i < prob.M && j < prob.N && (!mirror || i < j)) dstT[j * ldt + i] = T[r * kEpiStride + c];
+        float* dstT = mirror ? e.C : e.CT;
+        const int64_t ldt = mirror ? e.ldc : e.ldct;
+        const bool vt = aligned16(dstT) && (ldt & 3) == 0;
+#pragma unroll 2
+        for (int k = 0; k < 8; ++k) {
+          int c, r;
+          col_chunk(k, c, r);
+          const int64_t i = m0 + r, j = n0 + c;  // writes dstT[j][i .. i+3]
+          if (j >= e.N || (dbg & 64)) continue;
+          const float4 v = t_col4(r, c);
+          float* dst = dstT + j * ldt + i;
+          if (vt && i + 3 < e.M && (!mirror || i + 3 < j)) {
+            *reinterpret_cast<float4*>(dst) = v;
+          } else {
+            const float vv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+              if (i + q < e.M && (!mirror || i + q < j)) dst[q] = vv[q];
+          }
         }
       }
       break;
     }
     case EPI_UPDATE: {
       // Tile of P^T: rows = a-index (M = a), cols = g-index.  W is g x a
-      // row-major, so element (i = n0+c, j = m0+r) lives at W[i*a + j].
-      const int64_t a = prob.M;
-      const float eta = prob.scal ? prob.scal[0] : prob.eta;
-      const float mom = prob.scal ? prob.scal[1] : prob.momentum;
+      // row-major, so element (i = n0+c, j = m0+r) lives at W[i*a + j]:
+      // column chunks of T are contiguous in W.
+      const int64_t a = e.M;
+      const float eta = e.scal ? e.scal[0] : e.eta;
+      const float mom = e.scal ? e.scal[1] : e.momentum;
+      const bool vec = (a & 3) == 0 && (!e.W || (aligned16(e.W) && aligned16(e.V))) && (!e.P_out || aligned16(e.P_out));
       double ss = 0.0;
-      for (int idx = tid; idx < kTileM * kTileN; idx += nthr) {
-        const int c = idx >> 7, r = idx & 127;
-        const int64_t j = m0 + r, i = n0 + c;
-        if (j < prob.M && i < prob.N) {
-          const float p = prob.alpha * T[r * kEpiStride + c];
-          const int64_t w_idx = i * a + j;
-          if (prob.P_out) prob.P_out[w_idx] = p;
-          if (prob.W) {
-            const float w = prob.W[w_idx], vel = prob.V[w_idx];
-            const float nw = w - eta * p + mom * vel;  // fisher.cpp:332
-            prob.W[w_idx] = nw;
-            prob.V[w_idx] = nw - w;                                   // fisher.cpp:333
-            ss += double(nw) * double(nw);
+#pragma unroll 1
+      for (int k0 = 0; k0 < 8; k0 += 4) {
+        float4 w[4], vel[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {  // all loads first (W/V are also stored)
+          int c, r;
+          col_chunk(k0 + u, c, r);
+          const int64_t j = m0 + r, i = n0 + c;
+          w[u] = vel[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (!e.W || i >= e.N || j >= a) continue;
+          const int64_t o = i * a + j;
+          if (vec && j + 3 < a) {
+            w[u] = __ldg(reinterpret_cast<const float4*>(e.W + o));
+            vel[u] = __ldg(reinterpret_cast<const float4*>(e.V + o));
+          } else {
+            float* wp = &w[u].x;
+            float* vp = &vel[u].x;
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+              if (j + q < a) {
+                wp[q] = e.W[o + q];
+                vp[q] = e.V[o + q];
+              }
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          int c, r;
+          col_chunk(k0 + u, c, r);
+          const int64_t j = m0 + r, i = n0 + c;
+          if (i >= e.N || j >= a) continue;
+          const float4 t = t_col4(r, c);
+          const float4 p = make_float4(e.alpha * t.x, e.alpha * t.y, e.alpha * t.z, e.alpha * t.w);
+          float4 nw, nv;
+          nw.x = w[u].x - eta * p.x + mom * vel[u].x;  // fisher.cpp:332
+          nw.y = w[u].y - eta * p.y + mom * vel[u].y;
+          nw.z = w[u].z - eta * p.z + mom * vel[u].z;
+          nw.w = w[u].w - eta * p.w + mom * vel[u].w;
+          nv = make_float4(nw.x - w[u].x, nw.y - w[u].y, nw.z - w[u].z, nw.w - w[u].w);  // fisher.cpp:333
+          const int64_t o = i * a + j;
+          const int nq = (a - j) >= 4 ? 4 : int(a - j);
+          if (vec && nq == 4) {
+            if (e.P_out) *reinterpret_cast<float4*>(e.P_out + o) = p;
+            if (e.W) {
+              *reinterpret_cast<float4*>(e.W + o) = nw;
+              *reinterpret_cast<float4*>(e.V + o) = nv;
+            }
+          } else {
+            const float pp[4] = {p.x, p.y, p.z, p.w}, ww[4] = {nw.x, nw.y, nw.z, nw.w}, vv[4] = {nv.x, nv.y, nv.z, nv.w};
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+              if (q < nq) {
+                if (e.P_out) e.P_out[o + q] = pp[q];
+                if (e.W) {
+                  e.W[o + q] = ww[q];
+                  e.V[o + q] = vv[q];
+                }
+              }
+          }
+          if (e.W) {
+            const float ww[4] = {nw.x, nw.y, nw.z, nw.w};
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+              if (q < nq) ss += double(ww[q]) * double(ww[q]);
           }
         }
       }
-      if (prob.norm2) {
+      if (e.norm2) {
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
-        if (lane == 0) atomicAdd(prob.norm2, ss);
+        if (lane == 0) atomicAdd(e.norm2, ss);
       }
       break;
     }
     default:
       if (tid == 0) set_status(status, SPNGD_ERR_INVALID);
   }
+#ifdef SPNGD_GEMM_TRACE_BUILD
+  if (meta) {
+    __syncthreads();
+    if (tid == 0) meta[6] = clock64();
+  }
+#endif
 }
 
 __global__ void syrk_reduce_kernel(const SyrkReduceTask* __restrict__ tasks, const float* __restrict__ partials) {
@@ -568,6 +752,8 @@ void finalize_operand(GemmOperand& op, int64_t K, bool allow_tma) {
   }
 }
 
+int g_gemm_dbg_extra = 0;
+
 size_t gemm_smem_bytes() { return size_t(kStages) * kStageBytes + sizeof(SmemCtl) + 1024; }
 
 int launch_gemm(const GemmProblem* d_probs, const GemmWorkItem* d_items, int n_items, float* d_partials,
@@ -579,31 +765,41 @@ int launch_gemm(const GemmProblem* d_probs, const GemmWorkItem* d_items, int n_i
     SPNGD_CUDA_TRY(cudaFuncSetAttribute(gemm_tf32x3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     attr_set = true;
   }
-  static const int dbg = getenv("SPNGD_GEMM_DEBUG") ? atoi(getenv("SPNGD_GEMM_DEBUG")) : 0;
+  static const int dbg_env = getenv("SPNGD_GEMM_DEBUG") ? atoi(getenv("SPNGD_GEMM_DEBUG")) : 0;
+  const int dbg = dbg_env | g_gemm_dbg_extra;
   static long long* trace = nullptr;
+#ifdef SPNGD_GEMM_TRACE_BUILD
   static const bool want_trace = getenv("SPNGD_GEMM_TRACE") != nullptr;
+#else
+  constexpr bool want_trace = false;
+#endif
   if (want_trace && !trace) {
-    cudaMalloc(&trace, 4 * 64 * 4 * sizeof(long long));
-    cudaMemset(trace, 0, 4 * 64 * 4 * sizeof(long long));
+    cudaMalloc(&trace, 4 * 264 * sizeof(long long));
+    cudaMemset(trace, 0, 4 * 264 * sizeof(long long));
   }
   gemm_tf32x3_kernel<<<n_items, kGemmThreads, smem, stream>>>(d_probs, d_items, d_partials, d_status, dbg, trace);
-  if (want_trace && n_items >= 4) {
+  if (want_trace) {
     static int printed = 0;
-    if (printed++ < 2) {
-      long long h[4 * 64 * 4];
+    if (printed++ < 12) {
+      long long h[4 * 264];
       cudaStreamSynchronize(stream);
       cudaMemcpy(h, trace, sizeof(h), cudaMemcpyDeviceToHost);
-      for (int b = 0; b < 2; ++b) {
-        const long long t0 = h[b * 256];
-        printf("trace cta %d (cycles rel. to first TMA issue): stage issue raw full mma_done\n", b);
+      const long long* m = h + 256;
+
+      printf("gemm launch %d items %d: setup %lld tmem %lld mainloop(mma) %lld prod %lld epi-start %lld epi-mid %lld epi-end %lld cycles\n",
+             printed - 1, n_items, m[1] - m[0], m[2] - m[0], m[3] - m[0], m[4] - m[0], m[5] - m[0], m[7] ? m[7] - m[0] : -1, m[6] - m[0]);
+      for (int b = 0; b < (n_items >= 4 && printed <= 2 ? 2 : 1); ++b) {
+        const long long t0 = h[b * 264];
+        printf("trace cta %d (cycles rel. to first TMA issue; first issue at +%lld from entry): stage issue raw full mma_done\n", b,
+               h[b * 264] - h[b * 264 + 256]);
         for (int q = 0; q < 24; ++q) {
-          const long long* e = h + b * 256 + q * 4;
+          const long long* e = h + b * 264 + q * 4;
           if (!e[0] && !e[2]) break;
           printf("  %2d %8lld %8lld %8lld %8lld\n", q, e[0] ? e[0] - t0 : -1, e[1] ? e[1] - t0 : -1,
                  e[2] ? e[2] - t0 : -1, e[3] ? e[3] - t0 : -1);
         }
       }
-      cudaMemset(trace, 0, 4 * 64 * 4 * sizeof(long long));
+      cudaMemset(trace, 0, 4 * 264 * sizeof(long long));
     }
   }
   cudaError_t e = cudaGetLastError();

@@ -504,6 +504,12 @@ int run_inverse(spngd_ctx* ctx, const InversePlan& plan, const GemmProblem* d_pr
     int rc = launch_base(ctx, d_bases + r.base_off, r.base_cnt);
     if (rc) return rc;
     if (r.item_cnt > 0) {
+      static const bool warm = getenv("SPNGD_WARM_GEMM") != nullptr;  // debug: i-cache warm-up launch
+      if (warm) {
+        g_gemm_dbg_extra = 8 | 16 | 64;
+        launch_gemm(d_probs, d_items + r.item_off, r.item_cnt, nullptr, ctx->d_status, ctx->stream);
+        g_gemm_dbg_extra = 0;
+      }
       rc = launch_gemm(d_probs, d_items + r.item_off, r.item_cnt, nullptr, ctx->d_status, ctx->stream);
       if (rc) return rc;
       ctx->launches++;
