@@ -72,7 +72,20 @@ __device__ __forceinline__ void diag_subst_step(float (&col)[32], const float* L
 // warps solve the panel and apply the SYRK trailing update on 4x4 register
 // tiles; finally T = L^-1 by blocked forward substitution.  fp32 storage and
 // FMA (LAPACK spotrf class).
+#ifdef SPNGD_GEMM_TRACE_BUILD
+__device__ long long g_leaf_trace[32];
+#define LEAF_STAMP(i) \
+  do {                \
+    if (blockIdx.x == 0 && threadIdx.x == 0) g_leaf_trace[i] = clock64(); \
+  } while (0)
+#else
+#define LEAF_STAMP(i) \
+  do {                \
+  } while (0)
+#endif
+
 __global__ void __launch_bounds__(kBaseThreads, 1) base_chol_inv_kernel(const BaseTask* __restrict__ tasks, int* status) {
+  LEAF_STAMP(0);
   extern __shared__ __align__(16) uint8_t base_smem[];
   float* A = reinterpret_cast<float*>(base_smem);   // [128][129], lower = M -> L
   float* T = A + kBaseMax * kLd;                    // [128][129], T = L^-1
@@ -103,6 +116,7 @@ __global__ void __launch_bounds__(kBaseThreads, 1) base_chol_inv_kernel(const Ba
     }
   }
   __syncthreads();
+  LEAF_STAMP(1);
   bool bad = false;
   const int nblk = np / kPB;
   for (int kb = 0; kb < nblk; ++kb) {
@@ -125,6 +139,7 @@ __global__ void __launch_bounds__(kBaseThreads, 1) base_chol_inv_kernel(const Ba
       for (int i = 0; i < kPB; ++i) T[(k0 + i) * kLd + k0 + lane] = col[i];
     }
     __syncthreads();
+    LEAF_STAMP(2 + 3 * kb);
     const int m = np - k0 - kPB;  // trailing size
     if (m > 0) {
       // (2) panel: L[i][k0+j] = sum_{p<=j} A[i][k0+p] Dinv[j][p]; thread = (row group, column j).
@@ -147,6 +162,7 @@ __global__ void __launch_bounds__(kBaseThreads, 1) base_chol_inv_kernel(const Ba
       for (int q = 0; q < kRows; ++q)
         if (ibase + q * stride < np) A[(ibase + q * stride) * kLd + k0 + j] = res[q];
       __syncthreads();
+      LEAF_STAMP(3 + 3 * kb);
       // (3) trailing SYRK on 4x4 register tiles of the lower triangle.
       const int mt = m / 4;
       const int ntiles = mt * (mt + 1) / 2;
@@ -177,6 +193,7 @@ __global__ void __launch_bounds__(kBaseThreads, 1) base_chol_inv_kernel(const Ba
             if (j0 + y <= i0 + x) A[(i0 + x) * kLd + j0 + y] -= acc[x][y];
       }
       __syncthreads();
+      LEAF_STAMP(4 + 3 * kb);
     }
   }
   // (4) T = L^-1 off-diagonal 32x32 blocks, block row by block row:
@@ -233,6 +250,7 @@ __global__ void __launch_bounds__(kBaseThreads, 1) base_chol_inv_kernel(const Ba
 #pragma unroll
         for (int q = 0; q < 4; ++q) T[(ib * kPB + r0 + 8 * q) * kLd + jb * kPB + c] = -acc[jb][q];
     __syncthreads();
+    LEAF_STAMP(14 + ib);
   }
   if (bad) set_status(status, SPNGD_ERR_NOT_POSITIVE_DEFINITE);
   // Coalesced stores: T rows (lower) and T^T rows (upper, read transposed from smem).
@@ -241,6 +259,8 @@ __global__ void __launch_bounds__(kBaseThreads, 1) base_chol_inv_kernel(const Ba
       if (j <= i) t.tlow[int64_t(i) * t.ld + j] = T[i * kLd + j];
       if (j >= i) t.tup[int64_t(i) * t.ld + j] = T[j * kLd + i];
     }
+  __syncthreads();
+  LEAF_STAMP(18);
 }
 
 __global__ void pi_kernel(const PiTask* __restrict__ tasks) {
@@ -494,6 +514,17 @@ int launch_base(spngd_ctx* ctx, const BaseTask* d_tasks, int n) {
   }
   base_chol_inv_kernel<<<n, kBaseThreads, kBaseSmem, ctx->stream>>>(d_tasks, ctx->d_status);
   SPNGD_CUDA_TRY(cudaGetLastError());
+#ifdef SPNGD_GEMM_TRACE_BUILD
+  static int printed = 0;
+  if (getenv("SPNGD_GEMM_TRACE") && printed++ < 6) {
+    long long h[32];
+    cudaStreamSynchronize(ctx->stream);
+    cudaMemcpyFromSymbol(h, g_leaf_trace, sizeof(h));
+    printf("leaf launch (%d leaves): load %lld", n, h[1] - h[0]);
+    for (int kb = 0; kb < 4; ++kb) printf(" | kb%d diag %lld panel %lld syrk %lld", kb, h[2 + 3 * kb] - h[0], h[3 + 3 * kb] - h[0], h[4 + 3 * kb] - h[0]);
+    printf(" | T rows %lld %lld %lld | store %lld\n", h[15] - h[0], h[16] - h[0], h[17] - h[0], h[18] - h[0]);
+  }
+#endif
   ctx->launches++;
   return SPNGD_OK;
 }
@@ -504,12 +535,6 @@ int run_inverse(spngd_ctx* ctx, const InversePlan& plan, const GemmProblem* d_pr
     int rc = launch_base(ctx, d_bases + r.base_off, r.base_cnt);
     if (rc) return rc;
     if (r.item_cnt > 0) {
-      static const bool warm = getenv("SPNGD_WARM_GEMM") != nullptr;  // debug: i-cache warm-up launch
-      if (warm) {
-        g_gemm_dbg_extra = 8 | 16 | 64;
-        launch_gemm(d_probs, d_items + r.item_off, r.item_cnt, nullptr, ctx->d_status, ctx->stream);
-        g_gemm_dbg_extra = 0;
-      }
       rc = launch_gemm(d_probs, d_items + r.item_off, r.item_cnt, nullptr, ctx->d_status, ctx->stream);
       if (rc) return rc;
       ctx->launches++;
