@@ -229,11 +229,14 @@ typedef struct spngd_opt_config {
 
 /* Host-only planning of the hybrid schedule (no GPU needed): layer owners
  * (LPT on a^3 + g^3 + 2 g^2 a + 2 g a^2; the reference uses li % K,
- * dist.cpp:147-153 -- ownership never changes numerics) and the owner-major
- * segment offsets (floats) of every payload in the reduce-scatter buffer
- * (A, G packed; BN 3c moments; dW g*a or 2c) and the all-gather buffer
- * (W g*a or gamma|beta 2c).  -1 marks payloads a layer does not have.
- * seg_rs / seg_ag: padded per-owner segment sizes. */
+ * dist.cpp:147-153 -- ownership never changes numerics) and owner-major
+ * segment offsets (floats).  The reduce-scatter buffer has two regions, each
+ * owner-major: statistics (A, G packed; BN 3c moments -- off_A/off_G/off_M
+ * within the owner's seg_stat) and gradients (dW g*a or 2c -- off_dW within
+ * the owner's seg_grad), so gradients reduce every step and statistics only
+ * when due (stale gating).  All-gather buffer: W g*a or gamma|beta 2c.
+ * -1 marks payloads a layer does not have.  Send buffer layout:
+ * [world x seg_stat | world x seg_grad]; owner receive: [seg_stat | seg_grad]. */
 typedef struct spngd_layout_entry {
   int32_t owner;
   int32_t pad_;
@@ -241,7 +244,7 @@ typedef struct spngd_layout_entry {
   int64_t off_W;
 } spngd_layout_entry;
 int spngd_plan_layout(const spngd_layer_desc* layers, int n_layers, int world, spngd_layout_entry* out,
-                      int64_t* seg_rs, int64_t* seg_ag);
+                      int64_t* seg_stat, int64_t* seg_grad, int64_t* seg_ag);
 
 typedef struct spngd_opt spngd_opt;
 
@@ -267,6 +270,12 @@ int spngd_opt_step(spngd_opt* opt, int64_t step, double eta, double momentum);
 int spngd_opt_phase_ms(spngd_opt* opt, float* out6);
 /* Number of kernels the last step launched on this rank. */
 int64_t spngd_opt_launch_count(const spngd_opt* opt);
+/* Stale gating (cfg.stale): tracker state of statistic `which` (0 A, 1 G,
+ * 2 BN F) of `layer` -- next refresh step t_X, interval, refresh count --
+ * and whether it refreshed in the last step (StaleTracker, stale.hpp:92-132;
+ * gating dist.cpp:431-444). */
+int spngd_opt_stale_info(spngd_opt* opt, int layer, int which, int64_t* t_x, int64_t* delta,
+                         int64_t* refresh_count, int* due_last);
 
 #ifdef __cplusplus
 }

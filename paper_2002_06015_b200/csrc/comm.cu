@@ -6,6 +6,7 @@
 #include <nccl.h>
 
 #include <cstring>
+#include <vector>
 
 #include "ctx.cuh"
 
@@ -18,6 +19,33 @@ using namespace spngd;
   } while (0)
 
 namespace spngd {
+// Grouped ncclReduce(avg) of variable segments to their owners: the
+// ReduceScatterV of a partial (stale-gated) statistic set, dist.cpp:510-537.
+int comm_reduce_to_owners(spngd_ctx* ctx, const std::vector<OwnerReduce>& ops) {
+  if (ops.empty()) return SPNGD_OK;
+  if (ctx->world == 1) {
+    for (const OwnerReduce& r : ops)
+      if (r.send != r.recv && r.count > 0)
+        SPNGD_CUDA_TRY(cudaMemcpyAsync(r.recv, r.send, r.count * sizeof(float), cudaMemcpyDeviceToDevice, ctx->stream));
+    return SPNGD_OK;
+  }
+  if (!ctx->comm) return fail(SPNGD_ERR_NCCL, "reduce_to_owners: communicator not initialised");
+  ncclComm_t comm = reinterpret_cast<ncclComm_t>(ctx->comm);
+  SPNGD_NCCL_TRY(ncclGroupStart());
+  for (const OwnerReduce& r : ops)
+    SPNGD_NCCL_TRY(ncclReduce(r.send, r.recv, size_t(r.count), ncclFloat, ncclAvg, r.root, comm, ctx->stream));
+  SPNGD_NCCL_TRY(ncclGroupEnd());
+  return SPNGD_OK;
+}
+
+int comm_allreduce_sum_f64(spngd_ctx* ctx, double* buf, int64_t count) {
+  if (ctx->world == 1 || count <= 0) return SPNGD_OK;
+  if (!ctx->comm) return fail(SPNGD_ERR_NCCL, "allreduce: communicator not initialised");
+  SPNGD_NCCL_TRY(ncclAllReduce(buf, buf, size_t(count), ncclDouble, ncclSum, reinterpret_cast<ncclComm_t>(ctx->comm),
+                               ctx->stream));
+  return SPNGD_OK;
+}
+
 void comm_destroy(spngd_ctx* ctx) {
   if (ctx && ctx->comm) {
     ncclCommDestroy(reinterpret_cast<ncclComm_t>(ctx->comm));

@@ -55,6 +55,14 @@ inline int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
 
 // Chooses the split-K chunk so a grouped launch has ~`waves` work items per SM.
 void comm_destroy(spngd_ctx* ctx);  // comm.cu
+struct OwnerReduce {
+  const float* send;
+  float* recv;
+  int64_t count;
+  int root;
+};
+int comm_reduce_to_owners(spngd_ctx* ctx, const std::vector<OwnerReduce>& ops);  // comm.cu
+int comm_allreduce_sum_f64(spngd_ctx* ctx, double* buf, int64_t count);        // comm.cu
 
 int choose_kchunk(const std::vector<std::pair<int64_t, int64_t>>& tiles_and_k, int waves = 6);
 

@@ -1,8 +1,9 @@
 // The whole SP-NGD optimizer step on one rank: Stages 2-5 of
 // accumulate_microsteps (src/dist.cpp:406-675) with n = 1 micro-step.
 //
-//   factors + BN moments (local shard)  -> RS send buffer, owner-major
-//   ncclReduceScatter(avg)               -> owner receives the shard means
+//   factors + BN moments (local shard)  -> RS send buffer: a statistics region
+//                                           and a gradient region, each owner-major
+//   ncclReduceScatter(avg) per region    -> owner receives the shard means
 //   pi, damping, Cholesky inverse        (owned Kronecker layers)
 //   precondition + momentum + rescale    (owned FC/Conv layers, in place in
 //   BN 2x2 solve + update                 the all-gather buffer)
@@ -13,6 +14,16 @@
 // numerics.  All plans (GEMM problems, tiles, tasks) are built once at creation
 // and stay device-resident; a step is a fixed sequence of launches on the
 // context stream, bracketed by CUDA events per phase.
+//
+// Stale gating (cfg.stale, dist.cpp:431-444 / 514-537 / 588-601): every
+// statistic A:l, G:l, F:l has a StaleTracker (tracker.cu, identical on every
+// rank).  A step builds, reduces (grouped ncclReduce to the owners when only
+// some are due) and re-inverts only the due statistics -- both inverses of a
+// layer when either factor refreshed -- while gradients, precondition, update
+// and all-gather run every step.  The owner compares each fresh statistic
+// with its two retained snapshots on the device (K8), the distances are
+// all-reduced, and every rank's trackers advance from them at the start of
+// the next step (no mid-step host sync).
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -47,7 +58,8 @@ struct LayerState {
   float* grad = nullptr;
   float* gg = nullptr;
   float* gb = nullptr;
-  // RS send offsets (floats within this owner's segment)
+  // RS offsets: off_A/G/M within the owner's statistics segment, off_dW
+  // within the owner's gradient segment (floats)
   int64_t off_A = -1, off_G = -1, off_M = -1, off_dW = -1;
   // AG offsets (within the owner segment)
   int64_t off_W = -1;
@@ -57,6 +69,20 @@ struct LayerState {
   float* Ginv = nullptr; int64_t ldg = 0;
 };
 
+// One stale-gated statistic (A:l, G:l or F:l).
+struct StatState {
+  int layer = 0;
+  int kind = 0;            // 0 A, 1 G, 2 F (BN 3c moments)
+  int owner = 0;
+  int64_t off = 0;         // within the owner's statistics segment
+  int64_t count = 0;       // floats
+  int64_t dim = 0;         // packed dimension n (A/G) or channels c (F)
+  spngd_tracker* tr = nullptr;
+  int nsnap = 0;           // retained snapshots (identical on every rank)
+  float* snap[2] = {};     // owner only; snap[first] = x1, snap[first^1] = x2
+  int first = 0;
+};
+
 }  // namespace
 
 struct spngd_opt {
@@ -64,9 +90,9 @@ struct spngd_opt {
   spngd_opt_config cfg{};
   std::vector<LayerState> layers;
   int world = 1, rank = 0;
-  int64_t seg_rs = 0, seg_ag = 0;  // per-owner padded segment sizes (floats)
-  float* rs_send = nullptr;        // world * seg_rs
-  float* rs_recv = nullptr;        // seg_rs (== rs_send when world == 1)
+  int64_t seg_stat = 0, seg_grad = 0, seg_ag = 0;  // per-owner padded segment sizes (floats)
+  float* rs_send = nullptr;        // world * seg_stat | world * seg_grad
+  float* rs_recv = nullptr;        // seg_stat | seg_grad (== rs_send when world == 1)
   float* ag = nullptr;             // world * seg_ag
   std::vector<void*> owned;        // every device allocation
   // plans
@@ -85,6 +111,14 @@ struct spngd_opt {
     BaseTask* d_bases = nullptr;
     cudaStream_t stream = nullptr;
     cudaEvent_t done = nullptr;
+    // stale gating: the class members and room for a re-planned subset
+    std::vector<DenseMatrix> mats;
+    std::vector<int> mat_layer;
+    float* ws = nullptr;
+    InversePlan dyn;
+    GemmProblem* d_probs_dyn = nullptr;
+    GemmWorkItem* d_items_dyn = nullptr;
+    BaseTask* d_bases_dyn = nullptr;
   };
   std::vector<InvClass> inv;
   cudaEvent_t inv_fork = nullptr;
@@ -101,6 +135,20 @@ struct spngd_opt {
   cudaEvent_t ev[7] = {};
   int64_t launches = 0;
   bool timed = false;
+  // ---- stale gating
+  std::vector<StatState> stats;
+  std::vector<int> prob_stat, reduce_stat, repack_stat, bnm_stat;  // plan entry -> statistic
+  GemmWorkItem* d_fitems_dyn = nullptr; SyrkReduceTask* d_freduce_dyn = nullptr;
+  RepackTask* d_repack_dyn = nullptr; spngd_bn_moments_req* d_bnm_dyn = nullptr;
+  std::vector<int> pi_layer;                 // owned Kronecker layers in pis order
+  PiTask* d_pis_dyn = nullptr; UnpackTask* d_unpacks_dyn = nullptr;
+  spngd_stat_req* d_statreq = nullptr;
+  double* d_dist = nullptr; double* h_dist = nullptr;  // 4 per statistic
+  cudaEvent_t dist_ev = nullptr;
+  struct Pending { int q, has1, has2; };
+  std::vector<Pending> pending; int64_t pending_step = 0;
+  std::vector<char> due;
+  int64_t last_due = 0;
 
   float* alloc(size_t floats, bool zero = false) {
     void* p = nullptr;
@@ -120,6 +168,10 @@ struct spngd_opt {
       if (c.stream) cudaStreamDestroy(c.stream);
     }
     if (inv_fork) cudaEventDestroy(inv_fork);
+    if (dist_ev) cudaEventDestroy(dist_ev);
+    if (h_dist) cudaFreeHost(h_dist);
+    for (auto& st : stats)
+      if (st.tr) spngd_tracker_destroy(st.tr);
     for (auto& e : ev)
       if (e) cudaEventDestroy(e);
     for (void* p : owned) cudaFree(p);
@@ -137,7 +189,7 @@ double layer_cost(const spngd_layer_desc& d) {
 int build(spngd_opt* o, const spngd_layer_desc* descs, int n) {
   const int W = o->world;
   std::vector<spngd_layout_entry> lay(n);
-  int rc0 = spngd_plan_layout(descs, n, W, lay.data(), &o->seg_rs, &o->seg_ag);
+  int rc0 = spngd_plan_layout(descs, n, W, lay.data(), &o->seg_stat, &o->seg_grad, &o->seg_ag);
   if (rc0) return rc0;
   o->layers.resize(n);
   for (int li = 0; li < n; ++li) {
@@ -150,24 +202,37 @@ int build(spngd_opt* o, const spngd_layer_desc* descs, int n) {
     L.off_dW = lay[li].off_dW;
     L.off_W = lay[li].off_W;
   }
-  o->rs_send = o->alloc(size_t(W) * o->seg_rs, true);
-  o->rs_recv = (W == 1) ? o->rs_send : o->alloc(o->seg_rs, true);
+  o->rs_send = o->alloc(size_t(W) * (o->seg_stat + o->seg_grad), true);
+  o->rs_recv = (W == 1) ? o->rs_send : o->alloc(o->seg_stat + o->seg_grad, true);
   o->ag = o->alloc(size_t(W) * o->seg_ag, true);
   if (!o->rs_send || !o->rs_recv || !o->ag) return fail(SPNGD_ERR_CUDA, "opt: buffer allocation failed");
 
   const int64_t B = o->cfg.batch;
   std::vector<spngd_factor_req> freqs;
   std::vector<DenseMatrix> mats;
+  std::vector<int> mat_layer;
   std::vector<spngd_precond_req> preqs;
   int n_owned_kron = 0;
   for (int li = 0; li < n; ++li) {
     LayerState& L = o->layers[li];
-    float* seg = o->rs_send + int64_t(L.owner) * o->seg_rs;
+    float* seg = o->rs_send + int64_t(L.owner) * o->seg_stat;
+    auto add_stat = [&](int kind, int64_t off, int64_t count, int64_t dim) {
+      StatState st;
+      st.layer = li;
+      st.kind = kind;
+      st.owner = L.owner;
+      st.off = off;
+      st.count = count;
+      st.dim = dim;
+      o->stats.push_back(st);
+      return int(o->stats.size()) - 1;
+    };
     if (L.d.kind == SPNGD_BN) {
       const int64_t c = L.d.g;
       L.gg = o->alloc(size_t(B * c));
       L.gb = o->alloc(size_t(B * c));
       o->bnm.push_back({L.gg, L.gb, c, 0, B, seg + L.off_M});
+      o->bnm_stat.push_back(add_stat(2, L.off_M, 3 * c, c));
       o->bnm_maxc = std::max(o->bnm_maxc, c);
     } else {
       const bool conv = L.d.kind == SPNGD_CONV;
@@ -177,7 +242,9 @@ int build(spngd_opt* o, const spngd_layer_desc* descs, int n) {
       if (!L.act || !L.grad) return fail(SPNGD_ERR_CUDA, "opt: capture allocation failed");
       const double nb = double(B);
       freqs.push_back({L.act, L.d.a, hw, conv ? 1 : 0, 0, B, conv ? 1.0 / (nb * double(hw)) : 1.0 / nb, seg + L.off_A});
+      o->prob_stat.push_back(add_stat(0, L.off_A, L.d.a * (L.d.a + 1) / 2, L.d.a));
       freqs.push_back({L.grad, L.d.g, hw, conv ? 1 : 0, 0, B, 1.0 / nb, seg + L.off_G});
+      o->prob_stat.push_back(add_stat(1, L.off_G, L.d.g * (L.d.g + 1) / 2, L.d.g));
     }
   }
   // ---- owner-local state and plans
@@ -192,7 +259,7 @@ int build(spngd_opt* o, const spngd_layer_desc* descs, int n) {
       L.V = o->alloc(size_t(2 * c), true);
       spngd_bn_update_req r{};
       r.m3c = o->rs_recv + L.off_M;
-      r.grad = o->rs_recv + L.off_dW;
+      r.grad = o->rs_recv + o->seg_stat + L.off_dW;
       r.c = c;
       r.gamma = wseg + L.off_W;
       r.beta = wseg + L.off_W + c;
@@ -217,15 +284,18 @@ int build(spngd_opt* o, const spngd_layer_desc* descs, int n) {
     float* dA = o->d_damps + 2 * li;
     float* dG = dA + 1;
     o->pis.push_back({o->rs_recv + L.off_A, o->rs_recv + L.off_G, a, g, std::sqrt(o->cfg.lambda), dA, dG, nullptr});
+    o->pi_layer.push_back(li);
     o->unpacks.push_back({o->rs_recv + L.off_A, a, dA, 0.f, 0, L.Ainv, L.lda});
     o->unpacks.push_back({o->rs_recv + L.off_G, g, dG, 0.f, 0, L.Ginv, L.ldg});
     o->max_n = std::max({o->max_n, a, g});
     mats.push_back({L.Ainv, tla, tua, L.lda, a});
+    mat_layer.push_back(li);
     mats.push_back({L.Ginv, tlg, tug, L.ldg, g});
+    mat_layer.push_back(li);
     spngd_precond_req pr{};
     pr.Ginv = L.Ginv; pr.ldg = L.ldg;
     pr.Ainv = L.Ainv; pr.lda = L.lda;
-    pr.dW = o->rs_recv + L.off_dW;
+    pr.dW = o->rs_recv + o->seg_stat + L.off_dW;
     pr.g = g; pr.a = a;
     pr.W = wseg + L.off_W;
     pr.V = L.V;
@@ -259,18 +329,25 @@ int build(spngd_opt* o, const spngd_layer_desc* descs, int n) {
     sizes.erase(std::unique(sizes.begin(), sizes.end()), sizes.end());
     std::reverse(sizes.begin(), sizes.end());  // largest (critical path) first
     for (int64_t n : sizes) {
-      std::vector<DenseMatrix> cls;
-      for (const auto& m : mats)
-        if (m.n == n) cls.push_back(m);
       o->inv.emplace_back();
       spngd_opt::InvClass& c = o->inv.back();
+      for (size_t m = 0; m < mats.size(); ++m)
+        if (mats[m].n == n) {
+          c.mats.push_back(mats[m]);
+          c.mat_layer.push_back(mat_layer[m]);
+        }
       InversePlan sizing;
-      plan_inverse(cls, nullptr, sizing);
-      float* ws = o->alloc(sizing.workspace_floats);
-      plan_inverse(cls, ws, c.plan);
+      plan_inverse(c.mats, nullptr, sizing);
+      c.ws = o->alloc(sizing.workspace_floats);
+      plan_inverse(c.mats, c.ws, c.plan);
       c.d_probs = dev_upload(c.plan.probs, own);
       c.d_items = dev_upload(c.plan.items, own);
       c.d_bases = dev_upload(c.plan.bases, own);
+      if (o->cfg.stale) {  // room for a re-planned subset (never larger than the full class plan)
+        c.d_probs_dyn = dev_upload(c.plan.probs, own);
+        c.d_items_dyn = dev_upload(c.plan.items, own);
+        c.d_bases_dyn = dev_upload(c.plan.bases, own);
+      }
       SPNGD_CUDA_TRY(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
       SPNGD_CUDA_TRY(cudaEventCreateWithFlags(&c.done, cudaEventDisableTiming));
     }
@@ -292,6 +369,47 @@ int build(spngd_opt* o, const spngd_layer_desc* descs, int n) {
   o->d_rescale = dev_upload(o->pplan.rescale, own);
   o->d_bnu = dev_upload(o->bnu, own);
   for (auto& e : o->ev) SPNGD_CUDA_TRY(cudaEventCreate(&e));
+  if (o->cfg.stale) {
+    // plan entry -> statistic maps for the filtered (partial-refresh) launches
+    auto stat_of_ptr = [&](const float* p) {
+      for (size_t q = 0; q < o->stats.size(); ++q) {
+        const StatState& st = o->stats[q];
+        const float* b = o->rs_send + int64_t(st.owner) * o->seg_stat + st.off;
+        if (p >= b && p < b + st.count) return int(q);
+      }
+      return -1;
+    };
+    for (const auto& t : o->fplan.reduce) o->reduce_stat.push_back(stat_of_ptr(t.packed_out));
+    for (const auto& t : o->fplan.repacks) {
+      int q = -1;
+      for (size_t f = 0; f < freqs.size(); ++f)
+        if (freqs[f].x == t.src) q = o->prob_stat[f];
+      o->repack_stat.push_back(q);
+    }
+    for (int q : o->reduce_stat)
+      if (q < 0) return fail(SPNGD_ERR_INVALID, "opt: unmapped reduction task");
+    o->d_fitems_dyn = dev_upload(o->fplan.items, own);
+    o->d_freduce_dyn = dev_upload(o->fplan.reduce, own);
+    o->d_repack_dyn = dev_upload(o->fplan.repacks, own);
+    o->d_bnm_dyn = dev_upload(o->bnm, own);
+    o->d_pis_dyn = dev_upload(o->pis, own);
+    o->d_unpacks_dyn = dev_upload(o->unpacks, own);
+    std::vector<spngd_stat_req> sr(o->stats.size());
+    o->d_statreq = dev_upload(sr, own);
+    o->d_dist = reinterpret_cast<double*>(o->alloc(8 * o->stats.size(), true));
+    SPNGD_CUDA_TRY(cudaMallocHost(&o->h_dist, 4 * sizeof(double) * o->stats.size()));
+    SPNGD_CUDA_TRY(cudaEventCreateWithFlags(&o->dist_ev, cudaEventDisableTiming));
+    static const char* kinds[3] = {"A", "G", "F"};
+    for (auto& st : o->stats) {
+      const std::string id = std::string(kinds[st.kind]) + ":" + std::to_string(st.layer);
+      st.tr = spngd_tracker_create(id.c_str(), o->cfg.stale_alpha);
+      if (st.owner == o->rank) {
+        st.snap[0] = o->alloc(size_t(st.count));
+        st.snap[1] = o->alloc(size_t(st.count));
+        if (!st.snap[0] || !st.snap[1]) return fail(SPNGD_ERR_CUDA, "opt: snapshot allocation failed");
+      }
+    }
+  }
   SPNGD_CUDA_TRY(cudaDeviceSynchronize());
   return SPNGD_OK;
 }
@@ -300,8 +418,8 @@ int build(spngd_opt* o, const spngd_layer_desc* descs, int n) {
 
 extern "C" {
 
-int spngd_plan_layout(const spngd_layer_desc* descs, int n, int W, spngd_layout_entry* out, int64_t* seg_rs,
-                      int64_t* seg_ag) {
+int spngd_plan_layout(const spngd_layer_desc* descs, int n, int W, spngd_layout_entry* out, int64_t* seg_stat,
+                      int64_t* seg_grad, int64_t* seg_ag) {
   if (!descs || !out || n <= 0 || W < 1) return fail(SPNGD_ERR_INVALID, "spngd_plan_layout: bad argument");
   // ownership: LPT on inverse + precondition cost, deterministic tie-break
   std::vector<int> order(n);
@@ -314,8 +432,9 @@ int spngd_plan_layout(const spngd_layer_desc* descs, int n, int W, spngd_layout_
     out[li].owner = r;
     load[r] += layer_cost(descs[li]);
   }
-  // owner-major segment layout, 64-float aligned entries, in layer order
-  std::vector<int64_t> rs_fill(W, 0), ag_fill(W, 0);
+  // owner-major segment layouts (statistics, gradients, weights), 64-float
+  // aligned entries, in layer order
+  std::vector<int64_t> st_fill(W, 0), gr_fill(W, 0), ag_fill(W, 0);
   auto place = [](int64_t& fill, int64_t cnt) {
     const int64_t off = fill;
     fill += round_up(cnt, 64);
@@ -328,17 +447,18 @@ int spngd_plan_layout(const spngd_layer_desc* descs, int n, int W, spngd_layout_
     e.pad_ = 0;
     e.off_A = e.off_G = e.off_M = -1;
     if (d.kind == SPNGD_BN) {
-      e.off_M = place(rs_fill[r], 3 * d.g);
-      e.off_dW = place(rs_fill[r], 2 * d.g);
+      e.off_M = place(st_fill[r], 3 * d.g);
+      e.off_dW = place(gr_fill[r], 2 * d.g);
       e.off_W = place(ag_fill[r], 2 * d.g);
     } else {
-      e.off_A = place(rs_fill[r], d.a * (d.a + 1) / 2);
-      e.off_G = place(rs_fill[r], d.g * (d.g + 1) / 2);
-      e.off_dW = place(rs_fill[r], d.g * d.a);
+      e.off_A = place(st_fill[r], d.a * (d.a + 1) / 2);
+      e.off_G = place(st_fill[r], d.g * (d.g + 1) / 2);
+      e.off_dW = place(gr_fill[r], d.g * d.a);
       e.off_W = place(ag_fill[r], d.g * d.a);
     }
   }
-  if (seg_rs) *seg_rs = std::max<int64_t>(64, *std::max_element(rs_fill.begin(), rs_fill.end()));
+  if (seg_stat) *seg_stat = std::max<int64_t>(64, *std::max_element(st_fill.begin(), st_fill.end()));
+  if (seg_grad) *seg_grad = std::max<int64_t>(64, *std::max_element(gr_fill.begin(), gr_fill.end()));
   if (seg_ag) *seg_ag = std::max<int64_t>(64, *std::max_element(ag_fill.begin(), ag_fill.end()));
   return SPNGD_OK;
 }
@@ -348,7 +468,7 @@ int spngd_opt_create(spngd_ctx* ctx, const spngd_layer_desc* layers, int n_layer
   if (!ctx || !layers || n_layers <= 0 || !cfg || !out) return fail(SPNGD_ERR_INVALID, "spngd_opt_create: bad argument");
   if (!(cfg->lambda > 0.0)) return fail(SPNGD_ERR_NOT_POSITIVE_DEFINITE, "OptimizerConfig: lambda must be > 0");
   if (cfg->batch < 1) return fail(SPNGD_ERR_EMPTY_BATCH, "spngd_opt_create: empty per-rank batch");
-  if (cfg->stale) return fail(SPNGD_ERR_INVALID, "spngd_opt_create: stale gating runs through spngd_tracker_* (not fused yet)");
+  if (cfg->stale && !(cfg->stale_alpha > 0.0)) return fail(SPNGD_ERR_INVALID, "spngd_opt_create: stale_alpha must be > 0");
   for (int i = 0; i < n_layers; ++i) {
     const auto& d = layers[i];
     if (d.kind < 0 || d.kind > 2 || d.g <= 0 || (d.kind != SPNGD_BN && (d.a <= 0 || d.hw <= 0)))
@@ -384,7 +504,7 @@ float* spngd_opt_buffer(spngd_opt* o, int layer, int which, int64_t* ld) {
   switch (which) {
     case 0: return L.act;
     case 1: return L.grad;
-    case 2: return L.off_dW >= 0 ? o->rs_send + int64_t(L.owner) * o->seg_rs + L.off_dW : nullptr;
+    case 2: return L.off_dW >= 0 ? o->rs_send + int64_t(o->world) * o->seg_stat + int64_t(L.owner) * o->seg_grad + L.off_dW : nullptr;
     case 3: return o->ag + int64_t(L.owner) * o->seg_ag + L.off_W;
     case 4: return mine ? L.V : nullptr;
     case 5: return L.gg;
@@ -422,7 +542,12 @@ int issue_phase(spngd_opt* o, int phase) {
       if (!rc) rc = launch_bn_moments(ctx, o->d_bnm, int(o->bnm.size()), o->bnm_maxc);
       return rc;
     case 2:  // Stages 2-3: ReduceScatterV of A, G/F and grads (dist.cpp:510-537).
-      if (o->world > 1) rc = spngd_reduce_scatter_mean(ctx, o->rs_send, o->rs_recv, o->seg_rs);
+      if (o->world > 1) {
+        rc = spngd_reduce_scatter_mean(ctx, o->rs_send, o->rs_recv, o->seg_stat);
+        if (!rc)
+          rc = spngd_reduce_scatter_mean(ctx, o->rs_send + int64_t(o->world) * o->seg_stat, o->rs_recv + o->seg_stat,
+                                         o->seg_grad);
+      }
       return rc;
     case 3: {  // Stage 4a: pi, damping, inverse (dist.cpp:539-602); size classes
                // fork onto their own streams and join.
@@ -455,46 +580,256 @@ int issue_phase(spngd_opt* o, int phase) {
 
 }  // namespace
 
+namespace {
+
+template <typename T>
+int upload_async(spngd_ctx* ctx, T* dst, const std::vector<T>& v) {
+  // pageable source: staged before the call returns, so v may die right after
+  if (!v.empty()) SPNGD_CUDA_TRY(cudaMemcpyAsync(dst, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, ctx->stream));
+  return SPNGD_OK;
+}
+
+// Advances every tracker from the distances of the last refresh step
+// (StaleTracker::on_refresh, stale.hpp:100-114).
+int stale_apply_pending(spngd_opt* o) {
+  if (o->pending.empty()) return SPNGD_OK;
+  SPNGD_CUDA_TRY(cudaEventSynchronize(o->dist_ev));
+  for (const auto& p : o->pending) {
+    double d[4];  // the device reduction leaves weighted squares
+    for (int k = 0; k < 4; ++k) d[k] = std::sqrt(std::max(o->h_dist[4 * p.q + k], 0.0));
+    int64_t next = 0;
+    int reason = 0;
+    int rc = spngd_tracker_on_refresh(o->stats[p.q].tr, o->pending_step, p.has1, d[0], d[1], p.has2, d[2], d[3], &next,
+                                      &reason);
+    if (rc) return rc;
+  }
+  o->pending.clear();
+  return SPNGD_OK;
+}
+
+// Partial refresh: the factor, reduction, RS and inverse work of the due
+// statistics only (dist.cpp:510-602).
+int stale_partial_phase(spngd_opt* o, int phase) {
+  spngd_ctx* ctx = o->ctx;
+  cudaStream_t s = ctx->stream;
+  const auto& due = o->due;
+  int rc = SPNGD_OK;
+  switch (phase) {
+    case 0: {
+      std::vector<RepackTask> rp;
+      for (size_t i = 0; i < o->fplan.repacks.size(); ++i)
+        if (o->repack_stat[i] >= 0 && due[o->repack_stat[i]]) rp.push_back(o->fplan.repacks[i]);
+      std::vector<GemmWorkItem> it;
+      for (const auto& w : o->fplan.items)
+        if (due[o->prob_stat[w.problem]]) it.push_back(w);
+      if ((rc = upload_async(ctx, o->d_repack_dyn, rp))) return rc;
+      if ((rc = upload_async(ctx, o->d_fitems_dyn, it))) return rc;
+      rc = launch_repack(ctx, o->d_repack_dyn, int(rp.size()), o->fplan.repack_max);
+      if (!rc && !it.empty()) {
+        rc = launch_gemm(o->d_fprobs, o->d_fitems_dyn, int(it.size()), o->d_partials, ctx->d_status, s);
+        ctx->launches++;
+      }
+      return rc;
+    }
+    case 1: {
+      std::vector<SyrkReduceTask> red;
+      for (size_t i = 0; i < o->fplan.reduce.size(); ++i)
+        if (due[o->reduce_stat[i]]) red.push_back(o->fplan.reduce[i]);
+      std::vector<spngd_bn_moments_req> bm;
+      for (size_t i = 0; i < o->bnm.size(); ++i)
+        if (due[o->bnm_stat[i]]) bm.push_back(o->bnm[i]);
+      if ((rc = upload_async(ctx, o->d_freduce_dyn, red))) return rc;
+      if ((rc = upload_async(ctx, o->d_bnm_dyn, bm))) return rc;
+      rc = launch_syrk_reduce(o->d_freduce_dyn, int(red.size()), o->d_partials, s);
+      ctx->launches += !red.empty();
+      if (!rc) rc = launch_bn_moments(ctx, o->d_bnm_dyn, int(bm.size()), o->bnm_maxc);
+      return rc;
+    }
+    case 2: {  // gradients always; due statistics reduced to their owners
+      if (o->world > 1) {
+        rc = spngd_reduce_scatter_mean(ctx, o->rs_send + int64_t(o->world) * o->seg_stat, o->rs_recv + o->seg_stat,
+                                       o->seg_grad);
+        if (rc) return rc;
+      }
+      std::vector<OwnerReduce> ops;
+      for (size_t q = 0; q < o->stats.size(); ++q) {
+        if (!due[q]) continue;
+        const StatState& st = o->stats[q];
+        ops.push_back({o->rs_send + int64_t(st.owner) * o->seg_stat + st.off, o->rs_recv + st.off, st.count, st.owner});
+      }
+      return o->world > 1 ? comm_reduce_to_owners(ctx, ops) : SPNGD_OK;
+    }
+    case 3: {  // re-invert both factors of every owned layer with a refreshed A or G
+      std::vector<char> touched(o->layers.size(), 0);
+      for (size_t q = 0; q < o->stats.size(); ++q)
+        if (due[q] && o->stats[q].kind != 2) touched[o->stats[q].layer] = 1;
+      std::vector<PiTask> pis;
+      std::vector<UnpackTask> ups;
+      for (size_t k = 0; k < o->pi_layer.size(); ++k)
+        if (touched[o->pi_layer[k]]) {
+          pis.push_back(o->pis[k]);
+          ups.push_back(o->unpacks[2 * k]);
+          ups.push_back(o->unpacks[2 * k + 1]);
+        }
+      if (pis.empty()) return SPNGD_OK;
+      if ((rc = upload_async(ctx, o->d_pis_dyn, pis))) return rc;
+      if ((rc = upload_async(ctx, o->d_unpacks_dyn, ups))) return rc;
+      rc = launch_pi(ctx, o->d_pis_dyn, int(pis.size()));
+      if (!rc) rc = launch_unpack(ctx, o->d_unpacks_dyn, int(ups.size()), o->max_n);
+      if (rc) return rc;
+      SPNGD_CUDA_TRY(cudaEventRecord(o->inv_fork, s));
+      for (auto& c : o->inv) {
+        std::vector<DenseMatrix> sub;
+        for (size_t m = 0; m < c.mats.size(); ++m)
+          if (touched[c.mat_layer[m]]) sub.push_back(c.mats[m]);
+        if (sub.empty()) continue;
+        plan_inverse(sub, c.ws, c.dyn);
+        if ((rc = upload_async(ctx, c.d_probs_dyn, c.dyn.probs))) return rc;
+        if ((rc = upload_async(ctx, c.d_items_dyn, c.dyn.items))) return rc;
+        if ((rc = upload_async(ctx, c.d_bases_dyn, c.dyn.bases))) return rc;
+        SPNGD_CUDA_TRY(cudaStreamWaitEvent(c.stream, o->inv_fork, 0));
+        ctx->stream = c.stream;
+        rc = run_inverse(ctx, c.dyn, c.d_probs_dyn, c.d_items_dyn, c.d_bases_dyn);
+        ctx->stream = s;
+        if (rc) return rc;
+        SPNGD_CUDA_TRY(cudaEventRecord(c.done, c.stream));
+        SPNGD_CUDA_TRY(cudaStreamWaitEvent(s, c.done, 0));
+      }
+      return SPNGD_OK;
+    }
+  }
+  return SPNGD_OK;
+}
+
+// The owners compare every refreshed statistic with its retained snapshots
+// (similar(), stale.hpp:56-64, on the device), rotate the snapshots, and all
+// ranks receive the distances for the next step's tracker update.
+int stale_similarity(spngd_opt* o, int64_t step) {
+  spngd_ctx* ctx = o->ctx;
+  cudaStream_t s = ctx->stream;
+  std::vector<spngd_stat_req> reqs;
+  int64_t max_rows = 0;
+  o->pending.clear();
+  for (size_t q = 0; q < o->stats.size(); ++q) {
+    if (!o->due[q]) continue;
+    StatState& st = o->stats[q];
+    o->pending.push_back({int(q), st.nsnap >= 1 ? 1 : 0, st.nsnap >= 2 ? 1 : 0});
+    if (st.owner == o->rank) {
+      spngd_stat_req r{};
+      r.x = o->rs_recv + st.off;
+      r.x1 = st.nsnap >= 1 ? st.snap[st.first] : nullptr;
+      r.x2 = st.nsnap >= 2 ? st.snap[st.first ^ 1] : nullptr;
+      r.n = st.dim;
+      r.kind = st.kind == 2 ? 1 : 0;
+      r.out4 = o->d_dist + 4 * q;
+      reqs.push_back(r);
+      max_rows = std::max(max_rows, r.kind == 0 ? r.n : (3 * r.n + 255) / 256);
+    }
+  }
+  o->pending_step = step;
+  SPNGD_CUDA_TRY(cudaMemsetAsync(o->d_dist, 0, 4 * sizeof(double) * o->stats.size(), s));
+  int rc = upload_async(ctx, o->d_statreq, reqs);
+  if (!rc && !reqs.empty()) rc = launch_stat_distance(ctx, o->d_statreq, int(reqs.size()), max_rows);
+  if (rc) return rc;
+  // snapshot rotation (x2 <- x1, x1 <- x) after the distances read them
+  for (const auto& p : o->pending) {
+    StatState& st = o->stats[p.q];
+    if (st.owner == o->rank) {
+      float* dst = st.snap[st.first ^ 1];
+      SPNGD_CUDA_TRY(cudaMemcpyAsync(dst, o->rs_recv + st.off, st.count * sizeof(float), cudaMemcpyDeviceToDevice, s));
+      st.first ^= 1;
+    }
+    st.nsnap = std::min(2, st.nsnap + 1);
+  }
+  rc = comm_allreduce_sum_f64(ctx, o->d_dist, 4 * int64_t(o->stats.size()));
+  if (rc) return rc;
+  SPNGD_CUDA_TRY(cudaMemcpyAsync(o->h_dist, o->d_dist, 4 * sizeof(double) * o->stats.size(), cudaMemcpyDeviceToHost, s));
+  SPNGD_CUDA_TRY(cudaEventRecord(o->dist_ev, s));
+  return SPNGD_OK;
+}
+
+}  // namespace
+
 extern "C" {
 
 int spngd_opt_step(spngd_opt* o, int64_t step, double eta, double momentum) {
   if (!o) return fail(SPNGD_ERR_INVALID, "spngd_opt_step: opt is NULL");
-  (void)step;
   spngd_ctx* ctx = o->ctx;
   cudaStream_t s = ctx->stream;
   // Host scalars of this step -> device (outside the graphs).  Pageable
   // source: staged before cudaMemcpyAsync returns, so no host sync.
   const float scal[2] = {float(eta), float(momentum)};
   SPNGD_CUDA_TRY(cudaMemcpyAsync(o->d_scal, scal, sizeof(scal), cudaMemcpyHostToDevice, s));
-  const bool capture = o->use_graph && !o->graphs_ready;
+  // stale gating: which statistics refresh this step (dist.cpp:431-444)
+  bool full = true, any = true;
+  if (o->cfg.stale) {
+    int rc = stale_apply_pending(o);
+    if (rc) return rc;
+    o->due.assign(o->stats.size(), 0);
+    int64_t n_due = 0;
+    for (size_t q = 0; q < o->stats.size(); ++q) {
+      o->due[q] = char(spngd_tracker_should_refresh(o->stats[q].tr, step));
+      n_due += o->due[q];
+    }
+    o->last_due = n_due;
+    full = n_due == int64_t(o->stats.size());
+    any = n_due > 0;
+  }
+  const bool capture = o->use_graph && !o->graphs_ready && full;
   const int64_t l0 = ctx->launches;
   for (int ph = 0; ph < 6; ++ph) {
     SPNGD_CUDA_TRY(cudaEventRecord(o->ev[ph], s));
-    if (!o->use_graph) {
+    const bool gated = ph <= 3 && !full;
+    if (gated) {
+      if (any || ph == 2) {
+        int rc = stale_partial_phase(o, ph);
+        if (rc) return rc;
+      }
+    } else if (!o->use_graph || (!o->graphs_ready && !capture)) {
       int rc = issue_phase(o, ph);
       if (rc) return rc;
-      continue;
-    }
-    if (capture) {
-      SPNGD_CUDA_TRY(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
-      int rc = issue_phase(o, ph);
-      cudaGraph_t g = nullptr;
-      cudaError_t e = cudaStreamEndCapture(s, &g);
-      if (rc) {
-        if (g) cudaGraphDestroy(g);
-        return rc;
+    } else {
+      if (capture) {
+        SPNGD_CUDA_TRY(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+        int rc = issue_phase(o, ph);
+        cudaGraph_t g = nullptr;
+        cudaError_t e = cudaStreamEndCapture(s, &g);
+        if (rc) {
+          if (g) cudaGraphDestroy(g);
+          return rc;
+        }
+        if (e != cudaSuccess) return fail_cuda(e, "cudaStreamEndCapture");
+        o->graphs[ph] = g;
+        SPNGD_CUDA_TRY(cudaGraphInstantiate(&o->graph_exec[ph], g, 0));
       }
-      if (e != cudaSuccess) return fail_cuda(e, "cudaStreamEndCapture");
-      o->graphs[ph] = g;
-      SPNGD_CUDA_TRY(cudaGraphInstantiate(&o->graph_exec[ph], g, 0));
+      SPNGD_CUDA_TRY(cudaGraphLaunch(o->graph_exec[ph], s));
     }
-    SPNGD_CUDA_TRY(cudaGraphLaunch(o->graph_exec[ph], s));
+    if (ph == 3 && o->cfg.stale && any) {
+      int rc = stale_similarity(o, step);
+      if (rc) return rc;
+    }
   }
   SPNGD_CUDA_TRY(cudaEventRecord(o->ev[6], s));
-  if (capture || !o->use_graph) o->launches = ctx->launches - l0;
-  o->graphs_ready = o->use_graph;
+  if (capture || !o->use_graph || !full) o->launches = ctx->launches - l0;
+  if (capture) o->graphs_ready = true;
   o->timed = true;
   return SPNGD_OK;
+}
+
+int spngd_opt_stale_info(spngd_opt* o, int layer, int which, int64_t* t_x, int64_t* delta, int64_t* refresh_count,
+                         int* due_last) {
+  if (!o || !o->cfg.stale) return fail(SPNGD_ERR_INVALID, "spngd_opt_stale_info: stale gating is off");
+  int rc = stale_apply_pending(o);
+  if (rc) return rc;
+  for (size_t q = 0; q < o->stats.size(); ++q) {
+    const StatState& st = o->stats[q];
+    if (st.layer != layer || st.kind != which) continue;
+    int64_t dp = 0;
+    spngd_tracker_state(st.tr, t_x, delta, &dp, refresh_count);
+    if (due_last) *due_last = o->due.empty() ? 0 : o->due[q];
+    return SPNGD_OK;
+  }
+  return fail(SPNGD_ERR_SHAPE_MISMATCH, "spngd_opt_stale_info: layer %d has no statistic %d", layer, which);
 }
 
 int spngd_opt_phase_ms(spngd_opt* o, float* out6) {

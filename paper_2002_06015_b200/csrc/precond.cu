@@ -121,6 +121,15 @@ __global__ void stat_distance_kernel(const spngd_stat_req* __restrict__ reqs) {
     for (int k = 0; k < 4; ++k) atomicAdd(r.out4 + k, acc[k]);
 }
 
+// The distance kernel accumulates weighted squares; the public entry point
+// returns the norms themselves (weighted_norm, stale.hpp:49-51).
+__global__ void stat_sqrt_kernel(const spngd_stat_req* __restrict__ reqs, int n) {
+  for (int i = threadIdx.x; i < 4 * n; i += blockDim.x) {
+    double* o = reqs[i >> 2].out4 + (i & 3);
+    *o = sqrt(fmax(*o, 0.0));
+  }
+}
+
 GemmOperand dense_operand(const float* ptr, int64_t ld, int64_t rows, int64_t K) {
   GemmOperand o{};
   o.ptr = ptr;
@@ -275,5 +284,8 @@ extern "C" int spngd_stat_distance_batched(spngd_ctx* ctx, int n, const spngd_st
   auto* d = scratch.upload(v);
   int rc = launch_stat_distance(ctx, d, n, max_rows);
   if (rc) return rc;
+  stat_sqrt_kernel<<<1, 128, 0, ctx->stream>>>(d, n);
+  SPNGD_CUDA_TRY(cudaGetLastError());
+  ctx->launches++;
   return spngd_ctx_sync(ctx);
 }

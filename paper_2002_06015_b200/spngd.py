@@ -495,7 +495,7 @@ def stat_distances(x: torch.Tensor, x1: Optional[torch.Tensor], x2: Optional[tor
                     x2.data_ptr() if x2 is not None else None, n, kind, out.data_ptr())
     arr = (N.StatReq * 1)(req)
     check(N.lib().spngd_stat_distance_batched(context().h, 1, arr))
-    return [math.sqrt(max(v, 0.0)) for v in out.tolist()]
+    return out.tolist()
 
 
 REASONS = ["FirstBuild", "Dissimilar1", "Dissimilar2", "SimilarBoth"]

@@ -37,13 +37,17 @@ def layer_descs(layers: List[Layer]):
 
 
 def plan_layout(layers: List[Layer], world: int):
-    """Owners and owner-major RS/AG offsets (spngd_plan_layout, host only)."""
+    """Owners and owner-major RS/AG offsets (spngd_plan_layout, host only).
+
+    Returns (entries, seg_stat, seg_grad, seg_ag): A/G/M offsets are within the
+    owner's statistics segment, dW within the owner's gradient segment; the
+    send buffer is [world * seg_stat | world * seg_grad]."""
     arr = layer_descs(layers)
     out = (N.LayoutEntry * len(layers))()
-    seg_rs, seg_ag = C.c_int64(), C.c_int64()
-    check(N.lib().spngd_plan_layout(arr, len(layers), world, out, C.byref(seg_rs), C.byref(seg_ag)))
+    seg_st, seg_gr, seg_ag = C.c_int64(), C.c_int64(), C.c_int64()
+    check(N.lib().spngd_plan_layout(arr, len(layers), world, out, C.byref(seg_st), C.byref(seg_gr), C.byref(seg_ag)))
     return [dict(owner=e.owner, A=e.off_A, G=e.off_G, M=e.off_M, dW=e.off_dW, W=e.off_W) for e in out], \
-        seg_rs.value, seg_ag.value
+        seg_st.value, seg_gr.value, seg_ag.value
 
 
 class Comm:
@@ -60,7 +64,7 @@ class Comm:
 class Optimizer:
     def __init__(self, layers: List[Layer], batch: int, lam: float = 2.5e-4, rescale: bool = True,
                  device: int = 0, world: int = 1, rank: int = 0, nccl_id: Optional[bytes] = None,
-                 stream=None):
+                 stream=None, stale: bool = False, stale_alpha: float = 0.1):
         self.layers, self.batch, self.lam = layers, batch, lam
         self.world, self.rank, self.device = world, rank, device
         L = N.lib()
@@ -69,7 +73,7 @@ class Optimizer:
         if world > 1:
             check(L.spngd_ctx_init_comm(self.ctx, world, rank, C.create_string_buffer(nccl_id, 128)))
         arr = layer_descs(layers)
-        cfg = N.OptConfig(lam, int(rescale), 0, 0.1, batch)
+        cfg = N.OptConfig(lam, int(rescale), int(stale), stale_alpha, batch)
         self.h = C.c_void_p()
         check(L.spngd_opt_create(self.ctx, arr, len(layers), C.byref(cfg), C.byref(self.h)))
 
@@ -192,3 +196,12 @@ class Optimizer:
 
     def launch_count(self) -> int:
         return N.lib().spngd_opt_launch_count(self.h)
+
+    def stale_info(self, layer: int, which: str):
+        """Tracker state of statistic which in {"A", "G", "F"} of `layer`
+        (StaleTracker t_X / delta / refresh count) and whether it refreshed
+        in the last step."""
+        tx, d, rc, due = C.c_int64(), C.c_int64(), C.c_int64(), C.c_int()
+        check(N.lib().spngd_opt_stale_info(self.h, layer, {"A": 0, "G": 1, "F": 2}[which], C.byref(tx), C.byref(d),
+                                           C.byref(rc), C.byref(due)))
+        return dict(t_x=tx.value, delta=d.value, refreshes=rc.value, refreshed=bool(due.value))

@@ -96,19 +96,22 @@ def worker(rank, port, q):
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=WORLD)
     try:
-        lay, seg_rs, seg_ag = plan_layout(LAYERS, WORLD)
+        lay, seg_st, seg_gr, seg_ag = plan_layout(LAYERS, WORLD)
         mine = shard_inputs(rank)
-        send = np.zeros(WORLD * seg_rs)
+        # send buffer: [WORLD x statistics segment | WORLD x gradient segment]
+        send = np.zeros(WORLD * (seg_st + seg_gr))
         for li, l in enumerate(LAYERS):
-            base = lay[li]["owner"] * seg_rs
             st = stats(l, mine[li], M_PER_RANK)
             for key in ("A", "G", "M", "dW"):
                 if key in st:
                     v = st[key]
+                    base = (WORLD * seg_st + lay[li]["owner"] * seg_gr) if key == "dW" else lay[li]["owner"] * seg_st
                     send[base + lay[li][key]: base + lay[li][key] + v.size] = v
         t = torch.from_numpy(send)
         dist.all_reduce(t)                    # reduce_scatter_v = per-owner mean (dist.cpp:204-213)
-        recv = (t / WORLD).numpy()[rank * seg_rs:(rank + 1) * seg_rs]
+        full = (t / WORLD).numpy()
+        recv_st = full[rank * seg_st:(rank + 1) * seg_st]
+        recv_gr = full[WORLD * seg_st + rank * seg_gr: WORLD * seg_st + (rank + 1) * seg_gr]
         ps = params()
         ag = np.zeros(WORLD * seg_ag)
         for li, l in enumerate(LAYERS):
@@ -116,12 +119,12 @@ def worker(rank, port, q):
                 continue
             s = {}
             if l.kind == "bn":
-                s["M"] = recv[lay[li]["M"]: lay[li]["M"] + 3 * l.g]
-                s["dW"] = recv[lay[li]["dW"]: lay[li]["dW"] + 2 * l.g]
+                s["M"] = recv_st[lay[li]["M"]: lay[li]["M"] + 3 * l.g]
+                s["dW"] = recv_gr[lay[li]["dW"]: lay[li]["dW"] + 2 * l.g]
             else:
-                s["A"] = recv[lay[li]["A"]: lay[li]["A"] + l.a * (l.a + 1) // 2]
-                s["G"] = recv[lay[li]["G"]: lay[li]["G"] + l.g * (l.g + 1) // 2]
-                s["dW"] = recv[lay[li]["dW"]: lay[li]["dW"] + l.g * l.a]
+                s["A"] = recv_st[lay[li]["A"]: lay[li]["A"] + l.a * (l.a + 1) // 2]
+                s["G"] = recv_st[lay[li]["G"]: lay[li]["G"] + l.g * (l.g + 1) // 2]
+                s["dW"] = recv_gr[lay[li]["dW"]: lay[li]["dW"] + l.g * l.a]
             w = stage4(l, s, ps[li])
             off = rank * seg_ag + lay[li]["W"]
             ag[off: off + w.size] = w
@@ -168,10 +171,10 @@ def test_world2_reduce_scatter_owner_update_all_gather():
 
 def test_layout_every_payload_owned_once():
     for world in (1, 2, 4, 8):
-        lay, seg_rs, seg_ag = plan_layout(W.resnet50(), world)
+        lay, seg_st, seg_gr, seg_ag = plan_layout(W.resnet50(), world)
         for r in range(world):
-            spans = sorted((e[k], e[k]) for e in lay if e["owner"] == r for k in ("A", "G", "M", "dW") if e[k] >= 0)
-            offs = [s[0] for s in spans]
-            assert len(offs) == len(set(offs))   # no two payloads share an offset
+            for keys in (("A", "G", "M"), ("dW",)):  # statistics region, gradient region
+                offs = [e[k] for e in lay if e["owner"] == r for k in keys if e[k] >= 0]
+                assert len(offs) == len(set(offs))   # no two payloads share an offset
         assert all(0 <= e["owner"] < world for e in lay)
-        assert seg_rs % 64 == 0 and seg_ag % 64 == 0
+        assert seg_st % 64 == 0 and seg_gr % 64 == 0 and seg_ag % 64 == 0
