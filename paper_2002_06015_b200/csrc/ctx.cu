@@ -56,6 +56,13 @@ int spngd_ctx_create(int device, void* stream, spngd_ctx** out) {
   if (prop.major != 10)
     return spngd::fail(SPNGD_ERR_CUDA, "spngd_ctx_create: device %d is sm_%d%d, need sm_100 (B200)", device,
                        prop.major, prop.minor);
+  // Keep stream-ordered scratch (DeviceScratch) cached across calls instead of
+  // returning it to the driver at every synchronisation.
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+    uint64_t keep = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+  }
   auto* c = new spngd_ctx();
   c->device = device;
   if (stream) {

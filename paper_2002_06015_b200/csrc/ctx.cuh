@@ -3,6 +3,7 @@
 
 #include <cuda_runtime.h>
 
+#include <cstdlib>
 #include <string>
 #include <vector>
 
@@ -36,6 +37,8 @@ class DeviceScratch {
     void* p = nullptr;
     if (count == 0) count = 1;
     if (cudaMallocAsync(&p, count * sizeof(T), ctx_->stream) != cudaSuccess) return nullptr;
+    static const bool poison = getenv("SPNGD_POISON_SCRATCH") != nullptr;  // debug: NaN-fill fresh scratch
+    if (poison) cudaMemsetAsync(p, 0xff, count * sizeof(T), ctx_->stream);
     ptrs_.push_back(p);
     return static_cast<T*>(p);
   }

@@ -406,7 +406,14 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     if (produce) {
       if (tma) {
         tq = item.k0 / kTileK;
-        if (t == 0) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(tmap)) : "memory");
+        if (t == 0) {
+          // Descriptors live in global memory written by host copies; one-shot
+          // entry points reuse pooled addresses for new descriptors, so the
+          // tensormap proxy must re-acquire them (stale descriptor cache).
+          asm volatile("fence.proxy.tensormap::generic.acquire.gpu [%0], 128;" ::"l"(reinterpret_cast<uint64_t>(tmap))
+                       : "memory");
+          asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(tmap)) : "memory");
+        }
       } else {
         cur = cursor_at(op, item.k0 + 4 * c);
       }

@@ -92,8 +92,13 @@ class Context:
         self.device = device
         s = stream if stream is not None else torch.cuda.current_stream(device)
         self.stream = s
+        # torch's default stream has handle 0, which spngd_ctx_create reads as
+        # "no stream" (a private non-blocking stream, unordered with torch's
+        # work).  Pass cudaStreamLegacy (0x1) instead so calls are stream-ordered
+        # after the torch kernels that produced their inputs.
+        handle = s.cuda_stream if s.cuda_stream else 1
         h = C.c_void_p()
-        check(N.lib().spngd_ctx_create(device, C.c_void_p(s.cuda_stream), C.byref(h)))
+        check(N.lib().spngd_ctx_create(device, C.c_void_p(handle), C.byref(h)))
         self.h = h
 
     def sync(self):
@@ -384,6 +389,21 @@ def spd_inverse(m: SymMatrix, damping: float, dense: bool = False):
     check(N.lib().spngd_spd_inverse_batched(context().h, 1, arr))
     res = SymMatrix(n, out)
     return (res, dn[:, :n]) if dense else res
+
+
+def spd_inverse_batched(ms: List[SymMatrix], damping: float) -> List[SymMatrix]:
+    """spd_inverse (linalg.hpp:60) over many matrices in one batched call."""
+    reqs, outs = [], []
+    for m in ms:
+        if m.dim == 0:
+            raise ShapeMismatch("spd_inverse: empty matrix")
+        out = torch.empty(packed_size(m.dim), dtype=torch.float32, device=m.data.device)
+        reqs.append(N.SpdReq(m.data.data_ptr(), m.dim, damping, None, None, 0, out.data_ptr()))
+        outs.append(SymMatrix(m.dim, out))
+    if reqs:
+        arr = (N.SpdReq * len(reqs))(*reqs)
+        check(N.lib().spngd_spd_inverse_batched(context().h, len(reqs), arr))
+    return outs
 
 
 def damp_and_invert_batched(blocks: List[KroneckerBlock], lam: float):
