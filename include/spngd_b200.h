@@ -104,6 +104,25 @@ typedef struct spngd_bn_moments_req {
 } spngd_bn_moments_req;
 int spngd_bn_moments_batched(spngd_ctx* ctx, int n, const spngd_bn_moments_req* reqs);
 
+/* ---- BN per-sample parameter gradients ------------------
+ * Replaces the per-sample capture of src/net.cpp:467-475:
+ *   gg[s][ch] = sum_p dY[s][ch*S + p] * xhat[s][ch*S + p]
+ *   gb[s][ch] = sum_p dY[s][ch*S + p]
+ * dY, xhat: M x (c*S) row-major (the BN backward's output-gradient and
+ * normalised activation); gg, gb: M x c row-major -- exactly the
+ * bn_ggamma_true / bn_gbeta_true capture (net.hpp:95) that
+ * spngd_bn_moments_batched and the step consume.  One read of dY and xhat
+ * (HBM-bound), fp32 loads with fp32 accumulation per lane and a pairwise warp
+ * reduction. */
+typedef struct spngd_bn_grad_req {
+  const float* dy;
+  const float* xhat;
+  int64_t M, c, S;
+  float* gg;
+  float* gb;
+} spngd_bn_grad_req;
+int spngd_bn_grad_reduce_batched(spngd_ctx* ctx, int n, const spngd_bn_grad_req* reqs);
+
 /* ---- K3/K4: damped SPD inverse ---------------------------------------------
  * Replaces spd_inverse (src/linalg.cpp:29-48): (M + d I)^-1 of a packed
  * symmetric matrix.  `damping_dev` (device float) overrides `damping` when

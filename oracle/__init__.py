@@ -79,6 +79,7 @@ def _declare(L):
         "or_factor_A_f32": (C.c_int, [_fp, _i64, _i64, _i64, _i64, _i64, C.c_int, _dp]),
         "or_factor_G_f32": (C.c_int, [_fp, _i64, _i64, _i64, _i64, _i64, C.c_int, _dp]),
         "or_build_bn_block": (C.c_int, [_dp, _dp, _i64, _i64, _i64, C.c_int, _dp]),
+        "or_bn_grad_reduce": (C.c_int, [C.POINTER(C.c_float), C.POINTER(C.c_float), _i64, _i64, _i64, _dp, _dp]),
         "or_build_bn_full": (C.c_int, [_dp, _dp, _i64, _i64, _i64, C.c_int, _dp]),
         "or_damp_and_invert": (C.c_int, [_dp, _dp, _i64, _i64, C.c_double, _dp, _dp, _dp]),
         "or_damp_bn": (C.c_int, [_dp, _i64, C.c_double, _dp]),
@@ -223,6 +224,20 @@ def build_bn_block(gg, gb, lo, hi, compensated=False):
     _check(lib().or_build_bn_block(g_, b_, c, lo, hi, int(compensated),
                                    out.ctypes.data_as(_dp)), "build_bn_block")
     return out
+
+
+def bn_grad_reduce(dy, xhat, M, c, S):
+    """Per-sample BN gamma/beta gradients (net.cpp:467-475) -> (gg, gb), M x c."""
+    dy = np.ascontiguousarray(dy, dtype=np.float32)
+    xh = np.ascontiguousarray(xhat, dtype=np.float32)
+    if dy.size != M * c * S or xh.size != M * c * S:
+        raise OracleError(1, "bn_grad_reduce")
+    gg = np.empty(M * c)
+    gb = np.empty(M * c)
+    fp = C.POINTER(C.c_float)
+    _check(lib().or_bn_grad_reduce(dy.ctypes.data_as(fp), xh.ctypes.data_as(fp), M, c, S,
+                                   gg.ctypes.data_as(_dp), gb.ctypes.data_as(_dp)), "bn_grad_reduce")
+    return gg.reshape(M, c), gb.reshape(M, c)
 
 
 def build_bn_full(gg, gb, lo, hi, compensated=False):

@@ -356,6 +356,27 @@ int or_factor_G_f32(const float* grad, int64_t is_conv, int64_t g, int64_t hw,
   else mean_outer_t<float>(grad, hw, g, lo, hi, n, compensated, out);
   return OR_OK;
 }
+// Per-sample BN parameter gradients captured in the backward (net.cpp:467-475):
+// gg[s][ch] = sum_p dY[s][ch*S+p] * xhat[s][ch*S+p], gb[s][ch] = sum_p dY[...],
+// dY / xhat M x (c*S) row-major (fp32 inputs, fp64 sums), gg / gb M x c.
+int or_bn_grad_reduce(const float* dy, const float* xh, int64_t M, int64_t c, int64_t S, double* gg, double* gb) {
+  if (M <= 0) return 5;                   // EmptyBatch
+  if (c <= 0 || S <= 0) return 1;         // ShapeMismatch
+  for (int64_t s = 0; s < M; ++s)
+    for (int64_t ch = 0; ch < c; ++ch) {
+      const float* d = dy + (s * c + ch) * S;
+      const float* x = xh + (s * c + ch) * S;
+      double dot = 0.0, sum = 0.0;
+      for (int64_t p = 0; p < S; ++p) {
+        dot += double(d[p]) * double(x[p]);
+        sum += double(d[p]);
+      }
+      gg[s * c + ch] = dot;
+      gb[s * c + ch] = sum;
+    }
+  return 0;
+}
+
 // build_bn_block (fisher.cpp:147-185); gg, gb are M x c row-major.  Output is
 // the interleaved 3c wire payload of dist.cpp:283-292.
 int or_build_bn_block(const double* gg, const double* gb, int64_t c, int64_t lo,

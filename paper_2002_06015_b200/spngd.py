@@ -374,6 +374,30 @@ def build_bn_block(cap: CaptureBuffer, net: NetworkSpec, layer: int, mode=Fisher
     return UnitBnBlock(layer=layer, m3c=out)
 
 
+def bn_grad_reduce(dy: torch.Tensor, xhat: torch.Tensor, M: int, c: int, S: int):
+    """Per-sample BN parameter gradients of the backward (net.cpp:467-475):
+    dY, x_hat M x (c*S) -> (gg, gb) M x c, the bn_ggamma/bn_gbeta capture."""
+    return bn_grad_reduce_batched([(dy, xhat, M, c, S)])[0]
+
+
+def bn_grad_reduce_batched(items):
+    """bn_grad_reduce over several BN layers in one launch; items are
+    (dy, xhat, M, c, S) tuples."""
+    reqs, outs = [], []
+    for dy, xh, M, c, S in items:
+        _ptr(dy), _ptr(xh)  # contiguous float32 CUDA tensors
+        if M > 0 and (dy.numel() != M * c * S or xh.numel() != M * c * S):
+            raise ShapeMismatch("bn_grad_reduce: dY / x_hat must be M x (c*S)")
+        gg = torch.empty(M, c, dtype=torch.float32, device=dy.device)
+        gb = torch.empty(M, c, dtype=torch.float32, device=dy.device)
+        reqs.append(N.BnGradReq(dy.data_ptr(), xh.data_ptr(), M, c, S, gg.data_ptr(), gb.data_ptr()))
+        outs.append((gg, gb))
+    if reqs:
+        arr = (N.BnGradReq * len(reqs))(*reqs)
+        check(N.lib().spngd_bn_grad_reduce_batched(context().h, len(reqs), arr))
+    return outs
+
+
 # ---- K3 / K4 -------------------------------------------------------------------
 def spd_inverse(m: SymMatrix, damping: float, dense: bool = False):
     """linalg.hpp:60: (m + damping I)^-1, packed (and dense if requested)."""

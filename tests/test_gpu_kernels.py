@@ -206,3 +206,25 @@ def test_stat_distance_matches_oracle(cuda_dev):
     ref = np.zeros(6)
     assert O.similar(xn[:6], x1n[:6], np.ones(6), 0.5) == (np.linalg.norm(xn[:6] - x1n[:6]) /
                                                            np.linalg.norm(x1n[:6]) < 0.5)
+
+
+def test_bn_grad_reduce_matches_oracle(cuda_dev):
+    """per-sample BN gradients (net.cpp:467-475) from dY and
+    x_hat in one batched launch; odd S (scalar path), S % 4 == 0 (float4 path),
+    a large S and single-channel / single-sample edges."""
+    shapes = [(4, 16, 49), (3, 8, 196), (2, 4, 3136), (1, 1, 12544), (5, 1, 1), (2, 3, 4)]
+    g = torch.Generator(device="cuda").manual_seed(11)
+    items, host = [], []
+    for M, c, S in shapes:
+        dy = torch.randn(M, c * S, device="cuda", generator=g)
+        xh = torch.randn(M, c * S, device="cuda", generator=g)
+        items.append((dy, xh, M, c, S))
+        host.append((dy.cpu().numpy(), xh.cpu().numpy(), M, c, S))
+    outs = P.bn_grad_reduce_batched(items)
+    for (gg, gb), (dy, xh, M, c, S) in zip(outs, host):
+        wg, wb = O.bn_grad_reduce(dy, xh, M, c, S)
+        scale = np.sqrt(S)  # fp32 accumulation of S terms
+        assert np.abs(gg.cpu().numpy() - wg).max() <= 2e-6 * scale * max(1.0, np.abs(wg).max())
+        assert np.abs(gb.cpu().numpy() - wb).max() <= 2e-6 * scale * max(1.0, np.abs(wb).max())
+    with pytest.raises(P.EmptyBatch):
+        P.bn_grad_reduce(items[0][0], items[0][1], 0, 16, 49)

@@ -356,3 +356,17 @@ def test_synth_stream_deterministic():
     b = O.synth_normal(1234, 500, 500)
     assert np.array_equal(a[500:], b)
     assert abs(a.mean()) < 0.1 and abs(a.std() - 1) < 0.1
+
+
+def test_bn_grad_reduce_oracle():  # net.cpp:467-475 per-sample gamma/beta gradients
+    rng = np.random.default_rng(3)
+    M, c, S = 3, 5, 7
+    dy = rng.standard_normal((M, c * S)).astype(np.float32)
+    xh = rng.standard_normal((M, c * S)).astype(np.float32)
+    gg, gb = O.bn_grad_reduce(dy, xh, M, c, S)
+    d3 = dy.astype(np.float64).reshape(M, c, S)
+    x3 = xh.astype(np.float64).reshape(M, c, S)
+    assert np.allclose(gg, (d3 * x3).sum(-1), rtol=0, atol=1e-12)
+    assert np.allclose(gb, d3.sum(-1), rtol=0, atol=1e-12)
+    with pytest.raises(O.OracleError):
+        O.bn_grad_reduce(dy[:0], xh[:0], 0, c, S)   # EmptyBatch
