@@ -11,6 +11,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "ctx.cuh"
 #include "factor.cuh"
@@ -113,26 +114,71 @@ int plan_factors(const spngd_factor_req* reqs, int n, FactorPlan& plan, float* w
     const int64_t t = (r.dim + kTileM - 1) / kTileM;
     tk.push_back({t * (t + 1) / 2, K});
   }
+  // 2-CTA SYRK (opt-in, SPNGD_PAIR=1; see gemm_pair.cu for its status) when
+  // every operand is TMA-addressable (all ResNet-50 captures are, after the repack).
+  static const bool want_pair = getenv("SPNGD_PAIR") != nullptr;
+  plan.pair = want_pair;
+  for (const auto& p : plan.probs) plan.pair = plan.pair && p.A.mode != OP_ASYNC;
+  if (plan.pair) {
+    tk.clear();
+    for (const auto& p : plan.probs) {
+      const int64_t t = (p.M + kTileM - 1) / kTileM;
+      int64_t ctas = 0;
+      for (int64_t tn = 0; tn < t; ++tn) ctas += 2 * ((tn + 2) / 2);
+      tk.push_back({ctas, p.K});
+    }
+  }
   plan.kchunk = choose_kchunk(tk);
   int slot = 0;
   for (int i = 0; i < n; ++i) {
     GemmProblem& p = plan.probs[i];
     const bool split = p.K > plan.kchunk;
     p.mode = split ? EPI_PARTIAL : EPI_PACKED;
-    plan_problem_tiles(i, p, /*upper_only=*/true, split ? plan.kchunk : p.K + kTileK, plan.items, &plan.reduce,
-                       &slot, reqs[i].scale, reqs[i].packed_out);
+    const int kc = split ? plan.kchunk : p.K + kTileK;
+    if (plan.pair) {
+      plan_problem_pairs(i, p, kc, plan.items, &plan.reduce, &slot, reqs[i].scale, reqs[i].packed_out);
+      CUtensorMap hm;
+      if (encode_half_map(p.B, padded_k(p.B, p.K) >= p.K ? p.K : p.K, &hm) != SPNGD_OK) plan.pair = false;
+      plan.halfmaps.push_back(hm);
+    } else {
+      plan_problem_tiles(i, p, /*upper_only=*/true, kc, plan.items, &plan.reduce, &slot, reqs[i].scale,
+                         reqs[i].packed_out);
+    }
   }
+  if (!plan.pair && !plan.halfmaps.empty()) return fail(SPNGD_ERR_INVALID, "factor: half-box tensor map failed");
   plan.n_slots = slot;
-  // Longest work first: items are independent, so issue the big K ranges early.
-  std::stable_sort(plan.items.begin(), plan.items.end(), [](const GemmWorkItem& x, const GemmWorkItem& y) {
-    return (x.k1 - x.k0) > (y.k1 - y.k0);
-  });
+  // Longest work first: items are independent, so issue the big K ranges early
+  // (pairs move as units: both CTAs of a cluster read consecutive items).
+  if (plan.pair) {
+    std::vector<std::pair<GemmWorkItem, GemmWorkItem>> pairs;
+    for (size_t q = 0; q + 1 < plan.items.size(); q += 2) pairs.push_back({plan.items[q], plan.items[q + 1]});
+    std::stable_sort(pairs.begin(), pairs.end(), [](const auto& x, const auto& y) {
+      return (x.first.k1 - x.first.k0) > (y.first.k1 - y.first.k0);
+    });
+    plan.items.clear();
+    for (const auto& pr : pairs) {
+      plan.items.push_back(pr.first);
+      plan.items.push_back(pr.second);
+    }
+  } else {
+    std::stable_sort(plan.items.begin(), plan.items.end(), [](const GemmWorkItem& x, const GemmWorkItem& y) {
+      return (x.k1 - x.k0) > (y.k1 - y.k0);
+    });
+  }
   return SPNGD_OK;
 }
 
-int run_factors(spngd_ctx* ctx, const GemmProblem* d_probs, const GemmWorkItem* d_items, int n_items,
-                float* d_partials, const SyrkReduceTask* d_reduce, int n_reduce) {
-  int rc = launch_gemm(d_probs, d_items, n_items, d_partials, ctx->d_status, ctx->stream);
+int launch_factor_gemm(spngd_ctx* ctx, const FactorPlan& plan, const GemmProblem* d_probs,
+                       const CUtensorMap* d_halfmaps, const GemmWorkItem* d_items, int n_items, float* d_partials,
+                       cudaStream_t stream) {
+  if (plan.pair) return launch_gemm_pair(d_probs, d_halfmaps, d_items, n_items, d_partials, stream);
+  return launch_gemm(d_probs, d_items, n_items, d_partials, ctx->d_status, stream);
+}
+
+int run_factors(spngd_ctx* ctx, const FactorPlan& plan, const GemmProblem* d_probs, const CUtensorMap* d_halfmaps,
+                const GemmWorkItem* d_items, int n_items, float* d_partials, const SyrkReduceTask* d_reduce,
+                int n_reduce) {
+  int rc = launch_factor_gemm(ctx, plan, d_probs, d_halfmaps, d_items, n_items, d_partials, ctx->stream);
   if (rc) return rc;
   ctx->launches += n_items > 0;
   rc = launch_syrk_reduce(d_reduce, n_reduce, d_partials, ctx->stream);
@@ -168,9 +214,11 @@ extern "C" int spngd_factor_sym_batched(spngd_ctx* ctx, int n, const spngd_facto
   auto* d_probs = scratch.upload(plan.probs);
   auto* d_items = scratch.upload(plan.items);
   auto* d_reduce = scratch.upload(plan.reduce);
+  auto* d_half = scratch.upload(plan.halfmaps);
   float* d_partials = scratch.alloc<float>(size_t(std::max(plan.n_slots, 1)) * kTileM * kTileN);
   if (!d_probs || !d_items || !d_reduce || !d_partials) return fail(SPNGD_ERR_CUDA, "factor: workspace allocation failed");
-  rc = run_factors(ctx, d_probs, d_items, int(plan.items.size()), d_partials, d_reduce, int(plan.reduce.size()));
+  rc = run_factors(ctx, plan, d_probs, d_half, d_items, int(plan.items.size()), d_partials, d_reduce,
+                   int(plan.reduce.size()));
   if (rc) return rc;
   SPNGD_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
   return SPNGD_OK;

@@ -22,14 +22,23 @@ struct FactorPlan {
   std::vector<SyrkReduceTask> reduce;
   int n_slots = 0;
   int kchunk = 0;
+  // 2-CTA SYRK (gemm_pair.cu): items come in adjacent cluster pairs and
+  // halfmaps[problem] is the 64-row-box tensor map of the B operand.
+  bool pair = false;
+  std::vector<CUtensorMap> halfmaps;
 };
 
 // `ws` receives the repacked captures (sizing pass when null: only
 // repack_floats is meaningful).
 int plan_factors(const spngd_factor_req* reqs, int n, FactorPlan& plan, float* ws = nullptr);
 int launch_repack(spngd_ctx* ctx, const RepackTask* d_tasks, int n, int64_t max_elems);
-int run_factors(spngd_ctx* ctx, const GemmProblem* d_probs, const GemmWorkItem* d_items, int n_items,
-                float* d_partials, const SyrkReduceTask* d_reduce, int n_reduce);
+int run_factors(spngd_ctx* ctx, const FactorPlan& plan, const GemmProblem* d_probs, const CUtensorMap* d_halfmaps,
+                const GemmWorkItem* d_items, int n_items, float* d_partials, const SyrkReduceTask* d_reduce,
+                int n_reduce);
+// The factor SYRK launch alone (pair or single-CTA kernel per plan.pair).
+int launch_factor_gemm(spngd_ctx* ctx, const FactorPlan& plan, const GemmProblem* d_probs,
+                       const CUtensorMap* d_halfmaps, const GemmWorkItem* d_items, int n_items, float* d_partials,
+                       cudaStream_t stream);
 int launch_bn_moments(spngd_ctx* ctx, const spngd_bn_moments_req* d_reqs, int n, int64_t max_c);
 
 }  // namespace spngd

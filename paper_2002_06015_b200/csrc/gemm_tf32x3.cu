@@ -761,6 +761,66 @@ void finalize_operand(GemmOperand& op, int64_t K, bool allow_tma) {
 
 int g_gemm_dbg_extra = 0;
 
+// Same tensor as the operand's own map, 64-row boxes (the B half-tile of the
+// 2-CTA SYRK, gemm_pair.cu).  Valid for OP_TMA2D / OP_TMA3D operands.
+int encode_half_map(const GemmOperand& op, int64_t K, CUtensorMap* out) {
+  auto encode = tma_encode_fn();
+  if (!encode || (op.mode != OP_TMA2D && op.mode != OP_TMA3D)) return SPNGD_ERR_INVALID;
+  cuuint32_t box[3] = {32, 64, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r;
+  if (op.mode == OP_TMA2D) {
+    cuuint64_t dims[2] = {cuuint64_t(K), cuuint64_t(op.rows)};
+    cuuint64_t strides[1] = {cuuint64_t(op.row_stride) * 4};
+    r = encode(out, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(op.ptr), dims, strides, box, estr,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  } else {
+    cuuint64_t dims[3] = {cuuint64_t(op.seg_len), cuuint64_t(op.rows), cuuint64_t(op.nseg)};
+    cuuint64_t strides[2] = {cuuint64_t(op.row_stride) * 4, cuuint64_t(op.seg_stride) * 4};
+    r = encode(out, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(op.ptr), dims, strides, box, estr,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  }
+  return r == CUDA_SUCCESS ? SPNGD_OK : SPNGD_ERR_INVALID;
+}
+
+// SYRK (upper triangle) tiles as vertical CTA pairs (2p, 2p+1) x tn for the
+// 2-CTA kernel: both items of a pair share tn and the K range; a partner below
+// the diagonal or past the last row tile computes but keeps nothing (slot -1,
+// and the packed epilogue's i <= j mask).
+int plan_problem_pairs(int problem_index, const GemmProblem& p, int kchunk, std::vector<GemmWorkItem>& items,
+                       std::vector<SyrkReduceTask>* reduce, int* next_slot, double reduce_scale, float* packed_out) {
+  const int T = (p.M + kTileM - 1) / kTileM;
+  kchunk = std::max(kTileK, (kchunk / kTileK) * kTileK);
+  const int nchunks = std::max(1, (p.K + kchunk - 1) / kchunk);
+  int used = 0;
+  for (int tn = 0; tn < T; ++tn)
+    for (int tm0 = 0; tm0 <= tn; tm0 += 2) {
+      const bool keep1 = tm0 + 1 <= tn;  // tile (tm0+1, tn) in the upper triangle (and a real row tile)
+      if (nchunks == 1) {
+        items.push_back({problem_index, tm0, tn, 0, p.K, -1});
+        items.push_back({problem_index, tm0 + 1, tn, 0, p.K, -1});
+        continue;
+      }
+      const int s0 = *next_slot;
+      *next_slot += nchunks;
+      const int s1 = keep1 ? *next_slot : -1;
+      if (keep1) *next_slot += nchunks;
+      for (int q = 0; q < nchunks; ++q) {
+        const int k0 = q * kchunk, k1 = std::min(p.K, k0 + kchunk);
+        items.push_back({problem_index, tm0, tn, k0, k1, s0 + q});
+        items.push_back({problem_index, tm0 + 1, tn, k0, k1, keep1 ? s1 + q : -1});
+      }
+      used += nchunks * (keep1 ? 2 : 1);
+      if (reduce) {
+        reduce->push_back({tm0, tn, s0, nchunks, p.M, 0, reduce_scale, packed_out});
+        if (keep1) reduce->push_back({tm0 + 1, tn, s1, nchunks, p.M, 0, reduce_scale, packed_out});
+      }
+    }
+  return used;
+}
+
 size_t gemm_smem_bytes() { return size_t(kStages) * kStageBytes + sizeof(SmemCtl) + 1024; }
 
 int launch_gemm(const GemmProblem* d_probs, const GemmWorkItem* d_items, int n_items, float* d_partials,

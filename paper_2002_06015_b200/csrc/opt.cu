@@ -99,6 +99,7 @@ struct spngd_opt {
   FactorPlan fplan;
   GemmProblem* d_fprobs = nullptr; GemmWorkItem* d_fitems = nullptr; SyrkReduceTask* d_freduce = nullptr;
   RepackTask* d_repack = nullptr;
+  CUtensorMap* d_fhalf = nullptr;
   float* d_partials = nullptr;
   std::vector<spngd_bn_moments_req> bnm;
   spngd_bn_moments_req* d_bnm = nullptr; int64_t bnm_maxc = 0;
@@ -315,6 +316,7 @@ int build(spngd_opt* o, const spngd_layer_desc* descs, int n) {
   o->d_fprobs = dev_upload(o->fplan.probs, own);
   o->d_fitems = dev_upload(o->fplan.items, own);
   o->d_freduce = dev_upload(o->fplan.reduce, own);
+  o->d_fhalf = dev_upload(o->fplan.halfmaps, own);
   o->d_partials = o->alloc(size_t(std::max(o->fplan.n_slots, 1)) * kTileM * kTileN);
   o->d_bnm = dev_upload(o->bnm, own);
   o->d_pis = dev_upload(o->pis, own);
@@ -533,7 +535,8 @@ int issue_phase(spngd_opt* o, int phase) {
     case 0:  // Stages 1-3 local part: factor SYRK into the RS send buffer.
       rc = launch_repack(ctx, o->d_repack, int(o->fplan.repacks.size()), o->fplan.repack_max);
       if (rc) return rc;
-      rc = launch_gemm(o->d_fprobs, o->d_fitems, int(o->fplan.items.size()), o->d_partials, ctx->d_status, s);
+      rc = launch_factor_gemm(ctx, o->fplan, o->d_fprobs, o->d_fhalf, o->d_fitems, int(o->fplan.items.size()),
+                              o->d_partials, s);
       ctx->launches++;
       return rc;
     case 1:  // split-K reduction + BN moments.
@@ -626,7 +629,8 @@ int stale_partial_phase(spngd_opt* o, int phase) {
       if ((rc = upload_async(ctx, o->d_fitems_dyn, it))) return rc;
       rc = launch_repack(ctx, o->d_repack_dyn, int(rp.size()), o->fplan.repack_max);
       if (!rc && !it.empty()) {
-        rc = launch_gemm(o->d_fprobs, o->d_fitems_dyn, int(it.size()), o->d_partials, ctx->d_status, s);
+        rc = launch_factor_gemm(ctx, o->fplan, o->d_fprobs, o->d_fhalf, o->d_fitems_dyn, int(it.size()),
+                                o->d_partials, s);
         ctx->launches++;
       }
       return rc;
