@@ -228,6 +228,12 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   tc_fence_after();
   const uint32_t tmem = ctl->tmem_base;
   TRACE_STAMP(meta && threadIdx.x == 0, meta[2]);
+  // Programmatic dependent launch: everything above reads only the static
+  // plan, so it overlaps the tail of the previous kernel; operand data is read
+  // only after the prerequisite grid completed.  Let the next kernel start its
+  // own prologue now.
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
   float* T = reinterpret_cast<float*>(smem);  // 128 x 129 fp32 epilogue tile, reuses the stage ring
   if (warp >= 8) {
@@ -844,7 +850,23 @@ int launch_gemm(const GemmProblem* d_probs, const GemmWorkItem* d_items, int n_i
     cudaMalloc(&trace, 4 * 264 * sizeof(long long));
     cudaMemset(trace, 0, 4 * 264 * sizeof(long long));
   }
-  gemm_tf32x3_kernel<<<n_items, kGemmThreads, smem, stream>>>(d_probs, d_items, d_partials, d_status, dbg, trace);
+  {
+    // Launched with programmatic stream serialization (PDL): the kernel waits
+    // on griddepcontrol.wait before touching data of earlier kernels.
+    static const bool pdl = getenv("SPNGD_NO_PDL") == nullptr;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(unsigned(n_items));
+    cfg.blockDim = dim3(kGemmThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaError_t le = cudaLaunchKernelEx(&cfg, gemm_tf32x3_kernel, d_probs, d_items, d_partials, d_status, dbg, trace);
+    if (le != cudaSuccess) return fail(SPNGD_ERR_CUDA, "gemm launch failed: %s", cudaGetErrorString(le));
+  }
   if (want_trace) {
     static int printed = 0;
     if (printed++ < 12) {

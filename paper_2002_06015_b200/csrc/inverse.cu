@@ -17,6 +17,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 
 #include "ctx.cuh"
 #include "inverse.cuh"
@@ -34,23 +35,36 @@ constexpr size_t kBaseSmem = (2 * size_t(kBaseMax) * kLd + size_t(kNb) * kPB * k
 
 // Compile-time-unrolled steps of the 32x32 diagonal factorization (rows in
 // lanes) and of the column substitution, so `row`/`col` stay in registers.
-template <int K>
-__device__ __forceinline__ void diag_chol_step(float (&row)[32], int lane, float* rdiag, bool& bad) {
-  float p = __shfl_sync(0xffffffffu, row[K], K);
+// Step K with its pivot p = A_KK (already broadcast) and inv = 1/sqrt(p).
+// The next pivot depends only on column K+1, so it is updated and the next
+// broadcast + rsqrt issued before the remaining rank-1 columns of this step:
+// the serial pivot chain overlaps the bulk of the shuffles.
+__device__ __forceinline__ float pivot_rsqrt(float p, bool& bad) {
   if (!(p > 0.f) || !isfinite(p)) {
     bad = true;
     p = 1.f;
   }
-  float inv = rsqrtf(p);
-  inv = inv * fmaf(-0.5f * p, inv * inv, 1.5f);  // MUFU rsqrt + one Newton step
+  const float inv = rsqrtf(p);
+  return inv * fmaf(-0.5f * p, inv * inv, 1.5f);  // MUFU rsqrt + one Newton step
+}
+
+template <int K>
+__device__ __forceinline__ void diag_chol_step(float (&row)[32], int lane, float* rdiag, bool& bad, float p,
+                                               float inv) {
   if (lane == K) rdiag[K] = inv;
   row[K] = (lane == K) ? p * inv : (lane > K ? row[K] * inv : row[K]);
+  if constexpr (K + 1 < 32) {
+    const float l1 = __shfl_sync(0xffffffffu, row[K], K + 1);
+    row[K + 1] = (lane >= K + 1) ? fmaf(-row[K], l1, row[K + 1]) : row[K + 1];
+    const float pn = __shfl_sync(0xffffffffu, row[K + 1], K + 1);  // next pivot
+    const float invn = pivot_rsqrt(pn, bad);
 #pragma unroll
-  for (int j = K + 1; j < 32; ++j) {
-    const float ljk = __shfl_sync(0xffffffffu, row[K], j);
-    row[j] = (lane >= j) ? fmaf(-row[K], ljk, row[j]) : row[j];
+    for (int j = K + 2; j < 32; ++j) {
+      const float ljk = __shfl_sync(0xffffffffu, row[K], j);
+      row[j] = (lane >= j) ? fmaf(-row[K], ljk, row[j]) : row[j];
+    }
+    diag_chol_step<K + 1>(row, lane, rdiag, bad, pn, invn);
   }
-  if constexpr (K + 1 < 32) diag_chol_step<K + 1>(row, lane, rdiag, bad);
 }
 
 template <int I>
@@ -93,27 +107,35 @@ __global__ void __launch_bounds__(kBaseThreads, 1) base_chol_inv_kernel(const Ba
   float* rdiag = R + kNb * kPB * kPB;               // [128] 1 / L_ii
   const BaseTask t = tasks[blockIdx.x];
   const int n = t.n;
+  // PDL: the task table is static; the matrix comes from the previous kernel.
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const int np = (n + kPB - 1) / kPB * kPB;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  // Load M's lower triangle: each warp owns rows warp + 8 q; all loads of a
-  // row batch are issued before any smem store.
-  for (int jc = 0; jc < np; jc += 32) {
-    const int j = jc + lane;
-    float v[kBaseMax / 8];
+  // Load M's lower triangle: warp w owns rows w + 8 q, lane l columns
+  // 32 cc + l (coalesced 128-byte rows, conflict-free smem stores); all 64
+  // loads of a warp are in flight before any store.  Identity padding beyond
+  // n is inert.
+  {
+    float v[kNb][kBaseMax / 8];
 #pragma unroll
-    for (int q = 0; q < kBaseMax / 8; ++q) {
-      const int i = warp + 8 * q;
-      v[q] = (i == j) ? 1.f : 0.f;  // identity padding beyond n is inert
-      if (i < n && j < n && j <= i) v[q] = __ldg(t.m + int64_t(i) * t.ld + j);
-    }
+    for (int cc = 0; cc < kNb; ++cc)
 #pragma unroll
-    for (int q = 0; q < kBaseMax / 8; ++q) {
-      const int i = warp + 8 * q;
-      if (i < np) {
-        A[i * kLd + j] = v[q];
-        T[i * kLd + j] = 0.f;
+      for (int q = 0; q < kBaseMax / 8; ++q) {
+        const int i = warp + 8 * q, j = 32 * cc + lane;
+        v[cc][q] = (i == j) ? 1.f : 0.f;
+        if (i < n && j < n && j <= i) v[cc][q] = __ldg(t.m + int64_t(i) * t.ld + j);
       }
-    }
+#pragma unroll
+    for (int cc = 0; cc < kNb; ++cc)
+#pragma unroll
+      for (int q = 0; q < kBaseMax / 8; ++q) {
+        const int i = warp + 8 * q, j = 32 * cc + lane;
+        if (i < np && j < np) {
+          A[i * kLd + j] = v[cc][q];
+          T[i * kLd + j] = 0.f;
+        }
+      }
   }
   __syncthreads();
   LEAF_STAMP(1);
@@ -127,40 +149,59 @@ __global__ void __launch_bounds__(kBaseThreads, 1) base_chol_inv_kernel(const Ba
       float row[kPB];
 #pragma unroll
       for (int j = 0; j < kPB; ++j) row[j] = (j <= lane) ? A[(k0 + lane) * kLd + k0 + j] : 0.f;
-      diag_chol_step<0>(row, lane, rdiag + k0, bad);
+      if (kb == 0) LEAF_STAMP(20);
+      {
+        const float p0 = __shfl_sync(0xffffffffu, row[0], 0);
+        diag_chol_step<0>(row, lane, rdiag + k0, bad, p0, pivot_rsqrt(p0, bad));
+      }
+      if (kb == 0) LEAF_STAMP(21);
 #pragma unroll
       for (int j = 0; j < kPB; ++j)
         if (j <= lane) A[(k0 + lane) * kLd + k0 + j] = row[j];
       __syncwarp();
+      if (kb == 0) LEAF_STAMP(22);
       // Column `lane` of L_dd^-1 (forward substitution), into T's diagonal block.
       float col[kPB];
       diag_subst_step<0>(col, A + k0 * kLd + k0, kLd, rdiag + k0, lane);
+      if (kb == 0) LEAF_STAMP(23);
 #pragma unroll
       for (int i = 0; i < kPB; ++i) T[(k0 + i) * kLd + k0 + lane] = col[i];
+      if (kb == 0) LEAF_STAMP(24);
     }
     __syncthreads();
     LEAF_STAMP(2 + 3 * kb);
     const int m = np - k0 - kPB;  // trailing size
     if (m > 0) {
-      // (2) panel: L[i][k0+j] = sum_{p<=j} A[i][k0+p] Dinv[j][p]; thread = (row group, column j).
-      constexpr int kRows = (kBaseMax - kPB) / (kBaseThreads / kPB);  // 12 rows per thread max
-      const int j = tid & (kPB - 1);
-      const int ibase = k0 + kPB + (tid >> 5);
-      const int stride = kBaseThreads / kPB;
-      float res[kRows];
+      // (2) panel: L[i][k0+j] = sum_{p<=j} A[i][k0+p] Dinv[j][p] (Dinv = T's
+      //     diagonal block, lower) on 4x4 register tiles: thread (rg, cg) owns
+      //     rows k0+32+4rg.. and columns 4cg..; 8 shared loads per 16 FMA.
+      {
+        const int ntiles = (m / 4) * 8;
+        float acc[4][4] = {};
+        const int rg = tid >> 3, cg = tid & 7;
+        const int i0 = k0 + kPB + 4 * rg, j0 = 4 * cg;
+        if (tid < ntiles) {
+#pragma unroll 4
+          for (int p = 0; p < kPB; ++p) {
+            float a[4], d[4];
 #pragma unroll
-      for (int q = 0; q < kRows; ++q) res[q] = 0.f;
-#pragma unroll 8
-      for (int p = 0; p < kPB; ++p) {
-        const float d = (p <= j) ? T[(k0 + j) * kLd + k0 + p] : 0.f;
+            for (int q = 0; q < 4; ++q) {
+              a[q] = A[(i0 + q) * kLd + k0 + p];
+              d[q] = (p <= j0 + q) ? T[(k0 + j0 + q) * kLd + k0 + p] : 0.f;
+            }
 #pragma unroll
-        for (int q = 0; q < kRows; ++q)
-          if (ibase + q * stride < np) res[q] = fmaf(A[(ibase + q * stride) * kLd + k0 + p], d, res[q]);
+            for (int x = 0; x < 4; ++x)
+#pragma unroll
+              for (int y = 0; y < 4; ++y) acc[x][y] = fmaf(a[x], d[y], acc[x][y]);
+          }
+        }
+        __syncthreads();  // every read of the panel precedes its in-place overwrite
+        if (tid < ntiles)
+#pragma unroll
+          for (int x = 0; x < 4; ++x)
+#pragma unroll
+            for (int y = 0; y < 4; ++y) A[(i0 + x) * kLd + k0 + j0 + y] = acc[x][y];
       }
-      __syncthreads();
-#pragma unroll
-      for (int q = 0; q < kRows; ++q)
-        if (ibase + q * stride < np) A[(ibase + q * stride) * kLd + k0 + j] = res[q];
       __syncthreads();
       LEAF_STAMP(3 + 3 * kb);
       // (3) trailing SYRK on 4x4 register tiles of the lower triangle.
@@ -196,69 +237,90 @@ __global__ void __launch_bounds__(kBaseThreads, 1) base_chol_inv_kernel(const Ba
       LEAF_STAMP(4 + 3 * kb);
     }
   }
-  // (4) T = L^-1 off-diagonal 32x32 blocks, block row by block row:
+  // (4) T = L^-1 off-diagonal 32x32 blocks, block row by block row, on 4x4
+  //     register tiles (thread = (jb, tr, tc), 64 tiles per block):
   //     R[jb] = sum_{p in [32 jb, 32 ib)} L[ib][p] T[p][jb],  T[ib][jb] = -T[ib][ib] R[jb].
-  //     Thread owns 4 rows (r0 + 8 q) of column c for every jb: independent chains.
-  const int c = tid & 31, r0 = tid >> 5;
   for (int ib = 1; ib < nblk; ++ib) {
-    float acc[kNb - 1][4];
+    const int jb = tid >> 6, tr = (tid >> 3) & 7, tc = tid & 7;
+    const bool act = jb < ib;
+    const int r0 = ib * kPB + 4 * tr, c0 = jb * kPB + 4 * tc;
+    float acc[4][4] = {};
+    if (act) {
+      for (int p = jb * kPB; p < ib * kPB; ++p) {
+        float l[4], tv[4];
 #pragma unroll
-    for (int jb = 0; jb < kNb - 1; ++jb)
-#pragma unroll
-      for (int q = 0; q < 4; ++q) acc[jb][q] = 0.f;
-    for (int p = 0; p < ib * kPB; ++p) {
-      float l[4];
-#pragma unroll
-      for (int q = 0; q < 4; ++q) l[q] = A[(ib * kPB + r0 + 8 * q) * kLd + p];
-#pragma unroll
-      for (int jb = 0; jb < kNb - 1; ++jb)
-        if (jb < ib && jb * kPB <= p) {
-          const float tv = T[p * kLd + jb * kPB + c];
-#pragma unroll
-          for (int q = 0; q < 4; ++q) acc[jb][q] = fmaf(l[q], tv, acc[jb][q]);
+        for (int q = 0; q < 4; ++q) {
+          l[q] = A[(r0 + q) * kLd + p];
+          tv[q] = T[p * kLd + c0 + q];
         }
-    }
 #pragma unroll
-    for (int jb = 0; jb < kNb - 1; ++jb)
-      if (jb < ib)
+        for (int x = 0; x < 4; ++x)
 #pragma unroll
-        for (int q = 0; q < 4; ++q) R[(jb * kPB + r0 + 8 * q) * kPB + c] = acc[jb][q];
-    __syncthreads();
-#pragma unroll
-    for (int jb = 0; jb < kNb - 1; ++jb)
-#pragma unroll
-      for (int q = 0; q < 4; ++q) acc[jb][q] = 0.f;
-#pragma unroll 8
-    for (int qq = 0; qq < kPB; ++qq) {
-      float d[4];
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int r = r0 + 8 * q;
-        d[q] = (qq <= r) ? T[(ib * kPB + r) * kLd + ib * kPB + qq] : 0.f;
+          for (int y = 0; y < 4; ++y) acc[x][y] = fmaf(l[x], tv[y], acc[x][y]);
       }
 #pragma unroll
-      for (int jb = 0; jb < kNb - 1; ++jb)
-        if (jb < ib) {
-          const float rv = R[(jb * kPB + qq) * kPB + c];
+      for (int x = 0; x < 4; ++x)
 #pragma unroll
-          for (int q = 0; q < 4; ++q) acc[jb][q] = fmaf(d[q], rv, acc[jb][q]);
-        }
+        for (int y = 0; y < 4; ++y) R[(jb * kPB + 4 * tr + x) * kPB + 4 * tc + y] = acc[x][y];
     }
+    __syncthreads();
+    if (act) {
 #pragma unroll
-    for (int jb = 0; jb < kNb - 1; ++jb)
-      if (jb < ib)
+      for (int x = 0; x < 4; ++x)
 #pragma unroll
-        for (int q = 0; q < 4; ++q) T[(ib * kPB + r0 + 8 * q) * kLd + jb * kPB + c] = -acc[jb][q];
+        for (int y = 0; y < 4; ++y) acc[x][y] = 0.f;
+      const int qmax = 4 * tr + 4;  // T[ib][ib] is lower: row 4tr+x uses q <= 4tr+x
+      for (int q = 0; q < qmax; ++q) {
+        float d[4], rv[4];
+#pragma unroll
+        for (int x = 0; x < 4; ++x) d[x] = (q <= 4 * tr + x) ? T[(r0 + x) * kLd + ib * kPB + q] : 0.f;
+#pragma unroll
+        for (int y = 0; y < 4; ++y) rv[y] = R[(jb * kPB + q) * kPB + 4 * tc + y];
+#pragma unroll
+        for (int x = 0; x < 4; ++x)
+#pragma unroll
+          for (int y = 0; y < 4; ++y) acc[x][y] = fmaf(d[x], rv[y], acc[x][y]);
+      }
+#pragma unroll
+      for (int x = 0; x < 4; ++x)
+#pragma unroll
+        for (int y = 0; y < 4; ++y) T[(r0 + x) * kLd + c0 + y] = -acc[x][y];
+    }
     __syncthreads();
     LEAF_STAMP(14 + ib);
   }
   if (bad) set_status(status, SPNGD_ERR_NOT_POSITIVE_DEFINITE);
-  // Coalesced stores: T rows (lower) and T^T rows (upper, read transposed from smem).
-  for (int i = warp; i < n; i += kBaseThreads / 32)
-    for (int j = lane; j < n; j += 32) {
-      if (j <= i) t.tlow[int64_t(i) * t.ld + j] = T[i * kLd + j];
-      if (j >= i) t.tup[int64_t(i) * t.ld + j] = T[j * kLd + i];
+  // Stores: tlow row i = T row i (zeros above the diagonal are T's own), tup
+  // row i = T column i (read transposed from smem); float4 per lane where the
+  // chunk lies inside the block.
+  {
+    const int j0 = 4 * lane;
+    const bool vst = (t.ld & 3) == 0 && (reinterpret_cast<uintptr_t>(t.tlow) & 15) == 0 &&
+                     (reinterpret_cast<uintptr_t>(t.tup) & 15) == 0;
+    for (int i = warp; i < n; i += kBaseThreads / 32) {
+      if (j0 >= n) continue;
+      float lo[4], up[4];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const int j = j0 + c;
+        lo[c] = (j <= i && j < n) ? T[i * kLd + j] : 0.f;
+        up[c] = (j >= i && j < n) ? T[j * kLd + i] : 0.f;
+      }
+      float* dl = t.tlow + int64_t(i) * t.ld + j0;
+      float* du = t.tup + int64_t(i) * t.ld + j0;
+      if (vst && j0 + 3 < n) {
+        *reinterpret_cast<float4*>(dl) = make_float4(lo[0], lo[1], lo[2], lo[3]);
+        *reinterpret_cast<float4*>(du) = make_float4(up[0], up[1], up[2], up[3]);
+      } else {
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const int j = j0 + c;
+          if (j < n && j <= i) dl[c] = lo[c];
+          if (j < n && j >= i) du[c] = up[c];
+        }
+      }
     }
+  }
   __syncthreads();
   LEAF_STAMP(18);
 }
@@ -512,7 +574,20 @@ int launch_base(spngd_ctx* ctx, const BaseTask* d_tasks, int n) {
                                         int(kBaseSmem)));
     attr = true;
   }
-  base_chol_inv_kernel<<<n, kBaseThreads, kBaseSmem, ctx->stream>>>(d_tasks, ctx->d_status);
+  {
+    static const bool pdl = getenv("SPNGD_NO_PDL") == nullptr;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(unsigned(n));
+    cfg.blockDim = dim3(kBaseThreads);
+    cfg.dynamicSmemBytes = kBaseSmem;
+    cfg.stream = ctx->stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    SPNGD_CUDA_TRY(cudaLaunchKernelEx(&cfg, base_chol_inv_kernel, d_tasks, ctx->d_status));
+  }
   SPNGD_CUDA_TRY(cudaGetLastError());
 #ifdef SPNGD_GEMM_TRACE_BUILD
   static int printed = 0;
@@ -523,6 +598,8 @@ int launch_base(spngd_ctx* ctx, const BaseTask* d_tasks, int n) {
     printf("leaf launch (%d leaves): load %lld", n, h[1] - h[0]);
     for (int kb = 0; kb < 4; ++kb) printf(" | kb%d diag %lld panel %lld syrk %lld", kb, h[2 + 3 * kb] - h[0], h[3 + 3 * kb] - h[0], h[4 + 3 * kb] - h[0]);
     printf(" | T rows %lld %lld %lld | store %lld\n", h[15] - h[0], h[16] - h[0], h[17] - h[0], h[18] - h[0]);
+    printf("   kb0 diag: rows-in %lld chol %lld store %lld subst %lld T-store %lld\n", h[20] - h[1], h[21] - h[20],
+           h[22] - h[21], h[23] - h[22], h[24] - h[23]);
   }
 #endif
   ctx->launches++;
