@@ -104,6 +104,36 @@ typedef struct spngd_bn_moments_req {
 } spngd_bn_moments_req;
 int spngd_bn_moments_batched(spngd_ctx* ctx, int n, const spngd_bn_moments_req* reqs);
 
+/* ---- Full 2c x 2c BN blocks (BnMode::Full) ----------------
+ * spngd_bn_full_moments_batched replaces build_bn_full (src/fisher.cpp:187-216):
+ * F = mean_s u_s u_s^T over the interleaved u_s = (gg[s][0], gb[s][0], gg[s][1],
+ * gb[s][1], ...) (2c), packed upper triangle, samples [lo, hi).  Built by the
+ * 3xTF32 SYRK engine.  damp_bn_full (fisher.cpp:248-253) is
+ * spngd_spd_inverse_batched(F, lambda) with a dense output.
+ * spngd_bn_full_solve_update_batched replaces precondition_bn_full
+ * (fisher.cpp:278-296) + the BN branch of ngd_step (fisher.cpp:346-359):
+ * (pg, pb) = F_inv (grad_gamma, grad_beta) interleaved, then
+ * w' = w - eta p + m v, v' = w' - w for gamma and beta. */
+typedef struct spngd_bn_full_req {
+  const float* gg;
+  const float* gb;
+  int64_t c;
+  int64_t lo, hi;
+  float* packed_out;      /* 2c(2c+1)/2 */
+} spngd_bn_full_req;
+int spngd_bn_full_moments_batched(spngd_ctx* ctx, int n, const spngd_bn_full_req* reqs);
+typedef struct spngd_bn_full_update_req {
+  const float* finv;      /* dense 2c x 2c (row-major, leading dimension ld) */
+  int64_t ld;
+  const float* grad;      /* [grad_gamma (c) | grad_beta (c)] */
+  int64_t c;
+  float* gamma; float* beta;
+  float* vgamma; float* vbeta;
+  float* pg_out; float* pb_out;  /* optional preconditioned gradient */
+} spngd_bn_full_update_req;
+int spngd_bn_full_solve_update_batched(spngd_ctx* ctx, int n, const spngd_bn_full_update_req* reqs, double eta,
+                                       double momentum);
+
 /* ---- BN per-sample parameter gradients ------------------
  * Replaces the per-sample capture of src/net.cpp:467-475:
  *   gg[s][ch] = sum_p dY[s][ch*S + p] * xhat[s][ch*S + p]

@@ -22,6 +22,15 @@ class FactorReq(C.Structure):
                 ("hi", _i64), ("scale", C.c_double), ("packed_out", _fp)]
 
 
+class BnFullReq(C.Structure):
+    _fields_ = [("gg", _fp), ("gb", _fp), ("c", _i64), ("lo", _i64), ("hi", _i64), ("packed_out", _fp)]
+
+
+class BnFullUpdateReq(C.Structure):
+    _fields_ = [("finv", _fp), ("ld", _i64), ("grad", _fp), ("c", _i64), ("gamma", _fp), ("beta", _fp),
+                ("vgamma", _fp), ("vbeta", _fp), ("pg_out", _fp), ("pb_out", _fp)]
+
+
 class BnGradReq(C.Structure):
     _fields_ = [("dy", _fp), ("xhat", _fp), ("M", _i64), ("c", _i64), ("S", _i64), ("gg", _fp), ("gb", _fp)]
 
@@ -82,6 +91,7 @@ EXPORTS = [
     "spngd_last_error", "spngd_version", "spngd_ctx_create", "spngd_ctx_destroy", "spngd_ctx_sync",
     "spngd_ctx_stream", "spngd_copy", "spngd_host_alloc", "spngd_host_free", "spngd_event_time",
     "spngd_factor_sym_batched", "spngd_bn_moments_batched", "spngd_bn_grad_reduce_batched",
+    "spngd_bn_full_moments_batched", "spngd_bn_full_solve_update_batched",
     "spngd_spd_inverse_batched", "spngd_damp_and_invert_batched",
     "spngd_precondition_update_batched", "spngd_bn_solve_update_batched",
     "spngd_stat_distance_batched", "spngd_tracker_create", "spngd_tracker_destroy",
@@ -127,6 +137,9 @@ def _declare(L):
         "spngd_factor_sym_batched": (C.c_int, [P, C.c_int, C.POINTER(FactorReq)]),
         "spngd_bn_moments_batched": (C.c_int, [P, C.c_int, C.POINTER(BnMomentsReq)]),
         "spngd_bn_grad_reduce_batched": (C.c_int, [P, C.c_int, C.POINTER(BnGradReq)]),
+        "spngd_bn_full_moments_batched": (C.c_int, [P, C.c_int, C.POINTER(BnFullReq)]),
+        "spngd_bn_full_solve_update_batched": (C.c_int, [P, C.c_int, C.POINTER(BnFullUpdateReq), C.c_double,
+                                                         C.c_double]),
         "spngd_spd_inverse_batched": (C.c_int, [P, C.c_int, C.POINTER(SpdReq)]),
         "spngd_damp_and_invert_batched": (C.c_int, [P, C.c_int, C.POINTER(KronReq), C.c_double]),
         "spngd_precondition_update_batched": (C.c_int, [P, C.c_int, C.POINTER(PrecondReq),

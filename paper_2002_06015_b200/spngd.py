@@ -248,6 +248,16 @@ class KroneckerBlock:  # fisher.hpp:24-31
 
 
 @dataclass
+class FullBnBlock:  # fisher.hpp:45-51: full 2c x 2c block (BnMode::Full)
+    layer: int = -1
+    F: Optional["SymMatrix"] = None
+    F_inv: Optional["SymMatrix"] = None
+    F_inv_dense: Optional[torch.Tensor] = None
+    lam: float = 0.0
+    fresh_step: int = -1
+
+
+@dataclass
 class UnitBnBlock:  # fisher.hpp:36-42, moments interleaved (fgg, fgb, fbb)
     layer: int = -1
     m3c: Optional[torch.Tensor] = None
@@ -504,6 +514,68 @@ def kron_update(block: KroneckerBlock, grad: torch.Tensor, W: torch.Tensor, V: t
     arr = (N.PrecondReq * 1)(req)
     check(N.lib().spngd_precondition_update_batched(context().h, 1, arr, eta, momentum))
     return P
+
+
+def build_bn_full(cap: CaptureBuffer, net: NetworkSpec, layer: int, mode=FisherMode.Empirical, lo: int = 0,
+                  hi: Optional[int] = None) -> FullBnBlock:
+    """fisher.hpp:79-81 (build_bn_full, fisher.cpp:187-216): F = E[u u^T] over the
+    interleaved (g_gamma, g_beta) per-sample vector, packed 2c x 2c."""
+    _check_layer(cap, net, layer, "build_bn_full")
+    lo, hi = _range(cap, lo, hi, "build_bn_full")
+    L, lc = net.layers[layer], cap.layers[layer]
+    if L.kind != BN:
+        raise ShapeMismatch(f"build_bn_full: layer {layer} ({L.describe()}) is not BatchNorm")
+    if mode == FisherMode.OneMC:
+        gg, gb = lc.bn_ggamma_sampled, lc.bn_gbeta_sampled
+        if gg is None or gg.numel() == 0:
+            raise MissingMcPass("build_bn_full: no sampled-label backward was run")
+    else:
+        gg, gb = lc.bn_ggamma_true, lc.bn_gbeta_true
+        if gg is None or gg.numel() == 0:
+            raise EmptyBatch("build_bn_full: no captured gradients")
+    c = L.channels
+    out = torch.empty(packed_size(2 * c), dtype=torch.float32, device=gg.device)
+    arr = (N.BnFullReq * 1)(N.BnFullReq(gg.data_ptr(), gb.data_ptr(), c, lo, hi, out.data_ptr()))
+    check(N.lib().spngd_bn_full_moments_batched(context().h, 1, arr))
+    return FullBnBlock(layer=layer, F=SymMatrix(2 * c, out))
+
+
+def damp_bn_full(block: FullBnBlock, lam: float):
+    """fisher.hpp:90 (fisher.cpp:248-253): F_inv = (F + lam I)^-1."""
+    if not (lam > 0.0):
+        raise NotPositiveDefinite("damp_bn_full: lambda must be > 0")
+    block.F_inv, block.F_inv_dense = spd_inverse(block.F, lam, dense=True)
+    block.lam = lam
+
+
+def precondition_bn_full(block: FullBnBlock, grad_gamma: torch.Tensor, grad_beta: torch.Tensor):
+    """fisher.cpp:278-296: (pg, pb) = F_inv (g_gamma, g_beta) interleaved."""
+    c = grad_gamma.numel()
+    if grad_beta.numel() != c or block.F is None or block.F.dim != 2 * c:
+        raise ShapeMismatch("precondition_bn_full: gradient length mismatch")
+    if block.F_inv_dense is None:
+        raise StaleBeyondLimit("precondition_bn_full: block never inverted")
+    grad = torch.cat([grad_gamma.reshape(-1), grad_beta.reshape(-1)]).float().contiguous()
+    pg = torch.empty(c, dtype=torch.float32, device=grad.device)
+    pb = torch.empty(c, dtype=torch.float32, device=grad.device)
+    d = block.F_inv_dense
+    req = N.BnFullUpdateReq(d.data_ptr(), d.stride(0), grad.data_ptr(), c, None, None, None, None, pg.data_ptr(),
+                            pb.data_ptr())
+    arr = (N.BnFullUpdateReq * 1)(req)
+    check(N.lib().spngd_bn_full_solve_update_batched(context().h, 1, arr, 0.0, 0.0))
+    return pg, pb
+
+
+def bn_full_update(block: FullBnBlock, grad2c: torch.Tensor, gamma, beta, vgamma, vbeta, eta, momentum):
+    """precondition_bn_full + the BN branch of ngd_step (fisher.cpp:346-359), in place."""
+    c = grad2c.numel() // 2
+    if block.F_inv_dense is None:
+        raise StaleBeyondLimit("precondition_bn_full: block never inverted")
+    d = block.F_inv_dense
+    req = N.BnFullUpdateReq(d.data_ptr(), d.stride(0), grad2c.data_ptr(), c, gamma.data_ptr(), beta.data_ptr(),
+                            vgamma.data_ptr(), vbeta.data_ptr(), None, None)
+    arr = (N.BnFullUpdateReq * 1)(req)
+    check(N.lib().spngd_bn_full_solve_update_batched(context().h, 1, arr, eta, momentum))
 
 
 def precondition_bn(block: UnitBnBlock, grad_gamma: torch.Tensor, grad_beta: torch.Tensor, lam: float):

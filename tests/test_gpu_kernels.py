@@ -228,3 +228,32 @@ def test_bn_grad_reduce_matches_oracle(cuda_dev):
         assert np.abs(gb.cpu().numpy() - wb).max() <= 2e-6 * scale * max(1.0, np.abs(wb).max())
     with pytest.raises(P.EmptyBatch):
         P.bn_grad_reduce(items[0][0], items[0][1], 0, 16, 49)
+
+
+@pytest.mark.parametrize("m,c,lam", [(64, 16, 2.5e-4), (32, 32, 1e-2), (8, 1, 2.5e-4)])
+def test_bn_full_block_matches_oracle(cuda_dev, m, c, lam):
+    """BnMode::Full (SURVEY §8f row 4): build_bn_full (fisher.cpp:187-216),
+    damp_bn_full (:248-253), precondition_bn_full (:278-296) and the BN update
+    of ngd_step (:346-359) against the fp64 oracle."""
+    gg = torch.randn(m, c, device="cuda")
+    gb = 0.6 * gg + 0.8 * torch.randn(m, c, device="cuda")
+    cap = P.CaptureBuffer(m, [P.LayerCapture(bn_ggamma_true=gg, bn_gbeta_true=gb)])
+    net = P.NetworkSpec([P.LayerSpec.batch_norm(c)])
+    blk = P.build_bn_full(cap, net, 0)
+    want_f = O.build_bn_full(gg.cpu().numpy(), gb.cpu().numpy(), 0, m)
+    assert rel(blk.F.data.cpu().numpy(), want_f) <= 1e-6
+    P.damp_bn_full(blk, lam)
+    finv = O.spd_inverse(want_f, 2 * c, lam)
+    xg, xb = torch.randn(c, device="cuda"), torch.randn(c, device="cuda")
+    pg, pb = P.precondition_bn_full(blk, xg, xb)
+    wg, wb = O.precondition_bn_full(finv, xg.cpu().numpy(), xb.cpu().numpy())
+    assert rel(pg.cpu().numpy(), wg) <= 1e-4 and rel(pb.cpu().numpy(), wb) <= 1e-4
+    gamma, beta = torch.ones(c, device="cuda"), torch.zeros(c, device="cuda")
+    vg, vb = 0.01 * torch.randn(c, device="cuda"), 0.01 * torch.randn(c, device="cuda")
+    g0, b0, vg0, vb0 = gamma.cpu().numpy(), beta.cpu().numpy(), vg.cpu().numpy(), vb.cpu().numpy()
+    P.bn_full_update(blk, torch.cat([xg, xb]).contiguous(), gamma, beta, vg, vb, 1.25e-2, 0.993)
+    ng, nvg = O.ngd_update(g0, wg, vg0, 1.25e-2, 0.993)
+    nb, nvb = O.ngd_update(b0, wb, vb0, 1.25e-2, 0.993)
+    assert rel(gamma.cpu().numpy(), ng) <= 1e-4 and rel(beta.cpu().numpy(), nb) <= 1e-4
+    with pytest.raises(P.ShapeMismatch):
+        P.precondition_bn_full(blk, torch.zeros(c + 1, device="cuda"), xb)
