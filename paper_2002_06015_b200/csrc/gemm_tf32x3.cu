@@ -916,6 +916,10 @@ int plan_problem_tiles(int problem_index, const GemmProblem& p, bool upper_only,
   kchunk = std::max(kTileK, (kchunk / kTileK) * kTileK);
   const int nchunks = std::max(1, (p.K + kchunk - 1) / kchunk);
   int used = 0;
+  struct SplitTile {
+    int tm, tn, slot0;
+  };
+  std::vector<SplitTile> split_tiles;
   for (int tm = 0; tm < tiles_m; ++tm)
     for (int tn = upper_only ? tm : 0; tn < tiles_n; ++tn) {
       if (p.ktri) {  // triangular operands: one item over the nonzero K band
@@ -932,14 +936,18 @@ int plan_problem_tiles(int problem_index, const GemmProblem& p, bool upper_only,
         items.push_back({problem_index, tm, tn, 0, p.K, -1});
         continue;
       }
+      // split-K: reserve this tile's slots now; the items are emitted below
+      // chunk-major so CTAs running together share A/B panels in L2.
       const int slot0 = *next_slot;
-      for (int q = 0; q < nchunks; ++q) {
-        const int k0 = q * kchunk, k1 = std::min(p.K, k0 + kchunk);
-        items.push_back({problem_index, tm, tn, k0, k1, (*next_slot)++});
-      }
+      *next_slot += nchunks;
       used += nchunks;
       if (reduce) reduce->push_back({tm, tn, slot0, nchunks, p.M, 0, reduce_scale, packed_out});
+      split_tiles.push_back({tm, tn, slot0});
     }
+  for (int q = 0; q < nchunks && !split_tiles.empty(); ++q) {
+    const int k0 = q * kchunk, k1 = std::min(p.K, k0 + kchunk);
+    for (const auto& st : split_tiles) items.push_back({problem_index, st.tm, st.tn, k0, k1, st.slot0 + q});
+  }
   return used;
 }
 
