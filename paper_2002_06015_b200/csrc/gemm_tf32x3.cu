@@ -164,7 +164,7 @@ __device__ __forceinline__ void issue_stage(const GemmOperand& op, int32_t r0, i
 
 __global__ void __launch_bounds__(kGemmThreads, 1)
     gemm_tf32x3_kernel(const GemmProblem* __restrict__ probs, const GemmWorkItem* __restrict__ items,
-                       float* __restrict__ partials, int* status, int dbg, long long* trace) {
+                       float* __restrict__ partials, int* status, long long* trace) {
   // trace (debug): for CTAs < 4, stages < 64: [cta][stage][4] clock64 stamps
   // {A TMA issued, A raw landed, MMA saw full, drain saw MMA done}.
 #ifdef SPNGD_GEMM_TRACE_BUILD
@@ -251,7 +251,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       mbar_wait(&ctl->tmem_full[b], (j >> 1) & 1);
       tc_fence_after();
       TRACE_STAMP(warp == 8 && lane == 0 && tr && j < 64, tr[j * 4 + 3]);
-      if (!(dbg & 2)) {
+      {
         float v[32];
         tmem_ld_32x32b_x32(tmem + lane_base + b * 128 + col_base, v);
 #pragma unroll
@@ -282,13 +282,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         for (int kk = 0; kk < kTileK / 8; ++kk) {
           const uint32_t koff = kk * 32;  // 8 tf32 = 32 bytes along the swizzled row
           const uint64_t dbh = umma_desc_k_sw128(b_hi + koff), dbl = umma_desc_k_sw128(b_lo + koff);
-          if (!(dbg & 4)) {
-            umma_tf32_ts(dt, a_lo + kk * 8, dbh, idesc, kk > 0 ? 1u : 0u);
-            umma_tf32_ts(dt, a_hi + kk * 8, dbl, idesc, 1u);
-            umma_tf32_ts(dt, a_hi + kk * 8, dbh, idesc, 1u);
-          } else {
-            umma_tf32_ts(dt, a_hi + kk * 8, dbh, idesc, kk > 0 ? 1u : 0u);
-          }
+          umma_tf32_ts(dt, a_lo + kk * 8, dbh, idesc, kk > 0 ? 1u : 0u);
+          umma_tf32_ts(dt, a_hi + kk * 8, dbl, idesc, 1u);
+          umma_tf32_ts(dt, a_hi + kk * 8, dbh, idesc, 1u);
         }
         umma_commit(&ctl->empty[slot]);
         umma_commit(&ctl->tmem_full[b]);
@@ -357,10 +353,6 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     auto convert_a = [&](int it) {
       const int slot = it % kStages;
       uint8_t* stage = smem + slot * kStageBytes;
-      if (dbg & 1) {
-        mbar_arrive(&ctl->full[slot]);
-        return;
-      }
       const int r = t;  // row of the tile == TMEM lane
       float x[32], h[32];
 #pragma unroll
@@ -393,7 +385,6 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     auto convert_b = [&](int it) {
       const int slot = it % kStages;
       uint8_t* stage = smem + slot * kStageBytes;
-      if (!(dbg & 1))
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
         const int r = rbase + 16 * j;
@@ -566,7 +557,6 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           v.z = e.alpha * v.z + e.beta * cin[u].z;
           v.w = e.alpha * v.w + e.beta * cin[u].w;
           *tp = v;
-          if (dbg & 8) continue;
           float* dst = e.C + i * e.ldc + j;
           if (vec && j + 3 < e.N && (!mirror || i <= j)) {
             *reinterpret_cast<float4*>(dst) = v;
@@ -589,7 +579,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           int c, r;
           col_chunk(k, c, r);
           const int64_t i = m0 + r, j = n0 + c;  // writes dstT[j][i .. i+3]
-          if (j >= e.N || (dbg & 64)) continue;
+          if (j >= e.N) continue;
           const float4 v = t_col4(r, c);
           float* dst = dstT + j * ldt + i;
           if (vt && i + 3 < e.M && (!mirror || i + 3 < j)) {
@@ -765,8 +755,6 @@ void finalize_operand(GemmOperand& op, int64_t K, bool allow_tma) {
   }
 }
 
-int g_gemm_dbg_extra = 0;
-
 // Same tensor as the operand's own map, 64-row boxes (the B half-tile of the
 // 2-CTA SYRK, gemm_pair.cu).  Valid for OP_TMA2D / OP_TMA3D operands.
 int encode_half_map(const GemmOperand& op, int64_t K, CUtensorMap* out) {
@@ -838,8 +826,6 @@ int launch_gemm(const GemmProblem* d_probs, const GemmWorkItem* d_items, int n_i
     SPNGD_CUDA_TRY(cudaFuncSetAttribute(gemm_tf32x3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     attr_set = true;
   }
-  static const int dbg_env = getenv("SPNGD_GEMM_DEBUG") ? atoi(getenv("SPNGD_GEMM_DEBUG")) : 0;
-  const int dbg = dbg_env | g_gemm_dbg_extra;
   static long long* trace = nullptr;
 #ifdef SPNGD_GEMM_TRACE_BUILD
   static const bool want_trace = getenv("SPNGD_GEMM_TRACE") != nullptr;
@@ -864,7 +850,7 @@ int launch_gemm(const GemmProblem* d_probs, const GemmWorkItem* d_items, int n_i
     attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    cudaError_t le = cudaLaunchKernelEx(&cfg, gemm_tf32x3_kernel, d_probs, d_items, d_partials, d_status, dbg, trace);
+    cudaError_t le = cudaLaunchKernelEx(&cfg, gemm_tf32x3_kernel, d_probs, d_items, d_partials, d_status, trace);
     if (le != cudaSuccess) return fail(SPNGD_ERR_CUDA, "gemm launch failed: %s", cudaGetErrorString(le));
   }
   if (want_trace) {

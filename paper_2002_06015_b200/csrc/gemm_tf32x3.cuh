@@ -110,7 +110,6 @@ inline int64_t padded_k(const GemmOperand& op, int64_t K) {
 size_t gemm_smem_bytes();
 
 // Launch one grouped GEMM over device-resident problem/work arrays.
-extern int g_gemm_dbg_extra;  // debug: extra SPNGD_GEMM_DEBUG bits for the next launch
 int launch_gemm(const GemmProblem* d_probs, const GemmWorkItem* d_items, int n_items, float* d_partials,
                 int* d_status, cudaStream_t stream);
 int launch_syrk_reduce(const SyrkReduceTask* d_tasks, int n_tasks, const float* d_partials, cudaStream_t stream);

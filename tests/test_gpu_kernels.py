@@ -257,3 +257,18 @@ def test_bn_full_block_matches_oracle(cuda_dev, m, c, lam):
     assert rel(gamma.cpu().numpy(), ng) <= 1e-4 and rel(beta.cpu().numpy(), nb) <= 1e-4
     with pytest.raises(P.ShapeMismatch):
         P.precondition_bn_full(blk, torch.zeros(c + 1, device="cuda"), xb)
+
+
+def test_pair_sm_factor_kernel_subprocess(cuda_dev):
+    """The opt-in 2-CTA (cta_group::2) factor SYRK (SPNGD_PAIR=1, gemm_pair.cu)
+    passes the same factor parity tests (run in a subprocess: the switch is read
+    once per process)."""
+    import os
+    import subprocess
+    import sys
+    env = dict(os.environ, SPNGD_PAIR="1")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-p", "no:cacheprovider", "-k",
+                        "conv_factor_A or fc_factor", os.path.join(root, "tests", "test_gpu_kernels.py")],
+                       env=env, cwd=root, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
