@@ -172,7 +172,8 @@ int launch_factor_gemm(spngd_ctx* ctx, const FactorPlan& plan, const GemmProblem
                        const CUtensorMap* d_halfmaps, const GemmWorkItem* d_items, int n_items, float* d_partials,
                        cudaStream_t stream) {
   if (plan.pair) return launch_gemm_pair(d_probs, d_halfmaps, d_items, n_items, d_partials, stream);
-  return launch_gemm(d_probs, d_items, n_items, d_partials, ctx->d_status, stream);
+  return launch_gemm(d_probs, d_items, n_items, d_partials, ctx->d_status, stream,
+                     gemm_variant(plan.probs.data(), int(plan.probs.size())));
 }
 
 int run_factors(spngd_ctx* ctx, const FactorPlan& plan, const GemmProblem* d_probs, const CUtensorMap* d_halfmaps,

@@ -162,6 +162,12 @@ __device__ __forceinline__ void issue_stage(const GemmOperand& op, int32_t r0, i
   }
 }
 
+// kModes: bit set of the GemmEpi modes compiled in; kAsync: the cp.async
+// (OP_ASYNC) operand path is compiled in.  Each launch gets the smallest
+// variant its problems need: the inverse recursion issues ~100 short launches
+// per matrix that each start with a cold instruction cache, so code size is
+// latency.
+template <uint32_t kModes, bool kAsync>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     gemm_tf32x3_kernel(const GemmProblem* __restrict__ probs, const GemmWorkItem* __restrict__ items,
                        float* __restrict__ partials, int* status, long long* trace) {
@@ -325,7 +331,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     // tensor core truncates fp32 to tf32), each thread derives the lo plane
     // for its 8 16-byte chunks.
     const int32_t r0 = row0 + rbase;
-    const bool tma = op.mode != OP_ASYNC;
+    const bool tma = !kAsync || op.mode != OP_ASYNC;
     const CUtensorMap* tmap = is_b ? &probs[item.problem].B.tmap : &probs[item.problem].A.tmap;
     uint64_t* raw = ctl->raw[is_b ? 1 : 0];
     KCursor cur{};
@@ -345,7 +351,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           }
         }
         ++tq;
-      } else {
+      } else if constexpr (kAsync) {
         issue_stage(op, r0, rbase, c, cur, item.k1, plane);
         cursor_advance(op, cur, kTileK);
       }
@@ -411,13 +417,13 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                        : "memory");
           asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(tmap)) : "memory");
         }
-      } else {
+      } else if constexpr (kAsync) {
         cur = cursor_at(op, item.k0 + 4 * c);
       }
 #pragma unroll
       for (int q = 0; q < kStages - 1; ++q) {
         if (q < n_iters) issue(q);
-        cp_async_commit();
+        if constexpr (kAsync) cp_async_commit();
       }
     }
     for (int it = 0; it < n_iters; ++it) {
@@ -425,7 +431,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         if (tma) {
           mbar_wait(&raw[it % kStages], (it / kStages) & 1);
           TRACE_STAMP(tr && !is_b && t == 0 && it < 64, tr[it * 4 + 1]);
-        } else {
+        } else if constexpr (kAsync) {
           cp_async_wait<kStages - 2>();
           if (!is_b) asm volatile("bar.sync 2, 128;" ::: "memory");  // rows span other threads' copies
         }
@@ -436,7 +442,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           if (!tma || t == 0) mbar_wait(&ctl->empty[nx % kStages], ((nx / kStages) & 1) ^ 1);
           issue(nx);
         }
-        cp_async_commit();
+        if constexpr (kAsync) cp_async_commit();
       }
     }
     TRACE_STAMP(meta && threadIdx.x == 0, meta[4]);
@@ -491,7 +497,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   };
   auto aligned16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
   switch (e.mode) {
-    case EPI_PARTIAL: {
+    case EPI_PARTIAL: if constexpr ((kModes >> EPI_PARTIAL) & 1) {
       float4* dst = reinterpret_cast<float4*>(partials + int64_t(item.slot) * kTileM * kTileN);
 #pragma unroll 4
       for (int k = 0; k < 8; ++k) {
@@ -501,7 +507,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       }
       break;
     }
-    case EPI_PACKED: {
+    case EPI_PACKED: if constexpr ((kModes >> EPI_PACKED) & 1) {
       const int64_t n = e.M;
 #pragma unroll 2
       for (int k = 0; k < 8; ++k) {
@@ -520,7 +526,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       }
       break;
     }
-    case EPI_DENSE: {
+    case EPI_DENSE: if constexpr ((kModes >> EPI_DENSE) & 1) {
       const bool mirror = (e.flags & FLAG_SYM_MIRROR) != 0;
       const bool has_cin = e.beta != 0.f;
       const bool vec = aligned16(e.C) && (!has_cin || aligned16(e.Cin)) && (e.ldc & 3) == 0;
@@ -594,7 +600,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       }
       break;
     }
-    case EPI_UPDATE: {
+    case EPI_UPDATE: if constexpr ((kModes >> EPI_UPDATE) & 1) {
       // Tile of P^T: rows = a-index (M = a), cols = g-index.  W is g x a
       // row-major, so element (i = n0+c, j = m0+r) lives at W[i*a + j]:
       // column chunks of T are contiguous in W.
@@ -817,15 +823,56 @@ int plan_problem_pairs(int problem_index, const GemmProblem& p, int kchunk, std:
 
 size_t gemm_smem_bytes() { return size_t(kStages) * kStageBytes + sizeof(SmemCtl) + 1024; }
 
-int launch_gemm(const GemmProblem* d_probs, const GemmWorkItem* d_items, int n_items, float* d_partials,
-                int* d_status, cudaStream_t stream) {
-  if (n_items <= 0) return SPNGD_OK;
+uint32_t gemm_variant(const GemmProblem* probs, int n) {
+  uint32_t v = 0;
+  for (int i = 0; i < n; ++i) {
+    v |= 1u << probs[i].mode;
+    if (probs[i].A.mode == OP_ASYNC || probs[i].B.mode == OP_ASYNC) v |= kVariantAsync;
+  }
+  return v;
+}
+
+namespace {
+using GemmKernelFn = void (*)(const GemmProblem*, const GemmWorkItem*, float*, int*, long long*);
+
+template <uint32_t kModes, bool kAsync>
+GemmKernelFn gemm_instance(size_t smem, int* err) {
   static bool attr_set = false;
-  const size_t smem = gemm_smem_bytes();
   if (!attr_set) {
-    SPNGD_CUDA_TRY(cudaFuncSetAttribute(gemm_tf32x3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    if (cudaFuncSetAttribute(gemm_tf32x3_kernel<kModes, kAsync>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             int(smem)) != cudaSuccess) {
+      *err = 1;
+      return nullptr;
+    }
     attr_set = true;
   }
+  return gemm_tf32x3_kernel<kModes, kAsync>;
+}
+
+// The variants the planners produce (factor: PARTIAL|PACKED; inverse rounds
+// and precondition GEMM1: DENSE; precondition GEMM2: UPDATE), each with and
+// without the cp.async operand path; anything else runs the full kernel.
+GemmKernelFn select_gemm(uint32_t variant, size_t smem, int* err) {
+  constexpr uint32_t kPart = 1u << EPI_PARTIAL, kPack = 1u << EPI_PACKED, kDense = 1u << EPI_DENSE,
+                     kUpd = 1u << EPI_UPDATE;
+  const bool async = variant & kVariantAsync;
+  const uint32_t modes = variant & 0xFu;
+  if ((modes & ~(kPart | kPack)) == 0)
+    return async ? gemm_instance<kPart | kPack, true>(smem, err) : gemm_instance<kPart | kPack, false>(smem, err);
+  if (modes == kDense)
+    return async ? gemm_instance<kDense, true>(smem, err) : gemm_instance<kDense, false>(smem, err);
+  if (modes == kUpd) return async ? gemm_instance<kUpd, true>(smem, err) : gemm_instance<kUpd, false>(smem, err);
+  return gemm_instance<0xFu, true>(smem, err);
+}
+}  // namespace
+
+int launch_gemm(const GemmProblem* d_probs, const GemmWorkItem* d_items, int n_items, float* d_partials,
+                int* d_status, cudaStream_t stream, uint32_t variant) {
+  if (n_items <= 0) return SPNGD_OK;
+  const size_t smem = gemm_smem_bytes();
+  int aerr = 0;
+  GemmKernelFn kern = select_gemm(variant, smem, &aerr);
+  if (aerr) return fail(SPNGD_ERR_CUDA, "gemm smem attribute failed");
   static long long* trace = nullptr;
 #ifdef SPNGD_GEMM_TRACE_BUILD
   static const bool want_trace = getenv("SPNGD_GEMM_TRACE") != nullptr;
@@ -850,7 +897,7 @@ int launch_gemm(const GemmProblem* d_probs, const GemmWorkItem* d_items, int n_i
     attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    cudaError_t le = cudaLaunchKernelEx(&cfg, gemm_tf32x3_kernel, d_probs, d_items, d_partials, d_status, trace);
+    cudaError_t le = cudaLaunchKernelEx(&cfg, kern, d_probs, d_items, d_partials, d_status, trace);
     if (le != cudaSuccess) return fail(SPNGD_ERR_CUDA, "gemm launch failed: %s", cudaGetErrorString(le));
   }
   if (want_trace) {
@@ -880,7 +927,7 @@ int launch_gemm(const GemmProblem* d_probs, const GemmWorkItem* d_items, int n_i
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     cudaFuncAttributes fa{};
-    cudaFuncGetAttributes(&fa, gemm_tf32x3_kernel);
+    cudaFuncGetAttributes(&fa, reinterpret_cast<const void*>(kern));
     return fail(SPNGD_ERR_CUDA, "gemm launch failed: %s (regs %d, maxThreads %d, static smem %zu, dyn smem %zu)",
                 cudaGetErrorString(e), fa.numRegs, fa.maxThreadsPerBlock, fa.sharedSizeBytes, smem);
   }

@@ -109,9 +109,15 @@ inline int64_t padded_k(const GemmOperand& op, int64_t K) {
 }
 size_t gemm_smem_bytes();
 
+// Kernel variant a launch needs: bit (1 << mode) per epilogue mode in use,
+// plus kVariantAsync when any operand takes the cp.async path.  Computed at
+// plan time; launch_gemm runs the smallest compiled kernel that covers it.
+constexpr uint32_t kVariantAsync = 0x100u;
+uint32_t gemm_variant(const GemmProblem* probs, int n);
+
 // Launch one grouped GEMM over device-resident problem/work arrays.
 int launch_gemm(const GemmProblem* d_probs, const GemmWorkItem* d_items, int n_items, float* d_partials,
-                int* d_status, cudaStream_t stream);
+                int* d_status, cudaStream_t stream, uint32_t variant = 0xFu | kVariantAsync);
 int launch_syrk_reduce(const SyrkReduceTask* d_tasks, int n_tasks, const float* d_partials, cudaStream_t stream);
 
 // 2-CTA SYRK (gemm_pair.cu): items come in cluster pairs (2p, 2p+1) x tn;

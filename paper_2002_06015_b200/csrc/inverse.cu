@@ -608,11 +608,12 @@ int launch_base(spngd_ctx* ctx, const BaseTask* d_tasks, int n) {
 
 int run_inverse(spngd_ctx* ctx, const InversePlan& plan, const GemmProblem* d_probs, const GemmWorkItem* d_items,
                 const BaseTask* d_bases) {
+  const uint32_t variant = gemm_variant(plan.probs.data(), int(plan.probs.size()));
   for (const InverseRound& r : plan.rounds) {
     int rc = launch_base(ctx, d_bases + r.base_off, r.base_cnt);
     if (rc) return rc;
     if (r.item_cnt > 0) {
-      rc = launch_gemm(d_probs, d_items + r.item_off, r.item_cnt, nullptr, ctx->d_status, ctx->stream);
+      rc = launch_gemm(d_probs, d_items + r.item_off, r.item_cnt, nullptr, ctx->d_status, ctx->stream, variant);
       if (rc) return rc;
       ctx->launches++;
     }

@@ -192,9 +192,11 @@ int run_precondition(spngd_ctx* ctx, const PrecondPlan& plan, const GemmProblem*
                      double* d_norms) {
   if (d_norms && plan.n_norms > 0)
     SPNGD_CUDA_TRY(cudaMemsetAsync(d_norms, 0, sizeof(double) * plan.n_norms, ctx->stream));
-  int rc = launch_gemm(d_p1, d_i1, int(plan.items1.size()), nullptr, ctx->d_status, ctx->stream);
+  int rc = launch_gemm(d_p1, d_i1, int(plan.items1.size()), nullptr, ctx->d_status, ctx->stream,
+                       gemm_variant(plan.probs1.data(), int(plan.probs1.size())));
   if (rc) return rc;
-  rc = launch_gemm(d_p2, d_i2, int(plan.items2.size()), nullptr, ctx->d_status, ctx->stream);
+  rc = launch_gemm(d_p2, d_i2, int(plan.items2.size()), nullptr, ctx->d_status, ctx->stream,
+                   gemm_variant(plan.probs2.data(), int(plan.probs2.size())));
   if (rc) return rc;
   ctx->launches += 2;
   if (!plan.rescale.empty()) {
