@@ -27,18 +27,13 @@ namespace spngd {
 namespace {
 
 constexpr int kBaseMax = 128;
-constexpr int kPB = 32;                 // panel width = one warp of rows
-constexpr int kBaseThreads = 256;
+constexpr int kLeafWarps = 8;           // warp w owns rows 4 w + t + 32 g (t, g = 0..3)
+constexpr int kBaseThreads = 32 * kLeafWarps;
 constexpr int kLd = kBaseMax + 1;       // padded smem row (floats)
-constexpr int kNb = kBaseMax / kPB;
-constexpr size_t kBaseSmem = (2 * size_t(kBaseMax) * kLd + size_t(kNb) * kPB * kPB + kBaseMax) * sizeof(float);
+// staging [128][129] | published rows R [2][4][64] float2 | -L columns [2][128] float4
+constexpr size_t kBaseSmem = size_t(kBaseMax) * kLd * sizeof(float) + 2 * 4 * 64 * sizeof(float2) +
+                             2 * kBaseMax * sizeof(float4);
 
-// Compile-time-unrolled steps of the 32x32 diagonal factorization (rows in
-// lanes) and of the column substitution, so `row`/`col` stay in registers.
-// Step K with its pivot p = A_KK (already broadcast) and inv = 1/sqrt(p).
-// The next pivot depends only on column K+1, so it is updated and the next
-// broadcast + rsqrt issued before the remaining rank-1 columns of this step:
-// the serial pivot chain overlaps the bulk of the shuffles.
 __device__ __forceinline__ float pivot_rsqrt(float p, bool& bad) {
   if (!(p > 0.f) || !isfinite(p)) {
     bad = true;
@@ -48,46 +43,24 @@ __device__ __forceinline__ float pivot_rsqrt(float p, bool& bad) {
   return inv * fmaf(-0.5f * p, inv * inv, 1.5f);  // MUFU rsqrt + one Newton step
 }
 
-template <int K>
-__device__ __forceinline__ void diag_chol_step(float (&row)[32], int lane, float* rdiag, bool& bad, float p,
-                                               float inv) {
-  if (lane == K) rdiag[K] = inv;
-  row[K] = (lane == K) ? p * inv : (lane > K ? row[K] * inv : row[K]);
-  if constexpr (K + 1 < 32) {
-    const float l1 = __shfl_sync(0xffffffffu, row[K], K + 1);
-    row[K + 1] = (lane >= K + 1) ? fmaf(-row[K], l1, row[K + 1]) : row[K + 1];
-    const float pn = __shfl_sync(0xffffffffu, row[K + 1], K + 1);  // next pivot
-    const float invn = pivot_rsqrt(pn, bad);
-#pragma unroll
-    for (int j = K + 2; j < 32; ++j) {
-      const float ljk = __shfl_sync(0xffffffffu, row[K], j);
-      row[j] = (lane >= j) ? fmaf(-row[K], ljk, row[j]) : row[j];
-    }
-    diag_chol_step<K + 1>(row, lane, rdiag, bad, pn, invn);
-  }
-}
-
-template <int I>
-__device__ __forceinline__ void diag_subst_step(float (&col)[32], const float* Ld, int ld, const float* rdiag,
-                                                int lane) {
-  float a0 = (I == lane) ? 1.f : 0.f, a1 = 0.f;
-#pragma unroll
-  for (int p = 0; p < I; ++p) {
-    if (p & 1) a1 = fmaf(-Ld[I * ld + p], col[p], a1);
-    else a0 = fmaf(-Ld[I * ld + p], col[p], a0);
-  }
-  col[I] = (I < lane) ? 0.f : (a0 + a1) * rdiag[I];
-  if constexpr (I + 1 < 32) diag_subst_step<I + 1>(col, Ld, ld, rdiag, lane);
-}
-
-// One CTA per leaf (n <= 128): blocked right-looking Cholesky with 32-column
-// panels.  Warp 0 factors each 32x32 diagonal block with rows in lanes and
-// columns broadcast by shuffle, then inverts it by forward substitution; all
-// warps solve the panel and apply the SYRK trailing update on 4x4 register
-// tiles; finally T = L^-1 by blocked forward substitution.  fp32 storage and
-// FMA (LAPACK spotrf class).
+// One CTA per leaf (n <= 128): Cholesky by blocked column elimination with
+// T = L^-1 formed in the same pass; the whole 128x128 working matrix X sits in
+// registers (thread (w, l) holds rows 4w + t + 32g, columns 2l + 64p + {0,1}).
+//
+// Block b (rows/columns K = 4b..4b+3, one barrier): the warp owning rows K
+// takes the 4x4 Schur block D = X_KK (already updated by blocks < b), forms
+// L_d = chol(D) and T_d = L_d^-1 redundantly in every lane, and publishes
+//     R = T_d * X~_K.     (X~_K = rows K with the K columns replaced by I)
+// R holds T_Kj for j < 4b+4 (T_d itself in the K columns) and L_jK for j beyond
+// (the trailing part of X is kept symmetric, so row K = column K there).  Every
+// later row i then applies  X_i. -= L_iK R  with its K entries zeroed first:
+// the Schur update for trailing columns, and for columns already eliminated
+// the forward elimination T_ij = -(1/L_ii) sum_{k=j}^{i-1} L_ik T_kj carried
+// column-block-wise (the 1/L_ii arrives when row i's block publishes).  After
+// the last block the lower triangle of X is T.  Updates are packed fp32x2
+// FMAs; fp32 storage and arithmetic (LAPACK spotrf/strtri class).
 #ifdef SPNGD_GEMM_TRACE_BUILD
-__device__ long long g_leaf_trace[32];
+__device__ long long g_leaf_trace[8];
 #define LEAF_STAMP(i) \
   do {                \
     if (blockIdx.x == 0 && threadIdx.x == 0) g_leaf_trace[i] = clock64(); \
@@ -98,198 +71,215 @@ __device__ long long g_leaf_trace[32];
   } while (0)
 #endif
 
+struct LeafBufs {
+  float2* R;   // [2][4][64]: published rows by column pair
+  float4* L;   // [2][128]:  (-L_i,4b .. -L_i,4b+3) by row i
+};
+
+// Apply block b (column pair group P = b >> 4, pairs 2b, 2b+1 in lanes lk0,
+// lk0+1) to rows (G, t = 0..3) of this thread.
+template <int G, int P>
+__device__ __forceinline__ void leaf_apply(float2 (&x)[4][4][2], const float2 (&r)[4][2], const float4* lcol,
+                                           int row0, float m) {
+#pragma unroll
+  for (int t = 0; t < 4; ++t) {
+    const float4 nl = lcol[row0 + t];
+    x[G][t][P] = __fmul2_rn(x[G][t][P], make_float2(m, m));
+#pragma unroll
+    for (int p = 0; p < 2; ++p) {
+      float2 v = x[G][t][p];
+      v = __ffma2_rn(make_float2(nl.x, nl.x), r[0][p], v);
+      v = __ffma2_rn(make_float2(nl.y, nl.y), r[1][p], v);
+      v = __ffma2_rn(make_float2(nl.z, nl.z), r[2][p], v);
+      v = __ffma2_rn(make_float2(nl.w, nl.w), r[3][p], v);
+      x[G][t][p] = v;
+    }
+  }
+}
+
+// Row slots Gs..3 (slot Gs skipped when !first: already applied by the publisher).
+template <int Gs, int P>
+__device__ __forceinline__ void leaf_apply_rest(float2 (&x)[4][4][2], const float2 (&r)[4][2], const float4* lcol,
+                                                int row0, float m, bool first) {
+  if (first) leaf_apply<Gs, P>(x, r, lcol, row0 + 32 * Gs, m);
+  if constexpr (Gs < 3) leaf_apply_rest<Gs + 1, P>(x, r, lcol, row0, m, true);
+}
+
+// Factor and publish block b = 8 G + warp (rows slot G of this warp).
+template <int G>
+__device__ __forceinline__ void leaf_publish(float2 (&x)[4][4][2], int b, int lane, float2* R, float4* L, bool& bad) {
+  constexpr int P = G >> 1;
+  const int lk0 = (2 * b) & 31;
+  // D = X_KK gathered into every lane: lane lk0 holds columns (4b, 4b+1), lane
+  // lk0 + 1 columns (4b+2, 4b+3).
+  float d[4][4];
+#pragma unroll
+  for (int t = 0; t < 4; ++t) {
+    d[t][0] = __shfl_sync(0xffffffffu, x[G][t][P].x, lk0);
+    d[t][1] = __shfl_sync(0xffffffffu, x[G][t][P].y, lk0);
+    d[t][2] = __shfl_sync(0xffffffffu, x[G][t][P].x, lk0 + 1);
+    d[t][3] = __shfl_sync(0xffffffffu, x[G][t][P].y, lk0 + 1);
+  }
+  // L_d = chol(D), T_d = L_d^-1 (lower; r_t = 1 / L_tt).
+  const float r0 = pivot_rsqrt(d[0][0], bad);
+  const float l10 = d[1][0] * r0, l20 = d[2][0] * r0, l30 = d[3][0] * r0;
+  const float r1 = pivot_rsqrt(fmaf(-l10, l10, d[1][1]), bad);
+  const float l21 = fmaf(-l20, l10, d[2][1]) * r1, l31 = fmaf(-l30, l10, d[3][1]) * r1;
+  const float r2 = pivot_rsqrt(fmaf(-l21, l21, fmaf(-l20, l20, d[2][2])), bad);
+  const float l32 = fmaf(-l31, l21, fmaf(-l30, l20, d[3][2])) * r2;
+  const float r3 = pivot_rsqrt(fmaf(-l32, l32, fmaf(-l31, l31, fmaf(-l30, l30, d[3][3]))), bad);
+  const float t10 = -r1 * l10 * r0;
+  const float t21 = -r2 * l21 * r1;
+  const float t20 = -r2 * fmaf(l21, t10, l20 * r0);
+  const float t32 = -r3 * l32 * r2;
+  const float t31 = -r3 * fmaf(l32, t21, l31 * r1);
+  const float t30 = -r3 * fmaf(l32, t20, fmaf(l31, t10, l30 * r0));
+  // X~: the block's own columns become the identity.
+  if (lane == lk0) {
+    x[G][0][P] = make_float2(1.f, 0.f);
+    x[G][1][P] = make_float2(0.f, 1.f);
+    x[G][2][P] = make_float2(0.f, 0.f);
+    x[G][3][P] = make_float2(0.f, 0.f);
+  } else if (lane == lk0 + 1) {
+    x[G][0][P] = make_float2(0.f, 0.f);
+    x[G][1][P] = make_float2(0.f, 0.f);
+    x[G][2][P] = make_float2(1.f, 0.f);
+    x[G][3][P] = make_float2(0.f, 1.f);
+  }
+#pragma unroll
+  for (int p = 0; p < 2; ++p) {
+    const float2 x0 = x[G][0][p], x1 = x[G][1][p], x2 = x[G][2][p], x3 = x[G][3][p];
+    const float2 y0 = __fmul2_rn(make_float2(r0, r0), x0);
+    const float2 y1 = __ffma2_rn(make_float2(r1, r1), x1, __fmul2_rn(make_float2(t10, t10), x0));
+    const float2 y2 = __ffma2_rn(make_float2(r2, r2), x2,
+                                 __ffma2_rn(make_float2(t21, t21), x1, __fmul2_rn(make_float2(t20, t20), x0)));
+    const float2 y3 = __ffma2_rn(
+        make_float2(r3, r3), x3,
+        __ffma2_rn(make_float2(t32, t32), x2,
+                   __ffma2_rn(make_float2(t31, t31), x1, __fmul2_rn(make_float2(t30, t30), x0))));
+    x[G][0][p] = y0;
+    x[G][1][p] = y1;
+    x[G][2][p] = y2;
+    x[G][3][p] = y3;
+#pragma unroll
+    for (int t = 0; t < 4; ++t) R[t * 64 + 32 * p + lane] = x[G][t][p];
+    L[2 * lane + 64 * p] = make_float4(-y0.x, -y1.x, -y2.x, -y3.x);
+    L[2 * lane + 64 * p + 1] = make_float4(-y0.y, -y1.y, -y2.y, -y3.y);
+  }
+  __syncwarp();  // the publishing warp reads its own rows next without waiting at the barrier
+}
+
+// Blocks b = 8 G + wp, wp = 0..7 (G static: which register rows can still be
+// active and which column pair group holds the block are compile-time).  The
+// warp owning block b + 1 applies block b to those rows first and publishes,
+// then finishes its other rows while the CTA is still consuming block b; it
+// only arrives at the barrier (it needs nothing newer than its own rows).
+// Barrier ids alternate by parity so an arrive-only warp is never counted
+// twice in one barrier instance.
+template <int G>
+__device__ __forceinline__ void leaf_blocks(float2 (&x)[4][4][2], int nb, int warp, int lane, LeafBufs buf,
+                                            bool& bad) {
+  constexpr int P = G >> 1;
+  for (int wp = 0; wp < kLeafWarps; ++wp) {
+    const int b = kLeafWarps * G + wp;
+    if (b >= nb) return;
+    const float2* Rb = buf.R + (b & 1) * 256;
+    const float4* Lb = buf.L + (b & 1) * kBaseMax;
+    float2 r[4][2];
+#pragma unroll
+    for (int t = 0; t < 4; ++t)
+#pragma unroll
+      for (int p = 0; p < 2; ++p) r[t][p] = Rb[t * 64 + 32 * p + lane];
+    const float m = ((lane >> 1) == (b & 15)) ? 0.f : 1.f;  // zero the block's own columns first
+    const int b1 = b + 1;
+    const bool producer = b1 < nb && warp == (b1 & (kLeafWarps - 1));
+    float2* Rn = buf.R + (b1 & 1) * 256;
+    float4* Ln = buf.L + (b1 & 1) * kBaseMax;
+    if (producer) {
+      if (wp < kLeafWarps - 1) {
+        leaf_apply<G, P>(x, r, Lb, 4 * warp + 32 * G, m);
+        leaf_publish<G>(x, b1, lane, Rn, Ln, bad);
+      } else if constexpr (G < 3) {
+        leaf_apply<G + 1, P>(x, r, Lb, 4 * warp + 32 * (G + 1), m);
+        leaf_publish<G + 1>(x, b1, lane, Rn, Ln, bad);
+      }
+    }
+    if ((warp > wp) && !(producer && wp < kLeafWarps - 1)) leaf_apply<G, P>(x, r, Lb, 4 * warp + 32 * G, m);
+    if constexpr (G < 3) leaf_apply_rest<G + 1, P>(x, r, Lb, 4 * warp, m, !(producer && wp == kLeafWarps - 1));
+    if (producer) asm volatile("bar.arrive %0, %1;" ::"r"(1 + (b1 & 1)), "r"(kBaseThreads) : "memory");
+    else asm volatile("bar.sync %0, %1;" ::"r"(1 + (b1 & 1)), "r"(kBaseThreads) : "memory");
+  }
+  if constexpr (G < 3) leaf_blocks<G + 1>(x, nb, warp, lane, buf, bad);
+}
+
 __global__ void __launch_bounds__(kBaseThreads, 1) base_chol_inv_kernel(const BaseTask* __restrict__ tasks, int* status) {
   LEAF_STAMP(0);
   extern __shared__ __align__(16) uint8_t base_smem[];
-  float* A = reinterpret_cast<float*>(base_smem);   // [128][129], lower = M -> L
-  float* T = A + kBaseMax * kLd;                    // [128][129], T = L^-1
-  float* R = T + kBaseMax * kLd;                    // [4][32][32] scratch
-  float* rdiag = R + kNb * kPB * kPB;               // [128] 1 / L_ii
+  float* S = reinterpret_cast<float*>(base_smem);  // [128][129] staging (M in, T out)
+  LeafBufs buf;
+  buf.R = reinterpret_cast<float2*>(S + kBaseMax * kLd);
+  buf.L = reinterpret_cast<float4*>(buf.R + 2 * 4 * 64);
   const BaseTask t = tasks[blockIdx.x];
   const int n = t.n;
   // PDL: the task table is static; the matrix comes from the previous kernel.
   asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  const int np = (n + kPB - 1) / kPB * kPB;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  // Load M's lower triangle: warp w owns rows w + 8 q, lane l columns
-  // 32 cc + l (coalesced 128-byte rows, conflict-free smem stores); all 64
-  // loads of a warp are in flight before any store.  Identity padding beyond
-  // n is inert.
+  // Stage M's lower triangle (identity beyond n): warp w rows w + 8 q, lane
+  // columns 32 c + l; all loads of a thread in flight before any store.
   {
-    float v[kNb][kBaseMax / 8];
+    constexpr int kRows = kBaseMax / kLeafWarps;
+    float v[4][kRows];
 #pragma unroll
-    for (int cc = 0; cc < kNb; ++cc)
+    for (int c = 0; c < 4; ++c)
 #pragma unroll
-      for (int q = 0; q < kBaseMax / 8; ++q) {
-        const int i = warp + 8 * q, j = 32 * cc + lane;
-        v[cc][q] = (i == j) ? 1.f : 0.f;
-        if (i < n && j < n && j <= i) v[cc][q] = __ldg(t.m + int64_t(i) * t.ld + j);
+      for (int q = 0; q < kRows; ++q) {
+        const int i = warp + kLeafWarps * q, j = 32 * c + lane;
+        v[c][q] = (i == j) ? 1.f : 0.f;
+        if (i < n && j < n && j <= i) v[c][q] = __ldg(t.m + int64_t(i) * t.ld + j);
       }
 #pragma unroll
-    for (int cc = 0; cc < kNb; ++cc)
+    for (int c = 0; c < 4; ++c)
 #pragma unroll
-      for (int q = 0; q < kBaseMax / 8; ++q) {
-        const int i = warp + 8 * q, j = 32 * cc + lane;
-        if (i < np && j < np) {
-          A[i * kLd + j] = v[cc][q];
-          T[i * kLd + j] = 0.f;
-        }
+      for (int q = 0; q < kRows; ++q) {
+        const int i = warp + kLeafWarps * q, j = 32 * c + lane;
+        if (j <= i) S[i * kLd + j] = v[c][q];
       }
   }
   __syncthreads();
+  // Registers: the full symmetric matrix (upper read mirrored).
+  float2 x[4][4][2];
+#pragma unroll
+  for (int g = 0; g < 4; ++g)
+#pragma unroll
+    for (int tt = 0; tt < 4; ++tt)
+#pragma unroll
+      for (int p = 0; p < 2; ++p) {
+        const int i = 4 * warp + tt + 32 * g, j = 2 * lane + 64 * p;
+        x[g][tt][p].x = j <= i ? S[i * kLd + j] : S[j * kLd + i];
+        x[g][tt][p].y = j + 1 <= i ? S[i * kLd + j + 1] : S[(j + 1) * kLd + i];
+      }
   LEAF_STAMP(1);
   bool bad = false;
-  const int nblk = np / kPB;
-  for (int kb = 0; kb < nblk; ++kb) {
-    const int k0 = kb * kPB;
-    if (warp == 0) {
-      // (1) 32x32 diagonal block: lane i owns row i in registers; column k is
-      //     broadcast by shuffle.
-      float row[kPB];
-#pragma unroll
-      for (int j = 0; j < kPB; ++j) row[j] = (j <= lane) ? A[(k0 + lane) * kLd + k0 + j] : 0.f;
-      if (kb == 0) LEAF_STAMP(20);
-      {
-        const float p0 = __shfl_sync(0xffffffffu, row[0], 0);
-        diag_chol_step<0>(row, lane, rdiag + k0, bad, p0, pivot_rsqrt(p0, bad));
-      }
-      if (kb == 0) LEAF_STAMP(21);
-#pragma unroll
-      for (int j = 0; j < kPB; ++j)
-        if (j <= lane) A[(k0 + lane) * kLd + k0 + j] = row[j];
-      __syncwarp();
-      if (kb == 0) LEAF_STAMP(22);
-      // Column `lane` of L_dd^-1 (forward substitution), into T's diagonal block.
-      float col[kPB];
-      diag_subst_step<0>(col, A + k0 * kLd + k0, kLd, rdiag + k0, lane);
-      if (kb == 0) LEAF_STAMP(23);
-#pragma unroll
-      for (int i = 0; i < kPB; ++i) T[(k0 + i) * kLd + k0 + lane] = col[i];
-      if (kb == 0) LEAF_STAMP(24);
-    }
-    __syncthreads();
-    LEAF_STAMP(2 + 3 * kb);
-    const int m = np - k0 - kPB;  // trailing size
-    if (m > 0) {
-      // (2) panel: L[i][k0+j] = sum_{p<=j} A[i][k0+p] Dinv[j][p] (Dinv = T's
-      //     diagonal block, lower) on 4x4 register tiles: thread (rg, cg) owns
-      //     rows k0+32+4rg.. and columns 4cg..; 8 shared loads per 16 FMA.
-      {
-        const int ntiles = (m / 4) * 8;
-        float acc[4][4] = {};
-        const int rg = tid >> 3, cg = tid & 7;
-        const int i0 = k0 + kPB + 4 * rg, j0 = 4 * cg;
-        if (tid < ntiles) {
-#pragma unroll 4
-          for (int p = 0; p < kPB; ++p) {
-            float a[4], d[4];
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              a[q] = A[(i0 + q) * kLd + k0 + p];
-              d[q] = (p <= j0 + q) ? T[(k0 + j0 + q) * kLd + k0 + p] : 0.f;
-            }
-#pragma unroll
-            for (int x = 0; x < 4; ++x)
-#pragma unroll
-              for (int y = 0; y < 4; ++y) acc[x][y] = fmaf(a[x], d[y], acc[x][y]);
-          }
-        }
-        __syncthreads();  // every read of the panel precedes its in-place overwrite
-        if (tid < ntiles)
-#pragma unroll
-          for (int x = 0; x < 4; ++x)
-#pragma unroll
-            for (int y = 0; y < 4; ++y) A[(i0 + x) * kLd + k0 + j0 + y] = acc[x][y];
-      }
-      __syncthreads();
-      LEAF_STAMP(3 + 3 * kb);
-      // (3) trailing SYRK on 4x4 register tiles of the lower triangle.
-      const int mt = m / 4;
-      const int ntiles = mt * (mt + 1) / 2;
-      for (int tt = tid; tt < ntiles; tt += kBaseThreads) {
-        int ti = int((sqrtf(8.f * tt + 1.f) - 1.f) * 0.5f);
-        while ((ti + 1) * (ti + 2) / 2 <= tt) ++ti;
-        while (ti * (ti + 1) / 2 > tt) --ti;
-        const int tj = tt - ti * (ti + 1) / 2;
-        const int i0 = k0 + kPB + 4 * ti, j0 = k0 + kPB + 4 * tj;
-        float acc[4][4] = {};
-#pragma unroll 8
-        for (int p = 0; p < kPB; ++p) {
-          float a[4], b[4];
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            a[q] = A[(i0 + q) * kLd + k0 + p];
-            b[q] = A[(j0 + q) * kLd + k0 + p];
-          }
-#pragma unroll
-          for (int x = 0; x < 4; ++x)
-#pragma unroll
-            for (int y = 0; y < 4; ++y) acc[x][y] = fmaf(a[x], b[y], acc[x][y]);
-        }
-#pragma unroll
-        for (int x = 0; x < 4; ++x)
-#pragma unroll
-          for (int y = 0; y < 4; ++y)
-            if (j0 + y <= i0 + x) A[(i0 + x) * kLd + j0 + y] -= acc[x][y];
-      }
-      __syncthreads();
-      LEAF_STAMP(4 + 3 * kb);
-    }
-  }
-  // (4) T = L^-1 off-diagonal 32x32 blocks, block row by block row, on 4x4
-  //     register tiles (thread = (jb, tr, tc), 64 tiles per block):
-  //     R[jb] = sum_{p in [32 jb, 32 ib)} L[ib][p] T[p][jb],  T[ib][jb] = -T[ib][ib] R[jb].
-  for (int ib = 1; ib < nblk; ++ib) {
-    const int jb = tid >> 6, tr = (tid >> 3) & 7, tc = tid & 7;
-    const bool act = jb < ib;
-    const int r0 = ib * kPB + 4 * tr, c0 = jb * kPB + 4 * tc;
-    float acc[4][4] = {};
-    if (act) {
-      for (int p = jb * kPB; p < ib * kPB; ++p) {
-        float l[4], tv[4];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          l[q] = A[(r0 + q) * kLd + p];
-          tv[q] = T[p * kLd + c0 + q];
-        }
-#pragma unroll
-        for (int x = 0; x < 4; ++x)
-#pragma unroll
-          for (int y = 0; y < 4; ++y) acc[x][y] = fmaf(l[x], tv[y], acc[x][y]);
-      }
-#pragma unroll
-      for (int x = 0; x < 4; ++x)
-#pragma unroll
-        for (int y = 0; y < 4; ++y) R[(jb * kPB + 4 * tr + x) * kPB + 4 * tc + y] = acc[x][y];
-    }
-    __syncthreads();
-    if (act) {
-#pragma unroll
-      for (int x = 0; x < 4; ++x)
-#pragma unroll
-        for (int y = 0; y < 4; ++y) acc[x][y] = 0.f;
-      const int qmax = 4 * tr + 4;  // T[ib][ib] is lower: row 4tr+x uses q <= 4tr+x
-      for (int q = 0; q < qmax; ++q) {
-        float d[4], rv[4];
-#pragma unroll
-        for (int x = 0; x < 4; ++x) d[x] = (q <= 4 * tr + x) ? T[(r0 + x) * kLd + ib * kPB + q] : 0.f;
-#pragma unroll
-        for (int y = 0; y < 4; ++y) rv[y] = R[(jb * kPB + q) * kPB + 4 * tc + y];
-#pragma unroll
-        for (int x = 0; x < 4; ++x)
-#pragma unroll
-          for (int y = 0; y < 4; ++y) acc[x][y] = fmaf(d[x], rv[y], acc[x][y]);
-      }
-#pragma unroll
-      for (int x = 0; x < 4; ++x)
-#pragma unroll
-        for (int y = 0; y < 4; ++y) T[(r0 + x) * kLd + c0 + y] = -acc[x][y];
-    }
-    __syncthreads();
-    LEAF_STAMP(14 + ib);
-  }
+  const int nb = (n + 3) / 4;  // padded rows/columns are identity: inert
+  if (warp == 0) leaf_publish<0>(x, 0, lane, buf.R, buf.L, bad);
+  __syncthreads();
+  leaf_blocks<0>(x, nb, warp, lane, buf, bad);
+  LEAF_STAMP(2);
   if (bad) set_status(status, SPNGD_ERR_NOT_POSITIVE_DEFINITE);
+  // T = lower triangle of X -> staging (zeros above the diagonal).
+#pragma unroll
+  for (int g = 0; g < 4; ++g)
+#pragma unroll
+    for (int tt = 0; tt < 4; ++tt)
+#pragma unroll
+      for (int p = 0; p < 2; ++p) {
+        const int i = 4 * warp + tt + 32 * g, j = 2 * lane + 64 * p;
+        S[i * kLd + j] = j <= i ? x[g][tt][p].x : 0.f;
+        S[i * kLd + j + 1] = j + 1 <= i ? x[g][tt][p].y : 0.f;
+      }
+  __syncthreads();
+  float* T = S;
   // Stores: tlow row i = T row i (zeros above the diagonal are T's own), tup
   // row i = T column i (read transposed from smem); float4 per lane where the
   // chunk lies inside the block.
@@ -321,8 +311,7 @@ __global__ void __launch_bounds__(kBaseThreads, 1) base_chol_inv_kernel(const Ba
       }
     }
   }
-  __syncthreads();
-  LEAF_STAMP(18);
+  LEAF_STAMP(3);
 }
 
 __global__ void pi_kernel(const PiTask* __restrict__ tasks) {
@@ -591,15 +580,14 @@ int launch_base(spngd_ctx* ctx, const BaseTask* d_tasks, int n) {
   SPNGD_CUDA_TRY(cudaGetLastError());
 #ifdef SPNGD_GEMM_TRACE_BUILD
   static int printed = 0;
-  if (getenv("SPNGD_GEMM_TRACE") && printed++ < 6) {
-    long long h[32];
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(ctx->stream, &cap);
+  if (getenv("SPNGD_GEMM_TRACE") && cap == cudaStreamCaptureStatusNone && printed++ < 6) {
+    long long h[8];
     cudaStreamSynchronize(ctx->stream);
     cudaMemcpyFromSymbol(h, g_leaf_trace, sizeof(h));
-    printf("leaf launch (%d leaves): load %lld", n, h[1] - h[0]);
-    for (int kb = 0; kb < 4; ++kb) printf(" | kb%d diag %lld panel %lld syrk %lld", kb, h[2 + 3 * kb] - h[0], h[3 + 3 * kb] - h[0], h[4 + 3 * kb] - h[0]);
-    printf(" | T rows %lld %lld %lld | store %lld\n", h[15] - h[0], h[16] - h[0], h[17] - h[0], h[18] - h[0]);
-    printf("   kb0 diag: rows-in %lld chol %lld store %lld subst %lld T-store %lld\n", h[20] - h[1], h[21] - h[20],
-           h[22] - h[21], h[23] - h[22], h[24] - h[23]);
+    printf("leaf launch (%d leaves): load %lld eliminate %lld store %lld cycles\n", n, h[1] - h[0], h[2] - h[1],
+           h[3] - h[2]);
   }
 #endif
   ctx->launches++;
