@@ -313,9 +313,19 @@ int spngd_opt_owner(const spngd_opt* opt, int layer);
  * dist.cpp:406-675, n = 1 micro-step): factors + BN moments, RS, damped
  * inverse, precondition + update + rescale, BN solve + update, AG. */
 int spngd_opt_step(spngd_opt* opt, int64_t step, double eta, double momentum);
+/* Single-GPU schedule (world == 1, no stale gating; on by default, env
+ * SPNGD_NO_OVERLAP=1 starts it off): layers are split into waves by their
+ * larger Kronecker dimension, largest first, and each wave's damped-inverse
+ * recursion runs on high-priority streams while the later waves' factor
+ * SYRKs run -- the reference's step order (dist.cpp:406-675) with its stage-3/4
+ * barrier relaxed to per-layer dependencies.  on = 0 restores the
+ * phase-serial schedule (identical numerics: same kernels, same inputs). */
+int spngd_opt_set_overlap(spngd_opt* opt, int on);
 /* Per-phase device milliseconds of the last step: factor GEMM, factor
  * reduction + BN moments, reduce_scatter, inverse, precondition + BN update,
- * all_gather. */
+ * all_gather.  Overlapped steps: the factor phase ends after the last wave's
+ * SYRK (earlier waves' recursions already running) and the inverse phase is
+ * what the recursion adds after it. */
 int spngd_opt_phase_ms(spngd_opt* opt, float* out6);
 /* Number of kernels the last step launched on this rank. */
 int64_t spngd_opt_launch_count(const spngd_opt* opt);

@@ -98,7 +98,7 @@ EXPORTS = [
     "spngd_tracker_should_refresh", "spngd_tracker_on_refresh", "spngd_tracker_state",
     "spngd_nccl_unique_id", "spngd_ctx_init_comm", "spngd_reduce_scatter_mean", "spngd_all_gather",
     "spngd_plan_layout", "spngd_opt_create", "spngd_opt_destroy", "spngd_opt_buffer", "spngd_opt_owner", "spngd_opt_step",
-    "spngd_opt_phase_ms", "spngd_opt_launch_count", "spngd_opt_stale_info",
+    "spngd_opt_phase_ms", "spngd_opt_launch_count", "spngd_opt_stale_info", "spngd_opt_set_overlap",
 ]
 
 
@@ -167,6 +167,7 @@ def _declare(L):
         "spngd_opt_owner": (C.c_int, [P, C.c_int]),
         "spngd_opt_step": (C.c_int, [P, _i64, C.c_double, C.c_double]),
         "spngd_opt_phase_ms": (C.c_int, [P, C.POINTER(C.c_float)]),
+        "spngd_opt_set_overlap": (C.c_int, [P, C.c_int]),
         "spngd_opt_launch_count": (_i64, [P]),
         "spngd_opt_stale_info": (C.c_int, [P, C.c_int, C.c_int, C.POINTER(_i64), C.POINTER(_i64), C.POINTER(_i64),
                                            C.POINTER(C.c_int)]),

@@ -21,6 +21,7 @@ struct spngd_ctx {
   ncclComm* comm = nullptr;
   int world = 1, rank = 0;
   int64_t launches = 0;         // kernels launched through this context
+  int launch_prio = 0;          // != 0: cudaLaunchAttributePriority of the recursion kernels
 };
 
 namespace spngd {

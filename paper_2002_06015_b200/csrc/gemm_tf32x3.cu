@@ -823,6 +823,8 @@ int plan_problem_pairs(int problem_index, const GemmProblem& p, int kchunk, std:
 
 size_t gemm_smem_bytes() { return size_t(kStages) * kStageBytes + sizeof(SmemCtl) + 1024; }
 
+thread_local int g_gemm_launch_prio = 0;
+
 uint32_t gemm_variant(const GemmProblem* probs, int n) {
   uint32_t v = 0;
   for (int i = 0; i < n; ++i) {
@@ -892,11 +894,13 @@ int launch_gemm(const GemmProblem* d_probs, const GemmWorkItem* d_items, int n_i
     cfg.blockDim = dim3(kGemmThreads);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = stream;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
+    attr[1].id = cudaLaunchAttributePriority;
+    attr[1].val.priority = g_gemm_launch_prio;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = g_gemm_launch_prio ? 2 : 1;
     cudaError_t le = cudaLaunchKernelEx(&cfg, kern, d_probs, d_items, d_partials, d_status, trace);
     if (le != cudaSuccess) return fail(SPNGD_ERR_CUDA, "gemm launch failed: %s", cudaGetErrorString(le));
   }

@@ -115,6 +115,9 @@ size_t gemm_smem_bytes();
 constexpr uint32_t kVariantAsync = 0x100u;
 uint32_t gemm_variant(const GemmProblem* probs, int n);
 
+// Priority attribute of the next launch_gemm launches on this thread (0: none).
+extern thread_local int g_gemm_launch_prio;
+
 // Launch one grouped GEMM over device-resident problem/work arrays.
 int launch_gemm(const GemmProblem* d_probs, const GemmWorkItem* d_items, int n_items, float* d_partials,
                 int* d_status, cudaStream_t stream, uint32_t variant = 0xFu | kVariantAsync);

@@ -570,11 +570,13 @@ int launch_base(spngd_ctx* ctx, const BaseTask* d_tasks, int n) {
     cfg.blockDim = dim3(kBaseThreads);
     cfg.dynamicSmemBytes = kBaseSmem;
     cfg.stream = ctx->stream;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
+    attr[1].id = cudaLaunchAttributePriority;
+    attr[1].val.priority = ctx->launch_prio;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = ctx->launch_prio ? 2 : 1;
     SPNGD_CUDA_TRY(cudaLaunchKernelEx(&cfg, base_chol_inv_kernel, d_tasks, ctx->d_status));
   }
   SPNGD_CUDA_TRY(cudaGetLastError());
@@ -597,16 +599,19 @@ int launch_base(spngd_ctx* ctx, const BaseTask* d_tasks, int n) {
 int run_inverse(spngd_ctx* ctx, const InversePlan& plan, const GemmProblem* d_probs, const GemmWorkItem* d_items,
                 const BaseTask* d_bases) {
   const uint32_t variant = gemm_variant(plan.probs.data(), int(plan.probs.size()));
+  g_gemm_launch_prio = ctx->launch_prio;
+  int rc = SPNGD_OK;
   for (const InverseRound& r : plan.rounds) {
-    int rc = launch_base(ctx, d_bases + r.base_off, r.base_cnt);
-    if (rc) return rc;
+    rc = launch_base(ctx, d_bases + r.base_off, r.base_cnt);
+    if (rc) break;
     if (r.item_cnt > 0) {
       rc = launch_gemm(d_probs, d_items + r.item_off, r.item_cnt, nullptr, ctx->d_status, ctx->stream, variant);
-      if (rc) return rc;
+      if (rc) break;
       ctx->launches++;
     }
   }
-  return SPNGD_OK;
+  g_gemm_launch_prio = 0;
+  return rc;
 }
 
 }  // namespace spngd

@@ -106,6 +106,7 @@ struct spngd_opt {
   std::vector<PiTask> pis; PiTask* d_pis = nullptr;
   std::vector<UnpackTask> unpacks; UnpackTask* d_unpacks = nullptr; int64_t max_n = 0;
   struct InvClass {  // one recursion schedule per matrix size class, on its own stream
+    int wave = 0;
     InversePlan plan;
     GemmProblem* d_probs = nullptr;
     GemmWorkItem* d_items = nullptr;
@@ -123,6 +124,29 @@ struct spngd_opt {
   };
   std::vector<InvClass> inv;
   cudaEvent_t inv_fork = nullptr;
+  // Single-GPU full steps: layers fall into waves by matrix size, largest
+  // first.  Wave w's factor SYRK, reduction, pi and unpack run on the main
+  // stream, then its inverse classes fork onto high-priority streams and
+  // recurse while the next wave's factor SYRK fills the remaining SMs.
+  struct Wave {
+    std::vector<GemmWorkItem> items;
+    GemmWorkItem* d_items = nullptr;
+    std::vector<SyrkReduceTask> reduce;
+    SyrkReduceTask* d_reduce = nullptr;
+    std::vector<PiTask> pis;
+    PiTask* d_pis = nullptr;
+    std::vector<UnpackTask> unpacks;
+    UnpackTask* d_unpacks = nullptr;
+    int64_t max_n = 0;
+    cudaEvent_t fork = nullptr;
+  };
+  std::vector<Wave> waves;
+  bool overlap_ok = false;   // world == 1 and no stale gating
+  bool overlap_on = false;
+  int inv_prio = 0;          // greatest stream priority
+  cudaGraph_t graphs_ov[6] = {};
+  cudaGraphExec_t graph_ov_exec[6] = {};
+  bool graphs_ready_ov = false;
   float* d_scal = nullptr;         // {eta, momentum} read by the update kernels
   cudaGraph_t graphs[6] = {};
   cudaGraphExec_t graph_exec[6] = {};
@@ -163,7 +187,11 @@ struct spngd_opt {
     for (int i = 0; i < 6; ++i) {
       if (graph_exec[i]) cudaGraphExecDestroy(graph_exec[i]);
       if (graphs[i]) cudaGraphDestroy(graphs[i]);
+      if (graph_ov_exec[i]) cudaGraphExecDestroy(graph_ov_exec[i]);
+      if (graphs_ov[i]) cudaGraphDestroy(graphs_ov[i]);
     }
+    for (auto& w : waves)
+      if (w.fork) cudaEventDestroy(w.fork);
     for (auto& c : inv) {
       if (c.done) cudaEventDestroy(c.done);
       if (c.stream) cudaStreamDestroy(c.stream);
@@ -185,6 +213,13 @@ double layer_cost(const spngd_layer_desc& d) {
   if (d.kind == SPNGD_BN) return double(d.g);
   const double a = double(d.a), g = double(d.g);
   return a * a * a + g * g * g + 2 * g * g * a + 2 * g * a * a;
+}
+
+// Overlap waves by the larger Kronecker dimension (inverse recursion depth).
+int wave_of(const spngd_layer_desc& d) {
+  if (d.kind == SPNGD_BN) return 2;
+  const int64_t m = std::max<int64_t>(d.a, d.g);
+  return m > 3072 ? 0 : (m > 1536 ? 1 : 2);
 }
 
 int build(spngd_opt* o, const spngd_layer_desc* descs, int n) {
@@ -324,17 +359,26 @@ int build(spngd_opt* o, const spngd_layer_desc* descs, int n) {
   // inverse plans: one per matrix size class (owned matrices of equal n share
   // identical recursion schedules and batch into the same launches); classes
   // run concurrently on their own streams.
+  o->overlap_ok = W == 1 && !o->cfg.stale;
+  o->overlap_on = o->overlap_ok && getenv("SPNGD_NO_OVERLAP") == nullptr;
   {
-    std::vector<int64_t> sizes;
-    for (const auto& m : mats) sizes.push_back(m.n);
-    std::sort(sizes.begin(), sizes.end());
-    sizes.erase(std::unique(sizes.begin(), sizes.end()), sizes.end());
-    std::reverse(sizes.begin(), sizes.end());  // largest (critical path) first
-    for (int64_t n : sizes) {
+    int least = 0, greatest = 0;
+    SPNGD_CUDA_TRY(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+    o->inv_prio = greatest;
+  }
+  {
+    // class key: (wave, size); waves only matter when overlapping
+    std::vector<std::pair<int, int64_t>> keys;
+    auto mwave = [&](size_t m) { return o->overlap_ok ? wave_of(o->layers[mat_layer[m]].d) : 0; };
+    for (size_t m = 0; m < mats.size(); ++m) keys.push_back({mwave(m), -mats[m].n});
+    std::sort(keys.begin(), keys.end());  // earliest wave, then largest (critical path) first
+    keys.erase(std::unique(keys.begin(), keys.end()), keys.end());
+    for (const auto& key : keys) {
       o->inv.emplace_back();
       spngd_opt::InvClass& c = o->inv.back();
+      c.wave = key.first;
       for (size_t m = 0; m < mats.size(); ++m)
-        if (mats[m].n == n) {
+        if (mwave(m) == key.first && mats[m].n == -key.second) {
           c.mats.push_back(mats[m]);
           c.mat_layer.push_back(mat_layer[m]);
         }
@@ -350,7 +394,8 @@ int build(spngd_opt* o, const spngd_layer_desc* descs, int n) {
         c.d_items_dyn = dev_upload(c.plan.items, own);
         c.d_bases_dyn = dev_upload(c.plan.bases, own);
       }
-      SPNGD_CUDA_TRY(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
+      SPNGD_CUDA_TRY(cudaStreamCreateWithPriority(&c.stream, cudaStreamNonBlocking,
+                                                  o->overlap_ok ? o->inv_prio : 0));
       SPNGD_CUDA_TRY(cudaEventCreateWithFlags(&c.done, cudaEventDisableTiming));
     }
     SPNGD_CUDA_TRY(cudaEventCreateWithFlags(&o->inv_fork, cudaEventDisableTiming));
@@ -371,25 +416,49 @@ int build(spngd_opt* o, const spngd_layer_desc* descs, int n) {
   o->d_rescale = dev_upload(o->pplan.rescale, own);
   o->d_bnu = dev_upload(o->bnu, own);
   for (auto& e : o->ev) SPNGD_CUDA_TRY(cudaEventCreate(&e));
+  // plan entry -> statistic maps (filtered launches: stale gating, overlap waves)
+  auto stat_of_ptr = [&](const float* p) {
+    for (size_t q = 0; q < o->stats.size(); ++q) {
+      const StatState& st = o->stats[q];
+      const float* b = o->rs_send + int64_t(st.owner) * o->seg_stat + st.off;
+      if (p >= b && p < b + st.count) return int(q);
+    }
+    return -1;
+  };
+  for (const auto& t : o->fplan.reduce) o->reduce_stat.push_back(stat_of_ptr(t.packed_out));
+  for (int q : o->reduce_stat)
+    if (q < 0) return fail(SPNGD_ERR_INVALID, "opt: unmapped reduction task");
+  if (o->overlap_ok) {
+    int nw = 0;
+    for (const auto& c : o->inv) nw = std::max(nw, c.wave + 1);
+    for (const auto& L : o->layers) nw = std::max(nw, wave_of(L.d) + 1);
+    o->waves.resize(size_t(nw));
+    for (const auto& it : o->fplan.items)
+      o->waves[wave_of(o->layers[o->stats[o->prob_stat[it.problem]].layer].d)].items.push_back(it);
+    for (size_t i = 0; i < o->fplan.reduce.size(); ++i)
+      o->waves[wave_of(o->layers[o->stats[o->reduce_stat[i]].layer].d)].reduce.push_back(o->fplan.reduce[i]);
+    for (size_t k = 0; k < o->pi_layer.size(); ++k) {
+      spngd_opt::Wave& wv = o->waves[wave_of(o->layers[o->pi_layer[k]].d)];
+      wv.pis.push_back(o->pis[k]);
+      wv.unpacks.push_back(o->unpacks[2 * k]);
+      wv.unpacks.push_back(o->unpacks[2 * k + 1]);
+      wv.max_n = std::max({wv.max_n, o->unpacks[2 * k].n, o->unpacks[2 * k + 1].n});
+    }
+    for (auto& wv : o->waves) {
+      wv.d_items = dev_upload(wv.items, own);
+      wv.d_reduce = dev_upload(wv.reduce, own);
+      wv.d_pis = dev_upload(wv.pis, own);
+      wv.d_unpacks = dev_upload(wv.unpacks, own);
+      SPNGD_CUDA_TRY(cudaEventCreateWithFlags(&wv.fork, cudaEventDisableTiming));
+    }
+  }
   if (o->cfg.stale) {
-    // plan entry -> statistic maps for the filtered (partial-refresh) launches
-    auto stat_of_ptr = [&](const float* p) {
-      for (size_t q = 0; q < o->stats.size(); ++q) {
-        const StatState& st = o->stats[q];
-        const float* b = o->rs_send + int64_t(st.owner) * o->seg_stat + st.off;
-        if (p >= b && p < b + st.count) return int(q);
-      }
-      return -1;
-    };
-    for (const auto& t : o->fplan.reduce) o->reduce_stat.push_back(stat_of_ptr(t.packed_out));
     for (const auto& t : o->fplan.repacks) {
       int q = -1;
       for (size_t f = 0; f < freqs.size(); ++f)
         if (freqs[f].x == t.src) q = o->prob_stat[f];
       o->repack_stat.push_back(q);
     }
-    for (int q : o->reduce_stat)
-      if (q < 0) return fail(SPNGD_ERR_INVALID, "opt: unmapped reduction task");
     o->d_fitems_dyn = dev_upload(o->fplan.items, own);
     o->d_freduce_dyn = dev_upload(o->fplan.reduce, own);
     o->d_repack_dyn = dev_upload(o->fplan.repacks, own);
@@ -578,6 +647,59 @@ int issue_phase(spngd_opt* o, int phase) {
       if (o->world > 1) rc = spngd_all_gather(ctx, o->ag + int64_t(o->rank) * o->seg_ag, o->ag, o->seg_ag);
       return rc;
   }
+  return SPNGD_OK;
+}
+
+// Phases 0-3 of a single-GPU full step with the inverse recursion of each
+// wave overlapping the factor SYRK of the later waves.  The phase events
+// 1-3 are recorded on the main stream after the last wave's SYRK and
+// reduction (external event nodes when captured), so the phase split stays
+// comparable: phase 3 is what the inverse adds beyond the factor work.
+int issue_overlap(spngd_opt* o, bool capturing) {
+  spngd_ctx* ctx = o->ctx;
+  cudaStream_t s = ctx->stream;
+  auto mark = [&](cudaEvent_t e) {
+    return capturing ? cudaEventRecordWithFlags(e, s, cudaEventRecordExternal) : cudaEventRecord(e, s);
+  };
+  int rc = launch_repack(ctx, o->d_repack, int(o->fplan.repacks.size()), o->fplan.repack_max);
+  if (rc) return rc;
+  const int nw = int(o->waves.size());
+  for (int w = 0; w < nw; ++w) {
+    spngd_opt::Wave& wv = o->waves[w];
+    const bool last = w == nw - 1;
+    if (!wv.items.empty()) {
+      rc = launch_factor_gemm(ctx, o->fplan, o->d_fprobs, o->d_fhalf, wv.d_items, int(wv.items.size()),
+                              o->d_partials, s);
+      if (rc) return rc;
+      ctx->launches++;
+    }
+    if (last) SPNGD_CUDA_TRY(mark(o->ev[1]));
+    rc = launch_syrk_reduce(wv.d_reduce, int(wv.reduce.size()), o->d_partials, s);
+    ctx->launches += !wv.reduce.empty();
+    if (rc) return rc;
+    if (last) {
+      rc = launch_bn_moments(ctx, o->d_bnm, int(o->bnm.size()), o->bnm_maxc);
+      if (rc) return rc;
+      SPNGD_CUDA_TRY(mark(o->ev[2]));
+      SPNGD_CUDA_TRY(mark(o->ev[3]));
+    }
+    rc = launch_pi(ctx, wv.d_pis, int(wv.pis.size()));
+    if (!rc) rc = launch_unpack(ctx, wv.d_unpacks, int(wv.unpacks.size()), wv.max_n);
+    if (rc) return rc;
+    SPNGD_CUDA_TRY(cudaEventRecord(wv.fork, s));
+    for (auto& c : o->inv) {
+      if (c.wave != w) continue;
+      SPNGD_CUDA_TRY(cudaStreamWaitEvent(c.stream, wv.fork, 0));
+      ctx->stream = c.stream;
+      ctx->launch_prio = o->inv_prio;
+      rc = run_inverse(ctx, c.plan, c.d_probs, c.d_items, c.d_bases);
+      ctx->launch_prio = 0;
+      ctx->stream = s;
+      if (rc) return rc;
+      SPNGD_CUDA_TRY(cudaEventRecord(c.done, c.stream));
+    }
+  }
+  for (auto& c : o->inv) SPNGD_CUDA_TRY(cudaStreamWaitEvent(s, c.done, 0));
   return SPNGD_OK;
 }
 
@@ -779,23 +901,30 @@ int spngd_opt_step(spngd_opt* o, int64_t step, double eta, double momentum) {
     full = n_due == int64_t(o->stats.size());
     any = n_due > 0;
   }
-  const bool capture = o->use_graph && !o->graphs_ready && full;
+  // Overlapped single-GPU schedule: phases 0-3 run as one unit (own graphs).
+  const bool ov = o->overlap_on && full;
+  bool& ready = ov ? o->graphs_ready_ov : o->graphs_ready;
+  const bool capture = o->use_graph && !ready && full;
   const int64_t l0 = ctx->launches;
   for (int ph = 0; ph < 6; ++ph) {
+    if (ov && ph >= 1 && ph <= 3) continue;  // inside issue_overlap
     SPNGD_CUDA_TRY(cudaEventRecord(o->ev[ph], s));
     const bool gated = ph <= 3 && !full;
+    auto issue = [&](bool capturing) { return (ov && ph == 0) ? issue_overlap(o, capturing) : issue_phase(o, ph); };
     if (gated) {
       if (any || ph == 2) {
         int rc = stale_partial_phase(o, ph);
         if (rc) return rc;
       }
-    } else if (!o->use_graph || (!o->graphs_ready && !capture)) {
-      int rc = issue_phase(o, ph);
+    } else if (!o->use_graph || (!ready && !capture)) {
+      int rc = issue(false);
       if (rc) return rc;
     } else {
+      cudaGraph_t* graphs = ov ? o->graphs_ov : o->graphs;
+      cudaGraphExec_t* execs = ov ? o->graph_ov_exec : o->graph_exec;
       if (capture) {
         SPNGD_CUDA_TRY(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
-        int rc = issue_phase(o, ph);
+        int rc = issue(true);
         cudaGraph_t g = nullptr;
         cudaError_t e = cudaStreamEndCapture(s, &g);
         if (rc) {
@@ -803,10 +932,10 @@ int spngd_opt_step(spngd_opt* o, int64_t step, double eta, double momentum) {
           return rc;
         }
         if (e != cudaSuccess) return fail_cuda(e, "cudaStreamEndCapture");
-        o->graphs[ph] = g;
-        SPNGD_CUDA_TRY(cudaGraphInstantiate(&o->graph_exec[ph], g, 0));
+        graphs[ph] = g;
+        SPNGD_CUDA_TRY(cudaGraphInstantiateWithFlags(&execs[ph], g, cudaGraphInstantiateFlagUseNodePriority));
       }
-      SPNGD_CUDA_TRY(cudaGraphLaunch(o->graph_exec[ph], s));
+      SPNGD_CUDA_TRY(cudaGraphLaunch(execs[ph], s));
     }
     if (ph == 3 && o->cfg.stale && any) {
       int rc = stale_similarity(o, step);
@@ -815,7 +944,7 @@ int spngd_opt_step(spngd_opt* o, int64_t step, double eta, double momentum) {
   }
   SPNGD_CUDA_TRY(cudaEventRecord(o->ev[6], s));
   if (capture || !o->use_graph || !full) o->launches = ctx->launches - l0;
-  if (capture) o->graphs_ready = true;
+  if (capture) ready = true;
   o->timed = true;
   return SPNGD_OK;
 }
@@ -834,6 +963,14 @@ int spngd_opt_stale_info(spngd_opt* o, int layer, int which, int64_t* t_x, int64
     return SPNGD_OK;
   }
   return fail(SPNGD_ERR_SHAPE_MISMATCH, "spngd_opt_stale_info: layer %d has no statistic %d", layer, which);
+}
+
+int spngd_opt_set_overlap(spngd_opt* o, int on) {
+  if (!o) return fail(SPNGD_ERR_INVALID, "spngd_opt_set_overlap: opt is NULL");
+  if (on && !o->overlap_ok)
+    return fail(SPNGD_ERR_INVALID, "spngd_opt_set_overlap: overlap needs world == 1 and stale gating off");
+  o->overlap_on = on != 0;
+  return SPNGD_OK;
 }
 
 int spngd_opt_phase_ms(spngd_opt* o, float* out6) {

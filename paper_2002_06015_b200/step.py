@@ -197,6 +197,12 @@ class Optimizer:
     def launch_count(self) -> int:
         return N.lib().spngd_opt_launch_count(self.h)
 
+    def set_overlap(self, on: bool):
+        """Single-GPU wave schedule (inverse recursion of the largest factors
+        overlapping the remaining factor SYRKs); off = phase-serial.  Same
+        kernels and inputs either way (spngd_opt_set_overlap)."""
+        check(N.lib().spngd_opt_set_overlap(self.h, int(on)))
+
     def stale_info(self, layer: int, which: str):
         """Tracker state of statistic which in {"A", "G", "F"} of `layer`
         (StaleTracker t_X / delta / refresh count) and whether it refreshed

@@ -91,3 +91,23 @@ def test_resnet50_sampled_layers(cuda_dev):
     idx = {(l.a, l.g, l.hw): i for i, l in reversed(list(enumerate(layers)))}
     pick = [0, 1, idx[(576, 64, 3136)], idx[(1152, 128, 784)], len(layers) - 1]
     run_and_check(layers, 32, pick)
+
+
+def test_overlapped_schedule_is_bitwise_phase_serial(cuda_dev):
+    """The single-GPU wave schedule (inverse recursion of the largest factors
+    overlapping the remaining factor SYRKs) runs the same kernels on the same
+    inputs as the phase-serial schedule: results must be bit-identical."""
+    layers = W.resnet50()
+    outs = []
+    for overlap in (True, False):
+        opt = Optimizer(layers, 8, lam=LAM)
+        opt.set_overlap(overlap)
+        opt.synth(seed=5)
+        for s in range(2):
+            opt.step(s + 1, ETA, MOM)
+        opt.sync()
+        outs.append([(opt.download(li, WB).numpy().copy(), opt.download(li, V).numpy().copy())
+                     for li in range(len(layers))])
+        opt.close()
+    for li, ((w0, v0), (w1, v1)) in enumerate(zip(*outs)):
+        assert np.array_equal(w0, w1) and np.array_equal(v0, v1), f"layer {li} {layers[li]}"
