@@ -250,7 +250,7 @@ def run_ours(args):
     # the roofline (in the overlapped schedule it shares the GPU with the
     # inverse recursion, so its event span is not one kernel's duration).
     serial = None
-    if world == 1:
+    if True:
         opt.set_overlap(False)
         t0 = args.warmup + args.steps + args.e2e_steps + 1
         for s in range(3):
@@ -304,8 +304,8 @@ def run_ours(args):
                        "lambda": args.lam, "eta": 1.25e-2, "momentum": 0.993, "rescale": True,
                        "l2": f"inputs > L2: {W.capture_bytes(layers, batch) / 1e9:.2f} GB of captures per step"},
             "phases_ms_last_step": {k: round(v, 3) for k, v in phases.items()},
-            "schedule": ("overlapped: inverse recursion of the largest factors runs on high-priority streams "
-                         "while the remaining factor SYRKs run" if world == 1 else "phase-serial"),
+            "schedule": "waves: inverse recursion of the largest factors runs on high-priority streams while the "
+                        "remaining factor SYRKs run" + ("; per-wave owner reductions on a comm stream" if world > 1 else ""),
             "phase_serial": serial,
             "e2e": ({"value": round(e2e, 3), "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": out_bytes}
                     if e2e_ms else None),

@@ -313,13 +313,18 @@ int spngd_opt_owner(const spngd_opt* opt, int layer);
  * dist.cpp:406-675, n = 1 micro-step): factors + BN moments, RS, damped
  * inverse, precondition + update + rescale, BN solve + update, AG. */
 int spngd_opt_step(spngd_opt* opt, int64_t step, double eta, double momentum);
-/* Single-GPU schedule (world == 1, no stale gating; on by default, env
- * SPNGD_NO_OVERLAP=1 starts it off): layers are split into waves by their
- * larger Kronecker dimension, largest first, and each wave's damped-inverse
- * recursion runs on high-priority streams while the later waves' factor
- * SYRKs run -- the reference's step order (dist.cpp:406-675) with its stage-3/4
- * barrier relaxed to per-layer dependencies.  on = 0 restores the
- * phase-serial schedule (identical numerics: same kernels, same inputs). */
+/* Wave schedule (no stale gating; on by default, env SPNGD_NO_OVERLAP=1
+ * starts it off): layers are split into waves by their larger Kronecker
+ * dimension, largest first, and each wave's damped-inverse recursion runs on
+ * high-priority streams while the later waves' factor SYRKs run -- the
+ * reference's step order (dist.cpp:406-675) with its stage-3/4 barrier relaxed
+ * to per-layer dependencies.  world > 1: each wave's statistics go to their
+ * owners (grouped ncclReduce(avg)) on a communication stream as soon as the
+ * wave is reduced locally; gradients reduce-scatter there at the start.
+ * on = 0 restores the phase-serial schedule.  Same kernels on the same
+ * inputs (bit-identical at world == 1); at world > 1 the statistics are
+ * averaged by per-wave ncclReduce instead of one ncclReduceScatter, so only
+ * NCCL's summation order can differ.  Must match on every rank. */
 int spngd_opt_set_overlap(spngd_opt* opt, int on);
 /* Per-phase device milliseconds of the last step: factor GEMM, factor
  * reduction + BN moments, reduce_scatter, inverse, precondition + BN update,

@@ -138,10 +138,14 @@ struct spngd_opt {
     std::vector<UnpackTask> unpacks;
     UnpackTask* d_unpacks = nullptr;
     int64_t max_n = 0;
-    cudaEvent_t fork = nullptr;
+    std::vector<OwnerReduce> owner_ops;  // world > 1: this wave's statistics -> their owners
+    cudaEvent_t ready = nullptr;         // factors of this wave reduced locally
+    cudaEvent_t fork = nullptr;          // owner-side inputs of this wave's recursion ready
   };
   std::vector<Wave> waves;
-  bool overlap_ok = false;   // world == 1 and no stale gating
+  cudaStream_t comm_stream = nullptr;    // world > 1: NCCL + owner-side prep of the waves
+  cudaEvent_t comm_fork = nullptr, comm_done = nullptr;
+  bool overlap_ok = false;   // no stale gating
   bool overlap_on = false;
   int inv_prio = 0;          // greatest stream priority
   cudaGraph_t graphs_ov[6] = {};
@@ -190,8 +194,13 @@ struct spngd_opt {
       if (graph_ov_exec[i]) cudaGraphExecDestroy(graph_ov_exec[i]);
       if (graphs_ov[i]) cudaGraphDestroy(graphs_ov[i]);
     }
-    for (auto& w : waves)
+    for (auto& w : waves) {
       if (w.fork) cudaEventDestroy(w.fork);
+      if (w.ready) cudaEventDestroy(w.ready);
+    }
+    if (comm_fork) cudaEventDestroy(comm_fork);
+    if (comm_done) cudaEventDestroy(comm_done);
+    if (comm_stream) cudaStreamDestroy(comm_stream);
     for (auto& c : inv) {
       if (c.done) cudaEventDestroy(c.done);
       if (c.stream) cudaStreamDestroy(c.stream);
@@ -359,7 +368,7 @@ int build(spngd_opt* o, const spngd_layer_desc* descs, int n) {
   // inverse plans: one per matrix size class (owned matrices of equal n share
   // identical recursion schedules and batch into the same launches); classes
   // run concurrently on their own streams.
-  o->overlap_ok = W == 1 && !o->cfg.stale;
+  o->overlap_ok = !o->cfg.stale;
   o->overlap_on = o->overlap_ok && getenv("SPNGD_NO_OVERLAP") == nullptr;
   {
     int least = 0, greatest = 0;
@@ -444,7 +453,18 @@ int build(spngd_opt* o, const spngd_layer_desc* descs, int n) {
       wv.unpacks.push_back(o->unpacks[2 * k + 1]);
       wv.max_n = std::max({wv.max_n, o->unpacks[2 * k].n, o->unpacks[2 * k + 1].n});
     }
+    for (const StatState& st : o->stats) {
+      spngd_opt::Wave& wv = o->waves[wave_of(o->layers[st.layer].d)];
+      wv.owner_ops.push_back({o->rs_send + int64_t(st.owner) * o->seg_stat + st.off, o->rs_recv + st.off, st.count,
+                              st.owner});
+    }
+    if (W > 1) {
+      SPNGD_CUDA_TRY(cudaStreamCreateWithPriority(&o->comm_stream, cudaStreamNonBlocking, o->inv_prio));
+      SPNGD_CUDA_TRY(cudaEventCreateWithFlags(&o->comm_fork, cudaEventDisableTiming));
+      SPNGD_CUDA_TRY(cudaEventCreateWithFlags(&o->comm_done, cudaEventDisableTiming));
+    }
     for (auto& wv : o->waves) {
+      SPNGD_CUDA_TRY(cudaEventCreateWithFlags(&wv.ready, cudaEventDisableTiming));
       wv.d_items = dev_upload(wv.items, own);
       wv.d_reduce = dev_upload(wv.reduce, own);
       wv.d_pis = dev_upload(wv.pis, own);
@@ -650,18 +670,35 @@ int issue_phase(spngd_opt* o, int phase) {
   return SPNGD_OK;
 }
 
-// Phases 0-3 of a single-GPU full step with the inverse recursion of each
-// wave overlapping the factor SYRK of the later waves.  The phase events
-// 1-3 are recorded on the main stream after the last wave's SYRK and
-// reduction (external event nodes when captured), so the phase split stays
-// comparable: phase 3 is what the inverse adds beyond the factor work.
+// Phases 0-3 of a full step with the inverse recursion of each wave
+// overlapping the factor SYRK of the later waves.  world > 1: a communication
+// stream reduces each wave's statistics to their owners as soon as the wave's
+// factors are reduced locally (grouped ncclReduce(avg), the reference's
+// ReduceScatterV of stage 3 split by wave, dist.cpp:510-537), runs the
+// owner's pi + unpack, and forks the owner's recursion; the gradient
+// reduce-scatter runs on it at the start.  The phase events 1-3 are recorded
+// on the main stream after the last wave's SYRK, after its reduction + BN
+// moments, and after the communication stream joins (external event nodes
+// when captured), so phase 3 is what the inverse adds beyond the rest.
 int issue_overlap(spngd_opt* o, bool capturing) {
   spngd_ctx* ctx = o->ctx;
   cudaStream_t s = ctx->stream;
+  const bool dist = o->world > 1;
+  cudaStream_t prep = dist ? o->comm_stream : s;
   auto mark = [&](cudaEvent_t e) {
     return capturing ? cudaEventRecordWithFlags(e, s, cudaEventRecordExternal) : cudaEventRecord(e, s);
   };
-  int rc = launch_repack(ctx, o->d_repack, int(o->fplan.repacks.size()), o->fplan.repack_max);
+  int rc = SPNGD_OK;
+  if (dist) {  // gradients: independent of the factors
+    SPNGD_CUDA_TRY(cudaEventRecord(o->comm_fork, s));
+    SPNGD_CUDA_TRY(cudaStreamWaitEvent(prep, o->comm_fork, 0));
+    ctx->stream = prep;
+    rc = spngd_reduce_scatter_mean(ctx, o->rs_send + int64_t(o->world) * o->seg_stat, o->rs_recv + o->seg_stat,
+                                   o->seg_grad);
+    ctx->stream = s;
+    if (rc) return rc;
+  }
+  rc = launch_repack(ctx, o->d_repack, int(o->fplan.repacks.size()), o->fplan.repack_max);
   if (rc) return rc;
   const int nw = int(o->waves.size());
   for (int w = 0; w < nw; ++w) {
@@ -681,12 +718,18 @@ int issue_overlap(spngd_opt* o, bool capturing) {
       rc = launch_bn_moments(ctx, o->d_bnm, int(o->bnm.size()), o->bnm_maxc);
       if (rc) return rc;
       SPNGD_CUDA_TRY(mark(o->ev[2]));
-      SPNGD_CUDA_TRY(mark(o->ev[3]));
     }
-    rc = launch_pi(ctx, wv.d_pis, int(wv.pis.size()));
+    if (dist) {
+      SPNGD_CUDA_TRY(cudaEventRecord(wv.ready, s));
+      SPNGD_CUDA_TRY(cudaStreamWaitEvent(prep, wv.ready, 0));
+    }
+    ctx->stream = prep;
+    if (dist) rc = comm_reduce_to_owners(ctx, wv.owner_ops);
+    if (!rc) rc = launch_pi(ctx, wv.d_pis, int(wv.pis.size()));
     if (!rc) rc = launch_unpack(ctx, wv.d_unpacks, int(wv.unpacks.size()), wv.max_n);
+    ctx->stream = s;
     if (rc) return rc;
-    SPNGD_CUDA_TRY(cudaEventRecord(wv.fork, s));
+    SPNGD_CUDA_TRY(cudaEventRecord(wv.fork, prep));
     for (auto& c : o->inv) {
       if (c.wave != w) continue;
       SPNGD_CUDA_TRY(cudaStreamWaitEvent(c.stream, wv.fork, 0));
@@ -699,6 +742,11 @@ int issue_overlap(spngd_opt* o, bool capturing) {
       SPNGD_CUDA_TRY(cudaEventRecord(c.done, c.stream));
     }
   }
+  if (dist) {
+    SPNGD_CUDA_TRY(cudaEventRecord(o->comm_done, prep));
+    SPNGD_CUDA_TRY(cudaStreamWaitEvent(s, o->comm_done, 0));
+  }
+  SPNGD_CUDA_TRY(mark(o->ev[3]));
   for (auto& c : o->inv) SPNGD_CUDA_TRY(cudaStreamWaitEvent(s, c.done, 0));
   return SPNGD_OK;
 }
@@ -968,7 +1016,7 @@ int spngd_opt_stale_info(spngd_opt* o, int layer, int which, int64_t* t_x, int64
 int spngd_opt_set_overlap(spngd_opt* o, int on) {
   if (!o) return fail(SPNGD_ERR_INVALID, "spngd_opt_set_overlap: opt is NULL");
   if (on && !o->overlap_ok)
-    return fail(SPNGD_ERR_INVALID, "spngd_opt_set_overlap: overlap needs world == 1 and stale gating off");
+    return fail(SPNGD_ERR_INVALID, "spngd_opt_set_overlap: the wave schedule needs stale gating off");
   o->overlap_on = on != 0;
   return SPNGD_OK;
 }

@@ -18,7 +18,8 @@ from paper_2002_06015_b200.step import ACT, BN_GB, BN_GG, DW, GRAD, V, Comm, Opt
 from paper_2002_06015_b200.step import W as WB  # noqa: E402
 
 LAYERS = [W.conv(16, 32, 3, 1, 16), W.bn(32), W.conv(32, 64, 3, 2, 16), W.bn(64), W.conv(64, 128, 3, 1, 8),
-          W.bn(128), W.conv(128, 256, 3, 2, 8), W.bn(256), W.fc(1024, 10)]
+          W.bn(128), W.conv(128, 256, 3, 2, 8), W.bn(256), W.fc(1024, 10),
+          W.conv(256, 256, 3, 1, 4), W.conv(512, 512, 3, 1, 4)]  # inverse waves 1 and 0
 B = 8
 
 
