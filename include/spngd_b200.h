@@ -306,7 +306,9 @@ void spngd_opt_destroy(spngd_opt* opt);
  *   6 bn gb, 7 A_inv dense, 8 G_inv dense, 9 A packed (reduced), 10 G packed,
  *   11 BN moments 3c (reduced), 12 the whole weight all-gather buffer
  *   (ld = its float count). NULL if the layer has no such buffer or this
- *   rank does not own it. */
+ *   rank does not own it.  The step keeps only the triangular factors
+ *   T = chol(X + dI)^-1 (it preconditions with T^T T directly), so 7 / 8
+ *   form (X + dI)^-1 = T^T T on the call (one GEMM, synchronous). */
 float* spngd_opt_buffer(spngd_opt* opt, int layer, int which, int64_t* ld);
 int spngd_opt_owner(const spngd_opt* opt, int layer);
 /* One SP-NGD step over the resident inputs (accumulate_microsteps,

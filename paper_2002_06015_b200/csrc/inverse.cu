@@ -482,23 +482,26 @@ void gen_chol(const DenseMatrix& m, int64_t off, int64_t n, Gen& g, std::vector<
                         FLAG_TRANS, KTRI_A_LOWER, -1.f, 0.f, at(m.tlow, ld, o2, off), ld, at(m.tup, ld, off, o2), ld));
 }
 
-void gen_ops(const DenseMatrix& m, Gen& g, std::vector<Op>& ops) {
-  gen_chol(m, 0, m.n, g, ops);
+Op lauum_op(const DenseMatrix& m) {
   // X = T^T T = Tup Tup^T; row i of Tup is zero for k < i.
-  ops.push_back(gemm_op(dense_op(m.tup, m.ld, m.n, m.n), dense_op(m.tup, m.ld, m.n, m.n), m.n, m.n, m.n,
-                        FLAG_SAME_AB | FLAG_SYM_MIRROR, KTRI_A_UPPER | KTRI_B_UPPER, 1.f, 0.f, m.ptr, m.ld, nullptr, 0,
-                        true));
+  return gemm_op(dense_op(m.tup, m.ld, m.n, m.n), dense_op(m.tup, m.ld, m.n, m.n), m.n, m.n, m.n,
+                 FLAG_SAME_AB | FLAG_SYM_MIRROR, KTRI_A_UPPER | KTRI_B_UPPER, 1.f, 0.f, m.ptr, m.ld, nullptr, 0, true);
+}
+
+void gen_ops(const DenseMatrix& m, Gen& g, std::vector<Op>& ops, bool form_inverse) {
+  gen_chol(m, 0, m.n, g, ops);
+  if (form_inverse) ops.push_back(lauum_op(m));
 }
 
 }  // namespace
 
-void plan_inverse(const std::vector<DenseMatrix>& mats, float* workspace, InversePlan& plan) {
+void plan_inverse(const std::vector<DenseMatrix>& mats, float* workspace, InversePlan& plan, bool form_inverse) {
   plan = InversePlan();
   Gen g{workspace};
   std::vector<std::vector<Op>> per(mats.size());
   size_t max_ops = 0;
   for (size_t m = 0; m < mats.size(); ++m) {
-    gen_ops(mats[m], g, per[m]);
+    gen_ops(mats[m], g, per[m], form_inverse);
     max_ops = std::max(max_ops, per[m].size());
   }
   plan.workspace_floats = g.used;
@@ -594,6 +597,23 @@ int launch_base(spngd_ctx* ctx, const BaseTask* d_tasks, int n) {
 #endif
   ctx->launches++;
   return SPNGD_OK;
+}
+
+int materialize_inverse(spngd_ctx* ctx, const DenseMatrix& m) {
+  const Op op = lauum_op(m);
+  std::vector<GemmWorkItem> items;
+  int slot = 0;
+  plan_problem_tiles(0, op.prob, op.upper, op.prob.K + kTileK, items, nullptr, &slot, 1.0, nullptr);
+  DeviceScratch scratch(ctx);
+  std::vector<GemmProblem> probs{op.prob};
+  auto* d_probs = scratch.upload(probs);
+  auto* d_items = scratch.upload(items);
+  if (!d_probs || !d_items) return fail(SPNGD_ERR_CUDA, "materialize_inverse: scratch upload failed");
+  int rc = launch_gemm(d_probs, d_items, int(items.size()), nullptr, ctx->d_status, ctx->stream,
+                       gemm_variant(probs.data(), 1));
+  if (rc) return rc;
+  ctx->launches++;
+  return spngd_ctx_sync(ctx);
 }
 
 int run_inverse(spngd_ctx* ctx, const InversePlan& plan, const GemmProblem* d_probs, const GemmWorkItem* d_items,

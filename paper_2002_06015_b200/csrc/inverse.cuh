@@ -67,7 +67,11 @@ struct DenseMatrix {
 
 // Builds the plan; temporaries are carved from `workspace` (may be null for a
 // sizing pass, in which case only workspace_floats is meaningful).
-void plan_inverse(const std::vector<DenseMatrix>& mats, float* workspace, InversePlan& plan);
+// form_inverse = false stops after the factors: tlow = L^-1 and tup = L^-T
+// (the optimizer preconditions with them directly); ptr is scratch then.
+void plan_inverse(const std::vector<DenseMatrix>& mats, float* workspace, InversePlan& plan, bool form_inverse = true);
+// X = Tup Tup^T -> m.ptr (the lauum step alone), synchronous.
+int materialize_inverse(spngd_ctx* ctx, const DenseMatrix& m);
 
 int launch_pi(spngd_ctx* ctx, const PiTask* d_tasks, int n);
 int launch_unpack(spngd_ctx* ctx, const UnpackTask* d_tasks, int n, int64_t max_n);

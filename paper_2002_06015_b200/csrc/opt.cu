@@ -65,8 +65,9 @@ struct LayerState {
   int64_t off_W = -1;
   // owner-local
   float* V = nullptr;
-  float* Ainv = nullptr; int64_t lda = 0;
+  float* Ainv = nullptr; int64_t lda = 0;   // recursion scratch; the inverse on request
   float* Ginv = nullptr; int64_t ldg = 0;
+  float *tla = nullptr, *tua = nullptr, *tlg = nullptr, *tug = nullptr;  // T = L^-1 and T^T per factor
 };
 
 // One stale-gated statistic (A:l, G:l or F:l).
@@ -157,7 +158,8 @@ struct spngd_opt {
   bool use_graph = true;
   bool graphs_ready = false;
   PrecondPlan pplan;
-  GemmProblem *d_p1 = nullptr, *d_p2 = nullptr; GemmWorkItem *d_i1 = nullptr, *d_i2 = nullptr;
+  GemmProblem* d_pp[4] = {};
+  GemmWorkItem* d_pi[4] = {};
   RescaleTask* d_rescale = nullptr; double* d_norms = nullptr;
   std::vector<spngd_bn_update_req> bnu; spngd_bn_update_req* d_bnu = nullptr; int64_t bnu_maxc = 0;
   float* d_damps = nullptr;
@@ -225,8 +227,9 @@ double layer_cost(const spngd_layer_desc& d) {
 }
 
 // Overlap waves by the larger Kronecker dimension (inverse recursion depth).
+constexpr int kWaves = 3;
 int wave_of(const spngd_layer_desc& d) {
-  if (d.kind == SPNGD_BN) return 2;
+  if (d.kind == SPNGD_BN) return kWaves - 1;
   const int64_t m = std::max<int64_t>(d.a, d.g);
   return m > 3072 ? 0 : (m > 1536 ? 1 : 2);
 }
@@ -257,6 +260,7 @@ int build(spngd_opt* o, const spngd_layer_desc* descs, int n) {
   std::vector<DenseMatrix> mats;
   std::vector<int> mat_layer;
   std::vector<spngd_precond_req> preqs;
+  std::vector<PrecondTri> ptri;
   int n_owned_kron = 0;
   for (int li = 0; li < n; ++li) {
     LayerState& L = o->layers[li];
@@ -337,6 +341,8 @@ int build(spngd_opt* o, const spngd_layer_desc* descs, int n) {
     mat_layer.push_back(li);
     mats.push_back({L.Ginv, tlg, tug, L.ldg, g});
     mat_layer.push_back(li);
+    L.tla = tla; L.tua = tua; L.tlg = tlg; L.tug = tug;
+    ptri.push_back({tla, tua, tlg, tug});
     spngd_precond_req pr{};
     pr.Ginv = L.Ginv; pr.ldg = L.ldg;
     pr.Ainv = L.Ainv; pr.lda = L.lda;
@@ -392,9 +398,9 @@ int build(spngd_opt* o, const spngd_layer_desc* descs, int n) {
           c.mat_layer.push_back(mat_layer[m]);
         }
       InversePlan sizing;
-      plan_inverse(c.mats, nullptr, sizing);
+      plan_inverse(c.mats, nullptr, sizing, false);
       c.ws = o->alloc(sizing.workspace_floats);
-      plan_inverse(c.mats, c.ws, c.plan);
+      plan_inverse(c.mats, c.ws, c.plan, false);
       c.d_probs = dev_upload(c.plan.probs, own);
       c.d_items = dev_upload(c.plan.items, own);
       c.d_bases = dev_upload(c.plan.bases, own);
@@ -413,15 +419,16 @@ int build(spngd_opt* o, const spngd_layer_desc* descs, int n) {
   o->use_graph = getenv("SPNGD_NO_GRAPH") == nullptr;
   // precondition plan
   PrecondPlan psz;
-  rc = plan_precondition(preqs.data(), int(preqs.size()), 0.0, 0.0, nullptr, nullptr, psz);
+  rc = plan_precondition(preqs.data(), int(preqs.size()), 0.0, 0.0, nullptr, nullptr, psz, nullptr, ptri.data());
   if (rc) return rc;
   float* ptmp = o->alloc(psz.tmp_floats);
-  rc = plan_precondition(preqs.data(), int(preqs.size()), 0.0, 0.0, ptmp, o->d_norms, o->pplan, o->d_scal);
+  rc = plan_precondition(preqs.data(), int(preqs.size()), 0.0, 0.0, ptmp, o->d_norms, o->pplan, o->d_scal,
+                         ptri.data());
   if (rc) return rc;
-  o->d_p1 = dev_upload(o->pplan.probs1, own);
-  o->d_i1 = dev_upload(o->pplan.items1, own);
-  o->d_p2 = dev_upload(o->pplan.probs2, own);
-  o->d_i2 = dev_upload(o->pplan.items2, own);
+  for (int q = 0; q < o->pplan.stages; ++q) {
+    o->d_pp[q] = dev_upload(o->pplan.probs[q], own);
+    o->d_pi[q] = dev_upload(o->pplan.items[q], own);
+  }
   o->d_rescale = dev_upload(o->pplan.rescale, own);
   o->d_bnu = dev_upload(o->bnu, own);
   for (auto& e : o->ev) SPNGD_CUDA_TRY(cudaEventCreate(&e));
@@ -600,8 +607,15 @@ float* spngd_opt_buffer(spngd_opt* o, int layer, int which, int64_t* ld) {
     case 4: return mine ? L.V : nullptr;
     case 5: return L.gg;
     case 6: return L.gb;
-    case 7: if (ld) *ld = L.lda; return mine ? L.Ainv : nullptr;
-    case 8: if (ld) *ld = L.ldg; return mine ? L.Ginv : nullptr;
+    case 7:  // the step keeps only T = L^-1: the inverse T^T T is formed on request
+    case 8: {
+      const bool a = which == 7;
+      if (ld) *ld = a ? L.lda : L.ldg;
+      float* X = a ? L.Ainv : L.Ginv;
+      if (!mine || !X) return nullptr;
+      const DenseMatrix m{X, a ? L.tla : L.tlg, a ? L.tua : L.tug, a ? L.lda : L.ldg, a ? L.d.a : L.d.g};
+      return materialize_inverse(o->ctx, m) == SPNGD_OK ? X : nullptr;
+    }
     case 9: return (mine && L.off_A >= 0) ? o->rs_recv + L.off_A : nullptr;
     case 10: return (mine && L.off_G >= 0) ? o->rs_recv + L.off_G : nullptr;
     case 11: return (mine && L.off_M >= 0) ? o->rs_recv + L.off_M : nullptr;
@@ -659,7 +673,7 @@ int issue_phase(spngd_opt* o, int phase) {
       return SPNGD_OK;
     }
     case 4:  // Stage 4b: precondition + update + rescale, BN solve + update (dist.cpp:604-633).
-      rc = run_precondition(ctx, o->pplan, o->d_p1, o->d_i1, o->d_p2, o->d_i2, o->d_rescale, o->d_norms);
+      rc = run_precondition(ctx, o->pplan, o->d_pp, o->d_pi, o->d_rescale, o->d_norms);
       if (!rc)
         rc = launch_bn_update(ctx, o->d_bnu, int(o->bnu.size()), o->bnu_maxc, o->cfg.lambda, 0.0, 0.0, o->d_scal);
       return rc;
@@ -857,7 +871,7 @@ int stale_partial_phase(spngd_opt* o, int phase) {
         for (size_t m = 0; m < c.mats.size(); ++m)
           if (touched[c.mat_layer[m]]) sub.push_back(c.mats[m]);
         if (sub.empty()) continue;
-        plan_inverse(sub, c.ws, c.dyn);
+        plan_inverse(sub, c.ws, c.dyn, false);
         if ((rc = upload_async(ctx, c.d_probs_dyn, c.dyn.probs))) return rc;
         if ((rc = upload_async(ctx, c.d_items_dyn, c.dyn.items))) return rc;
         if ((rc = upload_async(ctx, c.d_bases_dyn, c.dyn.bases))) return rc;

@@ -4,11 +4,13 @@
 // K7: unit-wise BatchNorm 2x2 solve + update (src/fisher.cpp:259-276, 336-357).
 // K8: stale-statistics similarity norms (include/spngd/stale.hpp:23-64).
 //
-// P = G^-1 dW A^-1 runs as two back-to-back grouped 3xTF32 GEMMs over all
-// layers, both with K-major operands thanks to the symmetry of the inverses:
+// P = G^-1 dW A^-1 runs as back-to-back grouped 3xTF32 GEMMs over all
+// layers, with K-major operands thanks to the symmetry of the inverses:
 //   GEMM1  P1^T[j,i] = sum_k A^-1[j,k] dW[i,k]      (M=a, N=g, K=a)
 //   GEMM2  P^T [j,i] = sum_k P1^T[j,k] G^-1[i,k]    (M=a, N=g, K=g)
-// GEMM2's epilogue walks the P^T tile column-wise, i.e. along rows of the
+// or, inside the optimizer, from the triangular factors T = L^-1 without
+// ever forming the inverses (four half-flop GEMMs, plan_precondition).
+// The last GEMM's epilogue walks the P^T tile column-wise, i.e. along rows of the
 // g x a weight, so W' = W - eta P + m V and V' = W' - W are coalesced and
 // ||W'||_F^2 is reduced on the fly for the rescale pass.
 #include <cuda_runtime.h>
@@ -143,62 +145,98 @@ GemmOperand dense_operand(const float* ptr, int64_t ld, int64_t rows, int64_t K)
 }  // namespace
 
 int plan_precondition(const spngd_precond_req* reqs, int n, double eta, double momentum, float* tmp,
-                      double* norms, PrecondPlan& plan, const float* scal) {
+                      double* norms, PrecondPlan& plan, const float* scal, const PrecondTri* tri) {
   plan = PrecondPlan();
+  plan.stages = tri ? 4 : 2;
   size_t off = 0;
+  auto take = [&](int64_t floats) {
+    float* p = tmp ? tmp + off : nullptr;
+    off += size_t(round_up(floats, 64));
+    return p;
+  };
   for (int i = 0; i < n; ++i) {
     const spngd_precond_req& r = reqs[i];
     if (r.g <= 0 || r.a <= 0) return fail(SPNGD_ERR_SHAPE_MISMATCH, "kron_matvec: empty operand");
-    if (!r.Ginv || !r.Ainv || !r.dW) return fail(SPNGD_ERR_INVALID, "precondition: null pointer");
+    if (!r.dW || (!tri && (!r.Ginv || !r.Ainv))) return fail(SPNGD_ERR_INVALID, "precondition: null pointer");
+    if (tri && (!tri[i].tlA || !tri[i].tuA || !tri[i].tlG || !tri[i].tuG))
+      return fail(SPNGD_ERR_INVALID, "precondition: null triangular factor");
     if (r.ldg < r.g || r.lda < r.a) return fail(SPNGD_ERR_SHAPE_MISMATCH, "kron_matvec: X must be dim(G) x dim(A)");
     if (r.W && !r.V) return fail(SPNGD_ERR_INVALID, "ngd_step: velocity missing");
     const int64_t ldp = round_up(r.g, 4);
-    float* p1t = tmp ? tmp + off : nullptr;
-    off += size_t(round_up(r.a * ldp, 64));
-    GemmProblem p1{};
-    p1.A = dense_operand(r.Ainv, r.lda, r.a, r.a);
-    p1.B = dense_operand(r.dW, r.a, r.g, r.a);
-    p1.M = int32_t(r.a); p1.N = int32_t(r.g); p1.K = int32_t(r.a);
-    p1.mode = EPI_DENSE; p1.alpha = 1.f; p1.beta = 0.f;
-    p1.C = p1t; p1.ldc = ldp;
-    GemmProblem p2{};
-    p2.A = dense_operand(p1t, ldp, r.a, r.g);
-    p2.B = dense_operand(r.Ginv, r.ldg, r.g, r.g);
-    p2.M = int32_t(r.a); p2.N = int32_t(r.g); p2.K = int32_t(r.g);
-    p2.mode = EPI_UPDATE; p2.alpha = 1.f;
-    p2.W = r.W; p2.V = r.V; p2.P_out = r.P_out;
-    p2.eta = float(eta); p2.momentum = float(momentum);
-    p2.scal = scal;
-    p2.norm2 = (r.W && r.rescale && norms) ? norms + i : nullptr;
-    const int idx = int(plan.probs1.size());
-    plan.probs1.push_back(p1);
-    plan.probs2.push_back(p2);
-    int slot = 0;
-    plan_problem_tiles(idx, p1, false, p1.K + kTileK, plan.items1, nullptr, &slot, 1.0, nullptr);
-    plan_problem_tiles(idx, p2, false, p2.K + kTileK, plan.items2, nullptr, &slot, 1.0, nullptr);
+    GemmProblem st[4]{};
+    auto dense = [](GemmProblem& p, int64_t M, int64_t N, int64_t K, int32_t ktri, float* C, int64_t ldc) {
+      p.M = int32_t(M); p.N = int32_t(N); p.K = int32_t(K);
+      p.mode = EPI_DENSE; p.alpha = 1.f; p.beta = 0.f; p.ktri = ktri;
+      p.C = C; p.ldc = ldc;
+    };
+    GemmProblem* last = nullptr;
+    if (!tri) {
+      //   P1^T[j,i] = sum_k A^-1[j,k] dW[i,k]      (M=a, N=g, K=a)
+      //   P^T [j,i] = sum_k P1^T[j,k] G^-1[i,k]    (M=a, N=g, K=g)
+      float* p1t = take(r.a * ldp);
+      st[0].A = dense_operand(r.Ainv, r.lda, r.a, r.a);
+      st[0].B = dense_operand(r.dW, r.a, r.g, r.a);
+      dense(st[0], r.a, r.g, r.a, 0, p1t, ldp);
+      st[1].A = dense_operand(p1t, ldp, r.a, r.g);
+      st[1].B = dense_operand(r.Ginv, r.ldg, r.g, r.g);
+      last = &st[1];
+    } else {
+      // (A + dI)^-1 = T_A^T T_A, (G + dI)^-1 = T_G^T T_G, T lower (tl), T^T upper (tu):
+      //   Q^T [i,m] = sum_k dW[i,k]   T_A[m,k]     (M=g, N=a, K=a; B lower)
+      //   P1^T[j,i] = sum_m T_A^T[j,m] Q^T[i,m]     (M=a, N=g, K=a; A upper)
+      //   R   [j,l] = sum_k P1^T[j,k] T_G[l,k]     (M=a, N=g, K=g; B lower)
+      //   P^T [j,i] = sum_l R[j,l]   T_G^T[i,l]    (M=a, N=g, K=g; B upper)
+      const int64_t ldq = round_up(r.a, 4);
+      float* qt = take(r.g * ldq);
+      float* p1t = take(r.a * ldp);
+      float* rr = take(r.a * ldp);
+      st[0].A = dense_operand(r.dW, r.a, r.g, r.a);
+      st[0].B = dense_operand(tri[i].tlA, r.lda, r.a, r.a);
+      dense(st[0], r.g, r.a, r.a, KTRI_B_LOWER, qt, ldq);
+      st[1].A = dense_operand(tri[i].tuA, r.lda, r.a, r.a);
+      st[1].B = dense_operand(qt, ldq, r.g, r.a);
+      dense(st[1], r.a, r.g, r.a, KTRI_A_UPPER, p1t, ldp);
+      st[2].A = dense_operand(p1t, ldp, r.a, r.g);
+      st[2].B = dense_operand(tri[i].tlG, r.ldg, r.g, r.g);
+      dense(st[2], r.a, r.g, r.g, KTRI_B_LOWER, rr, ldp);
+      st[3].A = dense_operand(rr, ldp, r.a, r.g);
+      st[3].B = dense_operand(tri[i].tuG, r.ldg, r.g, r.g);
+      st[3].ktri = KTRI_B_UPPER;
+      last = &st[3];
+    }
+    GemmProblem& pu = *last;
+    pu.M = int32_t(r.a); pu.N = int32_t(r.g); pu.K = int32_t(r.g);
+    pu.mode = EPI_UPDATE; pu.alpha = 1.f;
+    pu.W = r.W; pu.V = r.V; pu.P_out = r.P_out;
+    pu.eta = float(eta); pu.momentum = float(momentum);
+    pu.scal = scal;
+    pu.norm2 = (r.W && r.rescale && norms) ? norms + i : nullptr;
+    const int idx = int(plan.probs[0].size());
+    for (int q = 0; q < plan.stages; ++q) {
+      plan.probs[q].push_back(st[q]);
+      int slot = 0;
+      plan_problem_tiles(idx, st[q], false, st[q].K + kTileK, plan.items[q], nullptr, &slot, 1.0, nullptr);
+    }
     if (r.W && r.rescale)
       plan.rescale.push_back({r.W, r.V, r.g * r.a, norms ? norms + i : nullptr, std::sqrt(2.0 * double(r.g))});
   }
   plan.tmp_floats = off;
   plan.n_norms = n;
   auto longest = [](const GemmWorkItem& x, const GemmWorkItem& y) { return (x.k1 - x.k0) > (y.k1 - y.k0); };
-  std::stable_sort(plan.items1.begin(), plan.items1.end(), longest);
-  std::stable_sort(plan.items2.begin(), plan.items2.end(), longest);
+  for (int q = 0; q < plan.stages; ++q) std::stable_sort(plan.items[q].begin(), plan.items[q].end(), longest);
   return SPNGD_OK;
 }
 
-int run_precondition(spngd_ctx* ctx, const PrecondPlan& plan, const GemmProblem* d_p1, const GemmWorkItem* d_i1,
-                     const GemmProblem* d_p2, const GemmWorkItem* d_i2, const RescaleTask* d_rescale,
-                     double* d_norms) {
+int run_precondition(spngd_ctx* ctx, const PrecondPlan& plan, GemmProblem* const* d_probs,
+                     GemmWorkItem* const* d_items, const RescaleTask* d_rescale, double* d_norms) {
   if (d_norms && plan.n_norms > 0)
     SPNGD_CUDA_TRY(cudaMemsetAsync(d_norms, 0, sizeof(double) * plan.n_norms, ctx->stream));
-  int rc = launch_gemm(d_p1, d_i1, int(plan.items1.size()), nullptr, ctx->d_status, ctx->stream,
-                       gemm_variant(plan.probs1.data(), int(plan.probs1.size())));
-  if (rc) return rc;
-  rc = launch_gemm(d_p2, d_i2, int(plan.items2.size()), nullptr, ctx->d_status, ctx->stream,
-                   gemm_variant(plan.probs2.data(), int(plan.probs2.size())));
-  if (rc) return rc;
-  ctx->launches += 2;
+  for (int q = 0; q < plan.stages; ++q) {
+    int rc = launch_gemm(d_probs[q], d_items[q], int(plan.items[q].size()), nullptr, ctx->d_status, ctx->stream,
+                         gemm_variant(plan.probs[q].data(), int(plan.probs[q].size())));
+    if (rc) return rc;
+    ctx->launches++;
+  }
   if (!plan.rescale.empty()) {
     dim3 grid(296, unsigned(plan.rescale.size()));
     rescale_kernel<<<grid, 256, 0, ctx->stream>>>(d_rescale);
@@ -243,12 +281,14 @@ extern "C" int spngd_precondition_update_batched(spngd_ctx* ctx, int n, const sp
   double* norms = scratch.alloc<double>(n);
   PrecondPlan plan;
   plan_precondition(reqs, n, eta, momentum, tmp, norms, plan);
-  auto* d_p1 = scratch.upload(plan.probs1);
-  auto* d_i1 = scratch.upload(plan.items1);
-  auto* d_p2 = scratch.upload(plan.probs2);
-  auto* d_i2 = scratch.upload(plan.items2);
+  GemmProblem* d_p[4] = {};
+  GemmWorkItem* d_i[4] = {};
+  for (int q = 0; q < plan.stages; ++q) {
+    d_p[q] = scratch.upload(plan.probs[q]);
+    d_i[q] = scratch.upload(plan.items[q]);
+  }
   auto* d_rs = scratch.upload(plan.rescale);
-  rc = run_precondition(ctx, plan, d_p1, d_i1, d_p2, d_i2, d_rs, norms);
+  rc = run_precondition(ctx, plan, d_p, d_i, d_rs, norms);
   if (rc) return rc;
   return spngd_ctx_sync(ctx);
 }

@@ -16,21 +16,36 @@ struct RescaleTask {  // rescale_weights + velocity fix, one FC/Conv layer
 };
 
 struct PrecondPlan {
-  std::vector<GemmProblem> probs1, probs2;
-  std::vector<GemmWorkItem> items1, items2;
+  // Grouped GEMM launches in order: dense inverses -> 2 (P1^T = A^-1 dW^T,
+  // P^T = P1^T G^-1 with EPI_UPDATE); triangular factors -> 4 (see
+  // plan_precondition).
+  int stages = 2;
+  std::vector<GemmProblem> probs[4];
+  std::vector<GemmWorkItem> items[4];
   std::vector<RescaleTask> rescale;
-  size_t tmp_floats = 0;    // P1^T scratch
+  size_t tmp_floats = 0;    // intermediate products
   int n_norms = 0;
 };
 
-// Builds the two grouped GEMM launches P1^T = A^-1 dW^T and
-// P^T = P1^T G^-1 (EPI_UPDATE).  `tmp` holds the P1^T buffers (sizing pass when
-// null) and `norms` one double per request.
+// Triangular factors of the damped inverses (A + dI)^-1 = T_A^T T_A: lower
+// T = L^-1 and upper T^T, same leading dimension as the request's lda / ldg.
+struct PrecondTri {
+  const float* tlA;
+  const float* tuA;
+  const float* tlG;
+  const float* tuG;
+};
+
+// Builds the grouped GEMM launches of P = G^-1 dW A^-1 fused with the
+// update.  `tmp` holds the intermediates (sizing pass when null), `norms` one
+// double per request.  With `tri` (one entry per request) the inverses are
+// never formed: P^T = T_A^T T_A dW^T T_G^T T_G as four half-flop triangular
+// GEMMs, reqs[i].Ainv / Ginv unused.
 int plan_precondition(const spngd_precond_req* reqs, int n, double eta, double momentum, float* tmp,
-                      double* norms, PrecondPlan& plan, const float* scal = nullptr);
-int run_precondition(spngd_ctx* ctx, const PrecondPlan& plan, const GemmProblem* d_p1, const GemmWorkItem* d_i1,
-                     const GemmProblem* d_p2, const GemmWorkItem* d_i2, const RescaleTask* d_rescale,
-                     double* d_norms);
+                      double* norms, PrecondPlan& plan, const float* scal = nullptr,
+                      const PrecondTri* tri = nullptr);
+int run_precondition(spngd_ctx* ctx, const PrecondPlan& plan, GemmProblem* const* d_probs,
+                     GemmWorkItem* const* d_items, const RescaleTask* d_rescale, double* d_norms);
 
 struct BnUpdateTask {
   spngd_bn_update_req r;
