@@ -274,6 +274,12 @@ typedef struct spngd_opt_config {
   int32_t stale;       /* stale_enabled */
   double stale_alpha;
   int64_t batch;       /* per-rank micro-batch M/K */
+  int32_t fisher_mode; /* OptimizerConfig::fisher_mode (dist.hpp:113-128): 0 Empirical
+                        * (G and F from grad_true, fisher.cpp:133-137), 1 OneMC (G and F
+                        * from the sampled-label backward's captures, buffers 13-15,
+                        * fisher.cpp:127-132; dist.cpp:476-480) */
+  int32_t elem_size;   /* ClusterConfig::elem_size, the ledger's modeled wire element
+                        * size in bytes (dist.hpp:58-60); 0 means 4 */
 } spngd_opt_config;
 
 /* Host-only planning of the hybrid schedule (no GPU needed): layer owners
@@ -305,7 +311,9 @@ void spngd_opt_destroy(spngd_opt* opt);
  *   g x a or 2c), 3 W (g x a, or gamma|beta 2c), 4 V, 5 bn gg (M x c),
  *   6 bn gb, 7 A_inv dense, 8 G_inv dense, 9 A packed (reduced), 10 G packed,
  *   11 BN moments 3c (reduced), 12 the whole weight all-gather buffer
- *   (ld = its float count). NULL if the layer has no such buffer or this
+ *   (ld = its float count), 13 sampled-label grad capture (OneMC only,
+ *   LayerCapture::grad_sampled, net.hpp:92), 14 / 15 sampled-label BN
+ *   gamma / beta grads (OneMC only, bn_g*_sampled, net.hpp:96-97). NULL if the layer has no such buffer or this
  *   rank does not own it.  The step keeps only the triangular factors
  *   T = chol(X + dI)^-1 (it preconditions with T^T T directly), so 7 / 8
  *   form (X + dI)^-1 = T^T T on the call (one GEMM, synchronous). */
@@ -342,6 +350,52 @@ int64_t spngd_opt_launch_count(const spngd_opt* opt);
  * gating dist.cpp:431-444). */
 int spngd_opt_stale_info(spngd_opt* opt, int layer, int which, int64_t* t_x, int64_t* delta,
                          int64_t* refresh_count, int* due_last);
+
+/* ---- communication ledger (CommLedger, dist.hpp:16-56, dist.cpp:42-133) -----
+ * One row per collective payload, in the reference's record order
+ * (accumulate_microsteps, dist.cpp:511-537, 661-662): stage 2 "RSV_A" --
+ * due A:l in plan order, then skipped A:l; stage 3 "RSV_G_F_grad" -- due
+ * G:l / F:l in plan order, then grad:0..L-1, then skipped G:l / F:l; stage 5
+ * "AGV_params" -- w:0..L-1.  elements = payload length when world > 1, else 0
+ * (dist.cpp:214, 231); bytes = elements * elem_size; skipped rows carry 0 / 0
+ * (dist.cpp:520, 537).  Payload lengths: A/G packed n(n+1)/2, F 3c (unit BN)
+ * or 2c(2c+1)/2 (full BN), grad and w g*a (BN 2c). */
+typedef enum spngd_ledger_collective {
+  SPNGD_RSV_A = 0,          /* stage 2 */
+  SPNGD_RSV_G_F_GRAD = 1,   /* stage 3 */
+  SPNGD_AGV_PARAMS = 2      /* stage 5 */
+} spngd_ledger_collective;
+typedef enum spngd_ledger_id_kind {
+  SPNGD_ID_A = 0, SPNGD_ID_G = 1, SPNGD_ID_F = 2, SPNGD_ID_GRAD = 3, SPNGD_ID_W = 4
+} spngd_ledger_id_kind;
+typedef struct spngd_ledger_row {
+  int64_t step;
+  int32_t stage;        /* 2, 3 or 5 */
+  int32_t collective;   /* spngd_ledger_collective */
+  int32_t id_kind;      /* spngd_ledger_id_kind: statistic_id = "<A|G|F|grad|w>:<layer>" */
+  int32_t layer;
+  int64_t elements;
+  int64_t bytes;
+  int32_t skipped;
+  int32_t pad_;
+} spngd_ledger_row;
+/* Host-only (no GPU): the rows one step appends, given the per-statistic
+ * refresh decisions `due` in plan_statistics order (dist.cpp:256-269: per
+ * layer A then G, or F for BatchNorm); due == NULL means every statistic is
+ * due.  bn_full selects the 2c x 2c F payload.  Returns the row count (rows
+ * are written while count <= cap) or a negative status. */
+int64_t spngd_ledger_step_rows(const spngd_layer_desc* layers, int n_layers, int world, int64_t step,
+                               const unsigned char* due, int elem_size, int bn_full,
+                               spngd_ledger_row* out, int64_t cap);
+/* The rows every spngd_opt_step of this optimizer appended so far (the
+ * CommLedger passed to run_step); returns the total count, copying at most
+ * cap.  _clear empties it. */
+int64_t spngd_opt_ledger(const spngd_opt* opt, spngd_ledger_row* out, int64_t cap);
+int spngd_opt_ledger_clear(spngd_opt* opt);
+/* Bytes this rank handed to NCCL in the last step (send side, padded
+ * owner-major segments as actually moved): reduce-scatter / owner reduces of
+ * statistics, of gradients, and the all-gather.  0 at world == 1. */
+int spngd_opt_wire_bytes(const spngd_opt* opt, int64_t* stat_bytes, int64_t* grad_bytes, int64_t* ag_bytes);
 
 #ifdef __cplusplus
 }

@@ -76,7 +76,14 @@ class LayoutEntry(C.Structure):
 
 class OptConfig(C.Structure):
     _fields_ = [("lambda_", C.c_double), ("rescale", C.c_int32), ("stale", C.c_int32),
-                ("stale_alpha", C.c_double), ("batch", _i64)]
+                ("stale_alpha", C.c_double), ("batch", _i64), ("fisher_mode", C.c_int32),
+                ("elem_size", C.c_int32)]
+
+
+class LedgerRowC(C.Structure):  # spngd_ledger_row
+    _fields_ = [("step", _i64), ("stage", C.c_int32), ("collective", C.c_int32), ("id_kind", C.c_int32),
+                ("layer", C.c_int32), ("elements", _i64), ("bytes", _i64), ("skipped", C.c_int32),
+                ("pad_", C.c_int32)]
 
 
 # status codes (include/spngd_b200.h) -> reference exception names (errors.hpp)
@@ -171,6 +178,11 @@ def _declare(L):
         "spngd_opt_launch_count": (_i64, [P]),
         "spngd_opt_stale_info": (C.c_int, [P, C.c_int, C.c_int, C.POINTER(_i64), C.POINTER(_i64), C.POINTER(_i64),
                                            C.POINTER(C.c_int)]),
+        "spngd_ledger_step_rows": (_i64, [C.POINTER(LayerDesc), C.c_int, C.c_int, _i64, C.POINTER(C.c_ubyte),
+                                          C.c_int, C.c_int, C.POINTER(LedgerRowC), _i64]),
+        "spngd_opt_ledger": (_i64, [P, C.POINTER(LedgerRowC), _i64]),
+        "spngd_opt_ledger_clear": (C.c_int, [P]),
+        "spngd_opt_wire_bytes": (C.c_int, [P, C.POINTER(_i64), C.POINTER(_i64), C.POINTER(_i64)]),
         "spngd_synth_normal": (C.c_int, [P, P, _i64, C.c_uint64, C.c_float, C.c_float, C.c_int]),
         "spngd_synth_conv_capture": (C.c_int, [P, P] + [_i64] * 7 + [C.c_uint64, C.c_int, C.c_float,
                                                                       C.c_float]),

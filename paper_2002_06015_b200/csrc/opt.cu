@@ -58,6 +58,10 @@ struct LayerState {
   float* grad = nullptr;
   float* gg = nullptr;
   float* gb = nullptr;
+  // OneMC: sampled-label captures (grad_sampled, bn_g*_sampled, net.hpp:92-97)
+  float* grad_s = nullptr;
+  float* gg_s = nullptr;
+  float* gb_s = nullptr;
   // RS offsets: off_A/G/M within the owner's statistics segment, off_dW
   // within the owner's gradient segment (floats)
   int64_t off_A = -1, off_G = -1, off_M = -1, off_dW = -1;
@@ -180,6 +184,10 @@ struct spngd_opt {
   std::vector<Pending> pending; int64_t pending_step = 0;
   std::vector<char> due;
   int64_t last_due = 0;
+  // ---- communication ledger (CommLedger) and NCCL bytes of the last step
+  std::vector<spngd_layer_desc> descs;
+  std::vector<spngd_ledger_row> ledger;
+  int64_t wire_stat = 0, wire_grad = 0, wire_ag = 0;
 
   float* alloc(size_t floats, bool zero = false) {
     void* p = nullptr;
@@ -276,11 +284,17 @@ int build(spngd_opt* o, const spngd_layer_desc* descs, int n) {
       o->stats.push_back(st);
       return int(o->stats.size()) - 1;
     };
+    const bool one_mc = o->cfg.fisher_mode == 1;
     if (L.d.kind == SPNGD_BN) {
       const int64_t c = L.d.g;
       L.gg = o->alloc(size_t(B * c));
       L.gb = o->alloc(size_t(B * c));
-      o->bnm.push_back({L.gg, L.gb, c, 0, B, seg + L.off_M});
+      if (one_mc) {  // build_bn_block(mode = OneMC) reads the sampled pair (fisher.cpp:158-159)
+        L.gg_s = o->alloc(size_t(B * c));
+        L.gb_s = o->alloc(size_t(B * c));
+        if (!L.gg_s || !L.gb_s) return fail(SPNGD_ERR_CUDA, "opt: capture allocation failed");
+      }
+      o->bnm.push_back({one_mc ? L.gg_s : L.gg, one_mc ? L.gb_s : L.gb, c, 0, B, seg + L.off_M});
       o->bnm_stat.push_back(add_stat(2, L.off_M, 3 * c, c));
       o->bnm_maxc = std::max(o->bnm_maxc, c);
     } else {
@@ -288,11 +302,12 @@ int build(spngd_opt* o, const spngd_layer_desc* descs, int n) {
       const int64_t hw = conv ? L.d.hw : 1;
       L.act = o->alloc(size_t(B * L.d.a * hw));
       L.grad = o->alloc(size_t(B * L.d.g * hw));
-      if (!L.act || !L.grad) return fail(SPNGD_ERR_CUDA, "opt: capture allocation failed");
+      if (one_mc) L.grad_s = o->alloc(size_t(B * L.d.g * hw));  // factor_G(OneMC), fisher.cpp:127-132
+      if (!L.act || !L.grad || (one_mc && !L.grad_s)) return fail(SPNGD_ERR_CUDA, "opt: capture allocation failed");
       const double nb = double(B);
       freqs.push_back({L.act, L.d.a, hw, conv ? 1 : 0, 0, B, conv ? 1.0 / (nb * double(hw)) : 1.0 / nb, seg + L.off_A});
       o->prob_stat.push_back(add_stat(0, L.off_A, L.d.a * (L.d.a + 1) / 2, L.d.a));
-      freqs.push_back({L.grad, L.d.g, hw, conv ? 1 : 0, 0, B, 1.0 / nb, seg + L.off_G});
+      freqs.push_back({one_mc ? L.grad_s : L.grad, L.d.g, hw, conv ? 1 : 0, 0, B, 1.0 / nb, seg + L.off_G});
       o->prob_stat.push_back(add_stat(1, L.off_G, L.d.g * (L.d.g + 1) / 2, L.d.g));
     }
   }
@@ -567,6 +582,9 @@ int spngd_opt_create(spngd_ctx* ctx, const spngd_layer_desc* layers, int n_layer
   if (!(cfg->lambda > 0.0)) return fail(SPNGD_ERR_NOT_POSITIVE_DEFINITE, "OptimizerConfig: lambda must be > 0");
   if (cfg->batch < 1) return fail(SPNGD_ERR_EMPTY_BATCH, "spngd_opt_create: empty per-rank batch");
   if (cfg->stale && !(cfg->stale_alpha > 0.0)) return fail(SPNGD_ERR_INVALID, "spngd_opt_create: stale_alpha must be > 0");
+  if (cfg->fisher_mode != 0 && cfg->fisher_mode != 1) return fail(SPNGD_ERR_INVALID, "spngd_opt_create: unknown fisher_mode");
+  if (cfg->elem_size != 0 && cfg->elem_size != 2 && cfg->elem_size != 4 && cfg->elem_size != 8)
+    return fail(SPNGD_ERR_INVALID, "spngd_opt_create: elem_size must be 2, 4 or 8");
   for (int i = 0; i < n_layers; ++i) {
     const auto& d = layers[i];
     if (d.kind < 0 || d.kind > 2 || d.g <= 0 || (d.kind != SPNGD_BN && (d.a <= 0 || d.hw <= 0)))
@@ -575,6 +593,8 @@ int spngd_opt_create(spngd_ctx* ctx, const spngd_layer_desc* layers, int n_layer
   auto* o = new spngd_opt();
   o->ctx = ctx;
   o->cfg = *cfg;
+  if (o->cfg.elem_size == 0) o->cfg.elem_size = 4;
+  o->descs.assign(layers, layers + n_layers);
   o->world = ctx->world;
   o->rank = ctx->rank;
   SPNGD_CUDA_TRY(cudaSetDevice(ctx->device));
@@ -620,6 +640,9 @@ float* spngd_opt_buffer(spngd_opt* o, int layer, int which, int64_t* ld) {
     case 10: return (mine && L.off_G >= 0) ? o->rs_recv + L.off_G : nullptr;
     case 11: return (mine && L.off_M >= 0) ? o->rs_recv + L.off_M : nullptr;
     case 12: if (ld) *ld = int64_t(o->world) * o->seg_ag; return o->ag;  // all weight replicas
+    case 13: return L.grad_s;
+    case 14: return L.gg_s;
+    case 15: return L.gb_s;
     default: return nullptr;
   }
 }
@@ -965,6 +988,29 @@ int spngd_opt_step(spngd_opt* o, int64_t step, double eta, double momentum) {
   }
   // Overlapped single-GPU schedule: phases 0-3 run as one unit (own graphs).
   const bool ov = o->overlap_on && full;
+  {  // CommLedger rows of this step (dist.cpp:511-537, 661-662) and NCCL bytes
+    const unsigned char* due = o->cfg.stale ? reinterpret_cast<const unsigned char*>(o->due.data()) : nullptr;
+    const int nl = int(o->descs.size());
+    const int64_t nrows = spngd_ledger_step_rows(o->descs.data(), nl, o->world, step, due, o->cfg.elem_size, 0,
+                                                 nullptr, 0);
+    if (nrows < 0) return int(-nrows);
+    const size_t at = o->ledger.size();
+    o->ledger.resize(at + size_t(nrows));
+    spngd_ledger_step_rows(o->descs.data(), nl, o->world, step, due, o->cfg.elem_size, 0, o->ledger.data() + at,
+                           nrows);
+    o->wire_stat = o->wire_grad = o->wire_ag = 0;
+    if (o->world > 1) {
+      const int64_t W = o->world;
+      if (full && !ov) {
+        o->wire_stat = W * o->seg_stat * int64_t(sizeof(float));  // one ncclReduceScatter
+      } else {  // grouped ncclReduce of the due statistics to their owners
+        for (size_t q = 0; q < o->stats.size(); ++q)
+          if (full || o->due[q]) o->wire_stat += o->stats[q].count * int64_t(sizeof(float));
+      }
+      o->wire_grad = W * o->seg_grad * int64_t(sizeof(float));
+      o->wire_ag = o->seg_ag * int64_t(sizeof(float));
+    }
+  }
   bool& ready = ov ? o->graphs_ready_ov : o->graphs_ready;
   const bool capture = o->use_graph && !ready && full;
   const int64_t l0 = ctx->launches;
@@ -1008,6 +1054,81 @@ int spngd_opt_step(spngd_opt* o, int64_t step, double eta, double momentum) {
   if (capture || !o->use_graph || !full) o->launches = ctx->launches - l0;
   if (capture) ready = true;
   o->timed = true;
+  return SPNGD_OK;
+}
+
+int64_t spngd_ledger_step_rows(const spngd_layer_desc* layers, int n, int world, int64_t step,
+                               const unsigned char* due, int elem_size, int bn_full, spngd_ledger_row* out,
+                               int64_t cap) {
+  if (!layers || n <= 0 || world < 1) return -int64_t(SPNGD_ERR_INVALID);
+  if (elem_size == 0) elem_size = 4;
+  // plan_statistics order (dist.cpp:256-269): per layer A, G or F
+  struct Stat { int layer, kind; int64_t len; bool due; };
+  std::vector<Stat> plan;
+  for (int li = 0; li < n; ++li) {
+    const spngd_layer_desc& d = layers[li];
+    if (d.kind == SPNGD_BN) {
+      const int64_t c = d.g;
+      plan.push_back({li, SPNGD_ID_F, bn_full ? (2 * c) * (2 * c + 1) / 2 : 3 * c, true});
+    } else {
+      plan.push_back({li, SPNGD_ID_A, d.a * (d.a + 1) / 2, true});
+      plan.push_back({li, SPNGD_ID_G, d.g * (d.g + 1) / 2, true});
+    }
+  }
+  if (due)
+    for (size_t q = 0; q < plan.size(); ++q) plan[q].due = due[q] != 0;
+  auto grad_len = [&](int li) { return layers[li].kind == SPNGD_BN ? 2 * layers[li].g : layers[li].g * layers[li].a; };
+  int64_t count = 0;
+  auto row = [&](int stage, int coll, int kind, int layer, int64_t len, bool skipped) {
+    if (out && count < cap) {
+      spngd_ledger_row& r = out[count];
+      r.step = step;
+      r.stage = stage;
+      r.collective = coll;
+      r.id_kind = kind;
+      r.layer = layer;
+      r.elements = skipped ? 0 : (world > 1 ? len : 0);  // dist.cpp:214, 231
+      r.bytes = r.elements * elem_size;
+      r.skipped = skipped ? 1 : 0;
+      r.pad_ = 0;
+    }
+    ++count;
+  };
+  // Stage 2: RSV_A over the due A payloads, then the skips (dist.cpp:511-520)
+  for (const Stat& st : plan)
+    if (st.kind == SPNGD_ID_A && st.due) row(2, SPNGD_RSV_A, st.kind, st.layer, st.len, false);
+  for (const Stat& st : plan)
+    if (st.kind == SPNGD_ID_A && !st.due) row(2, SPNGD_RSV_A, st.kind, st.layer, 0, true);
+  // Stage 3: due G/F, every grad:l, then the skips (dist.cpp:522-537)
+  for (const Stat& st : plan)
+    if (st.kind != SPNGD_ID_A && st.due) row(3, SPNGD_RSV_G_F_GRAD, st.kind, st.layer, st.len, false);
+  for (int li = 0; li < n; ++li) row(3, SPNGD_RSV_G_F_GRAD, SPNGD_ID_GRAD, li, grad_len(li), false);
+  for (const Stat& st : plan)
+    if (st.kind != SPNGD_ID_A && !st.due) row(3, SPNGD_RSV_G_F_GRAD, st.kind, st.layer, 0, true);
+  // Stage 5: AGV_params w:0..L-1 (dist.cpp:646-662)
+  for (int li = 0; li < n; ++li) row(5, SPNGD_AGV_PARAMS, SPNGD_ID_W, li, grad_len(li), false);
+  return count;
+}
+
+int64_t spngd_opt_ledger(const spngd_opt* o, spngd_ledger_row* out, int64_t cap) {
+  if (!o) return -int64_t(SPNGD_ERR_INVALID);
+  const int64_t n = int64_t(o->ledger.size());
+  if (out)
+    for (int64_t i = 0; i < std::min(n, cap); ++i) out[i] = o->ledger[size_t(i)];
+  return n;
+}
+
+int spngd_opt_ledger_clear(spngd_opt* o) {
+  if (!o) return fail(SPNGD_ERR_INVALID, "spngd_opt_ledger_clear: opt is NULL");
+  o->ledger.clear();
+  return SPNGD_OK;
+}
+
+int spngd_opt_wire_bytes(const spngd_opt* o, int64_t* stat_bytes, int64_t* grad_bytes, int64_t* ag_bytes) {
+  if (!o) return fail(SPNGD_ERR_INVALID, "spngd_opt_wire_bytes: opt is NULL");
+  if (stat_bytes) *stat_bytes = o->wire_stat;
+  if (grad_bytes) *grad_bytes = o->wire_grad;
+  if (ag_bytes) *ag_bytes = o->wire_ag;
   return SPNGD_OK;
 }
 

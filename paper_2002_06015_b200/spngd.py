@@ -72,6 +72,10 @@ class CudaError(Error):
     pass
 
 
+class ParseError(Error):  # errors.hpp: ledger / manifest parsing
+    pass
+
+
 _ERRORS = {1: ShapeMismatch, 2: NotPositiveDefinite, 3: SingularBlock, 4: ZeroReference,
            5: EmptyBatch, 6: MissingMcPass, 7: StaleBeyondLimit, 8: RefreshOutOfTurn,
            9: IndivisibleBatch, 10: MissingOwner, 11: EmptyAccumulation, 100: CudaError,
@@ -668,3 +672,128 @@ class StaleTracker:
 
     def ever_built(self):
         return self.refresh_count > 0
+
+
+# ---- communication ledger (include/spngd/dist.hpp:16-56, src/dist.cpp:42-133) ----
+LEDGER_HEADER = "step,stage,collective,statistic_id,elements,bytes,skipped"  # dist.cpp:14-15
+_COLLECTIVES = {0: "RSV_A", 1: "RSV_G_F_grad", 2: "AGV_params"}
+_ID_KINDS = {0: "A", 1: "G", 2: "F", 3: "grad", 4: "w"}
+
+
+@dataclass
+class LedgerRow:  # dist.hpp:19-27
+    step: int = 0
+    stage: int = 0
+    collective: str = ""
+    statistic_id: str = ""
+    elements: int = 0
+    bytes: int = 0
+    skipped: bool = False
+
+
+def _row_from_c(r) -> LedgerRow:
+    return LedgerRow(r.step, r.stage, _COLLECTIVES[r.collective], f"{_ID_KINDS[r.id_kind]}:{r.layer}",
+                     r.elements, r.bytes, bool(r.skipped))
+
+
+class CommLedger:  # dist.hpp:29-40
+    def __init__(self, rows: Optional[List[LedgerRow]] = None):
+        self._rows: List[LedgerRow] = list(rows or [])
+
+    def record(self, step, stage, collective, id, elements, bytes, skipped):  # dist.cpp:42-46
+        self._rows.append(LedgerRow(step, stage, collective, id, elements, bytes, bool(skipped)))
+
+    def rows(self) -> List[LedgerRow]:
+        return self._rows
+
+    def size(self) -> int:
+        return len(self._rows)
+
+    def write_csv(self, f) -> None:  # dist.cpp:48-54
+        f.write(LEDGER_HEADER + "\n")
+        for r in self._rows:
+            f.write(f"{r.step},{r.stage},{r.collective},{r.statistic_id},{r.elements},{r.bytes},"
+                    f"{1 if r.skipped else 0}\n")
+
+
+def ledger_step_rows(net_layers, world: int, step: int, due=None, elem_size: int = 4,
+                     bn_full: bool = False) -> List[LedgerRow]:
+    """Rows one accumulate_microsteps call appends (dist.cpp:511-537, 646-662),
+    computed by the native library's host planner (spngd_ledger_step_rows).
+    `net_layers` are workloads.Layer; `due` per statistic in plan_statistics
+    order (dist.cpp:256-269), None = all due."""
+    from .step import layer_descs
+    L = N.lib()
+    arr = layer_descs(net_layers)
+    d = None
+    if due is not None:
+        d = (C.c_ubyte * len(due))(*[1 if x else 0 for x in due])
+    n = L.spngd_ledger_step_rows(arr, len(net_layers), world, step, d, elem_size, int(bn_full), None, 0)
+    if n < 0:
+        check(int(-n))
+    out = (N.LedgerRowC * max(n, 1))()
+    L.spngd_ledger_step_rows(arr, len(net_layers), world, step, d, elem_size, int(bn_full), out, n)
+    return [_row_from_c(out[i]) for i in range(n)]
+
+
+def _is_statistic_id(i: str) -> bool:  # dist.cpp:22-24
+    return i.startswith("A:") or i.startswith("G:") or i.startswith("F:")
+
+
+@dataclass
+class LedgerReport:  # dist.hpp:42-52
+    steps: int = 0
+    total_bytes: int = 0
+    stat_bytes: int = 0
+    grad_bytes: int = 0
+    param_bytes: int = 0
+    stat_bytes_every_step: int = 0
+    reduction_rate: float = 1.0
+    per_step_bytes: list = field(default_factory=list)
+
+
+def ledger_report(rows) -> LedgerReport:  # dist.cpp:56-86
+    if isinstance(rows, CommLedger):
+        rows = rows.rows()
+    rep = LedgerReport()
+    steps, per_step, full = set(), {}, {}
+    for r in rows:
+        steps.add(r.step)
+        per_step[r.step] = per_step.get(r.step, 0) + r.bytes
+        rep.total_bytes += r.bytes
+        if _is_statistic_id(r.statistic_id):
+            if not r.skipped:
+                rep.stat_bytes += r.bytes
+                full[r.statistic_id] = r.bytes
+        elif r.statistic_id.startswith("grad:"):
+            rep.grad_bytes += r.bytes
+        elif r.statistic_id.startswith("w:"):
+            rep.param_bytes += r.bytes
+    rep.steps = len(steps)
+    for b in full.values():
+        rep.stat_bytes_every_step += b * rep.steps
+    rep.reduction_rate = 1.0 if rep.stat_bytes_every_step == 0 else rep.stat_bytes / rep.stat_bytes_every_step
+    rep.per_step_bytes = sorted(per_step.items())
+    return rep
+
+
+def read_ledger_csv(f) -> List[LedgerRow]:  # dist.cpp:92-133
+    lines = f.read().split("\n")
+    if not lines or lines == [""]:
+        raise ParseError("ledger: empty file")
+    if lines[0].rstrip("\r") != LEDGER_HEADER:
+        raise ParseError("ledger: unrecognized header")
+    rows = []
+    for lineno, line in enumerate(lines[1:], start=2):
+        line = line.rstrip("\r")
+        if not line:
+            continue
+        parts = line.split(",")
+        if len(parts) != 7:
+            raise ParseError(f"ledger: line {lineno}: expected 7 fields")
+        try:
+            rows.append(LedgerRow(int(parts[0]), int(parts[1]), parts[2], parts[3], int(parts[4]), int(parts[5]),
+                                  int(parts[6]) != 0))
+        except ValueError:
+            raise ParseError(f"ledger: line {lineno}: malformed numeric field") from None
+    return rows

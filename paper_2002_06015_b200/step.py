@@ -16,7 +16,9 @@ from . import _native as N
 from .spngd import check
 from .workloads import Layer
 
-ACT, GRAD, DW, W, V, BN_GG, BN_GB, AINV, GINV, A_PACKED, G_PACKED, BN_M3C, ALL_WEIGHTS = range(13)
+(ACT, GRAD, DW, W, V, BN_GG, BN_GB, AINV, GINV, A_PACKED, G_PACKED, BN_M3C, ALL_WEIGHTS,
+ GRAD_SAMPLED, BN_GG_SAMPLED, BN_GB_SAMPLED) = range(16)
+EMPIRICAL, ONE_MC = 0, 1  # FisherMode (fisher.hpp:18-21)
 PHASES = ["factor_gemm", "factor_reduce_bn", "reduce_scatter", "inverse", "precondition_update", "all_gather"]
 
 
@@ -64,8 +66,10 @@ class Comm:
 class Optimizer:
     def __init__(self, layers: List[Layer], batch: int, lam: float = 2.5e-4, rescale: bool = True,
                  device: int = 0, world: int = 1, rank: int = 0, nccl_id: Optional[bytes] = None,
-                 stream=None, stale: bool = False, stale_alpha: float = 0.1):
+                 stream=None, stale: bool = False, stale_alpha: float = 0.1, fisher_mode: int = EMPIRICAL,
+                 elem_size: int = 4):
         self.layers, self.batch, self.lam = layers, batch, lam
+        self.fisher_mode = fisher_mode
         self.world, self.rank, self.device = world, rank, device
         L = N.lib()
         self.ctx = C.c_void_p()
@@ -73,7 +77,7 @@ class Optimizer:
         if world > 1:
             check(L.spngd_ctx_init_comm(self.ctx, world, rank, C.create_string_buffer(nccl_id, 128)))
         arr = layer_descs(layers)
-        cfg = N.OptConfig(lam, int(rescale), int(stale), stale_alpha, batch)
+        cfg = N.OptConfig(lam, int(rescale), int(stale), stale_alpha, batch, int(fisher_mode), int(elem_size))
         self.h = C.c_void_p()
         check(L.spngd_opt_create(self.ctx, arr, len(layers), C.byref(cfg), C.byref(self.h)))
 
@@ -97,11 +101,11 @@ class Optimizer:
         l, B = self.layers[li], self.batch
         if which == ACT:
             return B * l.a * l.hw
-        if which == GRAD:
+        if which in (GRAD, GRAD_SAMPLED):
             return B * l.g * l.hw
         if which in (DW, W, V):
             return 2 * l.g if l.kind == "bn" else l.g * l.a
-        if which in (BN_GG, BN_GB):
+        if which in (BN_GG, BN_GB, BN_GG_SAMPLED, BN_GB_SAMPLED):
             return B * l.g
         if which == A_PACKED:
             return l.a * (l.a + 1) // 2
@@ -112,6 +116,9 @@ class Optimizer:
         raise ValueError(which)
 
     def ptr(self, li: int, which: int):
+        if which in (GRAD_SAMPLED, BN_GG_SAMPLED, BN_GB_SAMPLED) and self.fisher_mode != ONE_MC:
+            from .spngd import MissingMcPass
+            raise MissingMcPass(f"layer {li}: no sampled-label backward (fisher_mode is Empirical)")
         ld = C.c_int64()
         p = N.lib().spngd_opt_buffer(self.h, li, which, C.byref(ld))
         return p, ld.value
@@ -161,6 +168,10 @@ class Optimizer:
                 gg, _ = self.ptr(li, BN_GG)
                 gb, _ = self.ptr(li, BN_GB)
                 check(L.spngd_synth_bn_pairs(self.ctx, gg, gb, B * l.g, _mix(seed, li, 5, r)))
+                if self.fisher_mode == ONE_MC:
+                    sg, _ = self.ptr(li, BN_GG_SAMPLED)
+                    sb, _ = self.ptr(li, BN_GB_SAMPLED)
+                    check(L.spngd_synth_bn_pairs(self.ctx, sg, sb, B * l.g, _mix(seed, li, 7, r)))
                 dw, _ = self.ptr(li, DW)
                 check(L.spngd_synth_normal(self.ctx, dw, 2 * l.g, _mix(seed, li, 2, r), 0.1, 0.0, 0))
                 w, _ = self.ptr(li, W)
@@ -176,6 +187,10 @@ class Optimizer:
             grad, _ = self.ptr(li, GRAD)
             check(L.spngd_synth_normal(self.ctx, grad, B * l.g * l.hw, _mix(seed, li, 1, r),
                                        float((B * l.hw) ** -0.5), 0.0, 0))
+            if self.fisher_mode == ONE_MC:
+                gs, _ = self.ptr(li, GRAD_SAMPLED)
+                check(L.spngd_synth_normal(self.ctx, gs, B * l.g * l.hw, _mix(seed, li, 6, r),
+                                           float((B * l.hw) ** -0.5), 0.0, 0))
             dw, _ = self.ptr(li, DW)
             check(L.spngd_synth_normal(self.ctx, dw, l.g * l.a, _mix(seed, li, 2, r), float(l.a ** -0.5), 0.0, 0))
             w, _ = self.ptr(li, W)
@@ -193,6 +208,24 @@ class Optimizer:
         out = (C.c_float * 6)()
         check(N.lib().spngd_opt_phase_ms(self.h, out))
         return dict(zip(PHASES, list(out)))
+
+    def ledger(self):
+        """The CommLedger rows every step appended (dist.cpp:511-537, 661-662)."""
+        from .spngd import CommLedger, _row_from_c
+        L = N.lib()
+        n = L.spngd_opt_ledger(self.h, None, 0)
+        out = (N.LedgerRowC * max(n, 1))()
+        L.spngd_opt_ledger(self.h, out, n)
+        return CommLedger([_row_from_c(out[i]) for i in range(n)])
+
+    def clear_ledger(self):
+        check(N.lib().spngd_opt_ledger_clear(self.h))
+
+    def wire_bytes(self):
+        """Bytes this rank handed to NCCL in the last step: statistics, gradients, all-gather."""
+        a, b, c = C.c_int64(), C.c_int64(), C.c_int64()
+        check(N.lib().spngd_opt_wire_bytes(self.h, C.byref(a), C.byref(b), C.byref(c)))
+        return dict(stat=a.value, grad=b.value, all_gather=c.value)
 
     def launch_count(self) -> int:
         return N.lib().spngd_opt_launch_count(self.h)

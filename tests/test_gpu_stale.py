@@ -15,6 +15,7 @@ import pytest
 import torch
 
 import oracle as O
+from oracle import ledger as OL
 
 pytestmark = pytest.mark.gpu
 
@@ -120,6 +121,12 @@ def test_stale_gating_matches_tracker_schedule(cuda_dev):
             saw_partial |= 0 < sum(due.values()) < len(due)
             opt.step(step, 1.25e-2, 0.993)
             opt.sync()
+            # CommLedger rows of this step (dist.cpp:511-537, 661-662) follow the same decisions
+            plan_due = [due[(li, k)] for li, l in enumerate(LAYERS) for k in (("F",) if l.kind == "bn" else ("A", "G"))]
+            want_rows = OL.step_rows(LAYERS, 1, step, plan_due, 4)
+            got_rows = [(r.step, r.stage, r.collective, r.statistic_id, r.elements, r.bytes, r.skipped)
+                        for r in opt.ledger().rows() if r.step == step]
+            assert got_rows == want_rows, step
             for (li, k), tr in trackers.items():
                 info = opt.stale_info(li, k)
                 assert info["refreshed"] == due[(li, k)], (step, li, k)

@@ -15,6 +15,8 @@ pytestmark = pytest.mark.gpu
 
 from paper_2002_06015_b200 import workloads as W  # noqa: E402
 from paper_2002_06015_b200.step import ACT, BN_GB, BN_GG, DW, GRAD, V, Optimizer  # noqa: E402
+from paper_2002_06015_b200.step import (BN_GB_SAMPLED, BN_GG_SAMPLED, EMPIRICAL, GRAD_SAMPLED,  # noqa: E402
+                                        ONE_MC)
 from paper_2002_06015_b200.step import W as WB  # noqa: E402
 
 ETA, MOM, LAM = 1.25e-2, 0.993, 2.5e-4
@@ -26,6 +28,8 @@ def rel(a, b):
 
 def oracle_layer(l, batch, before):
     act, grad, dW, W0, V0 = (before[k] for k in (ACT, GRAD, DW, WB, V))
+    if GRAD_SAMPLED in before:  # factor_G(OneMC) reads grad_sampled (fisher.cpp:127-132)
+        grad = before[GRAD_SAMPLED]
     rec = O.OrLayer()
     wo, vo = np.empty(l.g * l.a), np.empty(l.g * l.a)
     rec.is_conv, rec.a, rec.g, rec.hw, rec.batch = int(l.kind == "conv"), l.a, l.g, l.hw, batch
@@ -38,19 +42,22 @@ def oracle_layer(l, batch, before):
 
 def oracle_bn(l, batch, before):
     c = l.g
-    m3 = O.build_bn_block(before[BN_GG].reshape(batch, c), before[BN_GB].reshape(batch, c), 0, batch)
+    gg, gb = (BN_GG_SAMPLED, BN_GB_SAMPLED) if BN_GG_SAMPLED in before else (BN_GG, BN_GB)  # fisher.cpp:158-159
+    m3 = O.build_bn_block(before[gg].reshape(batch, c), before[gb].reshape(batch, c), 0, batch)
     g2 = before[DW].astype(np.float64)
     pg, pb = O.precondition_bn(m3, g2[:c], g2[c:], LAM)
     return O.ngd_update(before[WB], np.concatenate([pg, pb]), before[V], ETA, MOM)
 
 
-def run_and_check(layers, batch, check_layers):
-    opt = Optimizer(layers, batch, lam=LAM)
+def run_and_check(layers, batch, check_layers, fisher_mode=EMPIRICAL):
+    opt = Optimizer(layers, batch, lam=LAM, fisher_mode=fisher_mode)
     opt.synth(seed=3)
     before = {}
     for li in check_layers:
         l = layers[li]
         ws = [BN_GG, BN_GB, DW, WB, V] if l.kind == "bn" else [ACT, GRAD, DW, WB, V]
+        if fisher_mode == ONE_MC:
+            ws += [BN_GG_SAMPLED, BN_GB_SAMPLED] if l.kind == "bn" else [GRAD_SAMPLED]
         before[li] = {w: opt.download(li, w).numpy() for w in ws}
     opt.step(1, ETA, MOM)
     opt.sync()
@@ -77,6 +84,22 @@ def test_small_convnet_full_step(cuda_dev):
     layers = [W.conv(3, 16, 3, 1, 16), W.bn(16), W.conv(16, 32, 3, 2, 16), W.bn(32), W.conv(32, 32, 1, 1, 8),
               W.bn(32), W.fc(32 * 4, 10)]
     run_and_check(layers, 16, range(len(layers)))
+
+
+def test_one_mc_full_step(cuda_dev):
+    """FisherMode::OneMC (dist.cpp:476-480): G and the BN moments come from the
+    sampled-label captures; dW stays the true-label gradient.  The sampled
+    buffers differ from the true ones, so a step that read the wrong capture
+    misses the oracle by O(1)."""
+    layers = [W.conv(3, 16, 3, 1, 16), W.bn(16), W.conv(16, 32, 3, 2, 16), W.bn(32), W.fc(32 * 64, 10)]
+    run_and_check(layers, 16, range(len(layers)), fisher_mode=ONE_MC)
+    from paper_2002_06015_b200.spngd import MissingMcPass
+    opt = Optimizer(layers, 16, lam=LAM)
+    try:
+        with pytest.raises(MissingMcPass):
+            opt.ptr(0, GRAD_SAMPLED)
+    finally:
+        opt.close()
 
 
 def test_resnet18_sampled_layers(cuda_dev):
