@@ -280,6 +280,11 @@ typedef struct spngd_opt_config {
                         * fisher.cpp:127-132; dist.cpp:476-480) */
   int32_t elem_size;   /* ClusterConfig::elem_size, the ledger's modeled wire element
                         * size in bytes (dist.hpp:58-60); 0 means 4 */
+  int32_t sgd;         /* OptimizerConfig::sgd: plain-gradient update, no statistics, no
+                        * rescaling (ngd_step with blocks == nullptr, fisher.cpp:320-333,
+                        * 348-356; dist.cpp:425, 539, 605): the step is gradient RS,
+                        * W' = W - eta dW + m V, V' = W' - W, AG */
+  int32_t pad_;
 } spngd_opt_config;
 
 /* Host-only planning of the hybrid schedule (no GPU needed): layer owners
@@ -382,10 +387,12 @@ typedef struct spngd_ledger_row {
 /* Host-only (no GPU): the rows one step appends, given the per-statistic
  * refresh decisions `due` in plan_statistics order (dist.cpp:256-269: per
  * layer A then G, or F for BatchNorm); due == NULL means every statistic is
- * due.  bn_full selects the 2c x 2c F payload.  Returns the row count (rows
+ * due.  flags: SPNGD_LEDGER_* bits.  Returns the row count (rows
  * are written while count <= cap) or a negative status. */
+#define SPNGD_LEDGER_BN_FULL 1 /* F payload is the 2c x 2c packed block (BnMode::FullBlockDiag2c) */
+#define SPNGD_LEDGER_SGD 2     /* OptimizerConfig::sgd: no statistics (plan_statistics returns none) */
 int64_t spngd_ledger_step_rows(const spngd_layer_desc* layers, int n_layers, int world, int64_t step,
-                               const unsigned char* due, int elem_size, int bn_full,
+                               const unsigned char* due, int elem_size, int flags,
                                spngd_ledger_row* out, int64_t cap);
 /* The rows every spngd_opt_step of this optimizer appended so far (the
  * CommLedger passed to run_step); returns the total count, copying at most

@@ -17,8 +17,10 @@ checker for the native host planner `spngd_ledger_step_rows`:
 from __future__ import annotations
 
 
-def plan_statistics(layers):  # dist.cpp:256-269
+def plan_statistics(layers, spngd=True):  # dist.cpp:256-269
     plans = []
+    if not spngd:
+        return plans
     for li, l in enumerate(layers):
         if l.kind == "bn":
             plans.append((f"F:{li}", li, "F"))
@@ -41,9 +43,9 @@ def _grad_len(l):  # dist.cpp:315-391
     return 2 * l.g if l.kind == "bn" else l.g * l.a
 
 
-def step_rows(layers, K, step, due=None, elem_size=4, bn_full=False):
+def step_rows(layers, K, step, due=None, elem_size=4, bn_full=False, sgd=False):
     """[(step, stage, collective, id, elements, bytes, skipped)] of one step."""
-    plans = plan_statistics(layers)
+    plans = plan_statistics(layers, not sgd)
     due_map = {p[0]: (True if due is None else bool(due[i])) for i, p in enumerate(plans)}
     rows = []
 

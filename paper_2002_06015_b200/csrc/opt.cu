@@ -157,6 +157,7 @@ struct spngd_opt {
   cudaGraphExec_t graph_ov_exec[6] = {};
   bool graphs_ready_ov = false;
   float* d_scal = nullptr;         // {eta, momentum} read by the update kernels
+  std::vector<SgdTask> sgd_tasks; SgdTask* d_sgd = nullptr;  // cfg.sgd: owned layers' plain update
   cudaGraph_t graphs[6] = {};
   cudaGraphExec_t graph_exec[6] = {};
   bool use_graph = true;
@@ -432,6 +433,16 @@ int build(spngd_opt* o, const spngd_layer_desc* descs, int n) {
   }
   o->d_scal = o->alloc(2);
   o->use_graph = getenv("SPNGD_NO_GRAPH") == nullptr;
+  if (o->cfg.sgd) {  // plain-gradient update over every owned layer (fisher.cpp:320-333, 348-356)
+    for (int li = 0; li < n; ++li) {
+      LayerState& L = o->layers[li];
+      if (L.owner != o->rank) continue;
+      const int64_t cnt = L.d.kind == SPNGD_BN ? 2 * L.d.g : L.d.g * L.d.a;
+      o->sgd_tasks.push_back({o->ag + int64_t(o->rank) * o->seg_ag + L.off_W, L.V,
+                              o->rs_recv + o->seg_stat + L.off_dW, cnt});
+    }
+    o->d_sgd = dev_upload(o->sgd_tasks, own);
+  }
   // precondition plan
   PrecondPlan psz;
   rc = plan_precondition(preqs.data(), int(preqs.size()), 0.0, 0.0, nullptr, nullptr, psz, nullptr, ptri.data());
@@ -583,6 +594,7 @@ int spngd_opt_create(spngd_ctx* ctx, const spngd_layer_desc* layers, int n_layer
   if (cfg->batch < 1) return fail(SPNGD_ERR_EMPTY_BATCH, "spngd_opt_create: empty per-rank batch");
   if (cfg->stale && !(cfg->stale_alpha > 0.0)) return fail(SPNGD_ERR_INVALID, "spngd_opt_create: stale_alpha must be > 0");
   if (cfg->fisher_mode != 0 && cfg->fisher_mode != 1) return fail(SPNGD_ERR_INVALID, "spngd_opt_create: unknown fisher_mode");
+  if (cfg->sgd && cfg->stale) return fail(SPNGD_ERR_INVALID, "spngd_opt_create: sgd has no statistics to gate");
   if (cfg->elem_size != 0 && cfg->elem_size != 2 && cfg->elem_size != 4 && cfg->elem_size != 8)
     return fail(SPNGD_ERR_INVALID, "spngd_opt_create: elem_size must be 2, 4 or 8");
   for (int i = 0; i < n_layers; ++i) {
@@ -991,17 +1003,20 @@ int spngd_opt_step(spngd_opt* o, int64_t step, double eta, double momentum) {
   {  // CommLedger rows of this step (dist.cpp:511-537, 661-662) and NCCL bytes
     const unsigned char* due = o->cfg.stale ? reinterpret_cast<const unsigned char*>(o->due.data()) : nullptr;
     const int nl = int(o->descs.size());
-    const int64_t nrows = spngd_ledger_step_rows(o->descs.data(), nl, o->world, step, due, o->cfg.elem_size, 0,
+    const int lf = o->cfg.sgd ? SPNGD_LEDGER_SGD : 0;
+    const int64_t nrows = spngd_ledger_step_rows(o->descs.data(), nl, o->world, step, due, o->cfg.elem_size, lf,
                                                  nullptr, 0);
     if (nrows < 0) return int(-nrows);
     const size_t at = o->ledger.size();
     o->ledger.resize(at + size_t(nrows));
-    spngd_ledger_step_rows(o->descs.data(), nl, o->world, step, due, o->cfg.elem_size, 0, o->ledger.data() + at,
+    spngd_ledger_step_rows(o->descs.data(), nl, o->world, step, due, o->cfg.elem_size, lf, o->ledger.data() + at,
                            nrows);
     o->wire_stat = o->wire_grad = o->wire_ag = 0;
     if (o->world > 1) {
       const int64_t W = o->world;
-      if (full && !ov) {
+      if (o->cfg.sgd) {
+        o->wire_stat = 0;
+      } else if (full && !ov) {
         o->wire_stat = W * o->seg_stat * int64_t(sizeof(float));  // one ncclReduceScatter
       } else {  // grouped ncclReduce of the due statistics to their owners
         for (size_t q = 0; q < o->stats.size(); ++q)
@@ -1010,6 +1025,25 @@ int spngd_opt_step(spngd_opt* o, int64_t step, double eta, double momentum) {
       o->wire_grad = W * o->seg_grad * int64_t(sizeof(float));
       o->wire_ag = o->seg_ag * int64_t(sizeof(float));
     }
+  }
+  if (o->cfg.sgd) {  // Stage 3 grads RS, plain update, Stage 5 AG (dist.cpp:522-537, 604-620, 646-663)
+    const int64_t l0 = ctx->launches;
+    for (int ph = 0; ph < 6; ++ph) {
+      SPNGD_CUDA_TRY(cudaEventRecord(o->ev[ph], s));
+      int rc = SPNGD_OK;
+      if (ph == 2 && o->world > 1)
+        rc = spngd_reduce_scatter_mean(ctx, o->rs_send + int64_t(o->world) * o->seg_stat, o->rs_recv + o->seg_stat,
+                                       o->seg_grad);
+      else if (ph == 4)
+        rc = launch_sgd_update(ctx, o->d_sgd, int(o->sgd_tasks.size()), o->d_scal);
+      else if (ph == 5 && o->world > 1)
+        rc = spngd_all_gather(ctx, o->ag + int64_t(o->rank) * o->seg_ag, o->ag, o->seg_ag);
+      if (rc) return rc;
+    }
+    SPNGD_CUDA_TRY(cudaEventRecord(o->ev[6], s));
+    o->launches = ctx->launches - l0;
+    o->timed = true;
+    return SPNGD_OK;
   }
   bool& ready = ov ? o->graphs_ready_ov : o->graphs_ready;
   const bool capture = o->use_graph && !ready && full;
@@ -1058,14 +1092,16 @@ int spngd_opt_step(spngd_opt* o, int64_t step, double eta, double momentum) {
 }
 
 int64_t spngd_ledger_step_rows(const spngd_layer_desc* layers, int n, int world, int64_t step,
-                               const unsigned char* due, int elem_size, int bn_full, spngd_ledger_row* out,
+                               const unsigned char* due, int elem_size, int flags, spngd_ledger_row* out,
                                int64_t cap) {
   if (!layers || n <= 0 || world < 1) return -int64_t(SPNGD_ERR_INVALID);
   if (elem_size == 0) elem_size = 4;
+  const bool bn_full = (flags & SPNGD_LEDGER_BN_FULL) != 0;
+  const bool sgd = (flags & SPNGD_LEDGER_SGD) != 0;
   // plan_statistics order (dist.cpp:256-269): per layer A, G or F
   struct Stat { int layer, kind; int64_t len; bool due; };
   std::vector<Stat> plan;
-  for (int li = 0; li < n; ++li) {
+  for (int li = 0; li < n && !sgd; ++li) {
     const spngd_layer_desc& d = layers[li];
     if (d.kind == SPNGD_BN) {
       const int64_t c = d.g;

@@ -84,6 +84,39 @@ __global__ void bn_update_kernel(const spngd_bn_update_req* __restrict__ reqs, d
   }
 }
 
+// HBM-bound: 16 bytes in / 8 out per element; float4 when every pointer is
+// 16-byte aligned and n % 4 == 0 (true for the owner-major 64-float entries).
+__global__ void sgd_update_kernel(const SgdTask* __restrict__ tasks, const float* __restrict__ scal) {
+  const SgdTask t = tasks[blockIdx.y];
+  const double eta = scal[0], mom = scal[1];
+  const bool vec = t.n % 4 == 0 && ((reinterpret_cast<uintptr_t>(t.W) | reinterpret_cast<uintptr_t>(t.V) |
+                                     reinterpret_cast<uintptr_t>(t.g)) & 15) == 0;
+  const int64_t n4 = vec ? t.n / 4 : 0;
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  auto upd = [&](float w, float v, float g, float& nw, float& nv) {
+    nw = float(double(w) - eta * double(g) + mom * double(v));  // fisher.cpp:332
+    nv = nw - w;                                                 // fisher.cpp:333
+  };
+  for (int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; q < n4; q += stride) {
+    const float4 w = reinterpret_cast<const float4*>(t.W)[q];
+    const float4 v = reinterpret_cast<const float4*>(t.V)[q];
+    const float4 g = __ldg(reinterpret_cast<const float4*>(t.g) + q);
+    float4 nw, nv;
+    upd(w.x, v.x, g.x, nw.x, nv.x);
+    upd(w.y, v.y, g.y, nw.y, nv.y);
+    upd(w.z, v.z, g.z, nw.z, nv.z);
+    upd(w.w, v.w, g.w, nw.w, nv.w);
+    reinterpret_cast<float4*>(t.W)[q] = nw;
+    reinterpret_cast<float4*>(t.V)[q] = nv;
+  }
+  for (int64_t i = 4 * n4 + int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < t.n; i += stride) {
+    float nw, nv;
+    upd(t.W[i], t.V[i], t.g[i], nw, nv);
+    t.W[i] = nw;
+    t.V[i] = nv;
+  }
+}
+
 // Weighted norms of x - x1, x1, x - x2, x2 (weights 1 on the diagonal, 2 off it
 // for packed statistics; 1,2,1 for BN 3c payloads), stale.hpp:23-64.
 __global__ void stat_distance_kernel(const spngd_stat_req* __restrict__ reqs) {
@@ -251,6 +284,15 @@ int launch_bn_update(spngd_ctx* ctx, const spngd_bn_update_req* d_reqs, int n, i
   if (n <= 0) return SPNGD_OK;
   dim3 grid(unsigned((max_c + 255) / 256), unsigned(n));
   bn_update_kernel<<<grid, 256, 0, ctx->stream>>>(d_reqs, lambda, eta, momentum, scal, ctx->d_status);
+  SPNGD_CUDA_TRY(cudaGetLastError());
+  ctx->launches++;
+  return SPNGD_OK;
+}
+
+int launch_sgd_update(spngd_ctx* ctx, const SgdTask* d_tasks, int n, const float* scal) {
+  if (n <= 0) return SPNGD_OK;
+  dim3 grid(296u, unsigned(n));  // 2 x 148 SMs
+  sgd_update_kernel<<<grid, 256, 0, ctx->stream>>>(d_tasks, scal);
   SPNGD_CUDA_TRY(cudaGetLastError());
   ctx->launches++;
   return SPNGD_OK;

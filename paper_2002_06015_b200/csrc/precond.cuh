@@ -52,6 +52,15 @@ struct BnUpdateTask {
 };
 int launch_bn_update(spngd_ctx* ctx, const spngd_bn_update_req* d_reqs, int n, int64_t max_c, double lambda,
                      double eta, double momentum, const float* scal = nullptr);
+// Plain-gradient update of one layer (ngd_step with blocks == nullptr,
+// fisher.cpp:320-333, 348-356): W' = W - eta g + m V, V' = W' - W.
+struct SgdTask {
+  float* W;
+  float* V;
+  const float* g;
+  int64_t n;
+};
+int launch_sgd_update(spngd_ctx* ctx, const SgdTask* d_tasks, int n, const float* scal);
 int launch_stat_distance(spngd_ctx* ctx, const spngd_stat_req* d_reqs, int n, int64_t max_rows);
 
 }  // namespace spngd

@@ -717,7 +717,7 @@ class CommLedger:  # dist.hpp:29-40
 
 
 def ledger_step_rows(net_layers, world: int, step: int, due=None, elem_size: int = 4,
-                     bn_full: bool = False) -> List[LedgerRow]:
+                     bn_full: bool = False, sgd: bool = False) -> List[LedgerRow]:
     """Rows one accumulate_microsteps call appends (dist.cpp:511-537, 646-662),
     computed by the native library's host planner (spngd_ledger_step_rows).
     `net_layers` are workloads.Layer; `due` per statistic in plan_statistics
@@ -728,11 +728,12 @@ def ledger_step_rows(net_layers, world: int, step: int, due=None, elem_size: int
     d = None
     if due is not None:
         d = (C.c_ubyte * len(due))(*[1 if x else 0 for x in due])
-    n = L.spngd_ledger_step_rows(arr, len(net_layers), world, step, d, elem_size, int(bn_full), None, 0)
+    flags = (1 if bn_full else 0) | (2 if sgd else 0)  # SPNGD_LEDGER_BN_FULL | SPNGD_LEDGER_SGD
+    n = L.spngd_ledger_step_rows(arr, len(net_layers), world, step, d, elem_size, flags, None, 0)
     if n < 0:
         check(int(-n))
     out = (N.LedgerRowC * max(n, 1))()
-    L.spngd_ledger_step_rows(arr, len(net_layers), world, step, d, elem_size, int(bn_full), out, n)
+    L.spngd_ledger_step_rows(arr, len(net_layers), world, step, d, elem_size, flags, out, n)
     return [_row_from_c(out[i]) for i in range(n)]
 
 

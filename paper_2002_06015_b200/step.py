@@ -67,9 +67,9 @@ class Optimizer:
     def __init__(self, layers: List[Layer], batch: int, lam: float = 2.5e-4, rescale: bool = True,
                  device: int = 0, world: int = 1, rank: int = 0, nccl_id: Optional[bytes] = None,
                  stream=None, stale: bool = False, stale_alpha: float = 0.1, fisher_mode: int = EMPIRICAL,
-                 elem_size: int = 4):
+                 elem_size: int = 4, sgd: bool = False):
         self.layers, self.batch, self.lam = layers, batch, lam
-        self.fisher_mode = fisher_mode
+        self.fisher_mode, self.sgd = fisher_mode, sgd
         self.world, self.rank, self.device = world, rank, device
         L = N.lib()
         self.ctx = C.c_void_p()
@@ -77,7 +77,7 @@ class Optimizer:
         if world > 1:
             check(L.spngd_ctx_init_comm(self.ctx, world, rank, C.create_string_buffer(nccl_id, 128)))
         arr = layer_descs(layers)
-        cfg = N.OptConfig(lam, int(rescale), int(stale), stale_alpha, batch, int(fisher_mode), int(elem_size))
+        cfg = N.OptConfig(lam, int(rescale), int(stale), stale_alpha, batch, int(fisher_mode), int(elem_size), int(sgd), 0)
         self.h = C.c_void_p()
         check(L.spngd_opt_create(self.ctx, arr, len(layers), C.byref(cfg), C.byref(self.h)))
 

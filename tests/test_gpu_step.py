@@ -134,3 +134,27 @@ def test_overlapped_schedule_is_bitwise_phase_serial(cuda_dev):
         opt.close()
     for li, ((w0, v0), (w1, v1)) in enumerate(zip(*outs)):
         assert np.array_equal(w0, w1) and np.array_equal(v0, v1), f"layer {li} {layers[li]}"
+
+
+def test_sgd_step(cuda_dev):
+    """OptimizerConfig::sgd (ngd_step with blocks == nullptr, fisher.cpp:320-333,
+    348-356): W' = W - eta g + m V, V' = W' - W for every layer, no statistics,
+    no rescale; the ledger ships only grads and weights."""
+    layers = [W.conv(3, 16, 3, 1, 16), W.bn(16), W.fc(16 * 256, 10)]
+    opt = Optimizer(layers, 8, lam=LAM, sgd=True)
+    try:
+        opt.synth(seed=4)
+        before = {li: {w: opt.download(li, w).numpy().astype(np.float64) for w in (DW, WB, V)}
+                  for li in range(len(layers))}
+        opt.step(1, ETA, MOM)
+        opt.sync()
+        for li in range(len(layers)):
+            b = before[li]
+            wn = b[WB] - ETA * b[DW] + MOM * b[V]
+            assert rel(opt.download(li, WB).numpy(), wn) <= 1e-6
+            assert np.allclose(opt.download(li, V).numpy(), wn - b[WB], atol=1e-6)
+        ids = [r.statistic_id for r in opt.ledger().rows()]
+        assert ids == ["grad:0", "grad:1", "grad:2", "w:0", "w:1", "w:2"]
+        assert opt.launch_count() == 1
+    finally:
+        opt.close()

@@ -34,6 +34,15 @@ def test_planner_matches_oracle(world, bn_full):
             assert _tuples(got) == want
 
 
+@pytest.mark.parametrize("world", [1, 4])
+def test_sgd_ledger_has_no_statistics(world):
+    """OptimizerConfig::sgd: plan_statistics is empty (dist.cpp:258), grads and weights still ship."""
+    net = small_net()
+    got = _tuples(S.ledger_step_rows(net, world, 2, sgd=True))
+    assert got == OL.step_rows(net, world, 2, sgd=True)
+    assert [r[3] for r in got] == ["grad:0", "grad:1", "grad:2", "w:0", "w:1", "w:2"]
+
+
 def test_symmetry_kat():
     """acceptance.cpp:318-338: fc(4,6)+fc(6,10) at K=2 ships tri(4)+tri(6)+tri(6)+tri(10)."""
     net = [W.fc(4, 6), W.fc(6, 10)]
