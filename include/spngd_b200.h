@@ -284,7 +284,11 @@ typedef struct spngd_opt_config {
                         * rescaling (ngd_step with blocks == nullptr, fisher.cpp:320-333,
                         * 348-356; dist.cpp:425, 539, 605): the step is gradient RS,
                         * W' = W - eta dW + m V, V' = W' - W, AG */
-  int32_t pad_;
+  int32_t bn_mode;     /* OptimizerConfig::bn_mode: 0 Unit (2x2 per channel), 1 FullBlockDiag2c:
+                        * F = mean u u^T over u = (g_gamma0, g_beta0, ...) (build_bn_full,
+                        * fisher.cpp:187-216) through the SYRK engine, (F + lambda I)^-1 by
+                        * the batched Cholesky (damp_bn_full, :248-253), precondition_bn_full
+                        * + BN update (:278-296, 346-359); the wave overlap is off */
 } spngd_opt_config;
 
 /* Host-only planning of the hybrid schedule (no GPU needed): layer owners
@@ -297,12 +301,18 @@ typedef struct spngd_opt_config {
  * when due (stale gating).  All-gather buffer: W g*a or gamma|beta 2c.
  * -1 marks payloads a layer does not have.  Send buffer layout:
  * [world x seg_stat | world x seg_grad]; owner receive: [seg_stat | seg_grad]. */
+#define SPNGD_LEDGER_BN_FULL 1 /* F payload is the 2c x 2c packed block (BnMode::FullBlockDiag2c) */
+#define SPNGD_LEDGER_SGD 2     /* OptimizerConfig::sgd: no statistics (plan_statistics returns none) */
 typedef struct spngd_layout_entry {
   int32_t owner;
   int32_t pad_;
   int64_t off_A, off_G, off_M, off_dW;
   int64_t off_W;
 } spngd_layout_entry;
+/* As spngd_plan_layout; flags SPNGD_LEDGER_BN_FULL sizes BN statistics as the
+ * packed 2c x 2c block instead of the 3c moments. */
+int spngd_plan_layout_ex(const spngd_layer_desc* layers, int n_layers, int world, int flags, spngd_layout_entry* out,
+                         int64_t* seg_stat, int64_t* seg_grad, int64_t* seg_ag);
 int spngd_plan_layout(const spngd_layer_desc* layers, int n_layers, int world, spngd_layout_entry* out,
                       int64_t* seg_stat, int64_t* seg_grad, int64_t* seg_ag);
 
@@ -315,13 +325,14 @@ void spngd_opt_destroy(spngd_opt* opt);
  *   which 0 act capture, 1 grad capture, 2 dW (this rank's shard-mean grad,
  *   g x a or 2c), 3 W (g x a, or gamma|beta 2c), 4 V, 5 bn gg (M x c),
  *   6 bn gb, 7 A_inv dense, 8 G_inv dense, 9 A packed (reduced), 10 G packed,
- *   11 BN moments 3c (reduced), 12 the whole weight all-gather buffer
+ *   11 BN moments 3c (reduced; bn_mode 1: the packed 2c x 2c F), 12 the whole weight all-gather buffer
  *   (ld = its float count), 13 sampled-label grad capture (OneMC only,
  *   LayerCapture::grad_sampled, net.hpp:92), 14 / 15 sampled-label BN
  *   gamma / beta grads (OneMC only, bn_g*_sampled, net.hpp:96-97). NULL if the layer has no such buffer or this
  *   rank does not own it.  The step keeps only the triangular factors
  *   T = chol(X + dI)^-1 (it preconditions with T^T T directly), so 7 / 8
- *   form (X + dI)^-1 = T^T T on the call (one GEMM, synchronous). */
+ *   form (X + dI)^-1 = T^T T on the call (one GEMM, synchronous); for a
+ *   BN layer in bn_mode 1, 7 is (F + lambda I)^-1 (2c x 2c, ld = ld). */
 float* spngd_opt_buffer(spngd_opt* opt, int layer, int which, int64_t* ld);
 int spngd_opt_owner(const spngd_opt* opt, int layer);
 /* One SP-NGD step over the resident inputs (accumulate_microsteps,
@@ -389,8 +400,6 @@ typedef struct spngd_ledger_row {
  * layer A then G, or F for BatchNorm); due == NULL means every statistic is
  * due.  flags: SPNGD_LEDGER_* bits.  Returns the row count (rows
  * are written while count <= cap) or a negative status. */
-#define SPNGD_LEDGER_BN_FULL 1 /* F payload is the 2c x 2c packed block (BnMode::FullBlockDiag2c) */
-#define SPNGD_LEDGER_SGD 2     /* OptimizerConfig::sgd: no statistics (plan_statistics returns none) */
 int64_t spngd_ledger_step_rows(const spngd_layer_desc* layers, int n_layers, int world, int64_t step,
                                const unsigned char* due, int elem_size, int flags,
                                spngd_ledger_row* out, int64_t cap);

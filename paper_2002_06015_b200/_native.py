@@ -77,7 +77,7 @@ class LayoutEntry(C.Structure):
 class OptConfig(C.Structure):
     _fields_ = [("lambda_", C.c_double), ("rescale", C.c_int32), ("stale", C.c_int32),
                 ("stale_alpha", C.c_double), ("batch", _i64), ("fisher_mode", C.c_int32),
-                ("elem_size", C.c_int32), ("sgd", C.c_int32), ("pad_", C.c_int32)]
+                ("elem_size", C.c_int32), ("sgd", C.c_int32), ("bn_mode", C.c_int32)]
 
 
 class LedgerRowC(C.Structure):  # spngd_ledger_row
@@ -165,6 +165,8 @@ def _declare(L):
         "spngd_ctx_init_comm": (C.c_int, [P, C.c_int, C.c_int, P]),
         "spngd_reduce_scatter_mean": (C.c_int, [P, P, P, _i64]),
         "spngd_all_gather": (C.c_int, [P, P, P, _i64]),
+        "spngd_plan_layout_ex": (C.c_int, [C.POINTER(LayerDesc), C.c_int, C.c_int, C.c_int, C.POINTER(LayoutEntry),
+                                           C.POINTER(_i64), C.POINTER(_i64), C.POINTER(_i64)]),
         "spngd_plan_layout": (C.c_int, [C.POINTER(LayerDesc), C.c_int, C.c_int, C.POINTER(LayoutEntry),
                                         C.POINTER(_i64), C.POINTER(_i64), C.POINTER(_i64)]),
         "spngd_opt_create": (C.c_int, [P, C.POINTER(LayerDesc), C.c_int, C.POINTER(OptConfig),

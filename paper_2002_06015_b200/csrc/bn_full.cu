@@ -10,18 +10,12 @@
 #include <algorithm>
 #include <vector>
 
+#include "bn_full.cuh"
 #include "ctx.cuh"
 #include "factor.cuh"
 
 namespace spngd {
 namespace {
-
-struct InterleaveTask {
-  const float* gg;
-  const float* gb;
-  float* u;  // (hi - lo) x 2c
-  int64_t c, lo, hi;
-};
 
 __global__ void bn_interleave_kernel(const InterleaveTask* __restrict__ tasks) {
   const InterleaveTask t = tasks[blockIdx.y];
@@ -34,7 +28,12 @@ __global__ void bn_interleave_kernel(const InterleaveTask* __restrict__ tasks) {
   }
 }
 
-__global__ void bn_full_update_kernel(const spngd_bn_full_update_req* __restrict__ reqs, double eta, double momentum) {
+__global__ void bn_full_update_kernel(const spngd_bn_full_update_req* __restrict__ reqs, double eta, double momentum,
+                                      const float* __restrict__ scal) {
+  if (scal) {
+    eta = scal[0];
+    momentum = scal[1];
+  }
   const spngd_bn_full_update_req r = reqs[blockIdx.y];
   const int lane = threadIdx.x & 31;
   const int64_t dim = 2 * r.c;
@@ -67,6 +66,26 @@ __global__ void bn_full_update_kernel(const spngd_bn_full_update_req* __restrict
 }
 
 }  // namespace
+
+int launch_bn_interleave(spngd_ctx* ctx, const InterleaveTask* d_tasks, int n, int64_t max_total) {
+  if (n <= 0) return SPNGD_OK;
+  dim3 grid(unsigned(std::min<int64_t>(std::max<int64_t>((max_total + 255) / 256, 1), 1024)), unsigned(n));
+  bn_interleave_kernel<<<grid, 256, 0, ctx->stream>>>(d_tasks);
+  SPNGD_CUDA_TRY(cudaGetLastError());
+  ctx->launches++;
+  return SPNGD_OK;
+}
+
+int launch_bn_full_update(spngd_ctx* ctx, const spngd_bn_full_update_req* d_reqs, int n, int64_t max_dim, double eta,
+                          double momentum, const float* scal) {
+  if (n <= 0) return SPNGD_OK;
+  dim3 grid(unsigned(std::min<int64_t>((max_dim + 7) / 8, 1024)), unsigned(n));
+  bn_full_update_kernel<<<grid, 256, 0, ctx->stream>>>(d_reqs, eta, momentum, scal);
+  SPNGD_CUDA_TRY(cudaGetLastError());
+  ctx->launches++;
+  return SPNGD_OK;
+}
+
 }  // namespace spngd
 
 using namespace spngd;
@@ -92,10 +111,8 @@ extern "C" int spngd_bn_full_moments_batched(spngd_ctx* ctx, int n, const spngd_
     max_total = std::max(max_total, m * r.c);
   }
   auto* d_il = scratch.upload(il);
-  dim3 grid(unsigned(std::min<int64_t>((max_total + 255) / 256, 1024)), unsigned(n));
-  bn_interleave_kernel<<<grid, 256, 0, ctx->stream>>>(d_il);
-  SPNGD_CUDA_TRY(cudaGetLastError());
-  ctx->launches++;
+  int rc = launch_bn_interleave(ctx, d_il, n, max_total);
+  if (rc) return rc;
   return spngd_factor_sym_batched(ctx, n, fr.data());  // the SYRK engine, then sync
 }
 
@@ -116,9 +133,7 @@ extern "C" int spngd_bn_full_solve_update_batched(spngd_ctx* ctx, int n, const s
   DeviceScratch scratch(ctx);
   std::vector<spngd_bn_full_update_req> v(reqs, reqs + n);
   auto* d = scratch.upload(v);
-  dim3 grid(unsigned(std::min<int64_t>((max_dim + 7) / 8, 1024)), unsigned(n));
-  bn_full_update_kernel<<<grid, 256, 0, ctx->stream>>>(d, eta, momentum);
-  SPNGD_CUDA_TRY(cudaGetLastError());
-  ctx->launches++;
+  int rc = launch_bn_full_update(ctx, d, n, max_dim, eta, momentum, nullptr);
+  if (rc) return rc;
   return spngd_ctx_sync(ctx);
 }

@@ -31,6 +31,7 @@
 #include <numeric>
 #include <vector>
 
+#include "bn_full.cuh"
 #include "ctx.cuh"
 #include "factor.cuh"
 #include "inverse.cuh"
@@ -72,6 +73,11 @@ struct LayerState {
   float* Ainv = nullptr; int64_t lda = 0;   // recursion scratch; the inverse on request
   float* Ginv = nullptr; int64_t ldg = 0;
   float *tla = nullptr, *tua = nullptr, *tlg = nullptr, *tug = nullptr;  // T = L^-1 and T^T per factor
+  // BN full mode: interleaved per-sample u (B x 2c); owner: F + lambda I
+  // recursion scratch / inverse on request, its factors, T u scratch (2c)
+  float* u = nullptr;
+  float* Finv = nullptr; int64_t ldf = 0;
+  float *tlf = nullptr, *tuf = nullptr, *yf = nullptr;
 };
 
 // One stale-gated statistic (A:l, G:l or F:l).
@@ -158,6 +164,13 @@ struct spngd_opt {
   bool graphs_ready_ov = false;
   float* d_scal = nullptr;         // {eta, momentum} read by the update kernels
   std::vector<SgdTask> sgd_tasks; SgdTask* d_sgd = nullptr;  // cfg.sgd: owned layers' plain update
+  // cfg.bn_mode == 1 (full 2c x 2c BN blocks)
+  std::vector<InterleaveTask> ilv; InterleaveTask* d_ilv = nullptr; int64_t ilv_max = 0;
+  std::vector<UnpackTask> bnf_unpacks; UnpackTask* d_bnf_unpacks = nullptr; UnpackTask* d_bnf_unpacks_dyn = nullptr;
+  std::vector<int> bnf_layer;               // owned BN layers in bnf_unpacks / bnf_upd order
+  int64_t bnf_maxn = 0;
+  std::vector<spngd_bn_full_update_req> bnf_upd[2];  // T u, then T^T (T u) + update
+  spngd_bn_full_update_req* d_bnf_upd[2] = {};
   cudaGraph_t graphs[6] = {};
   cudaGraphExec_t graph_exec[6] = {};
   bool use_graph = true;
@@ -229,7 +242,8 @@ struct spngd_opt {
 
 namespace {
 
-double layer_cost(const spngd_layer_desc& d) {
+double layer_cost(const spngd_layer_desc& d, bool bn_full = false) {
+  if (d.kind == SPNGD_BN && bn_full) return 8.0 * double(d.g) * double(d.g) * double(d.g);  // (2c)^3 inverse
   if (d.kind == SPNGD_BN) return double(d.g);
   const double a = double(d.a), g = double(d.g);
   return a * a * a + g * g * g + 2 * g * g * a + 2 * g * a * a;
@@ -246,7 +260,9 @@ int wave_of(const spngd_layer_desc& d) {
 int build(spngd_opt* o, const spngd_layer_desc* descs, int n) {
   const int W = o->world;
   std::vector<spngd_layout_entry> lay(n);
-  int rc0 = spngd_plan_layout(descs, n, W, lay.data(), &o->seg_stat, &o->seg_grad, &o->seg_ag);
+  const bool bnf = o->cfg.bn_mode == 1;
+  int rc0 = spngd_plan_layout_ex(descs, n, W, bnf ? SPNGD_LEDGER_BN_FULL : 0, lay.data(), &o->seg_stat, &o->seg_grad,
+                                 &o->seg_ag);
   if (rc0) return rc0;
   o->layers.resize(n);
   for (int li = 0; li < n; ++li) {
@@ -295,9 +311,18 @@ int build(spngd_opt* o, const spngd_layer_desc* descs, int n) {
         L.gb_s = o->alloc(size_t(B * c));
         if (!L.gg_s || !L.gb_s) return fail(SPNGD_ERR_CUDA, "opt: capture allocation failed");
       }
-      o->bnm.push_back({one_mc ? L.gg_s : L.gg, one_mc ? L.gb_s : L.gb, c, 0, B, seg + L.off_M});
-      o->bnm_stat.push_back(add_stat(2, L.off_M, 3 * c, c));
-      o->bnm_maxc = std::max(o->bnm_maxc, c);
+      if (bnf) {  // build_bn_full: interleave, then the SYRK engine (FC layout, scale 1/B)
+        L.u = o->alloc(size_t(B * 2 * c));
+        if (!L.u) return fail(SPNGD_ERR_CUDA, "opt: capture allocation failed");
+        o->ilv.push_back({one_mc ? L.gg_s : L.gg, one_mc ? L.gb_s : L.gb, L.u, c, 0, B});
+        o->ilv_max = std::max(o->ilv_max, B * c);
+        freqs.push_back({L.u, 2 * c, 1, 0, 0, B, 1.0 / double(B), seg + L.off_M});
+        o->prob_stat.push_back(add_stat(2, L.off_M, (2 * c) * (2 * c + 1) / 2, 2 * c));
+      } else {
+        o->bnm.push_back({one_mc ? L.gg_s : L.gg, one_mc ? L.gb_s : L.gb, c, 0, B, seg + L.off_M});
+        o->bnm_stat.push_back(add_stat(2, L.off_M, 3 * c, c));
+        o->bnm_maxc = std::max(o->bnm_maxc, c);
+      }
     } else {
       const bool conv = L.d.kind == SPNGD_CONV;
       const int64_t hw = conv ? L.d.hw : 1;
@@ -322,6 +347,29 @@ int build(spngd_opt* o, const spngd_layer_desc* descs, int n) {
     if (L.d.kind == SPNGD_BN) {
       const int64_t c = L.d.g;
       L.V = o->alloc(size_t(2 * c), true);
+      if (bnf) {  // damp_bn_full: (F + lambda I)^-1 = T^T T by the batched Cholesky (fisher.cpp:248-253)
+        const int64_t d2 = 2 * c;
+        L.ldf = round_up(d2, 32);
+        L.Finv = o->alloc(size_t(d2 * L.ldf));
+        L.tlf = o->alloc(size_t(d2 * L.ldf), true);
+        L.tuf = o->alloc(size_t(d2 * L.ldf), true);
+        L.yf = o->alloc(size_t(d2), true);
+        if (!L.Finv || !L.tlf || !L.tuf || !L.yf || !L.V) return fail(SPNGD_ERR_CUDA, "opt: owner state allocation failed");
+        o->bnf_unpacks.push_back({o->rs_recv + L.off_M, d2, nullptr, float(o->cfg.lambda), 0, L.Finv, L.ldf});
+        o->bnf_layer.push_back(li);
+        o->bnf_maxn = std::max(o->bnf_maxn, d2);
+        mats.push_back({L.Finv, L.tlf, L.tuf, L.ldf, d2});
+        mat_layer.push_back(li);
+        // precondition_bn_full (fisher.cpp:278-296): v = T^T (T u), then the BN update
+        spngd_bn_full_update_req r0{}, r1{};
+        r0.finv = L.tlf; r0.ld = L.ldf; r0.grad = o->rs_recv + o->seg_stat + L.off_dW; r0.c = c;
+        r0.pg_out = L.yf; r0.pb_out = L.yf + c;
+        r1.finv = L.tuf; r1.ld = L.ldf; r1.grad = L.yf; r1.c = c;
+        r1.gamma = wseg + L.off_W; r1.beta = wseg + L.off_W + c; r1.vgamma = L.V; r1.vbeta = L.V + c;
+        o->bnf_upd[0].push_back(r0);
+        o->bnf_upd[1].push_back(r1);
+        continue;
+      }
       spngd_bn_update_req r{};
       r.m3c = o->rs_recv + L.off_M;
       r.grad = o->rs_recv + o->seg_stat + L.off_dW;
@@ -390,7 +438,7 @@ int build(spngd_opt* o, const spngd_layer_desc* descs, int n) {
   // inverse plans: one per matrix size class (owned matrices of equal n share
   // identical recursion schedules and batch into the same launches); classes
   // run concurrently on their own streams.
-  o->overlap_ok = !o->cfg.stale;
+  o->overlap_ok = !o->cfg.stale && o->cfg.bn_mode == 0;
   o->overlap_on = o->overlap_ok && getenv("SPNGD_NO_OVERLAP") == nullptr;
   {
     int least = 0, greatest = 0;
@@ -433,6 +481,12 @@ int build(spngd_opt* o, const spngd_layer_desc* descs, int n) {
   }
   o->d_scal = o->alloc(2);
   o->use_graph = getenv("SPNGD_NO_GRAPH") == nullptr;
+  if (bnf) {
+    o->d_ilv = dev_upload(o->ilv, own);
+    o->d_bnf_unpacks = dev_upload(o->bnf_unpacks, own);
+    if (o->cfg.stale) o->d_bnf_unpacks_dyn = dev_upload(o->bnf_unpacks, own);
+    for (int k = 0; k < 2; ++k) o->d_bnf_upd[k] = dev_upload(o->bnf_upd[k], own);
+  }
   if (o->cfg.sgd) {  // plain-gradient update over every owned layer (fisher.cpp:320-333, 348-356)
     for (int li = 0; li < n; ++li) {
       LayerState& L = o->layers[li];
@@ -544,17 +598,23 @@ extern "C" {
 
 int spngd_plan_layout(const spngd_layer_desc* descs, int n, int W, spngd_layout_entry* out, int64_t* seg_stat,
                       int64_t* seg_grad, int64_t* seg_ag) {
+  return spngd_plan_layout_ex(descs, n, W, 0, out, seg_stat, seg_grad, seg_ag);
+}
+
+int spngd_plan_layout_ex(const spngd_layer_desc* descs, int n, int W, int flags, spngd_layout_entry* out,
+                         int64_t* seg_stat, int64_t* seg_grad, int64_t* seg_ag) {
   if (!descs || !out || n <= 0 || W < 1) return fail(SPNGD_ERR_INVALID, "spngd_plan_layout: bad argument");
+  const bool bn_full = (flags & SPNGD_LEDGER_BN_FULL) != 0;
   // ownership: LPT on inverse + precondition cost, deterministic tie-break
   std::vector<int> order(n);
   std::iota(order.begin(), order.end(), 0);
   std::stable_sort(order.begin(), order.end(),
-                   [&](int x, int y) { return layer_cost(descs[x]) > layer_cost(descs[y]); });
+                   [&](int x, int y) { return layer_cost(descs[x], bn_full) > layer_cost(descs[y], bn_full); });
   std::vector<double> load(W, 0.0);
   for (int li : order) {
     const int r = int(std::min_element(load.begin(), load.end()) - load.begin());
     out[li].owner = r;
-    load[r] += layer_cost(descs[li]);
+    load[r] += layer_cost(descs[li], bn_full);
   }
   // owner-major segment layouts (statistics, gradients, weights), 64-float
   // aligned entries, in layer order
@@ -571,7 +631,7 @@ int spngd_plan_layout(const spngd_layer_desc* descs, int n, int W, spngd_layout_
     e.pad_ = 0;
     e.off_A = e.off_G = e.off_M = -1;
     if (d.kind == SPNGD_BN) {
-      e.off_M = place(st_fill[r], 3 * d.g);
+      e.off_M = place(st_fill[r], bn_full ? (2 * d.g) * (2 * d.g + 1) / 2 : 3 * d.g);
       e.off_dW = place(gr_fill[r], 2 * d.g);
       e.off_W = place(ag_fill[r], 2 * d.g);
     } else {
@@ -595,6 +655,7 @@ int spngd_opt_create(spngd_ctx* ctx, const spngd_layer_desc* layers, int n_layer
   if (cfg->stale && !(cfg->stale_alpha > 0.0)) return fail(SPNGD_ERR_INVALID, "spngd_opt_create: stale_alpha must be > 0");
   if (cfg->fisher_mode != 0 && cfg->fisher_mode != 1) return fail(SPNGD_ERR_INVALID, "spngd_opt_create: unknown fisher_mode");
   if (cfg->sgd && cfg->stale) return fail(SPNGD_ERR_INVALID, "spngd_opt_create: sgd has no statistics to gate");
+  if (cfg->bn_mode != 0 && cfg->bn_mode != 1) return fail(SPNGD_ERR_INVALID, "spngd_opt_create: unknown bn_mode");
   if (cfg->elem_size != 0 && cfg->elem_size != 2 && cfg->elem_size != 4 && cfg->elem_size != 8)
     return fail(SPNGD_ERR_INVALID, "spngd_opt_create: elem_size must be 2, 4 or 8");
   for (int i = 0; i < n_layers; ++i) {
@@ -640,6 +701,13 @@ float* spngd_opt_buffer(spngd_opt* o, int layer, int which, int64_t* ld) {
     case 5: return L.gg;
     case 6: return L.gb;
     case 7:  // the step keeps only T = L^-1: the inverse T^T T is formed on request
+      if (L.d.kind == SPNGD_BN) {
+        if (!mine || !L.Finv) return nullptr;
+        if (ld) *ld = L.ldf;
+        const DenseMatrix m{L.Finv, L.tlf, L.tuf, L.ldf, 2 * L.d.g};
+        return materialize_inverse(o->ctx, m) == SPNGD_OK ? L.Finv : nullptr;
+      }
+      [[fallthrough]];
     case 8: {
       const bool a = which == 7;
       if (ld) *ld = a ? L.lda : L.ldg;
@@ -671,7 +739,8 @@ int issue_phase(spngd_opt* o, int phase) {
   int rc = SPNGD_OK;
   switch (phase) {
     case 0:  // Stages 1-3 local part: factor SYRK into the RS send buffer.
-      rc = launch_repack(ctx, o->d_repack, int(o->fplan.repacks.size()), o->fplan.repack_max);
+      rc = launch_bn_interleave(ctx, o->d_ilv, int(o->ilv.size()), o->ilv_max);
+      if (!rc) rc = launch_repack(ctx, o->d_repack, int(o->fplan.repacks.size()), o->fplan.repack_max);
       if (rc) return rc;
       rc = launch_factor_gemm(ctx, o->fplan, o->d_fprobs, o->d_fhalf, o->d_fitems, int(o->fplan.items.size()),
                               o->d_partials, s);
@@ -694,6 +763,7 @@ int issue_phase(spngd_opt* o, int phase) {
                // fork onto their own streams and join.
       rc = launch_pi(ctx, o->d_pis, int(o->pis.size()));
       if (!rc) rc = launch_unpack(ctx, o->d_unpacks, int(o->unpacks.size()), o->max_n);
+      if (!rc) rc = launch_unpack(ctx, o->d_bnf_unpacks, int(o->bnf_unpacks.size()), o->bnf_maxn);
       if (rc) return rc;
       SPNGD_CUDA_TRY(cudaEventRecord(o->inv_fork, s));
       for (auto& c : o->inv) {
@@ -711,6 +781,8 @@ int issue_phase(spngd_opt* o, int phase) {
       rc = run_precondition(ctx, o->pplan, o->d_pp, o->d_pi, o->d_rescale, o->d_norms);
       if (!rc)
         rc = launch_bn_update(ctx, o->d_bnu, int(o->bnu.size()), o->bnu_maxc, o->cfg.lambda, 0.0, 0.0, o->d_scal);
+      for (int k = 0; k < 2 && !rc; ++k)
+        rc = launch_bn_full_update(ctx, o->d_bnf_upd[k], int(o->bnf_upd[k].size()), o->bnf_maxn, 0.0, 0.0, o->d_scal);
       return rc;
     case 5:  // Stage 5: AllGatherV of the updated weights (dist.cpp:646-663), in place.
       if (o->world > 1) rc = spngd_all_gather(ctx, o->ag + int64_t(o->rank) * o->seg_ag, o->ag, o->seg_ag);
@@ -846,7 +918,8 @@ int stale_partial_phase(spngd_opt* o, int phase) {
         if (due[o->prob_stat[w.problem]]) it.push_back(w);
       if ((rc = upload_async(ctx, o->d_repack_dyn, rp))) return rc;
       if ((rc = upload_async(ctx, o->d_fitems_dyn, it))) return rc;
-      rc = launch_repack(ctx, o->d_repack_dyn, int(rp.size()), o->fplan.repack_max);
+      rc = launch_bn_interleave(ctx, o->d_ilv, int(o->ilv.size()), o->ilv_max);  // full BN (cheap, all layers)
+      if (!rc) rc = launch_repack(ctx, o->d_repack_dyn, int(rp.size()), o->fplan.repack_max);
       if (!rc && !it.empty()) {
         rc = launch_factor_gemm(ctx, o->fplan, o->d_fprobs, o->d_fhalf, o->d_fitems_dyn, int(it.size()),
                                 o->d_partials, s);
@@ -883,9 +956,17 @@ int stale_partial_phase(spngd_opt* o, int phase) {
       return o->world > 1 ? comm_reduce_to_owners(ctx, ops) : SPNGD_OK;
     }
     case 3: {  // re-invert both factors of every owned layer with a refreshed A or G
+               // (and every refreshed full BN block, damp_bn_full at dist.cpp:583-584)
       std::vector<char> touched(o->layers.size(), 0);
       for (size_t q = 0; q < o->stats.size(); ++q)
-        if (due[q] && o->stats[q].kind != 2) touched[o->stats[q].layer] = 1;
+        if (due[q] && (o->stats[q].kind != 2 || o->cfg.bn_mode == 1)) touched[o->stats[q].layer] = 1;
+      std::vector<UnpackTask> bups;
+      for (size_t k = 0; k < o->bnf_layer.size(); ++k)
+        if (touched[o->bnf_layer[k]]) bups.push_back(o->bnf_unpacks[k]);
+      if (!bups.empty()) {
+        if ((rc = upload_async(ctx, o->d_bnf_unpacks_dyn, bups))) return rc;
+        if ((rc = launch_unpack(ctx, o->d_bnf_unpacks_dyn, int(bups.size()), o->bnf_maxn))) return rc;
+      }
       std::vector<PiTask> pis;
       std::vector<UnpackTask> ups;
       for (size_t k = 0; k < o->pi_layer.size(); ++k)
@@ -894,12 +975,14 @@ int stale_partial_phase(spngd_opt* o, int phase) {
           ups.push_back(o->unpacks[2 * k]);
           ups.push_back(o->unpacks[2 * k + 1]);
         }
-      if (pis.empty()) return SPNGD_OK;
-      if ((rc = upload_async(ctx, o->d_pis_dyn, pis))) return rc;
-      if ((rc = upload_async(ctx, o->d_unpacks_dyn, ups))) return rc;
-      rc = launch_pi(ctx, o->d_pis_dyn, int(pis.size()));
-      if (!rc) rc = launch_unpack(ctx, o->d_unpacks_dyn, int(ups.size()), o->max_n);
-      if (rc) return rc;
+      if (pis.empty() && bups.empty()) return SPNGD_OK;
+      if (!pis.empty()) {
+        if ((rc = upload_async(ctx, o->d_pis_dyn, pis))) return rc;
+        if ((rc = upload_async(ctx, o->d_unpacks_dyn, ups))) return rc;
+        rc = launch_pi(ctx, o->d_pis_dyn, int(pis.size()));
+        if (!rc) rc = launch_unpack(ctx, o->d_unpacks_dyn, int(ups.size()), o->max_n);
+        if (rc) return rc;
+      }
       SPNGD_CUDA_TRY(cudaEventRecord(o->inv_fork, s));
       for (auto& c : o->inv) {
         std::vector<DenseMatrix> sub;
@@ -943,7 +1026,7 @@ int stale_similarity(spngd_opt* o, int64_t step) {
       r.x1 = st.nsnap >= 1 ? st.snap[st.first] : nullptr;
       r.x2 = st.nsnap >= 2 ? st.snap[st.first ^ 1] : nullptr;
       r.n = st.dim;
-      r.kind = st.kind == 2 ? 1 : 0;
+      r.kind = (st.kind == 2 && o->cfg.bn_mode == 0) ? 1 : 0;  // full BN blocks are packed symmetric
       r.out4 = o->d_dist + 4 * q;
       reqs.push_back(r);
       max_rows = std::max(max_rows, r.kind == 0 ? r.n : (3 * r.n + 255) / 256);
@@ -1003,7 +1086,7 @@ int spngd_opt_step(spngd_opt* o, int64_t step, double eta, double momentum) {
   {  // CommLedger rows of this step (dist.cpp:511-537, 661-662) and NCCL bytes
     const unsigned char* due = o->cfg.stale ? reinterpret_cast<const unsigned char*>(o->due.data()) : nullptr;
     const int nl = int(o->descs.size());
-    const int lf = o->cfg.sgd ? SPNGD_LEDGER_SGD : 0;
+    const int lf = (o->cfg.sgd ? SPNGD_LEDGER_SGD : 0) | (o->cfg.bn_mode == 1 ? SPNGD_LEDGER_BN_FULL : 0);
     const int64_t nrows = spngd_ledger_step_rows(o->descs.data(), nl, o->world, step, due, o->cfg.elem_size, lf,
                                                  nullptr, 0);
     if (nrows < 0) return int(-nrows);

@@ -18,7 +18,8 @@ from .workloads import Layer
 
 (ACT, GRAD, DW, W, V, BN_GG, BN_GB, AINV, GINV, A_PACKED, G_PACKED, BN_M3C, ALL_WEIGHTS,
  GRAD_SAMPLED, BN_GG_SAMPLED, BN_GB_SAMPLED) = range(16)
-EMPIRICAL, ONE_MC = 0, 1  # FisherMode (fisher.hpp:18-21)
+EMPIRICAL, ONE_MC = 0, 1  # FisherMode (fisher.hpp:14)
+BN_UNIT, BN_FULL = 0, 1   # BnMode (fisher.hpp:18)
 PHASES = ["factor_gemm", "factor_reduce_bn", "reduce_scatter", "inverse", "precondition_update", "all_gather"]
 
 
@@ -67,9 +68,9 @@ class Optimizer:
     def __init__(self, layers: List[Layer], batch: int, lam: float = 2.5e-4, rescale: bool = True,
                  device: int = 0, world: int = 1, rank: int = 0, nccl_id: Optional[bytes] = None,
                  stream=None, stale: bool = False, stale_alpha: float = 0.1, fisher_mode: int = EMPIRICAL,
-                 elem_size: int = 4, sgd: bool = False):
+                 elem_size: int = 4, sgd: bool = False, bn_mode: int = 0):
         self.layers, self.batch, self.lam = layers, batch, lam
-        self.fisher_mode, self.sgd = fisher_mode, sgd
+        self.fisher_mode, self.sgd, self.bn_mode = fisher_mode, sgd, bn_mode
         self.world, self.rank, self.device = world, rank, device
         L = N.lib()
         self.ctx = C.c_void_p()
@@ -77,7 +78,7 @@ class Optimizer:
         if world > 1:
             check(L.spngd_ctx_init_comm(self.ctx, world, rank, C.create_string_buffer(nccl_id, 128)))
         arr = layer_descs(layers)
-        cfg = N.OptConfig(lam, int(rescale), int(stale), stale_alpha, batch, int(fisher_mode), int(elem_size), int(sgd), 0)
+        cfg = N.OptConfig(lam, int(rescale), int(stale), stale_alpha, batch, int(fisher_mode), int(elem_size), int(sgd), int(bn_mode))
         self.h = C.c_void_p()
         check(L.spngd_opt_create(self.ctx, arr, len(layers), C.byref(cfg), C.byref(self.h)))
 
@@ -112,7 +113,7 @@ class Optimizer:
         if which == G_PACKED:
             return l.g * (l.g + 1) // 2
         if which == BN_M3C:
-            return 3 * l.g
+            return (2 * l.g) * (2 * l.g + 1) // 2 if self.bn_mode == BN_FULL else 3 * l.g
         raise ValueError(which)
 
     def ptr(self, li: int, which: int):
@@ -132,7 +133,8 @@ class Optimizer:
         if not p:
             raise ValueError(f"layer {li} buffer {which} not available on rank {self.rank}")
         if which in (AINV, GINV):
-            n = self.layers[li].a if which == AINV else self.layers[li].g
+            l = self.layers[li]
+            n = (2 * l.g if l.kind == "bn" else l.a) if which == AINV else l.g
             t = torch.empty(n, ld, dtype=torch.float32).pin_memory()
             check(N.lib().spngd_copy(self.ctx, C.c_void_p(t.data_ptr()), C.c_void_p(p), t.numel() * 4))
             self.sync()

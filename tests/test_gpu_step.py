@@ -158,3 +158,77 @@ def test_sgd_step(cuda_dev):
         assert opt.launch_count() == 1
     finally:
         opt.close()
+
+
+def test_accumulate_microsteps_equals_concatenated_batch(cuda_dev):
+    """accumulate_microsteps (dist.cpp:446-508) averages the per-micro shard
+    means of n equal micro-batches: mean_mi(1/m sum_{s in mi}) = 1/(n m) sum_all.
+    The device step therefore takes n micro-batches as one capture of n*m
+    samples in micro order (batch = n*m); here the oracle restates the
+    reference's per-micro accumulation literally and the step must match it."""
+    n_micro, m = 3, 4
+    layers = [W.conv(3, 8, 3, 1, 8), W.fc(8 * 64, 10)]
+    opt = Optimizer(layers, n_micro * m, lam=LAM)
+    try:
+        opt.synth(seed=9)
+        before = {li: {w: opt.download(li, w).numpy() for w in (ACT, GRAD, DW, WB, V)} for li in range(2)}
+        opt.step(1, ETA, MOM)
+        opt.sync()
+        for li, l in enumerate(layers):
+            b = before[li]
+            conv = l.kind == "conv"
+            hw = l.hw if conv else 1
+            act = b[ACT].astype(np.float64).reshape(n_micro * m * l.a, hw) if conv else \
+                b[ACT].astype(np.float64).reshape(n_micro * m, l.a)
+            grad = b[GRAD].astype(np.float64).reshape(n_micro * m * l.g, hw) if conv else \
+                b[GRAD].astype(np.float64).reshape(n_micro * m, l.g)
+            A = sum(O.factor_A(act, conv, l.a, hw, mi * m, (mi + 1) * m) for mi in range(n_micro)) / n_micro
+            G = sum(O.factor_G(grad, conv, l.g, hw, mi * m, (mi + 1) * m) for mi in range(n_micro)) / n_micro
+            _, Ai, Gi = O.damp_and_invert(A, G, l.a, l.g, LAM)
+            delta = O.kron_matvec(Gi, Ai, l.g, l.a, b[DW].astype(np.float64).reshape(l.g, l.a)).reshape(-1)
+            wn, _ = O.ngd_update(b[WB], delta, b[V], ETA, MOM)
+            wr, vr = O.rescale(wn, b[WB], l.g)
+            assert rel(opt.download(li, WB).numpy(), wr) <= 1e-4
+            assert rel(opt.download(li, V).numpy(), vr) <= 1e-4
+    finally:
+        opt.close()
+
+
+@pytest.mark.parametrize("stale", [False, True])
+def test_full_bn_mode_step(cuda_dev, stale):
+    """BnMode::FullBlockDiag2c inside the step (dist.cpp:572-586; build_bn_full,
+    damp_bn_full, precondition_bn_full + the BN update, fisher.cpp:187-216,
+    248-253, 278-296, 346-359): F from the interleaved per-sample pairs by the
+    SYRK engine, (F + lambda I)^-1 by the batched Cholesky, v = T^T (T u).
+    rel. Frobenius <= 1e-4 on F^-1, the updated gamma/beta and velocities."""
+    from paper_2002_06015_b200.step import AINV, BN_FULL, BN_M3C
+    layers = [W.conv(3, 16, 3, 1, 8), W.bn(16, 64), W.conv(16, 96, 3, 1, 8), W.bn(96, 64), W.fc(96, 10), W.bn(300)]
+    B = 24
+    opt = Optimizer(layers, B, lam=LAM, bn_mode=BN_FULL, stale=stale)
+    try:
+        opt.synth(seed=11)
+        bns = [li for li, l in enumerate(layers) if l.kind == "bn"]
+        before = {li: {w: opt.download(li, w).numpy() for w in (BN_GG, BN_GB, DW, WB, V)} for li in bns}
+        opt.step(1, ETA, MOM)
+        opt.sync()
+        for li in bns:
+            c, b = layers[li].g, before[li]
+            F = O.build_bn_full(b[BN_GG].reshape(B, c), b[BN_GB].reshape(B, c), 0, B)
+            got_F = opt.download(li, BN_M3C).numpy()
+            assert rel(got_F, F) <= 1e-5
+            finv = O.spd_inverse(F, 2 * c, LAM)
+            assert rel(opt.download(li, AINV).numpy(), O.unpack(finv, 2 * c)) <= 1e-4
+            g2 = b[DW].astype(np.float64)
+            pg, pb = O.precondition_bn_full(finv, g2[:c], g2[c:])
+            wo, vo = O.ngd_update(b[WB], np.concatenate([pg, pb]), b[V], ETA, MOM)
+            assert rel(opt.download(li, WB).numpy(), wo) <= 1e-4, li
+            assert rel(opt.download(li, V).numpy(), vo) <= 1e-4, li
+        ids = [r.statistic_id for r in opt.ledger().rows() if r.statistic_id.startswith("F:")]
+        assert ids == ["F:1", "F:3", "F:5"]
+        if stale:  # steps 2, 3 refresh (Fibonacci 1, 2, 3), 4 does not: every path runs
+            for step in (2, 3, 4):
+                opt.step(step, ETA, MOM)
+            opt.sync()
+            assert all(np.isfinite(opt.download(li, WB).numpy()).all() for li in bns)
+    finally:
+        opt.close()
