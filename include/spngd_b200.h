@@ -289,6 +289,11 @@ typedef struct spngd_opt_config {
                         * fisher.cpp:187-216) through the SYRK engine, (F + lambda I)^-1 by
                         * the batched Cholesky (damp_bn_full, :248-253), precondition_bn_full
                         * + BN update (:278-296, 346-359); the wave overlap is off */
+  int32_t wgrad;       /* 1: the step also forms this rank's shard-mean gradients from the
+                        * captures (grad_payload, dist.cpp:315-391: Conv sum_s G_s A_s^T / m,
+                        * FC grad^T act / m on the SYRK engine's operands, BN column means)
+                        * into buffer 2 before the reduce-scatter; 0: buffer 2 is an input */
+  int32_t pad_;
 } spngd_opt_config;
 
 /* Host-only planning of the hybrid schedule (no GPU needed): layer owners

@@ -77,7 +77,8 @@ class LayoutEntry(C.Structure):
 class OptConfig(C.Structure):
     _fields_ = [("lambda_", C.c_double), ("rescale", C.c_int32), ("stale", C.c_int32),
                 ("stale_alpha", C.c_double), ("batch", _i64), ("fisher_mode", C.c_int32),
-                ("elem_size", C.c_int32), ("sgd", C.c_int32), ("bn_mode", C.c_int32)]
+                ("elem_size", C.c_int32), ("sgd", C.c_int32), ("bn_mode", C.c_int32),
+                ("wgrad", C.c_int32), ("pad_", C.c_int32)]
 
 
 class LedgerRowC(C.Structure):  # spngd_ledger_row

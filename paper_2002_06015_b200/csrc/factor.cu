@@ -39,6 +39,20 @@ __global__ void bn_moments_kernel(const spngd_bn_moments_req* __restrict__ reqs)
   r.out3c[3 * ch + 2] = float(sbb * inv_n);
 }
 
+// BN branch of grad_payload (dist.cpp:364-371): [sum_s g_gamma / m | sum_s g_beta / m].
+__global__ void bn_grad_payload_kernel(const BnGradPayloadTask* __restrict__ tasks) {
+  const BnGradPayloadTask t = tasks[blockIdx.y];
+  const int64_t ch = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (ch >= t.c) return;
+  double sg = 0.0, sb = 0.0;
+  for (int64_t s = 0; s < t.m; ++s) {
+    sg += t.gg[s * t.c + ch];
+    sb += t.gb[s * t.c + ch];
+  }
+  t.out[ch] = float(sg / double(t.m));
+  t.out[t.c + ch] = float(sb / double(t.m));
+}
+
 // X'[i][s*hw + p] = X[(s*dim + i)*hw + p]: coalesced reads, runs of hw writes.
 __global__ void repack_kernel(const RepackTask* __restrict__ tasks) {
   const RepackTask t = tasks[blockIdx.y];
@@ -185,6 +199,15 @@ int run_factors(spngd_ctx* ctx, const FactorPlan& plan, const GemmProblem* d_pro
   rc = launch_syrk_reduce(d_reduce, n_reduce, d_partials, ctx->stream);
   ctx->launches += n_reduce > 0;
   return rc;
+}
+
+int launch_bn_grad_payload(spngd_ctx* ctx, const BnGradPayloadTask* d_tasks, int n, int64_t max_c) {
+  if (n <= 0) return SPNGD_OK;
+  dim3 grid(unsigned((max_c + 255) / 256), unsigned(n));
+  bn_grad_payload_kernel<<<grid, 256, 0, ctx->stream>>>(d_tasks);
+  SPNGD_CUDA_TRY(cudaGetLastError());
+  ctx->launches++;
+  return SPNGD_OK;
 }
 
 int launch_bn_moments(spngd_ctx* ctx, const spngd_bn_moments_req* d_reqs, int n, int64_t max_c) {

@@ -41,4 +41,12 @@ int launch_factor_gemm(spngd_ctx* ctx, const FactorPlan& plan, const GemmProblem
                        cudaStream_t stream);
 int launch_bn_moments(spngd_ctx* ctx, const spngd_bn_moments_req* d_reqs, int n, int64_t max_c);
 
+struct BnGradPayloadTask {  // grad_payload's BN branch (dist.cpp:364-371)
+  const float* gg;
+  const float* gb;
+  int64_t m, c;
+  float* out;  // 2c: gamma then beta
+};
+int launch_bn_grad_payload(spngd_ctx* ctx, const BnGradPayloadTask* d_tasks, int n, int64_t max_c);
+
 }  // namespace spngd

@@ -76,6 +76,7 @@ struct LayerState {
   // BN full mode: interleaved per-sample u (B x 2c); owner: F + lambda I
   // recursion scratch / inverse on request, its factors, T u scratch (2c)
   float* u = nullptr;
+  int fa = -1, fg = -1;  // factor-plan problem indices of A and G (wgrad reuses their operands)
   float* Finv = nullptr; int64_t ldf = 0;
   float *tlf = nullptr, *tuf = nullptr, *yf = nullptr;
 };
@@ -168,6 +169,12 @@ struct spngd_opt {
   std::vector<InterleaveTask> ilv; InterleaveTask* d_ilv = nullptr; int64_t ilv_max = 0;
   std::vector<UnpackTask> bnf_unpacks; UnpackTask* d_bnf_unpacks = nullptr; UnpackTask* d_bnf_unpacks_dyn = nullptr;
   std::vector<int> bnf_layer;               // owned BN layers in bnf_unpacks / bnf_upd order
+  // cfg.wgrad: grad_payload on the device (dense GEMM over the factor operands + BN column means)
+  FactorPlan wplan;                         // OneMC: the true-label grad operands (G reads grad_sampled)
+  RepackTask* d_wrepack = nullptr;
+  std::vector<GemmProblem> wprobs; std::vector<GemmWorkItem> witems;
+  GemmProblem* d_wprobs = nullptr; GemmWorkItem* d_witems = nullptr; uint32_t wvariant = 0;
+  std::vector<BnGradPayloadTask> wbn; BnGradPayloadTask* d_wbn = nullptr; int64_t wbn_maxc = 0;
   int64_t bnf_maxn = 0;
   std::vector<spngd_bn_full_update_req> bnf_upd[2];  // T u, then T^T (T u) + update
   spngd_bn_full_update_req* d_bnf_upd[2] = {};
@@ -331,8 +338,10 @@ int build(spngd_opt* o, const spngd_layer_desc* descs, int n) {
       if (one_mc) L.grad_s = o->alloc(size_t(B * L.d.g * hw));  // factor_G(OneMC), fisher.cpp:127-132
       if (!L.act || !L.grad || (one_mc && !L.grad_s)) return fail(SPNGD_ERR_CUDA, "opt: capture allocation failed");
       const double nb = double(B);
+      L.fa = int(freqs.size());
       freqs.push_back({L.act, L.d.a, hw, conv ? 1 : 0, 0, B, conv ? 1.0 / (nb * double(hw)) : 1.0 / nb, seg + L.off_A});
       o->prob_stat.push_back(add_stat(0, L.off_A, L.d.a * (L.d.a + 1) / 2, L.d.a));
+      L.fg = int(freqs.size());
       freqs.push_back({one_mc ? L.grad_s : L.grad, L.d.g, hw, conv ? 1 : 0, 0, B, 1.0 / nb, seg + L.off_G});
       o->prob_stat.push_back(add_stat(1, L.off_G, L.d.g * (L.d.g + 1) / 2, L.d.g));
     }
@@ -432,6 +441,59 @@ int build(spngd_opt* o, const spngd_layer_desc* descs, int n) {
   o->d_freduce = dev_upload(o->fplan.reduce, own);
   o->d_fhalf = dev_upload(o->fplan.halfmaps, own);
   o->d_partials = o->alloc(size_t(std::max(o->fplan.n_slots, 1)) * kTileM * kTileN);
+  if (o->cfg.wgrad) {  // grad_payload (dist.cpp:315-391) -> this rank's gradient region
+    const bool one_mc = o->cfg.fisher_mode == 1;
+    std::vector<spngd_factor_req> wreqs;
+    std::vector<int> wl;
+    for (int li = 0; li < n; ++li) {
+      const LayerState& L = o->layers[li];
+      if (L.d.kind == SPNGD_BN || !one_mc) continue;
+      const bool conv = L.d.kind == SPNGD_CONV;
+      wreqs.push_back({L.grad, L.d.g, conv ? L.d.hw : 1, conv ? 1 : 0, 0, B, 1.0, o->d_partials});
+      wl.push_back(li);
+    }
+    if (!wreqs.empty()) {
+      FactorPlan wsz;
+      if ((rc = plan_factors(wreqs.data(), int(wreqs.size()), wsz))) return rc;
+      float* wws = o->alloc(wsz.repack_floats);
+      if ((rc = plan_factors(wreqs.data(), int(wreqs.size()), o->wplan, wws))) return rc;
+      o->d_wrepack = dev_upload(o->wplan.repacks, own);
+    }
+    int slot = 0;
+    for (int li = 0, k = 0; li < n; ++li) {
+      LayerState& L = o->layers[li];
+      float* dW = o->rs_send + int64_t(W) * o->seg_stat + int64_t(L.owner) * o->seg_grad + L.off_dW;
+      if (L.d.kind == SPNGD_BN) {
+        const float* gg = L.gg;  // grad_payload reads the true-label pair in either Fisher mode
+        o->wbn.push_back({gg, L.gb, B, L.d.g, dW});
+        o->wbn_maxc = std::max(o->wbn_maxc, L.d.g);
+        continue;
+      }
+      const GemmProblem& pa = o->fplan.probs[L.fa];
+      const GemmProblem& pg = one_mc ? o->wplan.probs[k++] : o->fplan.probs[L.fg];
+      if (pa.K != pg.K) return fail(SPNGD_ERR_SHAPE_MISMATCH, "wgrad: layer %d operands disagree on K", li);
+      GemmProblem p{};
+      p.A = pg.A;  // rows: output channels, K: samples x positions (conv: sum_s G_s A_s^T)
+      p.B = pa.A;  // rows: c_in k^2 / d_in
+      p.M = int32_t(L.d.g);
+      p.N = int32_t(L.d.a);
+      p.K = pa.K;
+      p.mode = EPI_DENSE;
+      p.alpha = float(1.0 / double(B));
+      p.beta = 0.f;
+      p.C = dW;
+      p.ldc = L.d.a;
+      plan_problem_tiles(int(o->wprobs.size()), p, false, p.K + kTileK, o->witems, nullptr, &slot, 0.0, nullptr);
+      o->wprobs.push_back(p);
+    }
+    std::stable_sort(o->witems.begin(), o->witems.end(), [](const GemmWorkItem& x, const GemmWorkItem& y) {
+      return (x.k1 - x.k0) > (y.k1 - y.k0);
+    });
+    o->wvariant = gemm_variant(o->wprobs.data(), int(o->wprobs.size()));
+    o->d_wprobs = dev_upload(o->wprobs, own);
+    o->d_witems = dev_upload(o->witems, own);
+    o->d_wbn = dev_upload(o->wbn, own);
+  }
   o->d_bnm = dev_upload(o->bnm, own);
   o->d_pis = dev_upload(o->pis, own);
   o->d_unpacks = dev_upload(o->unpacks, own);
@@ -731,6 +793,25 @@ float* spngd_opt_buffer(spngd_opt* o, int layer, int which, int64_t* ld) {
 
 namespace {
 
+// cfg.wgrad: this rank's shard-mean gradients from the captures (grad_payload,
+// dist.cpp:315-391) into the gradient region of the send buffer.  The dense
+// GEMMs read the factor plan's operands, so the factor repack must have run
+// (repack = true runs it here first).
+int issue_wgrad(spngd_opt* o, bool repack) {
+  if (!o->cfg.wgrad) return SPNGD_OK;
+  spngd_ctx* ctx = o->ctx;
+  int rc = SPNGD_OK;
+  if (repack) rc = launch_repack(ctx, o->d_repack, int(o->fplan.repacks.size()), o->fplan.repack_max);
+  if (!rc) rc = launch_repack(ctx, o->d_wrepack, int(o->wplan.repacks.size()), o->wplan.repack_max);
+  if (!rc && !o->witems.empty()) {
+    rc = launch_gemm(o->d_wprobs, o->d_witems, int(o->witems.size()), o->d_partials, ctx->d_status, ctx->stream,
+                     o->wvariant);
+    ctx->launches++;
+  }
+  if (!rc) rc = launch_bn_grad_payload(ctx, o->d_wbn, int(o->wbn.size()), o->wbn_maxc);
+  return rc;
+}
+
 // The six phases of one step.  Each phase is captured once into its own CUDA
 // graph; phase events are recorded between graph launches.
 int issue_phase(spngd_opt* o, int phase) {
@@ -741,6 +822,7 @@ int issue_phase(spngd_opt* o, int phase) {
     case 0:  // Stages 1-3 local part: factor SYRK into the RS send buffer.
       rc = launch_bn_interleave(ctx, o->d_ilv, int(o->ilv.size()), o->ilv_max);
       if (!rc) rc = launch_repack(ctx, o->d_repack, int(o->fplan.repacks.size()), o->fplan.repack_max);
+      if (!rc) rc = issue_wgrad(o, false);
       if (rc) return rc;
       rc = launch_factor_gemm(ctx, o->fplan, o->d_fprobs, o->d_fhalf, o->d_fitems, int(o->fplan.items.size()),
                               o->d_partials, s);
@@ -809,7 +891,9 @@ int issue_overlap(spngd_opt* o, bool capturing) {
   auto mark = [&](cudaEvent_t e) {
     return capturing ? cudaEventRecordWithFlags(e, s, cudaEventRecordExternal) : cudaEventRecord(e, s);
   };
-  int rc = SPNGD_OK;
+  int rc = launch_repack(ctx, o->d_repack, int(o->fplan.repacks.size()), o->fplan.repack_max);
+  if (!rc) rc = issue_wgrad(o, false);
+  if (rc) return rc;
   if (dist) {  // gradients: independent of the factors
     SPNGD_CUDA_TRY(cudaEventRecord(o->comm_fork, s));
     SPNGD_CUDA_TRY(cudaStreamWaitEvent(prep, o->comm_fork, 0));
@@ -819,8 +903,6 @@ int issue_overlap(spngd_opt* o, bool capturing) {
     ctx->stream = s;
     if (rc) return rc;
   }
-  rc = launch_repack(ctx, o->d_repack, int(o->fplan.repacks.size()), o->fplan.repack_max);
-  if (rc) return rc;
   const int nw = int(o->waves.size());
   for (int w = 0; w < nw; ++w) {
     spngd_opt::Wave& wv = o->waves[w];
@@ -919,7 +1001,11 @@ int stale_partial_phase(spngd_opt* o, int phase) {
       if ((rc = upload_async(ctx, o->d_repack_dyn, rp))) return rc;
       if ((rc = upload_async(ctx, o->d_fitems_dyn, it))) return rc;
       rc = launch_bn_interleave(ctx, o->d_ilv, int(o->ilv.size()), o->ilv_max);  // full BN (cheap, all layers)
-      if (!rc) rc = launch_repack(ctx, o->d_repack_dyn, int(rp.size()), o->fplan.repack_max);
+      if (o->cfg.wgrad) {  // every layer's gradient is due every step: full repack + grad_payload
+        if (!rc) rc = issue_wgrad(o, true);
+      } else if (!rc) {
+        rc = launch_repack(ctx, o->d_repack_dyn, int(rp.size()), o->fplan.repack_max);
+      }
       if (!rc && !it.empty()) {
         rc = launch_factor_gemm(ctx, o->fplan, o->d_fprobs, o->d_fhalf, o->d_fitems_dyn, int(it.size()),
                                 o->d_partials, s);
@@ -1114,7 +1200,9 @@ int spngd_opt_step(spngd_opt* o, int64_t step, double eta, double momentum) {
     for (int ph = 0; ph < 6; ++ph) {
       SPNGD_CUDA_TRY(cudaEventRecord(o->ev[ph], s));
       int rc = SPNGD_OK;
-      if (ph == 2 && o->world > 1)
+      if (ph == 0)
+        rc = issue_wgrad(o, true);
+      else if (ph == 2 && o->world > 1)
         rc = spngd_reduce_scatter_mean(ctx, o->rs_send + int64_t(o->world) * o->seg_stat, o->rs_recv + o->seg_stat,
                                        o->seg_grad);
       else if (ph == 4)
@@ -1137,7 +1225,7 @@ int spngd_opt_step(spngd_opt* o, int64_t step, double eta, double momentum) {
     const bool gated = ph <= 3 && !full;
     auto issue = [&](bool capturing) { return (ov && ph == 0) ? issue_overlap(o, capturing) : issue_phase(o, ph); };
     if (gated) {
-      if (any || ph == 2) {
+      if (any || ph == 2 || (ph == 0 && o->cfg.wgrad)) {
         int rc = stale_partial_phase(o, ph);
         if (rc) return rc;
       }

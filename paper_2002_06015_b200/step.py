@@ -68,7 +68,8 @@ class Optimizer:
     def __init__(self, layers: List[Layer], batch: int, lam: float = 2.5e-4, rescale: bool = True,
                  device: int = 0, world: int = 1, rank: int = 0, nccl_id: Optional[bytes] = None,
                  stream=None, stale: bool = False, stale_alpha: float = 0.1, fisher_mode: int = EMPIRICAL,
-                 elem_size: int = 4, sgd: bool = False, bn_mode: int = 0):
+                 elem_size: int = 4, sgd: bool = False, bn_mode: int = 0,
+                 wgrad: bool = False):
         self.layers, self.batch, self.lam = layers, batch, lam
         self.fisher_mode, self.sgd, self.bn_mode = fisher_mode, sgd, bn_mode
         self.world, self.rank, self.device = world, rank, device
@@ -78,7 +79,7 @@ class Optimizer:
         if world > 1:
             check(L.spngd_ctx_init_comm(self.ctx, world, rank, C.create_string_buffer(nccl_id, 128)))
         arr = layer_descs(layers)
-        cfg = N.OptConfig(lam, int(rescale), int(stale), stale_alpha, batch, int(fisher_mode), int(elem_size), int(sgd), int(bn_mode))
+        cfg = N.OptConfig(lam, int(rescale), int(stale), stale_alpha, batch, int(fisher_mode), int(elem_size), int(sgd), int(bn_mode), int(wgrad), 0)
         self.h = C.c_void_p()
         check(L.spngd_opt_create(self.ctx, arr, len(layers), C.byref(cfg), C.byref(self.h)))
 

@@ -232,3 +232,44 @@ def test_full_bn_mode_step(cuda_dev, stale):
             assert all(np.isfinite(opt.download(li, WB).numpy()).all() for li in bns)
     finally:
         opt.close()
+
+
+@pytest.mark.parametrize("fisher_mode", [EMPIRICAL, ONE_MC])
+def test_wgrad_in_step(cuda_dev, fisher_mode):
+    """cfg.wgrad: the step forms grad_payload itself
+    (dist.cpp:315-391: conv sum_s G_s A_s^T / m, FC grad^T act / m, BN column
+    means) from the true-label captures -- also under OneMC, where G reads the
+    sampled capture -- then preconditions with it.  rel. Frobenius <= 1e-5 on
+    dW (fp64 reference), <= 1e-4 on the updated weights."""
+    layers = [W.conv(3, 16, 3, 1, 10), W.bn(16, 100), W.conv(16, 32, 3, 2, 10), W.fc(32 * 25, 10)]
+    B = 12
+    opt = Optimizer(layers, B, lam=LAM, wgrad=True, fisher_mode=fisher_mode)
+    try:
+        opt.synth(seed=21)
+        ws = {li: [ACT, GRAD, WB, V] + ([GRAD_SAMPLED] if fisher_mode == ONE_MC else []) for li in (0, 2, 3)}
+        ws[1] = [BN_GG, BN_GB, WB, V] + ([BN_GG_SAMPLED, BN_GB_SAMPLED] if fisher_mode == ONE_MC else [])
+        before = {li: {w: opt.download(li, w).numpy() for w in ws[li]} for li in ws}
+        opt.step(1, ETA, MOM)
+        opt.sync()
+        for li, l in enumerate(layers):
+            b = before[li]
+            if l.kind == "bn":
+                c = l.g
+                want = np.concatenate([b[BN_GG].reshape(B, c).astype(np.float64).mean(0),
+                                       b[BN_GB].reshape(B, c).astype(np.float64).mean(0)])
+            elif l.kind == "conv":
+                act = b[ACT].astype(np.float64).reshape(B, l.a, l.hw)
+                grad = b[GRAD].astype(np.float64).reshape(B, l.g, l.hw)
+                want = np.einsum("sgp,sap->ga", grad, act).reshape(-1) / B
+            else:
+                act = b[ACT].astype(np.float64).reshape(B, l.a)
+                grad = b[GRAD].astype(np.float64).reshape(B, l.g)
+                want = (grad.T @ act).reshape(-1) / B
+            got = opt.download(li, DW).numpy()
+            assert rel(got, want) <= 1e-5, (li, rel(got, want))
+            b[DW] = want.astype(np.float32)
+            wo, vo = (oracle_bn if l.kind == "bn" else oracle_layer)(l, B, b)
+            assert rel(opt.download(li, WB).numpy(), wo) <= 1e-4, li
+            assert rel(opt.download(li, V).numpy(), vo) <= 1e-4, li
+    finally:
+        opt.close()
