@@ -39,6 +39,7 @@ def parse():
     p.add_argument("--config", default="resnet50", choices=["resnet50", "resnet18", "mlp"])
     p.add_argument("--e2e-steps", type=int, default=3)
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-raw-e2e", action="store_true")
     p.add_argument("--lam", type=float, default=2.5e-4)
     return p.parse_args()
 
@@ -168,11 +169,14 @@ def run_ours(args):
     from paper_2002_06015_b200.step import ALL_WEIGHTS, Comm, Optimizer, ACT, GRAD, DW, BN_GG, BN_GB
 
     layers, batch, desc = workload(args.config)
-    nccl_id = None
-    if world > 1:
+    def new_nccl_id():
+        if world == 1:
+            return None
         obj = [Comm.unique_id() if rank == 0 else None]
         pg.broadcast_object_list(obj, src=0)
-        nccl_id = obj[0]
+        return obj[0]
+
+    nccl_id = new_nccl_id()
     opt = Optimizer(layers, batch, lam=args.lam, device=local, world=world, rank=rank, nccl_id=nccl_id)
     opt.synth(seed=42)
     L = N.lib()
@@ -209,42 +213,60 @@ def run_ours(args):
         step_ms = float(t.item())
 
     # ---- e2e through the public API with host-resident inputs (pinned) ----
-    bufs = []  # (device ptr, host ptr, bytes)
-    for li, l in enumerate(layers):
-        whichs = [BN_GG, BN_GB, DW] if l.kind == "bn" else [ACT, GRAD, DW]
-        for w in whichs:
-            p, _ = opt.ptr(li, w)
-            nbytes = opt.numel(li, w) * 4
+    def measure_e2e(o, step0):
+        bufs = []  # (device ptr, host ptr, bytes)
+        for li, w in o.input_buffers():
+            p, _ = o.ptr(li, w)
+            nbytes = o.numel(li, w) * 4
             hp = C.c_void_p()
             check(L.spngd_host_alloc(C.byref(hp), nbytes))
-            check(L.spngd_copy(opt.ctx, hp, C.c_void_p(p), nbytes))
+            check(L.spngd_copy(o.ctx, hp, C.c_void_p(p), nbytes))
             bufs.append((p, hp, nbytes))
-    wp, wcount = opt.ptr(0, ALL_WEIGHTS)
-    out_bytes = wcount * 4
-    hw_out = C.c_void_p()
-    check(L.spngd_host_alloc(C.byref(hw_out), out_bytes))
-    opt.sync()
-    h2d = sum(b for _, _, b in bufs)
-    e2e_ms = []
-    for s in range(args.e2e_steps):
-        barrier()
-        ev2 = (C.c_void_p * 2)()
-        check(L.spngd_event_time(opt.ctx, ev2, 0, C.byref(ms)))
-        for p, hp, nb in bufs:
-            check(L.spngd_copy(opt.ctx, C.c_void_p(p), hp, nb))
-        opt.step(args.warmup + args.steps + s + 1)
-        check(L.spngd_copy(opt.ctx, hw_out, C.c_void_p(wp), out_bytes))
-        check(L.spngd_event_time(opt.ctx, ev2, 1, C.byref(ms)))
-        e2e_ms.append(ms.value)
-    opt.sync()
-    e2e = sorted(e2e_ms)[len(e2e_ms) // 2] if e2e_ms else float("nan")
-    if pg:
-        t = torch.tensor([e2e], dtype=torch.float64)
-        pg.all_reduce(t, op=pg.ReduceOp.MAX)
-        e2e = float(t.item())
-    for _, hp, _ in bufs:
-        L.spngd_host_free(hp)
-    L.spngd_host_free(hw_out)
+        wp, wcount = o.ptr(0, ALL_WEIGHTS)
+        out_bytes = wcount * 4
+        hw_out = C.c_void_p()
+        check(L.spngd_host_alloc(C.byref(hw_out), out_bytes))
+        o.sync()
+        h2d = sum(b for _, _, b in bufs)
+        times = []
+        for s in range(args.e2e_steps):
+            barrier()
+            ev2 = (C.c_void_p * 2)()
+            check(L.spngd_event_time(o.ctx, ev2, 0, C.byref(ms)))
+            for p, hp, nb in bufs:
+                check(L.spngd_copy(o.ctx, C.c_void_p(p), hp, nb))
+            o.step(step0 + s)
+            check(L.spngd_copy(o.ctx, hw_out, C.c_void_p(wp), out_bytes))
+            check(L.spngd_event_time(o.ctx, ev2, 1, C.byref(ms)))
+            times.append(ms.value)
+        o.sync()
+        v = sorted(times)[len(times) // 2] if times else float("nan")
+        if pg:
+            t = torch.tensor([v], dtype=torch.float64)
+            pg.all_reduce(t, op=pg.ReduceOp.MAX)
+            v = float(t.item())
+        for _, hp, _ in bufs:
+            L.spngd_host_free(hp)
+        L.spngd_host_free(hw_out)
+        return v, h2d, out_bytes
+
+    e2e, h2d, out_bytes = measure_e2e(opt, args.warmup + args.steps + 1)
+    # Same step fed the raw conv inputs instead of the im2col captures (the
+    # device forms the captures, spngd_opt_enable_raw_inputs): fewer H2D bytes.
+    e2e_raw = None
+    if args.e2e_steps > 0 and any(l.kind == "conv" for l in layers) and not args.no_raw_e2e:
+        opt_r = Optimizer(layers, batch, lam=args.lam, device=local, world=world, rank=rank,
+                          nccl_id=new_nccl_id())
+        opt_r.enable_raw_inputs()
+        opt_r.synth(seed=42)
+        for s in range(args.warmup):
+            opt_r.step(s + 1)
+        opt_r.sync()
+        v, h2d_r, ob_r = measure_e2e(opt_r, args.warmup + 1)
+        e2e_raw = {"value": round(v, 3), "unit": UNIT, "h2d_bytes_per_step": h2d_r, "d2h_bytes_per_step": ob_r,
+                   "inputs": "raw conv layer inputs (B x c_in x h x w) expanded on the device by im2col "
+                             "(spngd_opt_enable_raw_inputs); 1x1 stride-1 inputs are the captures themselves"}
+        opt_r.close()
 
     # ---- phase-serial pass (single GPU): the factor SYRK launch alone, for
     # the roofline (in the overlapped schedule it shares the GPU with the
@@ -307,8 +329,9 @@ def run_ours(args):
             "schedule": "waves: inverse recursion of the largest factors runs on high-priority streams while the "
                         "remaining factor SYRKs run" + ("; per-wave owner reductions on a comm stream" if world > 1 else ""),
             "phase_serial": serial,
+            "e2e_raw_inputs": e2e_raw,
             "e2e": ({"value": round(e2e, 3), "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": out_bytes}
-                    if e2e_ms else None),
+                    if args.e2e_steps > 0 else None),
             "gpu_launches": launches * args.steps,
             "roofline": roofline,
             "cpu_baseline": cpu,

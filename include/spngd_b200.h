@@ -333,7 +333,8 @@ void spngd_opt_destroy(spngd_opt* opt);
  *   11 BN moments 3c (reduced; bn_mode 1: the packed 2c x 2c F), 12 the whole weight all-gather buffer
  *   (ld = its float count), 13 sampled-label grad capture (OneMC only,
  *   LayerCapture::grad_sampled, net.hpp:92), 14 / 15 sampled-label BN
- *   gamma / beta grads (OneMC only, bn_g*_sampled, net.hpp:96-97). NULL if the layer has no such buffer or this
+ *   gamma / beta grads (OneMC only, bn_g*_sampled, net.hpp:96-97), 16 raw
+ *   conv input B x c_in x h x w (after spngd_opt_enable_raw_inputs). NULL if the layer has no such buffer or this
  *   rank does not own it.  The step keeps only the triangular factors
  *   T = chol(X + dI)^-1 (it preconditions with T^T T directly), so 7 / 8
  *   form (X + dI)^-1 = T^T T on the call (one GEMM, synchronous); for a
@@ -417,6 +418,32 @@ int spngd_opt_ledger_clear(spngd_opt* opt);
  * owner-major segments as actually moved): reduce-scatter / owner reduces of
  * statistics, of gradients, and the all-gather.  0 at world == 1. */
 int spngd_opt_wire_bytes(const spngd_opt* opt, int64_t* stat_bytes, int64_t* grad_bytes, int64_t* ag_bytes);
+
+/* ---- raw layer inputs (first stage) ------------------------
+ * The reference's conv capture is im2col of the layer input, rows
+ * ch*k*k + ky*k + kx, columns oy*w_out + ox, zero in the padding (im2col,
+ * net.cpp:199-219; captured at net.cpp:287-307).  After this call the step
+ * takes the raw per-sample input B x c_in x h x w (buffer 16) of every conv
+ * layer and expands it on the device (one batched HBM-bound launch at the
+ * start of each step) into the capture the factor/wgrad GEMMs read.  1x1
+ * stride-1 unpadded convs need no expansion: their raw input IS the capture
+ * (buffer 16 == buffer 0), so host->device traffic and, for them, the
+ * expansion traffic drop to the raw tensor.  geoms[i] is read for conv layers
+ * only; c_in*k*k must equal a and h_out*w_out must equal hw (SHAPE_MISMATCH).
+ * Call once, before the first step. */
+typedef struct spngd_conv_geom {
+  int64_t c_in, h, w, k, stride, pad;
+} spngd_conv_geom;
+int spngd_opt_enable_raw_inputs(spngd_opt* opt, const spngd_conv_geom* geoms);
+/* Batched im2col alone (net.cpp:199-219) for `n` conv inputs, x: batch x
+ * c_in x h x w, out: batch x (c_in k k) x (h_out w_out), device pointers. */
+typedef struct spngd_im2col_req {
+  const float* x;
+  float* out;
+  int64_t batch;
+  spngd_conv_geom geom;
+} spngd_im2col_req;
+int spngd_im2col_batched(spngd_ctx* ctx, int n, const spngd_im2col_req* reqs);
 
 #ifdef __cplusplus
 }

@@ -81,6 +81,14 @@ class OptConfig(C.Structure):
                 ("wgrad", C.c_int32), ("pad_", C.c_int32)]
 
 
+class ConvGeom(C.Structure):  # spngd_conv_geom
+    _fields_ = [("c_in", _i64), ("h", _i64), ("w", _i64), ("k", _i64), ("stride", _i64), ("pad", _i64)]
+
+
+class Im2colReq(C.Structure):
+    _fields_ = [("x", C.c_void_p), ("out", C.c_void_p), ("batch", _i64), ("geom", ConvGeom)]
+
+
 class LedgerRowC(C.Structure):  # spngd_ledger_row
     _fields_ = [("step", _i64), ("stage", C.c_int32), ("collective", C.c_int32), ("id_kind", C.c_int32),
                 ("layer", C.c_int32), ("elements", _i64), ("bytes", _i64), ("skipped", C.c_int32),
@@ -183,6 +191,8 @@ def _declare(L):
                                            C.POINTER(C.c_int)]),
         "spngd_ledger_step_rows": (_i64, [C.POINTER(LayerDesc), C.c_int, C.c_int, _i64, C.POINTER(C.c_ubyte),
                                           C.c_int, C.c_int, C.POINTER(LedgerRowC), _i64]),
+        "spngd_opt_enable_raw_inputs": (C.c_int, [P, C.POINTER(ConvGeom)]),
+        "spngd_im2col_batched": (C.c_int, [P, C.c_int, C.POINTER(Im2colReq)]),
         "spngd_opt_ledger": (_i64, [P, C.POINTER(LedgerRowC), _i64]),
         "spngd_opt_ledger_clear": (C.c_int, [P]),
         "spngd_opt_wire_bytes": (C.c_int, [P, C.POINTER(_i64), C.POINTER(_i64), C.POINTER(_i64)]),

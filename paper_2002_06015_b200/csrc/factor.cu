@@ -39,6 +39,27 @@ __global__ void bn_moments_kernel(const spngd_bn_moments_req* __restrict__ reqs)
   r.out3c[3 * ch + 2] = float(sbb * inv_n);
 }
 
+// im2col (net.cpp:199-219) per sample: out[(s*rows + row)*hw + col], row =
+// ch*k*k + ky*k + kx, col = oy*wo + ox; coalesced writes, gathered reads that
+// hit L1/L2 k*k times.  HBM-bound: reads B*c*h*w, writes B*c*k*k*hw floats.
+__global__ void im2col_kernel(const spngd_im2col_req* __restrict__ reqs) {
+  const spngd_im2col_req r = reqs[blockIdx.y];
+  const spngd_conv_geom g = r.geom;
+  const int64_t ho = (g.h + 2 * g.pad - g.k) / g.stride + 1, wo = (g.w + 2 * g.pad - g.k) / g.stride + 1;
+  const int64_t kk = g.k * g.k, rows = g.c_in * kk, hw = ho * wo;
+  const int64_t total = r.batch * rows * hw;
+  for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < total; e += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t col = e % hw, rs = e / hw;
+    const int64_t row = rs % rows, s = rs / rows;
+    const int64_t ch = row / kk, kyx = row - ch * kk, ky = kyx / g.k, kx = kyx - ky * g.k;
+    const int64_t oy = col / wo, ox = col - oy * wo;
+    const int64_t iy = oy * g.stride + ky - g.pad, ix = ox * g.stride + kx - g.pad;
+    float v = 0.f;
+    if (iy >= 0 && iy < g.h && ix >= 0 && ix < g.w) v = __ldg(r.x + ((s * g.c_in + ch) * g.h + iy) * g.w + ix);
+    r.out[e] = v;
+  }
+}
+
 // BN branch of grad_payload (dist.cpp:364-371): [sum_s g_gamma / m | sum_s g_beta / m].
 __global__ void bn_grad_payload_kernel(const BnGradPayloadTask* __restrict__ tasks) {
   const BnGradPayloadTask t = tasks[blockIdx.y];
@@ -201,6 +222,25 @@ int run_factors(spngd_ctx* ctx, const FactorPlan& plan, const GemmProblem* d_pro
   return rc;
 }
 
+int launch_im2col(spngd_ctx* ctx, const spngd_im2col_req* d_reqs, int n) {
+  if (n <= 0) return SPNGD_OK;
+  dim3 grid(148u * 8u, unsigned(n));
+  im2col_kernel<<<grid, 256, 0, ctx->stream>>>(d_reqs);
+  SPNGD_CUDA_TRY(cudaGetLastError());
+  ctx->launches++;
+  return SPNGD_OK;
+}
+
+int check_conv_geom(const spngd_conv_geom& g, int64_t a, int64_t hw) {
+  if (g.c_in <= 0 || g.h <= 0 || g.w <= 0 || g.k <= 0 || g.stride <= 0 || g.pad < 0)
+    return fail(SPNGD_ERR_SHAPE_MISMATCH, "conv geometry must be positive");
+  const int64_t ho = (g.h + 2 * g.pad - g.k) / g.stride + 1, wo = (g.w + 2 * g.pad - g.k) / g.stride + 1;
+  if (ho <= 0 || wo <= 0) return fail(SPNGD_ERR_SHAPE_MISMATCH, "conv geometry: empty output");
+  if ((a >= 0 && g.c_in * g.k * g.k != a) || (hw >= 0 && ho * wo != hw))
+    return fail(SPNGD_ERR_SHAPE_MISMATCH, "conv geometry does not match the layer (a = c_in k^2, hw = h_out w_out)");
+  return SPNGD_OK;
+}
+
 int launch_bn_grad_payload(spngd_ctx* ctx, const BnGradPayloadTask* d_tasks, int n, int64_t max_c) {
   if (n <= 0) return SPNGD_OK;
   dim3 grid(unsigned((max_c + 255) / 256), unsigned(n));
@@ -265,4 +305,23 @@ extern "C" int spngd_bn_moments_batched(spngd_ctx* ctx, int n, const spngd_bn_mo
   if (rc) return rc;
   SPNGD_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
   return SPNGD_OK;
+}
+
+using namespace spngd;
+
+extern "C" int spngd_im2col_batched(spngd_ctx* ctx, int n, const spngd_im2col_req* reqs) {
+  if (!ctx || (n > 0 && !reqs)) return fail(SPNGD_ERR_INVALID, "spngd_im2col_batched: null argument");
+  if (n == 0) return SPNGD_OK;
+  for (int i = 0; i < n; ++i) {
+    if (!reqs[i].x || !reqs[i].out) return fail(SPNGD_ERR_INVALID, "im2col: null pointer");
+    if (reqs[i].batch <= 0) return fail(SPNGD_ERR_EMPTY_BATCH, "im2col: empty batch");
+    int rc = check_conv_geom(reqs[i].geom, -1, -1);
+    if (rc) return rc;
+  }
+  DeviceScratch scratch(ctx);
+  std::vector<spngd_im2col_req> v(reqs, reqs + n);
+  auto* d = scratch.upload(v);
+  int rc = launch_im2col(ctx, d, n);
+  if (rc) return rc;
+  return spngd_ctx_sync(ctx);
 }

@@ -48,5 +48,8 @@ struct BnGradPayloadTask {  // grad_payload's BN branch (dist.cpp:364-371)
   float* out;  // 2c: gamma then beta
 };
 int launch_bn_grad_payload(spngd_ctx* ctx, const BnGradPayloadTask* d_tasks, int n, int64_t max_c);
+int launch_im2col(spngd_ctx* ctx, const spngd_im2col_req* d_reqs, int n);
+// SHAPE_MISMATCH unless positive and (a, hw >= 0) c_in k^2 == a, h_out w_out == hw.
+int check_conv_geom(const spngd_conv_geom& g, int64_t a, int64_t hw);
 
 }  // namespace spngd

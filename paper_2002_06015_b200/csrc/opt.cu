@@ -76,6 +76,7 @@ struct LayerState {
   // BN full mode: interleaved per-sample u (B x 2c); owner: F + lambda I
   // recursion scratch / inverse on request, its factors, T u scratch (2c)
   float* u = nullptr;
+  float* raw = nullptr;  // raw conv input (enable_raw_inputs); == act for 1x1 stride-1 convs
   int fa = -1, fg = -1;  // factor-plan problem indices of A and G (wgrad reuses their operands)
   float* Finv = nullptr; int64_t ldf = 0;
   float *tlf = nullptr, *tuf = nullptr, *yf = nullptr;
@@ -169,6 +170,8 @@ struct spngd_opt {
   std::vector<InterleaveTask> ilv; InterleaveTask* d_ilv = nullptr; int64_t ilv_max = 0;
   std::vector<UnpackTask> bnf_unpacks; UnpackTask* d_bnf_unpacks = nullptr; UnpackTask* d_bnf_unpacks_dyn = nullptr;
   std::vector<int> bnf_layer;               // owned BN layers in bnf_unpacks / bnf_upd order
+  // raw conv inputs expanded by im2col at the start of each step
+  std::vector<spngd_im2col_req> i2c; spngd_im2col_req* d_i2c = nullptr; bool raw_inputs = false;
   // cfg.wgrad: grad_payload on the device (dense GEMM over the factor operands + BN column means)
   FactorPlan wplan;                         // OneMC: the true-label grad operands (G reads grad_sampled)
   RepackTask* d_wrepack = nullptr;
@@ -785,6 +788,7 @@ float* spngd_opt_buffer(spngd_opt* o, int layer, int which, int64_t* ld) {
     case 13: return L.grad_s;
     case 14: return L.gg_s;
     case 15: return L.gb_s;
+    case 16: return L.raw;
     default: return nullptr;
   }
 }
@@ -792,6 +796,11 @@ float* spngd_opt_buffer(spngd_opt* o, int layer, int which, int64_t* ld) {
 }  // extern "C"
 
 namespace {
+
+// Raw conv inputs -> the im2col captures the GEMMs read (net.cpp:199-219).
+int issue_inputs(spngd_opt* o) {
+  return launch_im2col(o->ctx, o->d_i2c, int(o->i2c.size()));
+}
 
 // cfg.wgrad: this rank's shard-mean gradients from the captures (grad_payload,
 // dist.cpp:315-391) into the gradient region of the send buffer.  The dense
@@ -820,7 +829,8 @@ int issue_phase(spngd_opt* o, int phase) {
   int rc = SPNGD_OK;
   switch (phase) {
     case 0:  // Stages 1-3 local part: factor SYRK into the RS send buffer.
-      rc = launch_bn_interleave(ctx, o->d_ilv, int(o->ilv.size()), o->ilv_max);
+      rc = issue_inputs(o);
+      if (!rc) rc = launch_bn_interleave(ctx, o->d_ilv, int(o->ilv.size()), o->ilv_max);
       if (!rc) rc = launch_repack(ctx, o->d_repack, int(o->fplan.repacks.size()), o->fplan.repack_max);
       if (!rc) rc = issue_wgrad(o, false);
       if (rc) return rc;
@@ -891,7 +901,8 @@ int issue_overlap(spngd_opt* o, bool capturing) {
   auto mark = [&](cudaEvent_t e) {
     return capturing ? cudaEventRecordWithFlags(e, s, cudaEventRecordExternal) : cudaEventRecord(e, s);
   };
-  int rc = launch_repack(ctx, o->d_repack, int(o->fplan.repacks.size()), o->fplan.repack_max);
+  int rc = issue_inputs(o);
+  if (!rc) rc = launch_repack(ctx, o->d_repack, int(o->fplan.repacks.size()), o->fplan.repack_max);
   if (!rc) rc = issue_wgrad(o, false);
   if (rc) return rc;
   if (dist) {  // gradients: independent of the factors
@@ -1000,7 +1011,8 @@ int stale_partial_phase(spngd_opt* o, int phase) {
         if (due[o->prob_stat[w.problem]]) it.push_back(w);
       if ((rc = upload_async(ctx, o->d_repack_dyn, rp))) return rc;
       if ((rc = upload_async(ctx, o->d_fitems_dyn, it))) return rc;
-      rc = launch_bn_interleave(ctx, o->d_ilv, int(o->ilv.size()), o->ilv_max);  // full BN (cheap, all layers)
+      rc = issue_inputs(o);  // every conv capture (cheap next to the refresh; wgrad needs them all)
+      if (!rc) rc = launch_bn_interleave(ctx, o->d_ilv, int(o->ilv.size()), o->ilv_max);  // full BN (cheap, all layers)
       if (o->cfg.wgrad) {  // every layer's gradient is due every step: full repack + grad_payload
         if (!rc) rc = issue_wgrad(o, true);
       } else if (!rc) {
@@ -1200,9 +1212,10 @@ int spngd_opt_step(spngd_opt* o, int64_t step, double eta, double momentum) {
     for (int ph = 0; ph < 6; ++ph) {
       SPNGD_CUDA_TRY(cudaEventRecord(o->ev[ph], s));
       int rc = SPNGD_OK;
-      if (ph == 0)
-        rc = issue_wgrad(o, true);
-      else if (ph == 2 && o->world > 1)
+      if (ph == 0 && o->cfg.wgrad) {
+        rc = issue_inputs(o);
+        if (!rc) rc = issue_wgrad(o, true);
+      } else if (ph == 2 && o->world > 1)
         rc = spngd_reduce_scatter_mean(ctx, o->rs_send + int64_t(o->world) * o->seg_stat, o->rs_recv + o->seg_stat,
                                        o->seg_grad);
       else if (ph == 4)
@@ -1323,6 +1336,32 @@ int64_t spngd_opt_ledger(const spngd_opt* o, spngd_ledger_row* out, int64_t cap)
   if (out)
     for (int64_t i = 0; i < std::min(n, cap); ++i) out[i] = o->ledger[size_t(i)];
   return n;
+}
+
+int spngd_opt_enable_raw_inputs(spngd_opt* o, const spngd_conv_geom* geoms) {
+  if (!o || !geoms) return fail(SPNGD_ERR_INVALID, "spngd_opt_enable_raw_inputs: null argument");
+  if (o->raw_inputs) return fail(SPNGD_ERR_INVALID, "spngd_opt_enable_raw_inputs: already enabled");
+  if (o->graphs_ready || o->graphs_ready_ov || o->timed)
+    return fail(SPNGD_ERR_INVALID, "spngd_opt_enable_raw_inputs: call before the first step");
+  const int64_t B = o->cfg.batch;
+  for (size_t li = 0; li < o->layers.size(); ++li) {
+    LayerState& L = o->layers[li];
+    if (L.d.kind != SPNGD_CONV) continue;
+    const spngd_conv_geom& g = geoms[li];
+    int rc = check_conv_geom(g, L.d.a, L.d.hw);
+    if (rc) return rc;
+    if (g.k == 1 && g.stride == 1 && g.pad == 0) {  // the raw input is already the capture layout
+      L.raw = L.act;
+      continue;
+    }
+    L.raw = o->alloc(size_t(B * g.c_in * g.h * g.w));
+    if (!L.raw) return fail(SPNGD_ERR_CUDA, "opt: raw input allocation failed");
+    o->i2c.push_back({L.raw, L.act, B, g});
+  }
+  o->d_i2c = dev_upload(o->i2c, o->owned);
+  if (!o->i2c.empty() && !o->d_i2c) return fail(SPNGD_ERR_CUDA, "opt: upload failed");
+  o->raw_inputs = true;
+  return SPNGD_OK;
 }
 
 int spngd_opt_ledger_clear(spngd_opt* o) {

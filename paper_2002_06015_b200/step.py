@@ -17,7 +17,7 @@ from .spngd import check
 from .workloads import Layer
 
 (ACT, GRAD, DW, W, V, BN_GG, BN_GB, AINV, GINV, A_PACKED, G_PACKED, BN_M3C, ALL_WEIGHTS,
- GRAD_SAMPLED, BN_GG_SAMPLED, BN_GB_SAMPLED) = range(16)
+ GRAD_SAMPLED, BN_GG_SAMPLED, BN_GB_SAMPLED, RAW_ACT) = range(17)
 EMPIRICAL, ONE_MC = 0, 1  # FisherMode (fisher.hpp:14)
 BN_UNIT, BN_FULL = 0, 1   # BnMode (fisher.hpp:18)
 PHASES = ["factor_gemm", "factor_reduce_bn", "reduce_scatter", "inverse", "precondition_update", "all_gather"]
@@ -103,6 +103,8 @@ class Optimizer:
         l, B = self.layers[li], self.batch
         if which == ACT:
             return B * l.a * l.hw
+        if which == RAW_ACT:
+            return B * (l.c_in * l.h_in * l.w_in if l.kind == "conv" else l.a)
         if which in (GRAD, GRAD_SAMPLED):
             return B * l.g * l.hw
         if which in (DW, W, V):
@@ -182,7 +184,11 @@ class Optimizer:
                 check(L.spngd_synth_normal(self.ctx, C.c_void_p(w + 4 * l.g), l.g, 0, 0.0, 0.0, 0))  # beta = 0
                 continue
             act, _ = self.ptr(li, ACT)
-            if l.kind == "conv":
+            if l.kind == "conv" and getattr(self, "raw_inputs", False):
+                raw, _ = self.ptr(li, RAW_ACT)  # same counters as the capture kernel: im2col(raw) == capture
+                check(L.spngd_synth_normal(self.ctx, raw, B * l.c_in * l.h_in * l.w_in, _mix(seed, li, 0, r), 1.0, 0.0,
+                                           1))
+            elif l.kind == "conv":
                 check(L.spngd_synth_conv_capture(self.ctx, act, B, l.c_in, l.h_in, l.w_in, l.k, l.stride, l.pad,
                                                  _mix(seed, li, 0, r), 1, 1.0, 0.0))
             else:
@@ -211,6 +217,29 @@ class Optimizer:
         out = (C.c_float * 6)()
         check(N.lib().spngd_opt_phase_ms(self.h, out))
         return dict(zip(PHASES, list(out)))
+
+    def enable_raw_inputs(self):
+        """The step takes each conv layer's raw input (RAW_ACT, B x c_in x h x w)
+        and forms the im2col capture on the device (spngd_opt_enable_raw_inputs,
+        net.cpp:199-219).  Call before the first step."""
+        g = (N.ConvGeom * len(self.layers))()
+        for i, l in enumerate(self.layers):
+            if l.kind == "conv":
+                g[i] = N.ConvGeom(l.c_in, l.h_in, l.w_in, l.k, l.stride, l.pad)
+        check(N.lib().spngd_opt_enable_raw_inputs(self.h, g))
+        self.raw_inputs = True
+
+    def input_buffers(self):
+        """(layer, which) of every per-step input the host supplies: raw conv
+        inputs when enabled (else the im2col captures), grads, BN pairs, dW."""
+        out = []
+        for li, l in enumerate(self.layers):
+            if l.kind == "bn":
+                out += [(li, BN_GG), (li, BN_GB), (li, DW)]
+            else:
+                a = RAW_ACT if (getattr(self, "raw_inputs", False) and l.kind == "conv") else ACT
+                out += [(li, a), (li, GRAD), (li, DW)]
+        return out
 
     def ledger(self):
         """The CommLedger rows every step appended (dist.cpp:511-537, 661-662)."""

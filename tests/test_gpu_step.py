@@ -273,3 +273,41 @@ def test_wgrad_in_step(cuda_dev, fisher_mode):
             assert rel(opt.download(li, V).numpy(), vo) <= 1e-4, li
     finally:
         opt.close()
+
+
+def test_raw_inputs_step(cuda_dev):
+    """spngd_opt_enable_raw_inputs (first stage): the step takes
+    each conv layer's raw input and forms the reference im2col capture on the
+    device (net.cpp:199-219, padding, stride 2, 7x7 and the 1x1 alias case).
+    The captures must equal the oracle's im2col of the same raw tensor bit for
+    bit, and the step must match the oracle on them."""
+    from paper_2002_06015_b200.step import A_PACKED, RAW_ACT
+    layers = [W.conv(3, 8, 7, 2, 20), W.bn(8, 100), W.conv(8, 16, 3, 1, 10), W.conv(16, 32, 1, 1, 10),
+              W.conv(32, 16, 1, 2, 10), W.fc(16 * 25, 10)]
+    B = 6
+    opt = Optimizer(layers, B, lam=LAM)
+    try:
+        opt.enable_raw_inputs()
+        opt.synth(seed=31)
+        raws = {li: opt.download(li, RAW_ACT).numpy() for li, l in enumerate(layers) if l.kind == "conv"}
+        before = {li: {w: opt.download(li, w).numpy() for w in (GRAD, DW, WB, V)} for li in raws}
+        opt.step(1, ETA, MOM)
+        opt.sync()
+        for li, x in raws.items():
+            l = layers[li]
+            cap = np.concatenate([O.im2col(x.reshape(B, l.c_in * l.h_in * l.w_in)[s], l.c_in, l.h_in, l.w_in, l.k,
+                                           l.stride, l.pad) for s in range(B)])
+            got = opt.download(li, ACT).numpy().reshape(B * l.a, l.hw)
+            assert np.array_equal(got, cap.astype(np.float32)), li
+            A = O.factor_A(cap, True, l.a, l.hw, 0, B)
+            assert rel(opt.download(li, A_PACKED).numpy(), A) <= 1e-5, li
+            b = dict(before[li])
+            b[ACT] = cap.astype(np.float32).reshape(-1)
+            wo, vo = oracle_layer(l, B, b)
+            assert rel(opt.download(li, WB).numpy(), wo) <= 1e-4, li
+            assert rel(opt.download(li, V).numpy(), vo) <= 1e-4, li
+        # 1x1 stride-1 convs alias the capture (no expansion, no extra memory)
+        assert opt.ptr(3, RAW_ACT)[0] == opt.ptr(3, ACT)[0]
+        assert opt.ptr(4, RAW_ACT)[0] != opt.ptr(4, ACT)[0]
+    finally:
+        opt.close()
