@@ -229,14 +229,14 @@ def run_ours(args):
         o.sync()
         h2d = sum(b for _, _, b in bufs)
         times = []
+        ins = [(li, w, hp.value) for (li, w), (_, hp, _) in zip(o.input_buffers(), bufs)]
         for s in range(args.e2e_steps):
             barrier()
             ev2 = (C.c_void_p * 2)()
             check(L.spngd_event_time(o.ctx, ev2, 0, C.byref(ms)))
-            for p, hp, nb in bufs:
-                check(L.spngd_copy(o.ctx, C.c_void_p(p), hp, nb))
-            o.step(step0 + s)
-            check(L.spngd_copy(o.ctx, hw_out, C.c_void_p(wp), out_bytes))
+            # spngd_opt_step_host: H2D of this step's inputs (copy stream, wave
+            # order) overlapped with the step, D2H of the weights at the end
+            o.step_host(step0 + s, ins, hw_out.value)
             check(L.spngd_event_time(o.ctx, ev2, 1, C.byref(ms)))
             times.append(ms.value)
         o.sync()

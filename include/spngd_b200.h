@@ -345,6 +345,24 @@ int spngd_opt_owner(const spngd_opt* opt, int layer);
  * dist.cpp:406-675, n = 1 micro-step): factors + BN moments, RS, damped
  * inverse, precondition + update + rescale, BN solve + update, AG. */
 int spngd_opt_step(spngd_opt* opt, int64_t step, double eta, double momentum);
+/* The same step fed from HOST memory -- the reference's run_step takes host
+ * captures (dist.cpp:677-682).  `in` lists (layer, buffer which, host pointer)
+ * for the inputs to refresh: 0/16 activation capture / raw conv input, 1 / 13
+ * grad capture (true / sampled), 2 dW, 5 / 6 / 14 / 15 BN pairs; sizes are the
+ * buffers'.  Pinned host memory makes the copies asynchronous.  With the wave
+ * schedule the copies run on a copy stream, dW first, then each wave's
+ * captures, and wave w's im2col / repack / factor SYRK start as soon as its
+ * captures have landed, so the host->device transfer overlaps the step;
+ * otherwise they precede the step on its stream.  host_weights_out (optional,
+ * world * seg_ag floats = buffer 12's ld) receives every weight replica after
+ * the all-gather.  Asynchronous: spngd_ctx_sync before reading it. */
+typedef struct spngd_host_input {
+  int32_t layer;
+  int32_t which;
+  const void* host;
+} spngd_host_input;
+int spngd_opt_step_host(spngd_opt* opt, int64_t step, double eta, double momentum, const spngd_host_input* in,
+                        int n, float* host_weights_out);
 /* Wave schedule (no stale gating; on by default, env SPNGD_NO_OVERLAP=1
  * starts it off): layers are split into waves by their larger Kronecker
  * dimension, largest first, and each wave's damped-inverse recursion runs on

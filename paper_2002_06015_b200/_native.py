@@ -89,6 +89,10 @@ class Im2colReq(C.Structure):
     _fields_ = [("x", C.c_void_p), ("out", C.c_void_p), ("batch", _i64), ("geom", ConvGeom)]
 
 
+class HostInput(C.Structure):  # spngd_host_input
+    _fields_ = [("layer", C.c_int32), ("which", C.c_int32), ("host", C.c_void_p)]
+
+
 class LedgerRowC(C.Structure):  # spngd_ledger_row
     _fields_ = [("step", _i64), ("stage", C.c_int32), ("collective", C.c_int32), ("id_kind", C.c_int32),
                 ("layer", C.c_int32), ("elements", _i64), ("bytes", _i64), ("skipped", C.c_int32),
@@ -191,6 +195,8 @@ def _declare(L):
                                            C.POINTER(C.c_int)]),
         "spngd_ledger_step_rows": (_i64, [C.POINTER(LayerDesc), C.c_int, C.c_int, _i64, C.POINTER(C.c_ubyte),
                                           C.c_int, C.c_int, C.POINTER(LedgerRowC), _i64]),
+        "spngd_opt_step_host": (C.c_int, [P, _i64, C.c_double, C.c_double, C.POINTER(HostInput), C.c_int,
+                                           C.c_void_p]),
         "spngd_opt_enable_raw_inputs": (C.c_int, [P, C.POINTER(ConvGeom)]),
         "spngd_im2col_batched": (C.c_int, [P, C.c_int, C.POINTER(Im2colReq)]),
         "spngd_opt_ledger": (_i64, [P, C.POINTER(LedgerRowC), _i64]),

@@ -77,6 +77,7 @@ struct LayerState {
   // recursion scratch / inverse on request, its factors, T u scratch (2c)
   float* u = nullptr;
   float* raw = nullptr;  // raw conv input (enable_raw_inputs); == act for 1x1 stride-1 convs
+  int64_t raw_floats = 0;
   int fa = -1, fg = -1;  // factor-plan problem indices of A and G (wgrad reuses their operands)
   float* Finv = nullptr; int64_t ldf = 0;
   float *tlf = nullptr, *tuf = nullptr, *yf = nullptr;
@@ -154,10 +155,20 @@ struct spngd_opt {
     std::vector<OwnerReduce> owner_ops;  // world > 1: this wave's statistics -> their owners
     cudaEvent_t ready = nullptr;         // factors of this wave reduced locally
     cudaEvent_t fork = nullptr;          // owner-side inputs of this wave's recursion ready
+    // spngd_opt_step_host: this wave's captures arrive from the host on the
+    // copy stream; its im2col / repack run right before its SYRK
+    std::vector<RepackTask> repacks;
+    RepackTask* d_repacks = nullptr;
+    int64_t repack_max = 0;
+    std::vector<spngd_im2col_req> i2c;
+    spngd_im2col_req* d_i2c = nullptr;
+    cudaEvent_t in_ready = nullptr;
   };
   std::vector<Wave> waves;
   cudaStream_t comm_stream = nullptr;    // world > 1: NCCL + owner-side prep of the waves
   cudaEvent_t comm_fork = nullptr, comm_done = nullptr;
+  cudaStream_t h2d_stream = nullptr;     // spngd_opt_step_host: host inputs, wave by wave
+  cudaEvent_t h2d_start = nullptr, grads_ready = nullptr;
   bool overlap_ok = false;   // no stale gating
   bool overlap_on = false;
   int inv_prio = 0;          // greatest stream priority
@@ -228,7 +239,11 @@ struct spngd_opt {
       if (graph_ov_exec[i]) cudaGraphExecDestroy(graph_ov_exec[i]);
       if (graphs_ov[i]) cudaGraphDestroy(graphs_ov[i]);
     }
+    if (h2d_start) cudaEventDestroy(h2d_start);
+    if (grads_ready) cudaEventDestroy(grads_ready);
+    if (h2d_stream) cudaStreamDestroy(h2d_stream);
     for (auto& w : waves) {
+      if (w.in_ready) cudaEventDestroy(w.in_ready);
       if (w.fork) cudaEventDestroy(w.fork);
       if (w.ready) cudaEventDestroy(w.ready);
     }
@@ -615,7 +630,18 @@ int build(spngd_opt* o, const spngd_layer_desc* descs, int n) {
       SPNGD_CUDA_TRY(cudaEventCreateWithFlags(&o->comm_fork, cudaEventDisableTiming));
       SPNGD_CUDA_TRY(cudaEventCreateWithFlags(&o->comm_done, cudaEventDisableTiming));
     }
+    for (const auto& t : o->fplan.repacks) {  // per-wave repacks (host-input steps)
+      int q = -1;
+      for (size_t f = 0; f < freqs.size(); ++f)
+        if (freqs[f].x == t.src) q = o->prob_stat[f];
+      if (q < 0) return fail(SPNGD_ERR_INVALID, "opt: unmapped repack task");
+      spngd_opt::Wave& wv = o->waves[wave_of(o->layers[o->stats[q].layer].d)];
+      wv.repacks.push_back(t);
+      wv.repack_max = std::max(wv.repack_max, t.n * t.dim * t.hw);
+    }
     for (auto& wv : o->waves) {
+      wv.d_repacks = dev_upload(wv.repacks, own);
+      SPNGD_CUDA_TRY(cudaEventCreateWithFlags(&wv.in_ready, cudaEventDisableTiming));
       SPNGD_CUDA_TRY(cudaEventCreateWithFlags(&wv.ready, cudaEventDisableTiming));
       wv.d_items = dev_upload(wv.items, own);
       wv.d_reduce = dev_upload(wv.reduce, own);
@@ -893,7 +919,7 @@ int issue_phase(spngd_opt* o, int phase) {
 // on the main stream after the last wave's SYRK, after its reduction + BN
 // moments, and after the communication stream joins (external event nodes
 // when captured), so phase 3 is what the inverse adds beyond the rest.
-int issue_overlap(spngd_opt* o, bool capturing) {
+int issue_overlap(spngd_opt* o, bool capturing, bool host_in = false) {
   spngd_ctx* ctx = o->ctx;
   cudaStream_t s = ctx->stream;
   const bool dist = o->world > 1;
@@ -901,10 +927,13 @@ int issue_overlap(spngd_opt* o, bool capturing) {
   auto mark = [&](cudaEvent_t e) {
     return capturing ? cudaEventRecordWithFlags(e, s, cudaEventRecordExternal) : cudaEventRecord(e, s);
   };
-  int rc = issue_inputs(o);
-  if (!rc) rc = launch_repack(ctx, o->d_repack, int(o->fplan.repacks.size()), o->fplan.repack_max);
-  if (!rc) rc = issue_wgrad(o, false);
-  if (rc) return rc;
+  int rc = SPNGD_OK;
+  if (!host_in) {  // host-input steps expand / repack wave by wave as the captures land
+    rc = issue_inputs(o);
+    if (!rc) rc = launch_repack(ctx, o->d_repack, int(o->fplan.repacks.size()), o->fplan.repack_max);
+    if (!rc) rc = issue_wgrad(o, false);
+    if (rc) return rc;
+  }
   if (dist) {  // gradients: independent of the factors
     SPNGD_CUDA_TRY(cudaEventRecord(o->comm_fork, s));
     SPNGD_CUDA_TRY(cudaStreamWaitEvent(prep, o->comm_fork, 0));
@@ -918,6 +947,12 @@ int issue_overlap(spngd_opt* o, bool capturing) {
   for (int w = 0; w < nw; ++w) {
     spngd_opt::Wave& wv = o->waves[w];
     const bool last = w == nw - 1;
+    if (host_in) {
+      SPNGD_CUDA_TRY(cudaStreamWaitEvent(s, wv.in_ready, 0));
+      rc = launch_im2col(ctx, wv.d_i2c, int(wv.i2c.size()));
+      if (!rc) rc = launch_repack(ctx, wv.d_repacks, int(wv.repacks.size()), wv.repack_max);
+      if (rc) return rc;
+    }
     if (!wv.items.empty()) {
       rc = launch_factor_gemm(ctx, o->fplan, o->d_fprobs, o->d_fhalf, wv.d_items, int(wv.items.size()),
                               o->d_partials, s);
@@ -1154,10 +1189,11 @@ int stale_similarity(spngd_opt* o, int64_t step) {
 
 }  // namespace
 
-extern "C" {
+namespace {
 
-int spngd_opt_step(spngd_opt* o, int64_t step, double eta, double momentum) {
-  if (!o) return fail(SPNGD_ERR_INVALID, "spngd_opt_step: opt is NULL");
+// One step; host_in: the inputs arrive wave by wave on the copy stream
+// (spngd_opt_step_host) -- direct launches, no graphs, per-wave waits.
+int step_impl(spngd_opt* o, int64_t step, double eta, double momentum, bool host_in) {
   spngd_ctx* ctx = o->ctx;
   cudaStream_t s = ctx->stream;
   // Host scalars of this step -> device (outside the graphs).  Pageable
@@ -1230,19 +1266,21 @@ int spngd_opt_step(spngd_opt* o, int64_t step, double eta, double momentum) {
     return SPNGD_OK;
   }
   bool& ready = ov ? o->graphs_ready_ov : o->graphs_ready;
-  const bool capture = o->use_graph && !ready && full;
+  const bool capture = o->use_graph && !ready && full && !host_in;
   const int64_t l0 = ctx->launches;
   for (int ph = 0; ph < 6; ++ph) {
     if (ov && ph >= 1 && ph <= 3) continue;  // inside issue_overlap
     SPNGD_CUDA_TRY(cudaEventRecord(o->ev[ph], s));
     const bool gated = ph <= 3 && !full;
-    auto issue = [&](bool capturing) { return (ov && ph == 0) ? issue_overlap(o, capturing) : issue_phase(o, ph); };
+    auto issue = [&](bool capturing) {
+      return (ov && ph == 0) ? issue_overlap(o, capturing, host_in) : issue_phase(o, ph);
+    };
     if (gated) {
       if (any || ph == 2 || (ph == 0 && o->cfg.wgrad)) {
         int rc = stale_partial_phase(o, ph);
         if (rc) return rc;
       }
-    } else if (!o->use_graph || (!ready && !capture)) {
+    } else if (!o->use_graph || host_in || (!ready && !capture)) {
       int rc = issue(false);
       if (rc) return rc;
     } else {
@@ -1269,9 +1307,88 @@ int spngd_opt_step(spngd_opt* o, int64_t step, double eta, double momentum) {
     }
   }
   SPNGD_CUDA_TRY(cudaEventRecord(o->ev[6], s));
-  if (capture || !o->use_graph || !full) o->launches = ctx->launches - l0;
+  if (capture || !o->use_graph || !full || host_in) o->launches = ctx->launches - l0;
   if (capture) ready = true;
   o->timed = true;
+  return SPNGD_OK;
+}
+
+// Bytes of per-step input buffer `which` of layer L (0 if it has none).
+int64_t input_floats(const spngd_opt* o, const LayerState& L, int which) {
+  const int64_t B = o->cfg.batch;
+  const bool bn = L.d.kind == SPNGD_BN;
+  switch (which) {
+    case 0: return bn ? 0 : B * L.d.a * L.d.hw;
+    case 1: case 13: return bn ? 0 : B * L.d.g * L.d.hw;
+    case 2: return bn ? 2 * L.d.g : L.d.g * L.d.a;
+    case 5: case 6: case 14: case 15: return bn ? B * L.d.g : 0;
+    case 16: return L.raw ? L.raw_floats : 0;
+    default: return 0;
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+int spngd_opt_step(spngd_opt* o, int64_t step, double eta, double momentum) {
+  if (!o) return fail(SPNGD_ERR_INVALID, "spngd_opt_step: opt is NULL");
+  return step_impl(o, step, eta, momentum, false);
+}
+
+int spngd_opt_step_host(spngd_opt* o, int64_t step, double eta, double momentum, const spngd_host_input* in, int n,
+                        float* host_weights_out) {
+  if (!o || (n > 0 && !in)) return fail(SPNGD_ERR_INVALID, "spngd_opt_step_host: null argument");
+  spngd_ctx* ctx = o->ctx;
+  cudaStream_t s = ctx->stream;
+  struct Copy { float* dst; const void* src; int64_t bytes; int wave; };
+  std::vector<Copy> copies;
+  const bool pipelined = o->overlap_on && o->overlap_ok && !o->cfg.wgrad && !o->cfg.sgd && !o->waves.empty();
+  for (int i = 0; i < n; ++i) {
+    if (in[i].layer < 0 || in[i].layer >= int(o->layers.size()) || !in[i].host)
+      return fail(SPNGD_ERR_INVALID, "spngd_opt_step_host: bad input %d", i);
+    LayerState& L = o->layers[in[i].layer];
+    float* dst = spngd_opt_buffer(o, in[i].layer, in[i].which, nullptr);
+    const int64_t cnt = input_floats(o, L, in[i].which);
+    if (!dst || cnt <= 0) return fail(SPNGD_ERR_INVALID, "spngd_opt_step_host: layer %d has no input %d", in[i].layer,
+                                      in[i].which);
+    // dW first (the gradient reduce-scatter and every update need it), then
+    // the captures in wave order (wave_of, largest factors first)
+    const int wave = in[i].which == 2 ? -1 : (pipelined ? wave_of(L.d) : 0);
+    copies.push_back({dst, in[i].host, cnt * int64_t(sizeof(float)), wave});
+  }
+  std::stable_sort(copies.begin(), copies.end(), [](const Copy& x, const Copy& y) { return x.wave < y.wave; });
+  if (!pipelined) {  // same inputs, copied before the step on its stream
+    for (const Copy& c : copies) SPNGD_CUDA_TRY(cudaMemcpyAsync(c.dst, c.src, c.bytes, cudaMemcpyHostToDevice, s));
+    int rc = step_impl(o, step, eta, momentum, false);
+    if (rc) return rc;
+  } else {
+    if (!o->h2d_stream) {
+      SPNGD_CUDA_TRY(cudaStreamCreateWithFlags(&o->h2d_stream, cudaStreamNonBlocking));
+      SPNGD_CUDA_TRY(cudaEventCreateWithFlags(&o->h2d_start, cudaEventDisableTiming));
+      SPNGD_CUDA_TRY(cudaEventCreateWithFlags(&o->grads_ready, cudaEventDisableTiming));
+    }
+    // the copies overwrite inputs the previous step may still read
+    SPNGD_CUDA_TRY(cudaEventRecord(o->h2d_start, s));
+    SPNGD_CUDA_TRY(cudaStreamWaitEvent(o->h2d_stream, o->h2d_start, 0));
+    size_t i = 0;
+    for (; i < copies.size() && copies[i].wave < 0; ++i)
+      SPNGD_CUDA_TRY(cudaMemcpyAsync(copies[i].dst, copies[i].src, copies[i].bytes, cudaMemcpyHostToDevice,
+                                     o->h2d_stream));
+    SPNGD_CUDA_TRY(cudaEventRecord(o->grads_ready, o->h2d_stream));
+    for (int w = 0; w < int(o->waves.size()); ++w) {
+      for (; i < copies.size() && copies[i].wave == w; ++i)
+        SPNGD_CUDA_TRY(cudaMemcpyAsync(copies[i].dst, copies[i].src, copies[i].bytes, cudaMemcpyHostToDevice,
+                                       o->h2d_stream));
+      SPNGD_CUDA_TRY(cudaEventRecord(o->waves[w].in_ready, o->h2d_stream));
+    }
+    SPNGD_CUDA_TRY(cudaStreamWaitEvent(s, o->grads_ready, 0));
+    int rc = step_impl(o, step, eta, momentum, true);
+    if (rc) return rc;
+  }
+  if (host_weights_out)
+    SPNGD_CUDA_TRY(cudaMemcpyAsync(host_weights_out, o->ag,
+                                   size_t(o->world) * o->seg_ag * sizeof(float), cudaMemcpyDeviceToHost, s));
   return SPNGD_OK;
 }
 
@@ -1352,12 +1469,16 @@ int spngd_opt_enable_raw_inputs(spngd_opt* o, const spngd_conv_geom* geoms) {
     if (rc) return rc;
     if (g.k == 1 && g.stride == 1 && g.pad == 0) {  // the raw input is already the capture layout
       L.raw = L.act;
+      L.raw_floats = B * L.d.a * L.d.hw;
       continue;
     }
-    L.raw = o->alloc(size_t(B * g.c_in * g.h * g.w));
+    L.raw_floats = B * g.c_in * g.h * g.w;
+    L.raw = o->alloc(size_t(L.raw_floats));
     if (!L.raw) return fail(SPNGD_ERR_CUDA, "opt: raw input allocation failed");
     o->i2c.push_back({L.raw, L.act, B, g});
+    if (o->overlap_ok) o->waves[wave_of(L.d)].i2c.push_back(o->i2c.back());
   }
+  for (auto& wv : o->waves) wv.d_i2c = dev_upload(wv.i2c, o->owned);
   o->d_i2c = dev_upload(o->i2c, o->owned);
   if (!o->i2c.empty() && !o->d_i2c) return fail(SPNGD_ERR_CUDA, "opt: upload failed");
   o->raw_inputs = true;

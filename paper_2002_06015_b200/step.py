@@ -213,6 +213,14 @@ class Optimizer:
     def step(self, step: int, eta: float = 1.25e-2, momentum: float = 0.993):
         check(N.lib().spngd_opt_step(self.h, step, eta, momentum))
 
+    def step_host(self, step: int, inputs, weights_out=None, eta: float = 1.25e-2, momentum: float = 0.993):
+        """The step fed from host memory (spngd_opt_step_host): `inputs` is a list
+        of (layer, which, host pointer) -- pinned memory makes the transfer
+        asynchronous and, with the wave schedule, overlapped with the step;
+        `weights_out` (host pointer, optional) receives every weight replica."""
+        arr = (N.HostInput * max(len(inputs), 1))(*[N.HostInput(li, w, hp) for li, w, hp in inputs])
+        check(N.lib().spngd_opt_step_host(self.h, step, eta, momentum, arr, len(inputs), weights_out))
+
     def phase_ms(self):
         out = (C.c_float * 6)()
         check(N.lib().spngd_opt_phase_ms(self.h, out))

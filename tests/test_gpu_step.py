@@ -202,8 +202,11 @@ def test_full_bn_mode_step(cuda_dev, stale):
     SYRK engine, (F + lambda I)^-1 by the batched Cholesky, v = T^T (T u).
     rel. Frobenius <= 1e-4 on F^-1, the updated gamma/beta and velocities."""
     from paper_2002_06015_b200.step import AINV, BN_FULL, BN_M3C
-    layers = [W.conv(3, 16, 3, 1, 8), W.bn(16, 64), W.conv(16, 96, 3, 1, 8), W.bn(96, 64), W.fc(96, 10), W.bn(300)]
-    B = 24
+    # B > 2c keeps F + lambda I well conditioned; with B < 2c (rank-deficient F,
+    # cond ~ |F| / lambda) fp32 inverses lose ~cond * 2^-24 like the config-5
+    # K < n sweep inputs (DESIGN.md §4)
+    layers = [W.conv(3, 16, 3, 1, 8), W.bn(16, 64), W.conv(16, 48, 3, 1, 8), W.bn(48, 64), W.fc(48, 10), W.bn(40)]
+    B = 160
     opt = Optimizer(layers, B, lam=LAM, bn_mode=BN_FULL, stale=stale)
     try:
         opt.synth(seed=11)
@@ -311,3 +314,43 @@ def test_raw_inputs_step(cuda_dev):
         assert opt.ptr(4, RAW_ACT)[0] != opt.ptr(4, ACT)[0]
     finally:
         opt.close()
+
+
+@pytest.mark.parametrize("raw", [False, True])
+def test_step_host_equals_device_step(cuda_dev, raw):
+    """spngd_opt_step_host: the same step fed from pinned host buffers, the H2D
+    copies overlapped wave by wave with the SYRKs (and im2col of raw inputs),
+    is bit-identical to the step on device-resident inputs."""
+    layers = [W.conv(3, 16, 3, 1, 12), W.bn(16, 144), W.conv(16, 64, 3, 2, 12), W.conv(64, 256, 1, 1, 6),
+              W.bn(256, 36), W.fc(256 * 36, 10)]
+    B = 8
+    outs = []
+    for host in (False, True):
+        opt = Optimizer(layers, B, lam=LAM)
+        try:
+            if raw:
+                opt.enable_raw_inputs()
+            opt.synth(seed=41)
+            if host:
+                keep = []
+                ins = []
+                for li, w in opt.input_buffers():
+                    t = opt.download(li, w).pin_memory()
+                    keep.append(t)
+                    ins.append((li, w, t.data_ptr()))
+                opt.synth(seed=99)  # clobber the device copies: the step must use the host inputs
+                wout = torch.empty(opt.ptr(0, 12)[1], dtype=torch.float32).pin_memory()
+                opt.step_host(1, ins, wout.data_ptr(), ETA, MOM)
+                opt.sync()
+                for li in range(len(layers)):  # the weights read back with the step
+                    off = (opt.ptr(li, WB)[0] - opt.ptr(0, 12)[0]) // 4
+                    w = opt.download(li, WB).numpy()
+                    assert np.array_equal(wout.numpy()[off:off + w.size], w), li
+            else:
+                opt.step(1, ETA, MOM)
+                opt.sync()
+            outs.append([opt.download(li, WB).numpy() for li in range(len(layers))])
+        finally:
+            opt.close()
+    for a, b in zip(*outs):
+        assert np.array_equal(a, b)
