@@ -164,6 +164,8 @@ int plan_factors(const spngd_factor_req* reqs, int n, FactorPlan& plan, float* w
     }
   }
   plan.kchunk = choose_kchunk(tk);
+  static const char* kc_env = getenv("SPNGD_KCHUNK");  // experiment override (multiple of 32)
+  if (kc_env && atoi(kc_env) >= 32) plan.kchunk = atoi(kc_env) / 32 * 32;
   int slot = 0;
   for (int i = 0; i < n; ++i) {
     GemmProblem& p = plan.probs[i];
