@@ -42,22 +42,38 @@ __global__ void bn_moments_kernel(const spngd_bn_moments_req* __restrict__ reqs)
 // im2col (net.cpp:199-219) per sample: out[(s*rows + row)*hw + col], row =
 // ch*k*k + ky*k + kx, col = oy*wo + ox; coalesced writes, gathered reads that
 // hit L1/L2 k*k times.  HBM-bound: reads B*c*h*w, writes B*c*k*k*hw floats.
-__global__ void im2col_kernel(const spngd_im2col_req* __restrict__ reqs) {
-  const spngd_im2col_req r = reqs[blockIdx.y];
+template <typename I>
+__device__ __forceinline__ void im2col_range(const spngd_im2col_req& r) {
   const spngd_conv_geom g = r.geom;
-  const int64_t ho = (g.h + 2 * g.pad - g.k) / g.stride + 1, wo = (g.w + 2 * g.pad - g.k) / g.stride + 1;
-  const int64_t kk = g.k * g.k, rows = g.c_in * kk, hw = ho * wo;
-  const int64_t total = r.batch * rows * hw;
-  for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < total; e += int64_t(gridDim.x) * blockDim.x) {
-    const int64_t col = e % hw, rs = e / hw;
-    const int64_t row = rs % rows, s = rs / rows;
-    const int64_t ch = row / kk, kyx = row - ch * kk, ky = kyx / g.k, kx = kyx - ky * g.k;
-    const int64_t oy = col / wo, ox = col - oy * wo;
-    const int64_t iy = oy * g.stride + ky - g.pad, ix = ox * g.stride + kx - g.pad;
+  const I h = I(g.h), w = I(g.w), k = I(g.k), st = I(g.stride), pad = I(g.pad), c = I(g.c_in);
+  const I ho = (h + 2 * pad - k) / st + 1, wo = (w + 2 * pad - k) / st + 1;
+  const I kk = k * k, rows = c * kk, hw = ho * wo;
+  const I total = I(r.batch) * rows * hw;
+  for (I e = I(blockIdx.x) * blockDim.x + threadIdx.x; e < total; e += I(gridDim.x) * blockDim.x) {
+    const I rs = e / hw, col = e - rs * hw;
+    const I s = rs / rows, row = rs - s * rows;
+    const I ch = row / kk, kyx = row - ch * kk, ky = kyx / k, kx = kyx - ky * k;
+    const I oy = col / wo, ox = col - oy * wo;
+    const I iy = oy * st + ky - pad, ix = ox * st + kx - pad;  // signed: padding reads as 0
     float v = 0.f;
-    if (iy >= 0 && iy < g.h && ix >= 0 && ix < g.w) v = __ldg(r.x + ((s * g.c_in + ch) * g.h + iy) * g.w + ix);
+    if (iy >= 0 && iy < h && ix >= 0 && ix < w) v = __ldg(r.x + (int64_t(s * c + ch) * h + iy) * w + ix);
     r.out[e] = v;
   }
+}
+
+// im2col (net.cpp:199-219) per sample: out[(s*rows + row)*hw + col], row =
+// ch*k*k + ky*k + kx, col = oy*wo + ox; coalesced writes, gathered reads that
+// hit L1/L2 k*k times.  HBM-bound: reads B*c*h*w, writes B*c*k*k*hw floats.
+// 32-bit index math whenever the capture has < 2^31 elements (always, at
+// ResNet-50 B = 256).
+__global__ void im2col_kernel(const spngd_im2col_req* __restrict__ reqs) {
+  const spngd_im2col_req r = reqs[blockIdx.y];
+  const spngd_conv_geom& g = r.geom;
+  const int64_t ho = (g.h + 2 * g.pad - g.k) / g.stride + 1, wo = (g.w + 2 * g.pad - g.k) / g.stride + 1;
+  if (r.batch * g.c_in * g.k * g.k * ho * wo < (int64_t(1) << 31))
+    im2col_range<int32_t>(r);
+  else
+    im2col_range<int64_t>(r);
 }
 
 // BN branch of grad_payload (dist.cpp:364-371): [sum_s g_gamma / m | sum_s g_beta / m].
@@ -75,14 +91,25 @@ __global__ void bn_grad_payload_kernel(const BnGradPayloadTask* __restrict__ tas
 }
 
 // X'[i][s*hw + p] = X[(s*dim + i)*hw + p]: coalesced reads, runs of hw writes.
+template <typename I>
+__device__ __forceinline__ void repack_range(const RepackTask& t) {
+  const I hw = I(t.hw), dim = I(t.dim), n = I(t.n);
+  const I total = n * dim * hw;
+  for (I e = I(blockIdx.x) * blockDim.x + threadIdx.x; e < total; e += I(gridDim.x) * blockDim.x) {
+    const I row = e / hw, p = e - row * hw;
+    const I s = row / dim, i = row - s * dim;
+    t.dst[int64_t(i) * (n * hw) + s * hw + p] = __ldg(t.src + e);
+  }
+}
+
+// 32-bit index math when the capture has < 2^31 elements (64-bit division
+// dominated the old kernel: 1.9 TB/s on ResNet-50's 196 MB).
 __global__ void repack_kernel(const RepackTask* __restrict__ tasks) {
   const RepackTask t = tasks[blockIdx.y];
-  const int64_t total = t.n * t.dim * t.hw;
-  for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < total; e += int64_t(gridDim.x) * blockDim.x) {
-    const int64_t p = e % t.hw, row = e / t.hw;
-    const int64_t i = row % t.dim, s = row / t.dim;
-    t.dst[i * (t.n * t.hw) + s * t.hw + p] = t.src[e];
-  }
+  if (t.n * t.dim * t.hw < (int64_t(1) << 31))
+    repack_range<int32_t>(t);
+  else
+    repack_range<int64_t>(t);
 }
 
 }  // namespace

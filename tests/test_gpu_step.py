@@ -338,7 +338,8 @@ def test_step_host_equals_device_step(cuda_dev, raw):
                     t = opt.download(li, w).pin_memory()
                     keep.append(t)
                     ins.append((li, w, t.data_ptr()))
-                opt.synth(seed=99)  # clobber the device copies: the step must use the host inputs
+                for li, w in opt.input_buffers():  # clobber the device copies: the step must use the host inputs
+                    opt.upload(li, w, torch.full((opt.numel(li, w),), 7.0))
                 wout = torch.empty(opt.ptr(0, 12)[1], dtype=torch.float32).pin_memory()
                 opt.step_host(1, ins, wout.data_ptr(), ETA, MOM)
                 opt.sync()
