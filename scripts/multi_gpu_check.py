@@ -1,9 +1,13 @@
 """K-invariance of the NCCL path (tests/test_dist.cpp:363-387 analogue).
 
-torchrun --nproc-per-node 2 scripts/multi_gpu_check.py
+torchrun --nproc-per-node 2 scripts/multi_gpu_check.py [--mode default|wgrad|bn_full|one_mc|sgd|host]
 Every rank runs one step at P = 2 on its own shard; rank 0 then replays the
 same step at P = 1 over the concatenated batch (mean dW) and compares all
-updated weights.  Replicas must be bit-identical across ranks.  Exit 0 on pass.
+updated weights.  Replicas must be bit-identical across ranks, and the step's
+CommLedger rows must equal the oracle restatement at P (oracle/ledger.py).
+Modes: the optimizer configurations of DESIGN.md §3.6 (wgrad forms dW on each
+rank from its shard; host feeds the rank's inputs through spngd_opt_step_host).
+Exit 0 on pass.
 """
 import os
 import sys
@@ -15,6 +19,8 @@ import torch.distributed as dist
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2002_06015_b200 import workloads as W  # noqa: E402
 from paper_2002_06015_b200.step import ACT, BN_GB, BN_GG, DW, GRAD, V, Comm, Optimizer  # noqa: E402
+from paper_2002_06015_b200.step import BN_GB_SAMPLED, BN_GG_SAMPLED, GRAD_SAMPLED  # noqa: E402
+from oracle import ledger as OL  # noqa: E402
 from paper_2002_06015_b200.step import W as WB  # noqa: E402
 
 LAYERS = [W.conv(16, 32, 3, 1, 16), W.bn(32), W.conv(32, 64, 3, 2, 16), W.bn(64), W.conv(64, 128, 3, 1, 8),
@@ -23,24 +29,50 @@ LAYERS = [W.conv(16, 32, 3, 1, 16), W.bn(32), W.conv(32, 64, 3, 2, 16), W.bn(64)
 B = 8
 
 
+MODES = {"default": {}, "wgrad": {"wgrad": True}, "bn_full": {"bn_mode": 1}, "one_mc": {"fisher_mode": 1},
+         "sgd": {"sgd": True}, "host": {}}
+
+
 def main():
+    mode = sys.argv[sys.argv.index("--mode") + 1] if "--mode" in sys.argv else "default"
+    kw = MODES[mode]
+    global B
+    if mode == "bn_full":
+        B = 320  # 2c <= 512 < P*B: full-rank F, so fp32 summation order stays below the 1e-4 gate
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", rank))
     torch.cuda.set_device(local)
     dist.init_process_group("gloo")
     obj = [Comm.unique_id() if rank == 0 else None]
     dist.broadcast_object_list(obj, src=0)
-    opt = Optimizer(LAYERS, B, device=local, world=world, rank=rank, nccl_id=obj[0])
+    opt = Optimizer(LAYERS, B, device=local, world=world, rank=rank, nccl_id=obj[0], **kw)
     opt.synth(seed=11)
     inputs = {}
-    for li, l in enumerate(LAYERS):
+
+    def in_whichs(l):
         ws = [BN_GG, BN_GB, DW] if l.kind == "bn" else [ACT, GRAD, DW]
-        inputs[li] = {w: opt.download(li, w).numpy() for w in ws}
+        if kw.get("fisher_mode") == 1:
+            ws += [BN_GG_SAMPLED, BN_GB_SAMPLED] if l.kind == "bn" else [GRAD_SAMPLED]
+        return ws
+
+    for li, l in enumerate(LAYERS):
+        inputs[li] = {w: opt.download(li, w).numpy() for w in in_whichs(l)}
         inputs[li][WB] = opt.download(li, WB).numpy()
         if opt.owner(li) == rank:
             inputs[li][V] = opt.download(li, V).numpy()
-    opt.step(1)
+    if mode == "host":
+        keep = [opt.download(li, w).pin_memory() for li, w in opt.input_buffers()]
+        for li, w in opt.input_buffers():
+            opt.upload(li, w, torch.full((opt.numel(li, w),), 3.0))
+        opt.step_host(1, [(li, w, t.data_ptr()) for (li, w), t in zip(opt.input_buffers(), keep)])
+    else:
+        opt.step(1)
     opt.sync()
+    rows = [(r.step, r.stage, r.collective, r.statistic_id, r.elements, r.bytes, r.skipped)
+            for r in opt.ledger().rows()]
+    want_rows = OL.step_rows(LAYERS, world, 1, None, 4, bn_full=kw.get("bn_mode") == 1, sgd=kw.get("sgd", False))
+    ledger_ok = rows == want_rows and all(r[4] > 0 for r in rows)
+    wire = opt.wire_bytes()
     after = [opt.download(li, WB).numpy() for li in range(len(LAYERS))]
     owners = [opt.owner(li) for li in range(len(LAYERS))]
     gathered = [None] * world
@@ -52,9 +84,9 @@ def main():
                 if not np.array_equal(gathered[r][1][li], after[li]):
                     print(f"replica mismatch rank {r} layer {li}")
                     ok = False
-        ref = Optimizer(LAYERS, B * world, device=local)
+        ref = Optimizer(LAYERS, B * world, device=local, **kw)
         for li, l in enumerate(LAYERS):
-            ws = [BN_GG, BN_GB] if l.kind == "bn" else [ACT, GRAD]
+            ws = [w for w in in_whichs(l) if w != DW]
             for w in ws:
                 ref.upload(li, w, torch.from_numpy(np.concatenate([gathered[r][0][li][w] for r in range(world)])))
             ref.upload(li, DW, torch.from_numpy(np.mean([gathered[r][0][li][DW] for r in range(world)], axis=0)))
@@ -70,9 +102,11 @@ def main():
             worst = max(worst, err)
             print(f"layer {li} {LAYERS[li].kind} owner {owners[li]} rel {err:.2e}")
         ok = ok and worst <= 1e-4
+        print("ledger rows match the oracle at P =", world, ledger_ok, "| NCCL bytes", wire)
+        ok = ok and ledger_ok
         ph = opt.phase_ms()
         print("phases", {k: round(v, 3) for k, v in ph.items()})
-        print("PASS" if ok else "FAIL", f"worst {worst:.2e}")
+        print("PASS" if ok else "FAIL", f"mode {mode} worst {worst:.2e}")
         ref.close()
     opt.close()
     t = torch.tensor([1 if ok else 0])
