@@ -178,6 +178,9 @@ def run_ours(args):
 
     nccl_id = new_nccl_id()
     opt = Optimizer(layers, batch, lam=args.lam, device=local, world=world, rank=rank, nccl_id=nccl_id)
+    p2p = world > 1 and os.environ.get("SPNGD_NO_P2P") is None
+    if p2p:  # Stage 5 as NVLink stores fused into the owners' rescale pass
+        opt.attach_peers(pg)
     opt.synth(seed=42)
     L = N.lib()
 
@@ -258,6 +261,8 @@ def run_ours(args):
         opt_r = Optimizer(layers, batch, lam=args.lam, device=local, world=world, rank=rank,
                           nccl_id=new_nccl_id())
         opt_r.enable_raw_inputs()
+        if p2p:
+            opt_r.attach_peers(pg)
         opt_r.synth(seed=42)
         for s in range(args.warmup):
             opt_r.step(s + 1)
@@ -327,7 +332,8 @@ def run_ours(args):
                        "l2": f"inputs > L2: {W.capture_bytes(layers, batch) / 1e9:.2f} GB of captures per step"},
             "phases_ms_last_step": {k: round(v, 3) for k, v in phases.items()},
             "schedule": "waves: inverse recursion of the largest factors runs on high-priority streams while the "
-                        "remaining factor SYRKs run" + ("; per-wave owner reductions on a comm stream" if world > 1 else ""),
+                        "remaining factor SYRKs run" + ("; per-wave owner reductions on a comm stream" if world > 1 else "")
+                        + ("; Stage 5 as NVLink peer stores fused into the rescale pass" if p2p else ""),
             "phase_serial": serial,
             "e2e_raw_inputs": e2e_raw,
             "e2e": ({"value": round(e2e, 3), "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": out_bytes}

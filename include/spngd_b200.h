@@ -437,6 +437,19 @@ int spngd_opt_ledger_clear(spngd_opt* opt);
  * statistics, of gradients, and the all-gather.  0 at world == 1. */
 int spngd_opt_wire_bytes(const spngd_opt* opt, int64_t* stat_bytes, int64_t* grad_bytes, int64_t* ag_bytes);
 
+/* ---- Stage 5 over NVLink peer memory ---------------------------------------
+ * One process per GPU: every rank exports its weight-replica buffer (buffer
+ * 12) with _ipc_handle (64 bytes, a cudaIpcMemHandle_t), the caller exchanges
+ * them (e.g. torch.distributed all_gather) and passes all `world` handles in
+ * rank order to _attach_peers before the first step.  From then on Stage 5
+ * (AllGatherV, dist.cpp:646-663) is no NCCL all-gather: the owners' rescale
+ * pass stores W'' into every peer's replica as it computes it (the update's
+ * last kernel and the collective are one kernel), BN / unrescaled layers go by
+ * one peer-copy launch, and a one-word NCCL all-reduce orders the stores
+ * before the step completes.  Same values bit for bit. */
+int spngd_opt_ipc_handle(spngd_opt* opt, void* out64);
+int spngd_opt_attach_peers(spngd_opt* opt, const void* handles);
+
 /* ---- raw layer inputs (first stage) ------------------------
  * The reference's conv capture is im2col of the layer input, rows
  * ch*k*k + ky*k + kx, columns oy*w_out + ox, zero in the padding (im2col,

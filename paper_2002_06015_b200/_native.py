@@ -197,6 +197,8 @@ def _declare(L):
                                           C.c_int, C.c_int, C.POINTER(LedgerRowC), _i64]),
         "spngd_opt_step_host": (C.c_int, [P, _i64, C.c_double, C.c_double, C.POINTER(HostInput), C.c_int,
                                            C.c_void_p]),
+        "spngd_opt_ipc_handle": (C.c_int, [P, C.c_void_p]),
+        "spngd_opt_attach_peers": (C.c_int, [P, C.c_void_p]),
         "spngd_opt_enable_raw_inputs": (C.c_int, [P, C.POINTER(ConvGeom)]),
         "spngd_im2col_batched": (C.c_int, [P, C.c_int, C.POINTER(Im2colReq)]),
         "spngd_opt_ledger": (_i64, [P, C.POINTER(LedgerRowC), _i64]),

@@ -27,6 +27,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstring>
 #include <cmath>
 #include <numeric>
 #include <vector>
@@ -167,6 +168,11 @@ struct spngd_opt {
   std::vector<Wave> waves;
   cudaStream_t comm_stream = nullptr;    // world > 1: NCCL + owner-side prep of the waves
   cudaEvent_t comm_fork = nullptr, comm_done = nullptr;
+  // spngd_opt_attach_peers: Stage 5 as NVLink stores into the peers' replica buffers
+  bool p2p = false;
+  float* peer_ag[8] = {};
+  std::vector<PeerCopyTask> pcopy; PeerCopyTask* d_pcopy = nullptr; int64_t pcopy_max = 0;
+  double* d_barrier = nullptr;
   cudaStream_t h2d_stream = nullptr;     // spngd_opt_step_host: host inputs, wave by wave
   cudaEvent_t h2d_start = nullptr, grads_ready = nullptr;
   bool overlap_ok = false;   // no stale gating
@@ -239,6 +245,8 @@ struct spngd_opt {
       if (graph_ov_exec[i]) cudaGraphExecDestroy(graph_ov_exec[i]);
       if (graphs_ov[i]) cudaGraphDestroy(graphs_ov[i]);
     }
+    for (float* p : peer_ag)
+      if (p) cudaIpcCloseMemHandle(p);
     if (h2d_start) cudaEventDestroy(h2d_start);
     if (grads_ready) cudaEventDestroy(grads_ready);
     if (h2d_stream) cudaStreamDestroy(h2d_stream);
@@ -823,6 +831,19 @@ float* spngd_opt_buffer(spngd_opt* o, int layer, int which, int64_t* ld) {
 
 namespace {
 
+// Stage 5 (AllGatherV of the updated weights, dist.cpp:646-663).  With peers
+// attached the owners' rescale pass already stored W'' into every replica
+// over NVLink; the rest (BN, unrescaled layers) goes by one peer-copy launch,
+// and a one-word all-reduce orders every rank's stores before its step ends.
+int issue_allgather(spngd_opt* o) {
+  spngd_ctx* ctx = o->ctx;
+  if (o->world == 1) return SPNGD_OK;
+  if (!o->p2p) return spngd_all_gather(ctx, o->ag + int64_t(o->rank) * o->seg_ag, o->ag, o->seg_ag);
+  int rc = launch_peer_copy(ctx, o->d_pcopy, int(o->pcopy.size()), o->pcopy_max);
+  if (!rc) rc = comm_allreduce_sum_f64(ctx, o->d_barrier, 1);
+  return rc;
+}
+
 // Raw conv inputs -> the im2col captures the GEMMs read (net.cpp:199-219).
 int issue_inputs(spngd_opt* o) {
   return launch_im2col(o->ctx, o->d_i2c, int(o->i2c.size()));
@@ -903,8 +924,7 @@ int issue_phase(spngd_opt* o, int phase) {
         rc = launch_bn_full_update(ctx, o->d_bnf_upd[k], int(o->bnf_upd[k].size()), o->bnf_maxn, 0.0, 0.0, o->d_scal);
       return rc;
     case 5:  // Stage 5: AllGatherV of the updated weights (dist.cpp:646-663), in place.
-      if (o->world > 1) rc = spngd_all_gather(ctx, o->ag + int64_t(o->rank) * o->seg_ag, o->ag, o->seg_ag);
-      return rc;
+      return issue_allgather(o);
   }
   return SPNGD_OK;
 }
@@ -1240,7 +1260,7 @@ int step_impl(spngd_opt* o, int64_t step, double eta, double momentum, bool host
           if (full || o->due[q]) o->wire_stat += o->stats[q].count * int64_t(sizeof(float));
       }
       o->wire_grad = W * o->seg_grad * int64_t(sizeof(float));
-      o->wire_ag = o->seg_ag * int64_t(sizeof(float));
+      o->wire_ag = o->seg_ag * int64_t(sizeof(float));  // P2P: the owned ranges, to world-1 peers
     }
   }
   if (o->cfg.sgd) {  // Stage 3 grads RS, plain update, Stage 5 AG (dist.cpp:522-537, 604-620, 646-663)
@@ -1256,8 +1276,8 @@ int step_impl(spngd_opt* o, int64_t step, double eta, double momentum, bool host
                                        o->seg_grad);
       else if (ph == 4)
         rc = launch_sgd_update(ctx, o->d_sgd, int(o->sgd_tasks.size()), o->d_scal);
-      else if (ph == 5 && o->world > 1)
-        rc = spngd_all_gather(ctx, o->ag + int64_t(o->rank) * o->seg_ag, o->ag, o->seg_ag);
+      else if (ph == 5)
+        rc = issue_allgather(o);
       if (rc) return rc;
     }
     SPNGD_CUDA_TRY(cudaEventRecord(o->ev[6], s));
@@ -1482,6 +1502,64 @@ int spngd_opt_enable_raw_inputs(spngd_opt* o, const spngd_conv_geom* geoms) {
   o->d_i2c = dev_upload(o->i2c, o->owned);
   if (!o->i2c.empty() && !o->d_i2c) return fail(SPNGD_ERR_CUDA, "opt: upload failed");
   o->raw_inputs = true;
+  return SPNGD_OK;
+}
+
+int spngd_opt_ipc_handle(spngd_opt* o, void* out64) {
+  if (!o || !out64) return fail(SPNGD_ERR_INVALID, "spngd_opt_ipc_handle: null argument");
+  cudaIpcMemHandle_t h;
+  SPNGD_CUDA_TRY(cudaIpcGetMemHandle(&h, o->ag));
+  static_assert(sizeof(h) == 64, "cudaIpcMemHandle_t is 64 bytes");
+  memcpy(out64, &h, sizeof(h));
+  return SPNGD_OK;
+}
+
+int spngd_opt_attach_peers(spngd_opt* o, const void* handles) {
+  if (!o || !handles) return fail(SPNGD_ERR_INVALID, "spngd_opt_attach_peers: null argument");
+  if (o->world < 2 || o->world > kMaxPeers + 1) return fail(SPNGD_ERR_INVALID, "spngd_opt_attach_peers: world must be 2..8");
+  if (o->p2p) return fail(SPNGD_ERR_INVALID, "spngd_opt_attach_peers: already attached");
+  if (o->graphs_ready || o->graphs_ready_ov || o->timed)
+    return fail(SPNGD_ERR_INVALID, "spngd_opt_attach_peers: call before the first step");
+  const auto* hs = static_cast<const cudaIpcMemHandle_t*>(handles);
+  for (int q = 0; q < o->world; ++q) {
+    if (q == o->rank) continue;
+    void* p = nullptr;
+    SPNGD_CUDA_TRY(cudaIpcOpenMemHandle(&p, hs[q], cudaIpcMemLazyEnablePeerAccess));
+    o->peer_ag[q] = static_cast<float*>(p);
+  }
+  auto peers_of = [&](const float* local, float** dst) {
+    const int64_t off = local - o->ag;
+    int k = 0;
+    for (int q = 0; q < o->world; ++q)
+      if (q != o->rank) dst[k++] = o->peer_ag[q] + off;
+    return k;
+  };
+  // rescaled layers: the rescale pass stores W'' to the peers too
+  std::vector<char> covered(o->layers.size(), 0);
+  if (!o->cfg.sgd) {
+    for (auto& t : o->pplan.rescale) {
+      t.n_peers = peers_of(t.W, t.peers);
+      for (size_t li = 0; li < o->layers.size(); ++li)
+        if (o->ag + int64_t(o->rank) * o->seg_ag + o->layers[li].off_W == t.W) covered[li] = 1;
+    }
+    if (!o->pplan.rescale.empty())
+      SPNGD_CUDA_TRY(cudaMemcpy(o->d_rescale, o->pplan.rescale.data(), o->pplan.rescale.size() * sizeof(RescaleTask),
+                                cudaMemcpyHostToDevice));
+  }
+  for (size_t li = 0; li < o->layers.size(); ++li) {
+    const LayerState& L = o->layers[li];
+    if (L.owner != o->rank || covered[li]) continue;
+    PeerCopyTask t{};
+    t.src = o->ag + int64_t(o->rank) * o->seg_ag + L.off_W;
+    t.n = L.d.kind == SPNGD_BN ? 2 * L.d.g : L.d.g * L.d.a;
+    t.n_peers = peers_of(t.src, t.dst);
+    o->pcopy.push_back(t);
+    o->pcopy_max = std::max(o->pcopy_max, t.n);
+  }
+  o->d_pcopy = dev_upload(o->pcopy, o->owned);
+  o->d_barrier = reinterpret_cast<double*>(o->alloc(2, true));
+  if ((!o->pcopy.empty() && !o->d_pcopy) || !o->d_barrier) return fail(SPNGD_ERR_CUDA, "opt: upload failed");
+  o->p2p = true;
   return SPNGD_OK;
 }
 

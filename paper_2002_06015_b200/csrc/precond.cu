@@ -42,12 +42,29 @@ __global__ void rescale_kernel(const RescaleTask* __restrict__ tasks) {
     v = make_float4(nw.x - w.x + v.x, nw.y - w.y + v.y, nw.z - w.z + v.z, nw.w - w.w + v.w);
     reinterpret_cast<float4*>(t.W)[q] = nw;
     reinterpret_cast<float4*>(t.V)[q] = v;
+    for (int p = 0; p < t.n_peers; ++p) reinterpret_cast<float4*>(t.peers[p])[q] = nw;  // Stage 5 over NVLink
   }
   for (int64_t i = 4 * n4 + int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < t.n; i += stride) {
     const float w = t.W[i], nw = s * w;
     t.V[i] = nw - w + t.V[i];
     t.W[i] = nw;
+    for (int p = 0; p < t.n_peers; ++p) t.peers[p][i] = nw;
   }
+  if (t.n_peers) __threadfence_system();
+}
+
+__global__ void peer_copy_kernel(const PeerCopyTask* __restrict__ tasks) {
+  const PeerCopyTask t = tasks[blockIdx.y];
+  const bool vec = t.n % 4 == 0 && (reinterpret_cast<uintptr_t>(t.src) & 15) == 0;
+  const int64_t n4 = vec ? t.n / 4 : 0;
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; q < n4; q += stride) {
+    const float4 v = reinterpret_cast<const float4*>(t.src)[q];
+    for (int p = 0; p < t.n_peers; ++p) reinterpret_cast<float4*>(t.dst[p])[q] = v;
+  }
+  for (int64_t i = 4 * n4 + int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < t.n; i += stride)
+    for (int p = 0; p < t.n_peers; ++p) t.dst[p][i] = t.src[i];
+  __threadfence_system();
 }
 
 __global__ void bn_update_kernel(const spngd_bn_update_req* __restrict__ reqs, double lambda, double eta,
@@ -276,6 +293,15 @@ int run_precondition(spngd_ctx* ctx, const PrecondPlan& plan, GemmProblem* const
     SPNGD_CUDA_TRY(cudaGetLastError());
     ctx->launches++;
   }
+  return SPNGD_OK;
+}
+
+int launch_peer_copy(spngd_ctx* ctx, const PeerCopyTask* d_tasks, int n, int64_t max_n) {
+  if (n <= 0) return SPNGD_OK;
+  dim3 grid(unsigned(std::min<int64_t>(std::max<int64_t>((max_n / 4 + 255) / 256, 1), 296)), unsigned(n));
+  peer_copy_kernel<<<grid, 256, 0, ctx->stream>>>(d_tasks);
+  SPNGD_CUDA_TRY(cudaGetLastError());
+  ctx->launches++;
   return SPNGD_OK;
 }
 

@@ -7,13 +7,31 @@
 
 namespace spngd {
 
+constexpr int kMaxPeers = 7;  // one process per GPU, <= 8 GPUs per box
+
 struct RescaleTask {  // rescale_weights + velocity fix, one FC/Conv layer
   float* W;
   float* V;
   int64_t n;
   const double* norm2;
   double target;  // sqrt(2 * d_out)
+  // P2P all-gather (spngd_opt_attach_peers): W'' is also stored to the same
+  // offset of every peer's replica buffer over NVLink (Stage 5 fused in)
+  float* peers[kMaxPeers];
+  int32_t n_peers;
+  int32_t pad_;
 };
+
+// Owned replica range -> every peer's replica buffer (NVLink stores), for the
+// layers whose final weights are not produced by the rescale pass.
+struct PeerCopyTask {
+  const float* src;
+  float* dst[kMaxPeers];
+  int32_t n_peers;
+  int32_t pad_;
+  int64_t n;
+};
+int launch_peer_copy(spngd_ctx* ctx, const PeerCopyTask* d_tasks, int n, int64_t max_n);
 
 struct PrecondPlan {
   // Grouped GEMM launches in order: dense inverses -> 2 (P1^T = A^-1 dW^T,

@@ -226,6 +226,17 @@ class Optimizer:
         check(N.lib().spngd_opt_phase_ms(self.h, out))
         return dict(zip(PHASES, list(out)))
 
+    def attach_peers(self, pg):
+        """Stage 5 over NVLink peer memory (spngd_opt_attach_peers): exchanges the
+        replica buffers' IPC handles over the torch.distributed group `pg` (the
+        control plane) and attaches them.  Call on every rank before the first step."""
+        h = C.create_string_buffer(64)
+        check(N.lib().spngd_opt_ipc_handle(self.h, h))
+        allh = [None] * self.world
+        pg.all_gather_object(allh, h.raw)
+        buf = C.create_string_buffer(b"".join(allh), 64 * self.world)
+        check(N.lib().spngd_opt_attach_peers(self.h, buf))
+
     def enable_raw_inputs(self):
         """The step takes each conv layer's raw input (RAW_ACT, B x c_in x h x w)
         and forms the im2col capture on the device (spngd_opt_enable_raw_inputs,

@@ -30,7 +30,7 @@ B = 8
 
 
 MODES = {"default": {}, "wgrad": {"wgrad": True}, "bn_full": {"bn_mode": 1}, "one_mc": {"fisher_mode": 1},
-         "sgd": {"sgd": True}, "host": {}}
+         "sgd": {"sgd": True}, "host": {}, "p2p": {}, "p2p_sgd": {"sgd": True}}
 
 
 def main():
@@ -46,6 +46,8 @@ def main():
     obj = [Comm.unique_id() if rank == 0 else None]
     dist.broadcast_object_list(obj, src=0)
     opt = Optimizer(LAYERS, B, device=local, world=world, rank=rank, nccl_id=obj[0], **kw)
+    if mode.startswith("p2p"):
+        opt.attach_peers(dist)
     opt.synth(seed=11)
     inputs = {}
 
