@@ -439,15 +439,22 @@ int spngd_opt_wire_bytes(const spngd_opt* opt, int64_t* stat_bytes, int64_t* gra
 
 /* ---- Stage 5 over NVLink peer memory ---------------------------------------
  * One process per GPU: every rank exports its weight-replica buffer (buffer
- * 12) with _ipc_handle (64 bytes, a cudaIpcMemHandle_t), the caller exchanges
- * them (e.g. torch.distributed all_gather) and passes all `world` handles in
- * rank order to _attach_peers before the first step.  From then on Stage 5
- * (AllGatherV, dist.cpp:646-663) is no NCCL all-gather: the owners' rescale
- * pass stores W'' into every peer's replica as it computes it (the update's
- * last kernel and the collective are one kernel), BN / unrescaled layers go by
- * one peer-copy launch, and a one-word NCCL all-reduce orders the stores
- * before the step completes.  Same values bit for bit. */
-int spngd_opt_ipc_handle(spngd_opt* opt, void* out64);
+ * 12) and, without stale gating, a statistics inbox (world x seg_stat floats)
+ * with _ipc_handle (128 bytes: two cudaIpcMemHandle_t), the caller exchanges
+ * them (e.g. torch.distributed all_gather) and passes all `world` records in
+ * rank order to _attach_peers before the first step.  From then on:
+ *  - Stages 2-3 (ReduceScatterV of the statistics, dist.cpp:510-537) are no
+ *    NCCL reduce-scatter: the factor SYRK epilogues, split-K reductions and BN
+ *    moment kernels store this rank's statistics straight into the owner's
+ *    inbox slot over NVLink as they are produced, and after a one-word NCCL
+ *    all-reduce (per wave in the wave schedule) the owner averages the slots
+ *    in rank order (reduce_scatter_v's mean, dist.cpp:204-213);
+ *  - Stage 5 (AllGatherV, dist.cpp:646-663) is no NCCL all-gather: the owners'
+ *    rescale pass stores W'' into every peer's replica as it computes it, BN /
+ *    unrescaled layers go by one peer-copy launch, and a one-word all-reduce
+ *    orders the stores before the step completes.
+ * Gradients still reduce-scatter through NCCL. */
+int spngd_opt_ipc_handle(spngd_opt* opt, void* out128);
 int spngd_opt_attach_peers(spngd_opt* opt, const void* handles);
 
 /* ---- raw layer inputs (first stage) ------------------------

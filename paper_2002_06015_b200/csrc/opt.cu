@@ -154,6 +154,9 @@ struct spngd_opt {
     UnpackTask* d_unpacks = nullptr;
     int64_t max_n = 0;
     std::vector<OwnerReduce> owner_ops;  // world > 1: this wave's statistics -> their owners
+    std::vector<SlotMeanTask> means;     // p2p_rs: this wave's owned statistics, slot means
+    SlotMeanTask* d_means = nullptr;
+    int64_t means_max = 0;
     cudaEvent_t ready = nullptr;         // factors of this wave reduced locally
     cudaEvent_t fork = nullptr;          // owner-side inputs of this wave's recursion ready
     // spngd_opt_step_host: this wave's captures arrive from the host on the
@@ -171,6 +174,13 @@ struct spngd_opt {
   // spngd_opt_attach_peers: Stage 5 as NVLink stores into the peers' replica buffers
   bool p2p = false;
   float* peer_ag[8] = {};
+  // fused reduce-scatter (no stale gating): the factor epilogues / split-K
+  // reductions / BN moments write this rank's statistics straight into the
+  // owner's inbox slot over NVLink; owners average the slots per wave
+  bool p2p_rs = false;
+  float* inbox = nullptr;            // world x seg_stat, slot q = rank q's statistics for this owner
+  float* peer_inbox[8] = {};
+  std::vector<SlotMeanTask> means; SlotMeanTask* d_means = nullptr; int64_t means_max = 0;
   std::vector<PeerCopyTask> pcopy; PeerCopyTask* d_pcopy = nullptr; int64_t pcopy_max = 0;
   double* d_barrier = nullptr;
   cudaStream_t h2d_stream = nullptr;     // spngd_opt_step_host: host inputs, wave by wave
@@ -246,6 +256,8 @@ struct spngd_opt {
       if (graphs_ov[i]) cudaGraphDestroy(graphs_ov[i]);
     }
     for (float* p : peer_ag)
+      if (p) cudaIpcCloseMemHandle(p);
+    for (float* p : peer_inbox)
       if (p) cudaIpcCloseMemHandle(p);
     if (h2d_start) cudaEventDestroy(h2d_start);
     if (grads_ready) cudaEventDestroy(grads_ready);
@@ -892,7 +904,12 @@ int issue_phase(spngd_opt* o, int phase) {
       return rc;
     case 2:  // Stages 2-3: ReduceScatterV of A, G/F and grads (dist.cpp:510-537).
       if (o->world > 1) {
-        rc = spngd_reduce_scatter_mean(ctx, o->rs_send, o->rs_recv, o->seg_stat);
+        if (o->p2p_rs) {  // statistics already in the owners' inboxes: barrier + slot means
+          rc = comm_allreduce_sum_f64(ctx, o->d_barrier, 1);
+          if (!rc) rc = launch_slot_mean(ctx, o->d_means, int(o->means.size()), o->means_max);
+        } else {
+          rc = spngd_reduce_scatter_mean(ctx, o->rs_send, o->rs_recv, o->seg_stat);
+        }
         if (!rc)
           rc = spngd_reduce_scatter_mean(ctx, o->rs_send + int64_t(o->world) * o->seg_stat, o->rs_recv + o->seg_stat,
                                          o->seg_grad);
@@ -993,7 +1010,12 @@ int issue_overlap(spngd_opt* o, bool capturing, bool host_in = false) {
       SPNGD_CUDA_TRY(cudaStreamWaitEvent(prep, wv.ready, 0));
     }
     ctx->stream = prep;
-    if (dist) rc = comm_reduce_to_owners(ctx, wv.owner_ops);
+    if (dist && o->p2p_rs) {  // every rank's wave-w statistics have landed in the inboxes after this
+      rc = comm_allreduce_sum_f64(ctx, o->d_barrier, 1);
+      if (!rc) rc = launch_slot_mean(ctx, wv.d_means, int(wv.means.size()), wv.means_max);
+    } else if (dist) {
+      rc = comm_reduce_to_owners(ctx, wv.owner_ops);
+    }
     if (!rc) rc = launch_pi(ctx, wv.d_pis, int(wv.pis.size()));
     if (!rc) rc = launch_unpack(ctx, wv.d_unpacks, int(wv.unpacks.size()), wv.max_n);
     ctx->stream = s;
@@ -1253,6 +1275,9 @@ int step_impl(spngd_opt* o, int64_t step, double eta, double momentum, bool host
       const int64_t W = o->world;
       if (o->cfg.sgd) {
         o->wire_stat = 0;
+      } else if (o->p2p_rs) {  // NVLink stores of the statistics owned by the other ranks
+        for (const auto& st : o->stats)
+          if (st.owner != o->rank) o->wire_stat += st.count * int64_t(sizeof(float));
       } else if (full && !ov) {
         o->wire_stat = W * o->seg_stat * int64_t(sizeof(float));  // one ncclReduceScatter
       } else {  // grouped ncclReduce of the due statistics to their owners
@@ -1505,12 +1530,18 @@ int spngd_opt_enable_raw_inputs(spngd_opt* o, const spngd_conv_geom* geoms) {
   return SPNGD_OK;
 }
 
-int spngd_opt_ipc_handle(spngd_opt* o, void* out64) {
-  if (!o || !out64) return fail(SPNGD_ERR_INVALID, "spngd_opt_ipc_handle: null argument");
-  cudaIpcMemHandle_t h;
-  SPNGD_CUDA_TRY(cudaIpcGetMemHandle(&h, o->ag));
-  static_assert(sizeof(h) == 64, "cudaIpcMemHandle_t is 64 bytes");
-  memcpy(out64, &h, sizeof(h));
+int spngd_opt_ipc_handle(spngd_opt* o, void* out128) {
+  if (!o || !out128) return fail(SPNGD_ERR_INVALID, "spngd_opt_ipc_handle: null argument");
+  static_assert(sizeof(cudaIpcMemHandle_t) == 64, "cudaIpcMemHandle_t is 64 bytes");
+  cudaIpcMemHandle_t h[2];
+  memset(h, 0, sizeof(h));
+  SPNGD_CUDA_TRY(cudaIpcGetMemHandle(&h[0], o->ag));
+  if (!o->cfg.stale && o->world > 1) {  // statistics inbox for the fused reduce-scatter
+    if (!o->inbox) o->inbox = o->alloc(size_t(o->world) * o->seg_stat, true);
+    if (!o->inbox) return fail(SPNGD_ERR_CUDA, "opt: inbox allocation failed");
+    SPNGD_CUDA_TRY(cudaIpcGetMemHandle(&h[1], o->inbox));
+  }
+  memcpy(out128, h, sizeof(h));
   return SPNGD_OK;
 }
 
@@ -1520,12 +1551,54 @@ int spngd_opt_attach_peers(spngd_opt* o, const void* handles) {
   if (o->p2p) return fail(SPNGD_ERR_INVALID, "spngd_opt_attach_peers: already attached");
   if (o->graphs_ready || o->graphs_ready_ov || o->timed)
     return fail(SPNGD_ERR_INVALID, "spngd_opt_attach_peers: call before the first step");
-  const auto* hs = static_cast<const cudaIpcMemHandle_t*>(handles);
+  const auto* hs = static_cast<const cudaIpcMemHandle_t*>(handles);  // 2 per rank: replicas, inbox
+  const bool fuse_rs = o->inbox != nullptr;
   for (int q = 0; q < o->world; ++q) {
     if (q == o->rank) continue;
     void* p = nullptr;
-    SPNGD_CUDA_TRY(cudaIpcOpenMemHandle(&p, hs[q], cudaIpcMemLazyEnablePeerAccess));
+    SPNGD_CUDA_TRY(cudaIpcOpenMemHandle(&p, hs[2 * q], cudaIpcMemLazyEnablePeerAccess));
     o->peer_ag[q] = static_cast<float*>(p);
+    if (fuse_rs) {
+      SPNGD_CUDA_TRY(cudaIpcOpenMemHandle(&p, hs[2 * q + 1], cudaIpcMemLazyEnablePeerAccess));
+      o->peer_inbox[q] = static_cast<float*>(p);
+    }
+  }
+  if (fuse_rs) {  // statistics producers write into the owners' inbox slots; owners average
+    const float* s0 = o->rs_send;
+    const float* s1 = o->rs_send + int64_t(o->world) * o->seg_stat;
+    auto remap = [&](float* p) -> float* {
+      if (p < s0 || p >= s1) return p;
+      const int64_t d = p - s0, owner = d / o->seg_stat, off = d - owner * o->seg_stat;
+      float* base = owner == o->rank ? o->inbox : o->peer_inbox[owner];
+      return base + int64_t(o->rank) * o->seg_stat + off;
+    };
+    for (auto& p : o->fplan.probs) p.C = remap(p.C);
+    for (auto& t : o->fplan.reduce) t.packed_out = remap(t.packed_out);
+    for (auto& r : o->bnm) r.out3c = remap(r.out3c);
+    auto put = [&](void* d, const void* h, size_t bytes) {
+      return (bytes && d) ? cudaMemcpy(d, h, bytes, cudaMemcpyHostToDevice) : cudaSuccess;
+    };
+    SPNGD_CUDA_TRY(put(o->d_fprobs, o->fplan.probs.data(), o->fplan.probs.size() * sizeof(GemmProblem)));
+    SPNGD_CUDA_TRY(put(o->d_freduce, o->fplan.reduce.data(), o->fplan.reduce.size() * sizeof(SyrkReduceTask)));
+    SPNGD_CUDA_TRY(put(o->d_bnm, o->bnm.data(), o->bnm.size() * sizeof(spngd_bn_moments_req)));
+    for (auto& wv : o->waves) {
+      for (auto& t : wv.reduce) t.packed_out = remap(t.packed_out);
+      SPNGD_CUDA_TRY(put(wv.d_reduce, wv.reduce.data(), wv.reduce.size() * sizeof(SyrkReduceTask)));
+    }
+    for (const StatState& st : o->stats) {
+      if (st.owner != o->rank) continue;
+      const SlotMeanTask t{o->inbox + st.off, o->rs_recv + st.off, o->seg_stat, st.count, o->world, 0};
+      o->means.push_back(t);
+      o->means_max = std::max(o->means_max, st.count);
+      if (o->overlap_ok) {
+        spngd_opt::Wave& wv = o->waves[wave_of(o->layers[st.layer].d)];
+        wv.means.push_back(t);
+        wv.means_max = std::max(wv.means_max, st.count);
+      }
+    }
+    o->d_means = dev_upload(o->means, o->owned);
+    for (auto& wv : o->waves) wv.d_means = dev_upload(wv.means, o->owned);
+    o->p2p_rs = true;
   }
   auto peers_of = [&](const float* local, float** dst) {
     const int64_t off = local - o->ag;

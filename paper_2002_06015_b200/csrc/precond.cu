@@ -296,6 +296,28 @@ int run_precondition(spngd_ctx* ctx, const PrecondPlan& plan, GemmProblem* const
   return SPNGD_OK;
 }
 
+namespace {
+__global__ void slot_mean_kernel(const SlotMeanTask* __restrict__ tasks) {
+  const SlotMeanTask t = tasks[blockIdx.y];
+  const float inv = 1.f / float(t.world);
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < t.n; i += stride) {
+    float acc = t.in[i];
+    for (int q = 1; q < t.world; ++q) acc += t.in[q * t.slot_stride + i];
+    t.out[i] = acc * inv;
+  }
+}
+}  // namespace
+
+int launch_slot_mean(spngd_ctx* ctx, const SlotMeanTask* d_tasks, int n, int64_t max_n) {
+  if (n <= 0) return SPNGD_OK;
+  dim3 grid(unsigned(std::min<int64_t>(std::max<int64_t>((max_n + 255) / 256, 1), 296)), unsigned(n));
+  slot_mean_kernel<<<grid, 256, 0, ctx->stream>>>(d_tasks);
+  SPNGD_CUDA_TRY(cudaGetLastError());
+  ctx->launches++;
+  return SPNGD_OK;
+}
+
 int launch_peer_copy(spngd_ctx* ctx, const PeerCopyTask* d_tasks, int n, int64_t max_n) {
   if (n <= 0) return SPNGD_OK;
   dim3 grid(unsigned(std::min<int64_t>(std::max<int64_t>((max_n / 4 + 255) / 256, 1), 296)), unsigned(n));

@@ -33,6 +33,19 @@ struct PeerCopyTask {
 };
 int launch_peer_copy(spngd_ctx* ctx, const PeerCopyTask* d_tasks, int n, int64_t max_n);
 
+// Owner side of the fused reduce-scatter: out = mean over the `world` source
+// slots (slot q at in + q * slot_stride), summed in ascending rank order
+// like reduce_scatter_v (dist.cpp:204-213).
+struct SlotMeanTask {
+  const float* in;
+  float* out;
+  int64_t slot_stride;
+  int64_t n;
+  int32_t world;
+  int32_t pad_;
+};
+int launch_slot_mean(spngd_ctx* ctx, const SlotMeanTask* d_tasks, int n, int64_t max_n);
+
 struct PrecondPlan {
   // Grouped GEMM launches in order: dense inverses -> 2 (P1^T = A^-1 dW^T,
   // P^T = P1^T G^-1 with EPI_UPDATE); triangular factors -> 4 (see

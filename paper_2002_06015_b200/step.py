@@ -227,14 +227,14 @@ class Optimizer:
         return dict(zip(PHASES, list(out)))
 
     def attach_peers(self, pg):
-        """Stage 5 over NVLink peer memory (spngd_opt_attach_peers): exchanges the
-        replica buffers' IPC handles over the torch.distributed group `pg` (the
+        """Stages 2-3 (statistics) and 5 over NVLink peer memory
+        (spngd_opt_attach_peers): exchanges the replica / inbox buffers' IPC handles over the torch.distributed group `pg` (the
         control plane) and attaches them.  Call on every rank before the first step."""
-        h = C.create_string_buffer(64)
+        h = C.create_string_buffer(128)
         check(N.lib().spngd_opt_ipc_handle(self.h, h))
         allh = [None] * self.world
         pg.all_gather_object(allh, h.raw)
-        buf = C.create_string_buffer(b"".join(allh), 64 * self.world)
+        buf = C.create_string_buffer(b"".join(allh), 128 * self.world)
         check(N.lib().spngd_opt_attach_peers(self.h, buf))
 
     def enable_raw_inputs(self):
