@@ -52,6 +52,14 @@ def main():
         if pg:
             pg.all_reduce(t, op=pg.ReduceOp.MAX)
         rows.append((step, refreshed, float(t.item()), {k: round(v, 3) for k, v in ph.items()}))
+    # CommLedger of the run (dist.cpp:42-133): the reference's Fig. 6 reduction
+    # rate of statistic traffic (stale-gated bytes / every-step counterfactual)
+    from paper_2002_06015_b200.spngd import ledger_report
+    rep = ledger_report(opt.ledger())
+    ledger = {"steps": rep.steps, "stat_bytes": rep.stat_bytes, "stat_bytes_every_step": rep.stat_bytes_every_step,
+              "reduction_rate": round(rep.reduction_rate, 4), "grad_bytes": rep.grad_bytes,
+              "param_bytes": rep.param_bytes, "total_bytes": rep.total_bytes,
+              "note": "reference ledger semantics: elements are 0 at one worker (dist.cpp:214)"}
     opt.close()
     if rank == 0:
         ref = [r[2] for r in rows[1:] if r[1]]       # step 1 includes graph capture
@@ -65,6 +73,7 @@ def main():
             "amortized_ms": round(sum(r[2] for r in rows[1:]) / max(1, len(rows) - 1), 3),
             "per_step": [dict(step=r[0], refreshed=r[1], ms=round(r[2], 3), phases=r[3]) for r in rows],
             "data": "synthetic, captures held fixed (Fibonacci refresh pattern)",
+            "ledger": ledger,
         }
         print(json.dumps(out), flush=True)
     if pg:
