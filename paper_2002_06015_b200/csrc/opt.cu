@@ -216,6 +216,22 @@ struct spngd_opt {
   GemmProblem* d_pp[4] = {};
   GemmWorkItem* d_pi[4] = {};
   RescaleTask* d_rescale = nullptr; double* d_norms = nullptr;
+  // Wave schedule: the precondition of layers whose inverses finish before the
+  // last inverse wave runs on its own stream beside that wave's recursion
+  // (which leaves most SMs idle); phase 4 then covers the rest.
+  struct PrePart {
+    PrecondPlan plan;
+    GemmProblem* d_pp[4] = {};
+    GemmWorkItem* d_pi[4] = {};
+    RescaleTask* d_rescale = nullptr;
+    double* d_norms = nullptr;
+  };
+  PrePart pre[2];
+  bool pre_split = false;
+  int pre_cut = 0;                 // layers of waves < pre_cut are early
+  cudaStream_t pre_stream = nullptr;
+  cudaEvent_t pre_done = nullptr;
+  bool ov_now = false;             // the running step uses the wave schedule
   std::vector<spngd_bn_update_req> bnu; spngd_bn_update_req* d_bnu = nullptr; int64_t bnu_maxc = 0;
   float* d_damps = nullptr;
   cudaEvent_t ev[7] = {};
@@ -259,6 +275,8 @@ struct spngd_opt {
       if (p) cudaIpcCloseMemHandle(p);
     for (float* p : peer_inbox)
       if (p) cudaIpcCloseMemHandle(p);
+    if (pre_done) cudaEventDestroy(pre_done);
+    if (pre_stream) cudaStreamDestroy(pre_stream);
     if (h2d_start) cudaEventDestroy(h2d_start);
     if (grads_ready) cudaEventDestroy(grads_ready);
     if (h2d_stream) cudaStreamDestroy(h2d_stream);
@@ -330,6 +348,7 @@ int build(spngd_opt* o, const spngd_layer_desc* descs, int n) {
   std::vector<DenseMatrix> mats;
   std::vector<int> mat_layer;
   std::vector<spngd_precond_req> preqs;
+  std::vector<int> preq_layer;
   std::vector<PrecondTri> ptri;
   int n_owned_kron = 0;
   for (int li = 0; li < n; ++li) {
@@ -463,6 +482,7 @@ int build(spngd_opt* o, const spngd_layer_desc* descs, int n) {
     pr.V = L.V;
     pr.rescale = o->cfg.rescale;
     preqs.push_back(pr);
+    preq_layer.push_back(li);
     ++n_owned_kron;
   }
   std::vector<void*>& own = o->owned;
@@ -610,6 +630,40 @@ int build(spngd_opt* o, const spngd_layer_desc* descs, int n) {
     o->d_pi[q] = dev_upload(o->pplan.items[q], own);
   }
   o->d_rescale = dev_upload(o->pplan.rescale, own);
+  if (o->overlap_ok && !o->cfg.sgd && !o->inv.empty()) {  // early / late precondition parts
+    int last = 0;
+    for (const auto& c : o->inv) last = std::max(last, c.wave);
+    o->pre_cut = last;
+    std::vector<spngd_precond_req> part[2];
+    std::vector<PrecondTri> ptr[2];
+    for (size_t i = 0; i < preqs.size(); ++i) {
+      const int k = wave_of(o->layers[preq_layer[i]].d) < last ? 0 : 1;
+      part[k].push_back(preqs[i]);
+      ptr[k].push_back(ptri[i]);
+    }
+    if (!part[0].empty() && !part[1].empty()) {
+      for (int k = 0; k < 2; ++k) {
+        spngd_opt::PrePart& pp = o->pre[k];
+        PrecondPlan sz;
+        if ((rc = plan_precondition(part[k].data(), int(part[k].size()), 0.0, 0.0, nullptr, nullptr, sz, nullptr,
+                                    ptr[k].data())))
+          return rc;
+        float* tmp = o->alloc(sz.tmp_floats);
+        pp.d_norms = reinterpret_cast<double*>(o->alloc(2 * part[k].size() + 2));
+        if ((rc = plan_precondition(part[k].data(), int(part[k].size()), 0.0, 0.0, tmp, pp.d_norms, pp.plan, o->d_scal,
+                                    ptr[k].data())))
+          return rc;
+        for (int q = 0; q < pp.plan.stages; ++q) {
+          pp.d_pp[q] = dev_upload(pp.plan.probs[q], own);
+          pp.d_pi[q] = dev_upload(pp.plan.items[q], own);
+        }
+        pp.d_rescale = dev_upload(pp.plan.rescale, own);
+      }
+      SPNGD_CUDA_TRY(cudaStreamCreateWithFlags(&o->pre_stream, cudaStreamNonBlocking));
+      SPNGD_CUDA_TRY(cudaEventCreateWithFlags(&o->pre_done, cudaEventDisableTiming));
+      o->pre_split = true;
+    }
+  }
   o->d_bnu = dev_upload(o->bnu, own);
   for (auto& e : o->ev) SPNGD_CUDA_TRY(cudaEventCreate(&e));
   // plan entry -> statistic maps (filtered launches: stale gating, overlap waves)
@@ -934,7 +988,12 @@ int issue_phase(spngd_opt* o, int phase) {
       return SPNGD_OK;
     }
     case 4:  // Stage 4b: precondition + update + rescale, BN solve + update (dist.cpp:604-633).
-      rc = run_precondition(ctx, o->pplan, o->d_pp, o->d_pi, o->d_rescale, o->d_norms);
+      if (o->ov_now && o->pre_split) {  // the early part already ran inside the wave schedule
+        const spngd_opt::PrePart& pp = o->pre[1];
+        rc = run_precondition(ctx, pp.plan, pp.d_pp, pp.d_pi, pp.d_rescale, pp.d_norms);
+      } else {
+        rc = run_precondition(ctx, o->pplan, o->d_pp, o->d_pi, o->d_rescale, o->d_norms);
+      }
       if (!rc)
         rc = launch_bn_update(ctx, o->d_bnu, int(o->bnu.size()), o->bnu_maxc, o->cfg.lambda, 0.0, 0.0, o->d_scal);
       for (int k = 0; k < 2 && !rc; ++k)
@@ -1036,6 +1095,17 @@ int issue_overlap(spngd_opt* o, bool capturing, bool host_in = false) {
   if (dist) {
     SPNGD_CUDA_TRY(cudaEventRecord(o->comm_done, prep));
     SPNGD_CUDA_TRY(cudaStreamWaitEvent(s, o->comm_done, 0));
+  }
+  if (o->pre_split) {  // early precondition beside the last wave's recursion
+    for (auto& c : o->inv)
+      if (c.wave < o->pre_cut) SPNGD_CUDA_TRY(cudaStreamWaitEvent(o->pre_stream, c.done, 0));
+    ctx->stream = o->pre_stream;
+    const spngd_opt::PrePart& pp = o->pre[0];
+    rc = run_precondition(ctx, pp.plan, pp.d_pp, pp.d_pi, pp.d_rescale, pp.d_norms);
+    ctx->stream = s;
+    if (rc) return rc;
+    SPNGD_CUDA_TRY(cudaEventRecord(o->pre_done, o->pre_stream));
+    SPNGD_CUDA_TRY(cudaStreamWaitEvent(s, o->pre_done, 0));
   }
   SPNGD_CUDA_TRY(mark(o->ev[3]));
   for (auto& c : o->inv) SPNGD_CUDA_TRY(cudaStreamWaitEvent(s, c.done, 0));
@@ -1310,6 +1380,7 @@ int step_impl(spngd_opt* o, int64_t step, double eta, double momentum, bool host
     o->timed = true;
     return SPNGD_OK;
   }
+  o->ov_now = ov;
   bool& ready = ov ? o->graphs_ready_ov : o->graphs_ready;
   const bool capture = o->use_graph && !ready && full && !host_in;
   const int64_t l0 = ctx->launches;
@@ -1618,6 +1689,12 @@ int spngd_opt_attach_peers(spngd_opt* o, const void* handles) {
     if (!o->pplan.rescale.empty())
       SPNGD_CUDA_TRY(cudaMemcpy(o->d_rescale, o->pplan.rescale.data(), o->pplan.rescale.size() * sizeof(RescaleTask),
                                 cudaMemcpyHostToDevice));
+    for (auto& pp : o->pre) {
+      for (auto& t : pp.plan.rescale) t.n_peers = peers_of(t.W, t.peers);
+      if (!pp.plan.rescale.empty())
+        SPNGD_CUDA_TRY(cudaMemcpy(pp.d_rescale, pp.plan.rescale.data(), pp.plan.rescale.size() * sizeof(RescaleTask),
+                                  cudaMemcpyHostToDevice));
+    }
   }
   for (size_t li = 0; li < o->layers.size(); ++li) {
     const LayerState& L = o->layers[li];
