@@ -699,7 +699,7 @@ int build(spngd_opt* o, const spngd_layer_desc* descs, int n) {
       wv.owner_ops.push_back({o->rs_send + int64_t(st.owner) * o->seg_stat + st.off, o->rs_recv + st.off, st.count,
                               st.owner});
     }
-    if (W > 1) {
+    {  // world > 1: NCCL + owner prep; world 1: pi + unpack beside the next wave's SYRK
       SPNGD_CUDA_TRY(cudaStreamCreateWithPriority(&o->comm_stream, cudaStreamNonBlocking, o->inv_prio));
       SPNGD_CUDA_TRY(cudaEventCreateWithFlags(&o->comm_fork, cudaEventDisableTiming));
       SPNGD_CUDA_TRY(cudaEventCreateWithFlags(&o->comm_done, cudaEventDisableTiming));
@@ -1019,7 +1019,7 @@ int issue_overlap(spngd_opt* o, bool capturing, bool host_in = false) {
   spngd_ctx* ctx = o->ctx;
   cudaStream_t s = ctx->stream;
   const bool dist = o->world > 1;
-  cudaStream_t prep = dist ? o->comm_stream : s;
+  cudaStream_t prep = o->comm_stream ? o->comm_stream : s;
   auto mark = [&](cudaEvent_t e) {
     return capturing ? cudaEventRecordWithFlags(e, s, cudaEventRecordExternal) : cudaEventRecord(e, s);
   };
@@ -1064,7 +1064,7 @@ int issue_overlap(spngd_opt* o, bool capturing, bool host_in = false) {
       if (rc) return rc;
       SPNGD_CUDA_TRY(mark(o->ev[2]));
     }
-    if (dist) {
+    if (prep != s) {
       SPNGD_CUDA_TRY(cudaEventRecord(wv.ready, s));
       SPNGD_CUDA_TRY(cudaStreamWaitEvent(prep, wv.ready, 0));
     }
@@ -1092,7 +1092,7 @@ int issue_overlap(spngd_opt* o, bool capturing, bool host_in = false) {
       SPNGD_CUDA_TRY(cudaEventRecord(c.done, c.stream));
     }
   }
-  if (dist) {
+  if (prep != s) {
     SPNGD_CUDA_TRY(cudaEventRecord(o->comm_done, prep));
     SPNGD_CUDA_TRY(cudaStreamWaitEvent(s, o->comm_done, 0));
   }
