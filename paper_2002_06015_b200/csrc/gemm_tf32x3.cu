@@ -35,19 +35,12 @@ namespace spngd {
 namespace {
 
 constexpr int kOperandBytes = kTileM * kTileK * 4;     // 16 KB (128 rows x 128 B)
-// smem: a kStages-deep ring of raw TMA tiles (A raw | B raw = B hi) and a
-// separate 2-slot ring of B lo planes.  The lo plane lives only from the B
-// conversion to its MMA, so keeping it out of the raw ring deepens the TMA
-// prefetch (kStages - 1 stages in flight) within the 227 KB budget.
-constexpr int kStageBytes = 2 * kOperandBytes;         // A raw, B raw (= B hi)
-constexpr int kLoSlots = 2;                            // B lo planes
-constexpr int kASlots = 4;                             // TMEM A hi|lo slots
-constexpr int kLoBase = kStages * kStageBytes;
+constexpr int kStageBytes = 3 * kOperandBytes;         // A raw, B raw (= B hi), B lo
 // Epilogue tile row stride: 132 floats keeps rows 16-byte aligned (float4
 // row access is conflict-free) and makes the (16 columns x 2 row-quads) column
 // access of the transposed/update stores conflict-free too (528 = 16 mod 32).
 constexpr int kEpiStride = kTileN + 4;
-constexpr int kTmemCols = 512;  // 2 x 128 accumulator columns + kASlots x (A hi | A lo) x 32
+constexpr int kTmemCols = 512;  // 2 x 128 accumulator columns + kStages x (A hi | A lo) x 32
 constexpr uint32_t kTmemA = 256;                       // first A-operand column
 
 struct __align__(64) SmemCtl {
@@ -56,8 +49,6 @@ struct __align__(64) SmemCtl {
   uint64_t tmem_full[2];
   uint64_t tmem_empty[2];
   uint64_t raw[2][kStages];  // TMA raw-tile arrival per operand (A, B)
-  uint64_t ta_empty[kASlots];  // MMA done with TMEM A slot
-  uint64_t lo_empty[kLoSlots]; // MMA done with B lo slot
   uint32_t tmem_base;
   int32_t pad;
   GemmProblem prob;
@@ -201,7 +192,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   // derived pointer keeps the shared address space: LDS/STS, not generic
   // LD/ST (which cost ~10k cycles per epilogue tile and slowed `prob` reads).
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  SmemCtl* ctl = reinterpret_cast<SmemCtl*>(smem + kLoBase + kLoSlots * kOperandBytes);
+  SmemCtl* ctl = reinterpret_cast<SmemCtl*>(smem + kStages * kStageBytes);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -234,8 +225,6 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       mbar_init(&ctl->tmem_empty[b], 256);
       for (int q = 0; q < kStages; ++q) mbar_init(&ctl->raw[b][q], 1);
     }
-    for (int q = 0; q < kASlots; ++q) mbar_init(&ctl->ta_empty[q], 1);
-    for (int q = 0; q < kLoSlots; ++q) mbar_init(&ctl->lo_empty[q], 1);
     mbar_fence_init();
   }
   TRACE_STAMP(meta && threadIdx.x == 0, meta[1]);
@@ -292,8 +281,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       if (lane == 0) {
         const uint32_t base = smem_u32(smem + slot * kStageBytes);
         const uint32_t b_hi = diag_shared ? base : base + kOperandBytes;
-        const uint32_t b_lo = smem_u32(smem + kLoBase + (it % kLoSlots) * kOperandBytes);
-        const uint32_t a_hi = tmem + kTmemA + (it % kASlots) * 64, a_lo = a_hi + 32;
+        const uint32_t b_lo = base + 2 * kOperandBytes;
+        const uint32_t a_hi = tmem + kTmemA + slot * 64, a_lo = a_hi + 32;
         const uint32_t dt = tmem + b * 128;
 #pragma unroll
         for (int kk = 0; kk < kTileK / 8; ++kk) {
@@ -304,8 +293,6 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           umma_tf32_ts(dt, a_hi + kk * 8, dbh, idesc, 1u);
         }
         umma_commit(&ctl->empty[slot]);
-        umma_commit(&ctl->ta_empty[it % kASlots]);
-        umma_commit(&ctl->lo_empty[it % kLoSlots]);
         umma_commit(&ctl->tmem_full[b]);
       }
       __syncwarp();
@@ -336,10 +323,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     const int rbase = t >> 3;      // cp.async: 0..15
     const int32_t row0 = (is_b ? item.tn : item.tm) * kTileM;
     const uint32_t raw_off = is_b ? kOperandBytes : 0;
-    auto lo_plane = [&](int it) {  // B lo slot of stage `it`, free once the MMA of stage it - kLoSlots is done
-      if (it >= kLoSlots) mbar_wait(&ctl->lo_empty[it % kLoSlots], ((it / kLoSlots) + 1) & 1);
-      return smem + kLoBase + (it % kLoSlots) * kOperandBytes;
-    };
+    const uint32_t blo_off = 2 * kOperandBytes;
     // Raw fp32 tiles land three stages ahead -- by TMA (one elected thread,
     // mbarrier complete_tx) when the layout allows, else by per-thread
     // cp.async.  A: each thread takes one row, writes tf32 hi/lo into TMEM
@@ -384,9 +368,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       }
 #pragma unroll
       for (int q = 0; q < 32; ++q) h[q] = __uint_as_float(__float_as_uint(x[q]) & 0xffffe000u);
-      if (it >= kASlots) mbar_wait(&ctl->ta_empty[it % kASlots], ((it / kASlots) + 1) & 1);
-      tc_fence_after();
-      const uint32_t ta = tmem + (uint32_t(warp * 32) << 16) + kTmemA + (it % kASlots) * 64;
+      const uint32_t ta = tmem + (uint32_t(warp * 32) << 16) + kTmemA + slot * 64;
       tmem_st_32x32b_x32(ta, h);
 #pragma unroll
       for (int q = 0; q < 32; ++q) {
@@ -396,10 +378,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       }
       tmem_st_32x32b_x32(ta + 32, x);
       if (diag_shared) {  // the same rows are the B operand: lo plane in smem too
-        uint8_t* lo = lo_plane(it);
 #pragma unroll
         for (int q = 0; q < 8; ++q)
-          *reinterpret_cast<float4*>(lo + r * 128 + ((q ^ (r & 7)) << 4)) =
+          *reinterpret_cast<float4*>(stage + blo_off + r * 128 + ((q ^ (r & 7)) << 4)) =
               make_float4(x[4 * q], x[4 * q + 1], x[4 * q + 2], x[4 * q + 3]);
         fence_proxy_async_smem();
       }
@@ -410,7 +391,6 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     auto convert_b = [&](int it) {
       const int slot = it % kStages;
       uint8_t* stage = smem + slot * kStageBytes;
-      uint8_t* lo = lo_plane(it);
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
         const int r = rbase + 16 * j;
@@ -421,7 +401,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         l.y = tf32_lo(x.y);
         l.z = tf32_lo(x.z);
         l.w = tf32_lo(x.w);
-        *reinterpret_cast<float4*>(lo + off) = l;
+        *reinterpret_cast<float4*>(stage + blo_off + off) = l;
       }
       fence_proxy_async_smem();
       mbar_arrive(&ctl->full[slot]);
@@ -841,7 +821,7 @@ int plan_problem_pairs(int problem_index, const GemmProblem& p, int kchunk, std:
   return used;
 }
 
-size_t gemm_smem_bytes() { return size_t(kLoBase) + size_t(kLoSlots) * kOperandBytes + sizeof(SmemCtl) + 1024; }
+size_t gemm_smem_bytes() { return size_t(kStages) * kStageBytes + sizeof(SmemCtl) + 1024; }
 
 thread_local int g_gemm_launch_prio = 0;
 

@@ -97,7 +97,7 @@ struct SyrkReduceTask {
 constexpr int kTileM = 128;
 constexpr int kTileN = 128;
 constexpr int kTileK = 32;     // fp32 elements per stage = one 128-byte swizzle row
-constexpr int kStages = 6;     // raw TMA ring depth (A raw | B raw, 32 KB per stage)
+constexpr int kStages = 4;
 constexpr int kGemmThreads = 512;  // 4 A-producer, 4 B-producer, 8 drain warps (warp 8 also issues MMAs)
 
 // Chooses the operand mode and encodes its TMA descriptor.  `K` is the true
