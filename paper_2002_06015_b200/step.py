@@ -39,8 +39,9 @@ def layer_descs(layers: List[Layer]):
     return (N.LayerDesc * len(descs))(*descs)
 
 
-def plan_layout(layers: List[Layer], world: int):
-    """Owners and owner-major RS/AG offsets (spngd_plan_layout, host only).
+def plan_layout(layers: List[Layer], world: int, bn_full: bool = False):
+    """Owners and owner-major RS/AG offsets (spngd_plan_layout_ex, host only;
+    bn_full sizes BN statistics as the packed 2c x 2c block).
 
     Returns (entries, seg_stat, seg_grad, seg_ag): A/G/M offsets are within the
     owner's statistics segment, dW within the owner's gradient segment; the
@@ -48,7 +49,8 @@ def plan_layout(layers: List[Layer], world: int):
     arr = layer_descs(layers)
     out = (N.LayoutEntry * len(layers))()
     seg_st, seg_gr, seg_ag = C.c_int64(), C.c_int64(), C.c_int64()
-    check(N.lib().spngd_plan_layout(arr, len(layers), world, out, C.byref(seg_st), C.byref(seg_gr), C.byref(seg_ag)))
+    check(N.lib().spngd_plan_layout_ex(arr, len(layers), world, 1 if bn_full else 0, out, C.byref(seg_st),
+                                       C.byref(seg_gr), C.byref(seg_ag)))
     return [dict(owner=e.owner, A=e.off_A, G=e.off_G, M=e.off_M, dW=e.off_dW, W=e.off_W) for e in out], \
         seg_st.value, seg_gr.value, seg_ag.value
 

@@ -125,3 +125,32 @@ def test_planner_rejects_bad_arguments():
     arr = layer_descs(small_net())
     assert N.lib().spngd_ledger_step_rows(arr, 3, 0, 1, None, 4, 0, None, 0) < 0
     assert N.lib().spngd_ledger_step_rows(arr, 0, 1, 1, None, 4, 0, None, 0) < 0
+
+
+@pytest.mark.parametrize("world", [1, 3, 8])
+def test_layout_entries_hold_their_payloads(world):
+    """Owner-major layout (spngd_plan_layout_ex): every statistic / gradient /
+    weight entry fits before the next one of its owner, 64-float aligned, inside
+    the padded segment; full BN sizes F as the packed 2c x 2c block."""
+    from paper_2002_06015_b200.step import plan_layout
+    net = W.resnet18_cifar()
+    for bn_full in (False, True):
+        ents, seg_st, seg_gr, seg_ag = plan_layout(net, world, bn_full)
+        spans = {}
+        for li, (l, e) in enumerate(zip(net, ents)):
+            assert 0 <= e["owner"] < world
+            if l.kind == "bn":
+                c = l.g
+                stat = [(e["M"], (2 * c) * (2 * c + 1) // 2 if bn_full else 3 * c)]
+                g_len = 2 * c
+            else:
+                stat = [(e["A"], l.a * (l.a + 1) // 2), (e["G"], l.g * (l.g + 1) // 2)]
+                g_len = l.g * l.a
+            for region, items, seg in (("st", stat, seg_st), ("gr", [(e["dW"], g_len)], seg_gr),
+                                       ("ag", [(e["W"], g_len)], seg_ag)):
+                for off, n in items:
+                    assert off % 64 == 0 and off + n <= seg
+                    spans.setdefault((region, e["owner"]), []).append((off, off + n))
+        for iv in spans.values():
+            iv.sort()
+            assert all(a[1] <= b[0] for a, b in zip(iv, iv[1:]))
