@@ -313,11 +313,33 @@ double layer_cost(const spngd_layer_desc& d, bool bn_full = false) {
 }
 
 // Overlap waves by the larger Kronecker dimension (inverse recursion depth).
-constexpr int kWaves = 3;
+// Wave boundaries on the larger Kronecker dimension, largest first; BN layers
+// (no inverse) join the last wave.  SPNGD_WAVES="3072,1536" overrides (experiments).
+const std::vector<int64_t>& wave_bounds() {
+  static const std::vector<int64_t> b = [] {
+    std::vector<int64_t> v = {3072, 1536};
+    if (const char* e = getenv("SPNGD_WAVES")) {
+      v.clear();
+      for (const char* p = e; *p;) {
+        char* end = nullptr;
+        const long long x = strtoll(p, &end, 10);
+        if (end == p) break;
+        v.push_back(x);
+        p = *end ? end + 1 : end;
+      }
+    }
+    return v;
+  }();
+  return b;
+}
+
 int wave_of(const spngd_layer_desc& d) {
-  if (d.kind == SPNGD_BN) return kWaves - 1;
+  const auto& b = wave_bounds();
+  if (d.kind == SPNGD_BN) return int(b.size());
   const int64_t m = std::max<int64_t>(d.a, d.g);
-  return m > 3072 ? 0 : (m > 1536 ? 1 : 2);
+  int w = 0;
+  while (w < int(b.size()) && m <= b[size_t(w)]) ++w;
+  return w;
 }
 
 int build(spngd_opt* o, const spngd_layer_desc* descs, int n) {
