@@ -1078,19 +1078,22 @@ int issue_overlap(spngd_opt* o, bool capturing, bool host_in = false) {
       ctx->launches++;
     }
     if (last) SPNGD_CUDA_TRY(mark(o->ev[1]));
-    rc = launch_syrk_reduce(wv.d_reduce, int(wv.reduce.size()), o->d_partials, s);
-    ctx->launches += !wv.reduce.empty();
-    if (rc) return rc;
-    if (last) {
-      rc = launch_bn_moments(ctx, o->d_bnm, int(o->bnm.size()), o->bnm_maxc);
-      if (rc) return rc;
-      SPNGD_CUDA_TRY(mark(o->ev[2]));
-    }
+    // The wave's split-K reduction and (last wave) BN moments run on the
+    // high-priority prep stream: on the main stream they queued behind the
+    // next wave's SYRK CTAs and the inverse streams' high-priority work.
     if (prep != s) {
       SPNGD_CUDA_TRY(cudaEventRecord(wv.ready, s));
       SPNGD_CUDA_TRY(cudaStreamWaitEvent(prep, wv.ready, 0));
     }
     ctx->stream = prep;
+    rc = launch_syrk_reduce(wv.d_reduce, int(wv.reduce.size()), o->d_partials, prep);
+    ctx->launches += !wv.reduce.empty();
+    if (!rc && last) rc = launch_bn_moments(ctx, o->d_bnm, int(o->bnm.size()), o->bnm_maxc);
+    if (rc) {
+      ctx->stream = s;
+      return rc;
+    }
+    if (last) SPNGD_CUDA_TRY(mark(o->ev[2]));  // main stream: after the last SYRK (reduction on prep)
     if (dist && o->p2p_rs) {  // every rank's wave-w statistics have landed in the inboxes after this
       rc = comm_allreduce_sum_f64(ctx, o->d_barrier, 1);
       if (!rc) rc = launch_slot_mean(ctx, wv.d_means, int(wv.means.size()), wv.means_max);
