@@ -30,14 +30,15 @@ B = 8
 
 
 MODES = {"default": {}, "wgrad": {"wgrad": True}, "bn_full": {"bn_mode": 1}, "one_mc": {"fisher_mode": 1},
-         "sgd": {"sgd": True}, "host": {}, "p2p": {}, "p2p_sgd": {"sgd": True}}
+         "sgd": {"sgd": True}, "host": {}, "p2p": {}, "p2p_sgd": {"sgd": True},
+         "p2p_bn_full": {"bn_mode": 1}, "p2p_wgrad": {"wgrad": True}, "p2p_host": {}}
 
 
 def main():
     mode = sys.argv[sys.argv.index("--mode") + 1] if "--mode" in sys.argv else "default"
     kw = MODES[mode]
     global B
-    if mode == "bn_full":
+    if mode.endswith("bn_full"):
         B = 320  # 2c <= 512 < P*B: full-rank F, so fp32 summation order stays below the 1e-4 gate
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", rank))
@@ -62,7 +63,7 @@ def main():
         inputs[li][WB] = opt.download(li, WB).numpy()
         if opt.owner(li) == rank:
             inputs[li][V] = opt.download(li, V).numpy()
-    if mode == "host":
+    if mode.endswith("host"):
         keep = [opt.download(li, w).pin_memory() for li, w in opt.input_buffers()]
         for li, w in opt.input_buffers():
             opt.upload(li, w, torch.full((opt.numel(li, w),), 3.0))
