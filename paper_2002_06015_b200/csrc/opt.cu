@@ -184,6 +184,8 @@ struct spngd_opt {
   std::vector<PeerCopyTask> pcopy; PeerCopyTask* d_pcopy = nullptr; int64_t pcopy_max = 0;
   double* d_barrier = nullptr;
   cudaStream_t h2d_stream = nullptr;     // spngd_opt_step_host: host inputs, wave by wave
+  cudaStream_t d2h_stream = nullptr;     // and the early layers' weights back
+  cudaEvent_t d2h_done = nullptr;
   cudaEvent_t h2d_start = nullptr, grads_ready = nullptr;
   bool overlap_ok = false;   // no stale gating
   bool overlap_on = false;
@@ -277,6 +279,8 @@ struct spngd_opt {
       if (p) cudaIpcCloseMemHandle(p);
     if (pre_done) cudaEventDestroy(pre_done);
     if (pre_stream) cudaStreamDestroy(pre_stream);
+    if (d2h_done) cudaEventDestroy(d2h_done);
+    if (d2h_stream) cudaStreamDestroy(d2h_stream);
     if (h2d_start) cudaEventDestroy(h2d_start);
     if (grads_ready) cudaEventDestroy(grads_ready);
     if (h2d_stream) cudaStreamDestroy(h2d_stream);
@@ -1527,9 +1531,28 @@ int spngd_opt_step_host(spngd_opt* o, int64_t step, double eta, double momentum,
     int rc = step_impl(o, step, eta, momentum, true);
     if (rc) return rc;
   }
-  if (host_weights_out)
-    SPNGD_CUDA_TRY(cudaMemcpyAsync(host_weights_out, o->ag,
-                                   size_t(o->world) * o->seg_ag * sizeof(float), cudaMemcpyDeviceToHost, s));
+  if (!host_weights_out) return SPNGD_OK;
+  if (pipelined && o->world == 1 && o->pre_split) {
+    // One GPU: the early-preconditioned layers' weights are final when that
+    // part ends (no all-gather), so they stream back while the last inverse
+    // wave and phase 4 still run; the rest follows the step.
+    if (!o->d2h_stream) {
+      SPNGD_CUDA_TRY(cudaStreamCreateWithFlags(&o->d2h_stream, cudaStreamNonBlocking));
+      SPNGD_CUDA_TRY(cudaEventCreateWithFlags(&o->d2h_done, cudaEventDisableTiming));
+    }
+    SPNGD_CUDA_TRY(cudaStreamWaitEvent(o->d2h_stream, o->pre_done, 0));
+    for (const LayerState& L : o->layers) {
+      const int64_t cnt = L.d.kind == SPNGD_BN ? 2 * L.d.g : L.d.g * L.d.a;
+      const bool early = L.d.kind != SPNGD_BN && wave_of(L.d) < o->pre_cut;
+      SPNGD_CUDA_TRY(cudaMemcpyAsync(host_weights_out + L.off_W, o->ag + L.off_W, size_t(cnt) * sizeof(float),
+                                     cudaMemcpyDeviceToHost, early ? o->d2h_stream : s));
+    }
+    SPNGD_CUDA_TRY(cudaEventRecord(o->d2h_done, o->d2h_stream));
+    SPNGD_CUDA_TRY(cudaStreamWaitEvent(s, o->d2h_done, 0));
+    return SPNGD_OK;
+  }
+  SPNGD_CUDA_TRY(cudaMemcpyAsync(host_weights_out, o->ag, size_t(o->world) * o->seg_ag * sizeof(float),
+                                 cudaMemcpyDeviceToHost, s));
   return SPNGD_OK;
 }
 

@@ -321,8 +321,10 @@ def test_step_host_equals_device_step(cuda_dev, raw):
     """spngd_opt_step_host: the same step fed from pinned host buffers, the H2D
     copies overlapped wave by wave with the SYRKs (and im2col of raw inputs),
     is bit-identical to the step on device-resident inputs."""
+    # conv(256, 64, 3) has a = 2304 > 1536: an earlier wave, so its precondition
+    # runs beside the last inverse wave and its weights stream back early
     layers = [W.conv(3, 16, 3, 1, 12), W.bn(16, 144), W.conv(16, 64, 3, 2, 12), W.conv(64, 256, 1, 1, 6),
-              W.bn(256, 36), W.fc(256 * 36, 10)]
+              W.bn(256, 36), W.fc(256 * 36, 10), W.conv(256, 64, 3, 1, 6)]
     B = 8
     outs = []
     for host in (False, True):
