@@ -148,6 +148,12 @@ int main() {
       cfgs.push_back({rows, cols, 32, 256, depth, 0, 3, "2x 2d 32x128 /bar", 2});
       cfgs.push_back({rows, cols, 32, 256, depth, 0, 3, "4x 2d 32x64 /bar", 4});
       cfgs.push_back({rows, cols, 128, 128, depth, 1, 0, "bulk1d 64KB", 1});
+      // wide-row boxes (no swizzle): does the per-row request rate bound ingress?
+      cfgs.push_back({rows, cols, 64, 128, depth, 0, 0, "2d 64x128 noswz (32KB)", 1});
+      cfgs.push_back({rows, cols, 128, 64, depth, 0, 0, "2d 128x64 noswz (32KB)", 1});
+      cfgs.push_back({rows, cols, 256, 32, depth, 0, 0, "2d 256x32 noswz (32KB)", 1});
+      cfgs.push_back({rows, cols, 32, 256, depth, 0, 0, "2d 32x256 noswz (32KB)", 1});
+      cfgs.push_back({rows, cols, 128, 32, depth, 1, 0, "bulk1d 16KB", 1});
       cfgs.push_back({rows, cols, 32, 128, depth, 2, 0, "ldgsts 16KB", 1});
       cfgs.push_back({rows, cols, 32, 256, depth, 2, 0, "ldgsts 32KB", 1});
     }
