@@ -246,7 +246,7 @@ struct spngd_opt {
   RepackTask* d_repack_dyn = nullptr; spngd_bn_moments_req* d_bnm_dyn = nullptr;
   std::vector<int> pi_layer;                 // owned Kronecker layers in pis order
   PiTask* d_pis_dyn = nullptr; UnpackTask* d_unpacks_dyn = nullptr;
-  spngd_stat_req* d_statreq = nullptr;
+  StatJob* d_statreq = nullptr;
   double* d_dist = nullptr; double* h_dist = nullptr;  // 4 per statistic
   cudaEvent_t dist_ev = nullptr;
   struct Pending { int q, has1, has2; };
@@ -763,7 +763,7 @@ int build(spngd_opt* o, const spngd_layer_desc* descs, int n) {
     o->d_bnm_dyn = dev_upload(o->bnm, own);
     o->d_pis_dyn = dev_upload(o->pis, own);
     o->d_unpacks_dyn = dev_upload(o->unpacks, own);
-    std::vector<spngd_stat_req> sr(o->stats.size());
+    std::vector<StatJob> sr(o->stats.size());
     o->d_statreq = dev_upload(sr, own);
     o->d_dist = reinterpret_cast<double*>(o->alloc(8 * o->stats.size(), true));
     SPNGD_CUDA_TRY(cudaMallocHost(&o->h_dist, 4 * sizeof(double) * o->stats.size()));
@@ -1287,7 +1287,7 @@ int stale_partial_phase(spngd_opt* o, int phase) {
 int stale_similarity(spngd_opt* o, int64_t step) {
   spngd_ctx* ctx = o->ctx;
   cudaStream_t s = ctx->stream;
-  std::vector<spngd_stat_req> reqs;
+  std::vector<StatJob> reqs;
   int64_t max_rows = 0;
   o->pending.clear();
   for (size_t q = 0; q < o->stats.size(); ++q) {
@@ -1302,25 +1302,19 @@ int stale_similarity(spngd_opt* o, int64_t step) {
       r.n = st.dim;
       r.kind = (st.kind == 2 && o->cfg.bn_mode == 0) ? 1 : 0;  // full BN blocks are packed symmetric
       r.out4 = o->d_dist + 4 * q;
-      reqs.push_back(r);
+      // snapshot rotation (x2 <- x1, x1 <- x) fused into the distance pass:
+      // x lands in x2's slot after the kernel has read x2 there
+      reqs.push_back(StatJob{r, st.snap[st.first ^ 1]});
       max_rows = std::max(max_rows, r.kind == 0 ? r.n : (3 * r.n + 255) / 256);
+      st.first ^= 1;
     }
+    st.nsnap = std::min(2, st.nsnap + 1);
   }
   o->pending_step = step;
   SPNGD_CUDA_TRY(cudaMemsetAsync(o->d_dist, 0, 4 * sizeof(double) * o->stats.size(), s));
   int rc = upload_async(ctx, o->d_statreq, reqs);
   if (!rc && !reqs.empty()) rc = launch_stat_distance(ctx, o->d_statreq, int(reqs.size()), max_rows);
   if (rc) return rc;
-  // snapshot rotation (x2 <- x1, x1 <- x) after the distances read them
-  for (const auto& p : o->pending) {
-    StatState& st = o->stats[p.q];
-    if (st.owner == o->rank) {
-      float* dst = st.snap[st.first ^ 1];
-      SPNGD_CUDA_TRY(cudaMemcpyAsync(dst, o->rs_recv + st.off, st.count * sizeof(float), cudaMemcpyDeviceToDevice, s));
-      st.first ^= 1;
-    }
-    st.nsnap = std::min(2, st.nsnap + 1);
-  }
   rc = comm_allreduce_sum_f64(ctx, o->d_dist, 4 * int64_t(o->stats.size()));
   if (rc) return rc;
   SPNGD_CUDA_TRY(cudaMemcpyAsync(o->h_dist, o->d_dist, 4 * sizeof(double) * o->stats.size(), cudaMemcpyDeviceToHost, s));

@@ -136,8 +136,9 @@ __global__ void sgd_update_kernel(const SgdTask* __restrict__ tasks, const float
 
 // Weighted norms of x - x1, x1, x - x2, x2 (weights 1 on the diagonal, 2 off it
 // for packed statistics; 1,2,1 for BN 3c payloads), stale.hpp:23-64.
-__global__ void stat_distance_kernel(const spngd_stat_req* __restrict__ reqs) {
-  const spngd_stat_req r = reqs[blockIdx.y];
+__global__ void stat_distance_kernel(const StatJob* __restrict__ jobs) {
+  const spngd_stat_req r = jobs[blockIdx.y].r;
+  float* __restrict__ rot = jobs[blockIdx.y].rot;
   double acc[4] = {0, 0, 0, 0};
   if (r.kind == 0) {
     for (int64_t i = blockIdx.x; i < r.n; i += gridDim.x) {
@@ -155,6 +156,7 @@ __global__ void stat_distance_kernel(const spngd_stat_req* __restrict__ reqs) {
           acc[2] += w * (x - y) * (x - y);
           acc[3] += w * y * y;
         }
+        if (rot) rot[base + j - i] = float(x);
       }
     }
   } else {
@@ -163,6 +165,7 @@ __global__ void stat_distance_kernel(const spngd_stat_req* __restrict__ reqs) {
       const double x = r.x[q];
       if (r.x1) { const double y = r.x1[q]; acc[0] += w * (x - y) * (x - y); acc[1] += w * y * y; }
       if (r.x2) { const double y = r.x2[q]; acc[2] += w * (x - y) * (x - y); acc[3] += w * y * y; }
+      if (rot) rot[q] = float(x);
     }
   }
 #pragma unroll
@@ -175,9 +178,9 @@ __global__ void stat_distance_kernel(const spngd_stat_req* __restrict__ reqs) {
 
 // The distance kernel accumulates weighted squares; the public entry point
 // returns the norms themselves (weighted_norm, stale.hpp:49-51).
-__global__ void stat_sqrt_kernel(const spngd_stat_req* __restrict__ reqs, int n) {
+__global__ void stat_sqrt_kernel(const StatJob* __restrict__ jobs, int n) {
   for (int i = threadIdx.x; i < 4 * n; i += blockDim.x) {
-    double* o = reqs[i >> 2].out4 + (i & 3);
+    double* o = jobs[i >> 2].r.out4 + (i & 3);
     *o = sqrt(fmax(*o, 0.0));
   }
 }
@@ -346,10 +349,10 @@ int launch_sgd_update(spngd_ctx* ctx, const SgdTask* d_tasks, int n, const float
   return SPNGD_OK;
 }
 
-int launch_stat_distance(spngd_ctx* ctx, const spngd_stat_req* d_reqs, int n, int64_t max_rows) {
+int launch_stat_distance(spngd_ctx* ctx, const StatJob* d_jobs, int n, int64_t max_rows) {
   if (n <= 0) return SPNGD_OK;
   dim3 grid(unsigned(std::min<int64_t>(std::max<int64_t>(max_rows, 1), 256)), unsigned(n));
-  stat_distance_kernel<<<grid, 256, 0, ctx->stream>>>(d_reqs);
+  stat_distance_kernel<<<grid, 256, 0, ctx->stream>>>(d_jobs);
   SPNGD_CUDA_TRY(cudaGetLastError());
   ctx->launches++;
   return SPNGD_OK;
@@ -412,7 +415,8 @@ extern "C" int spngd_stat_distance_batched(spngd_ctx* ctx, int n, const spngd_st
   }
   if (n == 0) return SPNGD_OK;
   DeviceScratch scratch(ctx);
-  std::vector<spngd_stat_req> v(reqs, reqs + n);
+  std::vector<StatJob> v(n);
+  for (int i = 0; i < n; ++i) v[i] = StatJob{reqs[i], nullptr};
   auto* d = scratch.upload(v);
   int rc = launch_stat_distance(ctx, d, n, max_rows);
   if (rc) return rc;

@@ -92,6 +92,14 @@ struct SgdTask {
   int64_t n;
 };
 int launch_sgd_update(spngd_ctx* ctx, const SgdTask* d_tasks, int n, const float* scal);
-int launch_stat_distance(spngd_ctx* ctx, const spngd_stat_req* d_reqs, int n, int64_t max_rows);
+// One similarity job: the public request plus, on the optimizer path, the
+// snapshot slot the statistic rotates into (x2 <- x1 <- x).  The kernel writes
+// rot[q] = x[q] right after reading x2[q] (rot is x2's slot when it exists), so
+// the rotation costs no separate copy pass.
+struct StatJob {
+  spngd_stat_req r;
+  float* rot;  // NULL: no rotation (public entry point)
+};
+int launch_stat_distance(spngd_ctx* ctx, const StatJob* d_jobs, int n, int64_t max_rows);
 
 }  // namespace spngd
