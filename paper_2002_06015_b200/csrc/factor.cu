@@ -42,22 +42,36 @@ __global__ void bn_moments_kernel(const spngd_bn_moments_req* __restrict__ reqs)
 // im2col (net.cpp:199-219) per sample: out[(s*rows + row)*hw + col], row =
 // ch*k*k + ky*k + kx, col = oy*wo + ox; coalesced writes, gathered reads that
 // hit L1/L2 k*k times.  HBM-bound: reads B*c*h*w, writes B*c*k*k*hw floats.
+// One warp per output row (s, ch, ky, kx): the row decomposition is
+// warp-uniform, and each lane walks its columns incrementally (one division
+// per lane per row) -- the per-element div/mod chain of a flat mapping made
+// the kernel issue-bound at ~0.8 TB/s (ncu, profiles/r01_kernel_captures.json).
 template <typename I>
 __device__ __forceinline__ void im2col_range(const spngd_im2col_req& r) {
   const spngd_conv_geom g = r.geom;
   const I h = I(g.h), w = I(g.w), k = I(g.k), st = I(g.stride), pad = I(g.pad), c = I(g.c_in);
   const I ho = (h + 2 * pad - k) / st + 1, wo = (w + 2 * pad - k) / st + 1;
   const I kk = k * k, rows = c * kk, hw = ho * wo;
-  const I total = I(r.batch) * rows * hw;
-  for (I e = I(blockIdx.x) * blockDim.x + threadIdx.x; e < total; e += I(gridDim.x) * blockDim.x) {
-    const I rs = e / hw, col = e - rs * hw;
+  const I nrows = I(r.batch) * rows;
+  const int lane = threadIdx.x & 31;
+  const I warps = I(gridDim.x) * (blockDim.x >> 5);
+  const I oy0 = I(lane) / wo, ox0 = I(lane) - oy0 * wo;
+  const I dy = I(32) / wo, dx = I(32) - dy * wo;  // advancing col by 32
+  for (I rs = I(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5); rs < nrows; rs += warps) {
     const I s = rs / rows, row = rs - s * rows;
     const I ch = row / kk, kyx = row - ch * kk, ky = kyx / k, kx = kyx - ky * k;
-    const I oy = col / wo, ox = col - oy * wo;
-    const I iy = oy * st + ky - pad, ix = ox * st + kx - pad;  // signed: padding reads as 0
-    float v = 0.f;
-    if (iy >= 0 && iy < h && ix >= 0 && ix < w) v = __ldg(r.x + (int64_t(s * c + ch) * h + iy) * w + ix);
-    r.out[e] = v;
+    const float* __restrict__ src = r.x + int64_t(s * c + ch) * h * w;
+    float* __restrict__ dst = r.out + int64_t(rs) * hw;
+    I oy = oy0, ox = ox0;
+    for (I col = lane; col < hw; col += 32) {
+      const I iy = oy * st + ky - pad, ix = ox * st + kx - pad;  // signed: padding reads as 0
+      float v = 0.f;
+      if (iy >= 0 && iy < h && ix >= 0 && ix < w) v = __ldg(src + iy * w + ix);
+      dst[col] = v;
+      oy += dy;
+      ox += dx;
+      if (ox >= wo) { ox -= wo; ++oy; }
+    }
   }
 }
 
