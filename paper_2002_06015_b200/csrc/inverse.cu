@@ -340,38 +340,51 @@ __global__ void pi_kernel(const PiTask* __restrict__ tasks) {
 
 // dense = unpack(packed) + d I, by 32x32 tiles of the upper triangle so both
 // the packed reads and the mirrored (transposed) dense writes are coalesced.
-__global__ void unpack_damp_kernel(const UnpackTask* __restrict__ tasks, int* status) {
-  const UnpackTask t = tasks[blockIdx.y];
+// 32-bit index math whenever the dense square fits (every ResNet-50 factor):
+// the 64-bit products made the kernel issue-bound at ~2.2 TB/s (ncu,
+// profiles/r01_kernel_captures.json).
+template <typename I>
+__device__ __forceinline__ bool unpack_damp_tiles(const UnpackTask& t, float (*s)[33]) {
   const float d = t.damp_dev ? t.damp_dev[0] : t.damp;
-  __shared__ float s[32][33];
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
-  const int64_t tn = (t.n + 31) / 32;
+  const I n = I(t.n), ld = I(t.ld);
+  const I tn = (n + 31) / 32;
   bool bad = false;
-  for (int64_t tt = blockIdx.x; tt < tn * tn; tt += gridDim.x) {
-    const int64_t ti = tt / tn, tj = tt % tn;
+  for (I tt = blockIdx.x; tt < tn * tn; tt += gridDim.x) {
+    const I ti = tt / tn, tj = tt - ti * tn;
     if (ti > tj) continue;
     __syncthreads();
+#pragma unroll
     for (int q = 0; q < 4; ++q) {
-      const int64_t i = ti * 32 + ty + 8 * q, j = tj * 32 + tx;
+      const I i = ti * 32 + ty + 8 * q, j = tj * 32 + tx;
       float v = 0.f;
-      if (i < t.n && j < t.n && j >= i) {
-        v = t.packed[i * t.n - i * (i - 1) / 2 + (j - i)];
+      if (i < n && j < n && j >= i) {
+        v = t.packed[i * n - i * (i - 1) / 2 + (j - i)];
         bad |= !isfinite(v);
         if (i == j) v += d;
       }
       s[ty + 8 * q][tx] = v;
     }
     __syncthreads();
+#pragma unroll
     for (int q = 0; q < 4; ++q) {
       const int li = ty + 8 * q;
-      const int64_t i = ti * 32 + li, j = tj * 32 + tx;
-      if (i < t.n && j < t.n) t.dense[i * t.ld + j] = (j >= i) ? s[li][tx] : s[tx][li];
+      const I i = ti * 32 + li, j = tj * 32 + tx;
+      if (i < n && j < n) t.dense[i * ld + j] = (j >= i) ? s[li][tx] : s[tx][li];
       if (ti != tj) {
-        const int64_t r = tj * 32 + li, c = ti * 32 + tx;  // transposed tile
-        if (r < t.n && c < t.n) t.dense[r * t.ld + c] = s[tx][li];
+        const I r = tj * 32 + li, c = ti * 32 + tx;  // transposed tile
+        if (r < n && c < n) t.dense[r * ld + c] = s[tx][li];
       }
     }
   }
+  return bad;
+}
+
+__global__ void unpack_damp_kernel(const UnpackTask* __restrict__ tasks, int* status) {
+  const UnpackTask t = tasks[blockIdx.y];
+  __shared__ float s[32][33];
+  const int64_t span = (t.ld > t.n ? t.ld : t.n) * (t.n + 32);
+  const bool bad = span < (int64_t(1) << 31) ? unpack_damp_tiles<int32_t>(t, s) : unpack_damp_tiles<int64_t>(t, s);
   if (bad) set_status(status, SPNGD_ERR_NOT_POSITIVE_DEFINITE);
 }
 
