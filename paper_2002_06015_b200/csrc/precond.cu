@@ -141,32 +141,22 @@ __global__ void stat_distance_kernel(const StatJob* __restrict__ jobs) {
   float* __restrict__ rot = jobs[blockIdx.y].rot;
   double acc[4] = {0, 0, 0, 0};
   if (r.kind == 0) {
-    // Four columns per thread per pass, all loads issued before the rotation
-    // stores (which may alias x2): the one-column loop was latency-bound at
-    // 0.75 TB/s (ncu, profiles/r01_kernel_captures.json).
-    const bool has1 = r.x1 != nullptr, has2 = r.x2 != nullptr;
-    const int64_t n = r.n, step = blockDim.x;
-    for (int64_t i = blockIdx.x; i < n; i += gridDim.x) {
-      const int64_t base = i * n - i * (i - 1) / 2 - i;  // packed index of (i, j) = base + j
-      for (int64_t j0 = i + threadIdx.x; j0 < n; j0 += 4 * step) {
-        float xv[4], y1[4], y2[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int64_t j = j0 + u * step;
-          const bool ok = j < n;
-          xv[u] = ok ? r.x[base + j] : 0.f;
-          y1[u] = (ok && has1) ? r.x1[base + j] : 0.f;
-          y2[u] = (ok && has2) ? r.x2[base + j] : 0.f;
+    for (int64_t i = blockIdx.x; i < r.n; i += gridDim.x) {
+      const int64_t base = i * r.n - i * (i - 1) / 2;
+      for (int64_t j = i + threadIdx.x; j < r.n; j += blockDim.x) {
+        const double w = (i == j) ? 1.0 : 2.0;
+        const double x = r.x[base + j - i];
+        if (r.x1) {
+          const double y = r.x1[base + j - i];
+          acc[0] += w * (x - y) * (x - y);
+          acc[1] += w * y * y;
         }
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int64_t j = j0 + u * step;
-          const double w = (i == j) ? 1.0 : 2.0;
-          const double x = xv[u], a = y1[u], b = y2[u];
-          if (has1) { acc[0] += w * (x - a) * (x - a); acc[1] += w * a * a; }
-          if (has2) { acc[2] += w * (x - b) * (x - b); acc[3] += w * b * b; }
-          if (rot && j < n) rot[base + j] = xv[u];
+        if (r.x2) {
+          const double y = r.x2[base + j - i];
+          acc[2] += w * (x - y) * (x - y);
+          acc[3] += w * y * y;
         }
+        if (rot) rot[base + j - i] = float(x);
       }
     }
   } else {
