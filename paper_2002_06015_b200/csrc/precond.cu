@@ -141,56 +141,22 @@ __global__ void stat_distance_kernel(const StatJob* __restrict__ jobs) {
   float* __restrict__ rot = jobs[blockIdx.y].rot;
   double acc[4] = {0, 0, 0, 0};
   if (r.kind == 0) {
-    // Flat over the packed triangle, four entries per thread (16-B loads when
-    // all four pointers are 16-B aligned, as the optimizer's buffers are).  The row of the first
-    // entry comes from the quadratic base(i) = i(2n - i + 1)/2 <= q; the rest
-    // walk forward, so the diagonal weight costs a compare.  A row-per-block
-    // mapping left most lanes idle on the short rows and ran at 0.75 TB/s.
-    const int64_t n = r.n, total = n * (n + 1) / 2;
-    const bool has1 = r.x1 != nullptr, has2 = r.x2 != nullptr;
-    const double tn1 = double(2 * n + 1);
-    const bool vec = ((reinterpret_cast<uintptr_t>(r.x) | reinterpret_cast<uintptr_t>(r.x1) |
-                       reinterpret_cast<uintptr_t>(r.x2) | reinterpret_cast<uintptr_t>(rot)) & 15) == 0;
-    for (int64_t q0 = 4 * (int64_t(blockIdx.x) * blockDim.x + threadIdx.x); q0 < total;
-         q0 += 4 * int64_t(gridDim.x) * blockDim.x) {
-      int64_t i = int64_t((tn1 - sqrt(tn1 * tn1 - 8.0 * double(q0))) * 0.5);
-      i = i < 0 ? 0 : (i >= n ? n - 1 : i);
-      while (i > 0 && i * (2 * n - i + 1) / 2 > q0) --i;
-      while ((i + 1) * (2 * n - i) / 2 <= q0) ++i;
-      int64_t base = i * (2 * n - i + 1) / 2, next = base + (n - i);
-      float xv[4], y1[4] = {0, 0, 0, 0}, y2[4] = {0, 0, 0, 0};
-      if (vec && q0 + 4 <= total) {
-        *reinterpret_cast<float4*>(xv) = *reinterpret_cast<const float4*>(r.x + q0);
-        if (has1) *reinterpret_cast<float4*>(y1) = *reinterpret_cast<const float4*>(r.x1 + q0);
-        if (has2) *reinterpret_cast<float4*>(y2) = *reinterpret_cast<const float4*>(r.x2 + q0);
-      } else {
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const bool ok = q0 + u < total;
-          xv[u] = ok ? r.x[q0 + u] : 0.f;
-          if (has1) y1[u] = ok ? r.x1[q0 + u] : 0.f;
-          if (has2) y2[u] = ok ? r.x2[q0 + u] : 0.f;
+    for (int64_t i = blockIdx.x; i < r.n; i += gridDim.x) {
+      const int64_t base = i * r.n - i * (i - 1) / 2;
+      for (int64_t j = i + threadIdx.x; j < r.n; j += blockDim.x) {
+        const double w = (i == j) ? 1.0 : 2.0;
+        const double x = r.x[base + j - i];
+        if (r.x1) {
+          const double y = r.x1[base + j - i];
+          acc[0] += w * (x - y) * (x - y);
+          acc[1] += w * y * y;
         }
-      }
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int64_t q = q0 + u;
-        while (q >= next && i + 1 < n) {  // entries past total are zeros
-          ++i;
-          base = next;
-          next += n - i;
+        if (r.x2) {
+          const double y = r.x2[base + j - i];
+          acc[2] += w * (x - y) * (x - y);
+          acc[3] += w * y * y;
         }
-        const double w = (q == base) ? 1.0 : 2.0;
-        const double x = xv[u], a = y1[u], b = y2[u];
-        if (has1) { acc[0] += w * (x - a) * (x - a); acc[1] += w * a * a; }
-        if (has2) { acc[2] += w * (x - b) * (x - b); acc[3] += w * b * b; }
-      }
-      if (rot) {
-        if (vec && q0 + 4 <= total) {
-          *reinterpret_cast<float4*>(rot + q0) = *reinterpret_cast<const float4*>(xv);
-        } else {
-          for (int u = 0; u < 4 && q0 + u < total; ++u) rot[q0 + u] = xv[u];
-        }
+        if (rot) rot[base + j - i] = float(x);
       }
     }
   } else {
