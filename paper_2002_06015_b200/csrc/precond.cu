@@ -172,7 +172,10 @@ __global__ void stat_distance_kernel(const StatJob* __restrict__ jobs) {
   for (int k = 0; k < 4; ++k)
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) acc[k] += __shfl_xor_sync(0xffffffffu, acc[k], o);
-  if ((threadIdx.x & 31) == 0)
+  // Warps that saw no entries skip their atomics: most of the grid's blocks
+  // (small statistics, short tails) had nothing to add and stalled at exit
+  // draining four atomics each (ncu: drain was the top stall reason).
+  if ((threadIdx.x & 31) == 0 && (acc[0] != 0.0 || acc[1] != 0.0 || acc[2] != 0.0 || acc[3] != 0.0))
     for (int k = 0; k < 4; ++k) atomicAdd(r.out4 + k, acc[k]);
 }
 
