@@ -10,9 +10,10 @@ weak scaling): factors + BN moments, NCCL reduce-scatter to layer owners,
 damped Cholesky inverses, preconditioning + momentum/rescale update, BN 2x2
 solve, NCCL all-gather.  Rank 0 prints one JSON line.
 
---impl reference times the reference path's CPU restatement (oracle/,
-the reference itself needs Eigen which is absent) on the host cores; under
-torchrun only rank 0 runs it.
+--gpus N without torchrun re-executes itself under torch.distributed.run with
+N ranks.  --impl reference times the reference path's fp64 CPU restatement
+(oracle/blas_step.py; the reference itself needs Eigen, which is absent) on
+the full configuration on all host cores; under torchrun only rank 0 runs it.
 """
 from __future__ import annotations
 
@@ -65,41 +66,77 @@ def peaks():
 
 
 # ---------------------------------------------------------------- CPU legs
-def cpu_sample_run(layers, batch, threads, steps, warmup):
-    from oracle.cpu_step import CpuStep
-    cs = CpuStep(layers, batch, sample_batch=2, threads=threads)
-    for _ in range(warmup):
-        cs.run()
-    ests = []
-    for _ in range(steps):
-        est, phases, wall = cs.run()
-        ests.append(est)
-    ests.sort()
-    return ests[len(ests) // 2], phases, cs.describe()
+# The reference (C++/Eigen, single-threaded) cannot be built here (no Eigen,
+# SURVEY.md §8c); its path is timed as the fp64 BLAS/LAPACK restatement in
+# oracle/blas_step.py (validated against the line-by-line oracle in
+# tests/test_blas_step.py) on the full configuration.
+def cpu_full_step(layers, batch, threads, warmup, steps, budget_s):
+    """Times whole steps of the restated reference path on `threads` BLAS
+    threads: `warmup` untimed steps, then up to `steps` timed steps while the
+    time budget lasts (at least one).  Returns (median ms, phases, n timed)."""
+    from oracle.blas_step import BlasStep, blas_threads
+    bs = BlasStep(layers, batch)
+    runs = []
+    with blas_threads(threads):
+        for _ in range(warmup):
+            bs.run()
+        t0 = time.time()
+        for _ in range(max(1, steps)):
+            runs.append(bs.run())
+            if time.time() - t0 > budget_s:
+                break
+    runs.sort(key=lambda r: r[0])
+    wall, phases, _ = runs[len(runs) // 2]
+    return wall, phases, len(runs), bs
+
+
+def cpu_single_thread(bs, layers, batch):
+    """the faithful single-threaded path on a layer sample
+    (one layer per distinct shape class plus all three 4608^2 factors); the
+    full-step figure adds each remaining layer at its class's measured time."""
+    from oracle.blas_step import blas_threads, sample_classes
+    sub = sample_classes(layers)
+    with blas_threads(1):
+        wall, phases, per = bs.run(subset=sub)
+    cls = {}
+    for i, ms in zip(sub, per):
+        l = layers[i]
+        cls.setdefault((l.kind, l.a, l.g, l.hw), ms)
+    est = sum(per) + sum(cls[(l.kind, l.a, l.g, l.hw)] for i, l in enumerate(layers) if i not in set(sub))
+    return {"sample_ms": round(wall, 1), "sample_layers": len(sub), "cores": 1,
+            "phases_ms": {k: round(v, 1) for k, v in phases.items()},
+            "full_step_ms_est": round(est, 1),
+            "sample": f"{len(sub)} of {len(layers)} layers (one per (kind, a, g, hw) class + all 4608^2 factors), "
+                      f"batch {batch}; full step = sample + remaining layers at their class's measured time"}
 
 
 def run_reference(args):
     rank, world, _ = dist_env()
     if rank != 0:
         return 0
-    from oracle.cpu_step import cpu_model, host_threads
+    from oracle.blas_step import cpu_model, host_threads
     layers, batch, desc = workload(args.config)
     threads = host_threads()
-    steps = max(1, min(args.steps, 8))
-    warm = min(args.warmup, 1)
     t0 = time.time()
-    value, phases, sample = cpu_sample_run(layers, batch, threads, steps, warm)
+    budget = float(os.environ.get("SPNGD_REF_BUDGET_S", "150"))
+    warm = min(args.warmup, 1)
+    value, phases, steps, _ = cpu_full_step(layers, batch, threads, warm, args.steps, budget)
     line = {
         "impl": "reference", "metric": METRIC, "value": round(value, 3), "unit": UNIT,
         "n_gpus": args.gpus, "steps": steps, "warmup": warm, "ms_per_step": round(value, 3),
         "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
-        "config": {"workload": f"{desc} (CPU restatement of the reference path, sampled)",
-                   "global_batch": batch * args.gpus, "per_gpu_batch": batch, "parallelism": "host threads"},
+        "config": {"workload": desc, "global_batch": batch * args.gpus, "per_gpu_batch": batch,
+                   "parallelism": f"host BLAS threads x{threads} (one rank's shard)"},
         "cpu_baseline": {"value": round(value, 3), "unit": UNIT, "cores": threads, "kind": "port",
-                         "cpu": cpu_model(), "sample": sample, "phases_ms": {k: round(v, 1) for k, v in phases.items()}},
+                         "cpu": cpu_model(),
+                         "sample": f"the full {len(layers)}-layer step (no sampling), {steps} timed step(s) after "
+                                   f"{warm} warm-up, median",
+                         "phases_ms": {k: round(v, 1) for k, v in phases.items()}},
         "e2e": {"value": round(value, 3), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        "note": "reference C++ needs Eigen3 (absent); timed its fp64 restatement oracle/spngd_oracle.cpp",
+        "note": ("reference C++/Eigen is not buildable here (no Eigen3); timed its fp64 restatement "
+                 "oracle/blas_step.py (Eigen's LLT/solve(I)/GEMM/row-dot calls as LAPACK/BLAS, per-sample "
+                 "factor accumulation as in mean_outer), steps capped by a %.0f s budget" % budget),
         "wall_s": round(time.time() - t0, 1),
     }
     print(json.dumps(line), flush=True)
@@ -314,13 +351,38 @@ def run_ours(args):
                                       "CUDA events around the factor SYRK launch in the timed steps"),
                     "step_share": round(fac_ms / max(sum((serial or {}).get("phases_ms_last_step", phases).values()),
                                                      1e-9), 3)}
+        # The other two tensor-core phases of north_star's target, from the
+        # same phase-serial pass (CUDA events on the library stream; each span
+        # is the phase's grouped GEMM launches plus its small helpers).
+        sp = (serial or {}).get("phases_ms_last_step", phases)
+        rooflines = {
+            "factor_syrk": {k: roofline[k] for k in ("achieved", "peak", "frac", "launch_ms")},
+            "precondition": {"achieved": round(fp / (sp["precondition_update"] * 1e-3) / 1e12, 2),
+                             "peak": round(peak, 2), "unit": "TFLOP/s",
+                             "frac": round(fp / (sp["precondition_update"] * 1e-3) / 1e12 / peak, 4),
+                             "span_ms": sp["precondition_update"],
+                             "algorithmic": f"{fp / 1e9:.1f} GF (SURVEY §8d F_pre = sum 2g^2a + 2ga^2)",
+                             "span": "four triangular 3xTF32 GEMM launches (T_A, T_A^T, T_G, T_G^T) with the "
+                                     "momentum/velocity/norm epilogue + rescale + BN det check + BN solve/update"},
+            "inverse": {"achieved": round(fi / (sp["inverse"] * 1e-3) / 1e12, 2), "peak": round(peak, 2),
+                        "unit": "TFLOP/s", "frac": round(fi / (sp["inverse"] * 1e-3) / 1e12 / peak, 4),
+                        "span_ms": sp["inverse"],
+                        "algorithmic": f"{fi / 1e9:.1f} GF (SURVEY §8d F_inv = sum a^3 + g^3)",
+                        "span": "pi + unpack/damping + every recursion round (leaves + grouped 3xTF32 GEMMs) of "
+                                "all 108 factors, size classes on concurrent streams"},
+        }
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
-            from oracle.cpu_step import cpu_model, host_threads
+            from oracle.blas_step import cpu_model, host_threads
             thr = host_threads()
-            v, ph, sample = cpu_sample_run(layers, batch, thr, 3, 1)
+            v, ph, nsteps, bs = cpu_full_step(layers, batch, thr, 0, 1, 0.0)
+            single = cpu_single_thread(bs, layers, batch)
+            del bs
             cpu = {"value": round(v, 1), "unit": UNIT, "cores": thr, "kind": "port", "cpu": cpu_model(),
-                   "sample": sample, "phases_ms": {k: round(x, 1) for k, x in ph.items()}}
+                   "sample": f"the full {len(layers)}-layer step at batch {batch} (no sampling), one timed step, "
+                             "fp64 BLAS/LAPACK restatement of the reference path (oracle/blas_step.py)",
+                   "phases_ms": {k: round(x, 1) for k, x in ph.items()},
+                   "single_thread": single}
         line = {
             "metric": METRIC, "value": round(step_ms, 4), "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(step_ms, 4), "higher_is_better": False,
@@ -330,7 +392,7 @@ def run_ours(args):
                        "per_gpu_batch": batch, "seq_len": None, "parallelism": f"hybrid dp/mp x{world}",
                        "lambda": args.lam, "eta": 1.25e-2, "momentum": 0.993, "rescale": True,
                        "l2": f"inputs > L2: {W.capture_bytes(layers, batch) / 1e9:.2f} GB of captures per step"},
-            "phases_ms_last_step": {k: round(v, 3) for k, v in phases.items()},
+            "phases_ms_last_step": overlap_labels(phases, world),
             "schedule": "waves: inverse recursion of the largest factors runs on high-priority streams while the "
                         "remaining factor SYRKs run" + ("; per-wave owner reductions on a comm stream" if world > 1 else "")
                         + ("; Stage 5 as NVLink peer stores fused into the rescale pass" if p2p else ""),
@@ -340,6 +402,7 @@ def run_ours(args):
                     if args.e2e_steps > 0 else None),
             "gpu_launches": launches * args.steps,
             "roofline": roofline,
+            "rooflines": rooflines,
             "cpu_baseline": cpu,
             "clocks": clocks,
             "wall_s_timed": round(wall_s, 3),
@@ -352,6 +415,18 @@ def run_ours(args):
     return 0
 
 
+def overlap_labels(phases, world):
+    """The six event spans of an overlapped (wave) step, named by what runs in
+    them: in that schedule the inverse recursion runs beside the factor SYRKs,
+    so the phase-serial names (factor_gemm, ..., inverse) do not apply."""
+    v = list(phases.values())
+    names = ["factor_syrk_waves (earlier waves' inverses overlapped)", "last_wave_reduce_and_bn_moments",
+             ("comm_join_and_" if world > 1 else "") + "early_precondition (layers of the earlier waves)",
+             "inverse_tail (last wave's recursion)", "precondition_update_late_and_bn",
+             "all_gather" if world > 1 else "all_gather (none at P=1)"]
+    return {n: round(x, 3) for n, x in zip(names, v)}
+
+
 def load_traffic():
     """dram bytes per launch of the factor GEMM from the committed ncu capture."""
     p = os.path.join(ROOT, "profiles", "factor_gemm_traffic.json")
@@ -362,10 +437,33 @@ def load_traffic():
         return None
 
 
+def relaunch(args):
+    """`bench.py --gpus N` outside torchrun: re-exec under torch.distributed.run
+    with N ranks on this node (rendezvous on 127.0.0.1), same arguments."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    os.execv(sys.executable, cmd)
+
+
 def main():
     args = parse()
+    world_env = os.environ.get("WORLD_SIZE")
     if args.impl == "reference":
         return run_reference(args)
+    if world_env is None and args.gpus > 1:
+        relaunch(args)
+    world = int(world_env or 1)
+    if world != args.gpus:
+        print(json.dumps({"error": f"--gpus {args.gpus} but WORLD_SIZE={world}: launch one rank per GPU"}),
+              flush=True)
+        return 2
+    if world > 1:  # NCCL's init lines (ranks, transports) stay in the log
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
     return run_ours(args)
 
 

@@ -168,7 +168,13 @@ typedef struct spngd_spd_req {
   int64_t ld;
   float* packed_out;     /* may be NULL */
 } spngd_spd_req;
-int spngd_spd_inverse_batched(spngd_ctx* ctx, int n, const spngd_spd_req* reqs);
+/* info: host array of n ints (may be NULL), 0 or the error code of each
+ * request; the returned status is that of the first failing request and
+ * spngd_last_error() names it (request index, factor, n).  Matrices whose
+ * ||M + dI||_F / d exceeds 1.5e4 (an upper bound of cond(M + dI)) get one
+ * step of iterative refinement with a residual formed from exact tf32 splits
+ * (SPNGD_REFINE_COND overrides the threshold; < 0 disables). */
+int spngd_spd_inverse_batched(spngd_ctx* ctx, int n, const spngd_spd_req* reqs, int* info);
 
 /* Replaces damp_and_invert (src/fisher.cpp:218-228) incl. avg_eigenvalue
  * (src/linalg.cpp:64-69): pi = sqrt((trA/a)/(trG/g)) (1 if either < 1e-12),
@@ -183,7 +189,8 @@ typedef struct spngd_kron_req {
   float* Ginv_packed;
   float* pi_out;                    /* device float (may be NULL) */
 } spngd_kron_req;
-int spngd_damp_and_invert_batched(spngd_ctx* ctx, int n, const spngd_kron_req* reqs, double lambda);
+/* info: as for spngd_spd_inverse_batched, per request (either factor). */
+int spngd_damp_and_invert_batched(spngd_ctx* ctx, int n, const spngd_kron_req* reqs, double lambda, int* info);
 
 /* ---- K5/K6: preconditioning + momentum/rescale update ------------------------
  * Replaces precondition/kron_matvec (src/fisher.cpp:255-257,
@@ -375,6 +382,12 @@ int spngd_opt_step_host(spngd_opt* opt, int64_t step, double eta, double momentu
  * inputs (bit-identical at world == 1); at world > 1 the statistics are
  * averaged by per-wave ncclReduce instead of one ncclReduceScatter, so only
  * NCCL's summation order can differ.  Must match on every rank. */
+/* spngd_ctx_sync for the optimizer: a failed step (NotPositiveDefinite,
+ * SingularBlock) is reported with the layer tag of the first failing factor
+ * or BN channel (fisher.cpp:48-51 layer_tag).  Parameters are untouched by a
+ * failed phase-serial step; with the wave overlap (spngd_opt_set_overlap 1)
+ * layers preconditioned before the last inverse wave may already be updated. */
+int spngd_opt_sync(spngd_opt* opt);
 int spngd_opt_set_overlap(spngd_opt* opt, int on);
 /* Per-phase device milliseconds of the last step: factor GEMM, factor
  * reduction + BN moments, reduce_scatter, inverse, precondition + BN update,

@@ -118,7 +118,7 @@ EXPORTS = [
     "spngd_tracker_should_refresh", "spngd_tracker_on_refresh", "spngd_tracker_state",
     "spngd_nccl_unique_id", "spngd_ctx_init_comm", "spngd_reduce_scatter_mean", "spngd_all_gather",
     "spngd_plan_layout", "spngd_opt_create", "spngd_opt_destroy", "spngd_opt_buffer", "spngd_opt_owner", "spngd_opt_step",
-    "spngd_opt_phase_ms", "spngd_opt_launch_count", "spngd_opt_stale_info", "spngd_opt_set_overlap",
+    "spngd_opt_phase_ms", "spngd_opt_launch_count", "spngd_opt_stale_info", "spngd_opt_set_overlap", "spngd_opt_sync",
 ]
 
 
@@ -160,8 +160,9 @@ def _declare(L):
         "spngd_bn_full_moments_batched": (C.c_int, [P, C.c_int, C.POINTER(BnFullReq)]),
         "spngd_bn_full_solve_update_batched": (C.c_int, [P, C.c_int, C.POINTER(BnFullUpdateReq), C.c_double,
                                                          C.c_double]),
-        "spngd_spd_inverse_batched": (C.c_int, [P, C.c_int, C.POINTER(SpdReq)]),
-        "spngd_damp_and_invert_batched": (C.c_int, [P, C.c_int, C.POINTER(KronReq), C.c_double]),
+        "spngd_spd_inverse_batched": (C.c_int, [P, C.c_int, C.POINTER(SpdReq), C.POINTER(C.c_int)]),
+        "spngd_damp_and_invert_batched": (C.c_int, [P, C.c_int, C.POINTER(KronReq), C.c_double,
+                                                   C.POINTER(C.c_int)]),
         "spngd_precondition_update_batched": (C.c_int, [P, C.c_int, C.POINTER(PrecondReq),
                                                         C.c_double, C.c_double]),
         "spngd_bn_solve_update_batched": (C.c_int, [P, C.c_int, C.POINTER(BnUpdateReq), C.c_double,
@@ -190,6 +191,7 @@ def _declare(L):
         "spngd_opt_step": (C.c_int, [P, _i64, C.c_double, C.c_double]),
         "spngd_opt_phase_ms": (C.c_int, [P, C.POINTER(C.c_float)]),
         "spngd_opt_set_overlap": (C.c_int, [P, C.c_int]),
+        "spngd_opt_sync": (C.c_int, [P]),
         "spngd_opt_launch_count": (_i64, [P]),
         "spngd_opt_stale_info": (C.c_int, [P, C.c_int, C.c_int, C.POINTER(_i64), C.POINTER(_i64), C.POINTER(_i64),
                                            C.POINTER(C.c_int)]),

@@ -29,7 +29,8 @@ __global__ void bn_interleave_kernel(const InterleaveTask* __restrict__ tasks) {
 }
 
 __global__ void bn_full_update_kernel(const spngd_bn_full_update_req* __restrict__ reqs, double eta, double momentum,
-                                      const float* __restrict__ scal) {
+                                      const float* __restrict__ scal, const int* __restrict__ status) {
+  if (*status) return;  // see rescale_kernel (precond.cu)
   if (scal) {
     eta = scal[0];
     momentum = scal[1];
@@ -80,7 +81,7 @@ int launch_bn_full_update(spngd_ctx* ctx, const spngd_bn_full_update_req* d_reqs
                           double momentum, const float* scal) {
   if (n <= 0) return SPNGD_OK;
   dim3 grid(unsigned(std::min<int64_t>((max_dim + 7) / 8, 1024)), unsigned(n));
-  bn_full_update_kernel<<<grid, 256, 0, ctx->stream>>>(d_reqs, eta, momentum, scal);
+  bn_full_update_kernel<<<grid, 256, 0, ctx->stream>>>(d_reqs, eta, momentum, scal, ctx->d_status);
   SPNGD_CUDA_TRY(cudaGetLastError());
   ctx->launches++;
   return SPNGD_OK;

@@ -56,15 +56,24 @@ int spngd_ctx_create(int device, void* stream, spngd_ctx** out) {
   if (prop.major != 10)
     return spngd::fail(SPNGD_ERR_CUDA, "spngd_ctx_create: device %d is sm_%d%d, need sm_100 (B200)", device,
                        prop.major, prop.minor);
-  // Keep stream-ordered scratch (DeviceScratch) cached across calls instead of
-  // returning it to the driver at every synchronisation.
-  cudaMemPool_t pool;
-  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
-    uint64_t keep = UINT64_MAX;
-    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
-  }
   auto* c = new spngd_ctx();
   c->device = device;
+  // A private stream-ordered pool for DeviceScratch, kept cached across calls
+  // (release threshold = max) without touching the device's default pool,
+  // which other cudaMallocAsync users (e.g. PyTorch's async allocator) share.
+  {
+    cudaMemPoolProps props{};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = device;
+    cudaError_t pe = cudaMemPoolCreate(&c->pool, &props);
+    if (pe != cudaSuccess) {
+      delete c;
+      return spngd::fail_cuda(pe, "cudaMemPoolCreate");
+    }
+    uint64_t keep = UINT64_MAX;
+    cudaMemPoolSetAttribute(c->pool, cudaMemPoolAttrReleaseThreshold, &keep);
+  }
   if (stream) {
     c->stream = static_cast<cudaStream_t>(stream);
   } else {
@@ -86,6 +95,7 @@ void spngd_ctx_destroy(spngd_ctx* ctx) {
   if (ctx->h_status) cudaFreeHost(ctx->h_status);
   if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
   spngd::comm_destroy(ctx);
+  if (ctx->pool) cudaMemPoolDestroy(ctx->pool);
   delete ctx;
 }
 

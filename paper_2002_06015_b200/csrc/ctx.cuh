@@ -22,11 +22,12 @@ struct spngd_ctx {
   int world = 1, rank = 0;
   int64_t launches = 0;         // kernels launched through this context
   int launch_prio = 0;          // != 0: cudaLaunchAttributePriority of the recursion kernels
+  cudaMemPool_t pool = nullptr; // private stream-ordered pool of DeviceScratch (kept cached)
 };
 
 namespace spngd {
 
-// Stream-ordered scratch buffer (cudaMallocAsync) released at scope exit.
+// Stream-ordered scratch buffer from the context's private pool, released at scope exit.
 class DeviceScratch {
  public:
   DeviceScratch(spngd_ctx* ctx) : ctx_(ctx) {}
@@ -37,7 +38,7 @@ class DeviceScratch {
   T* alloc(size_t count) {
     void* p = nullptr;
     if (count == 0) count = 1;
-    if (cudaMallocAsync(&p, count * sizeof(T), ctx_->stream) != cudaSuccess) return nullptr;
+    if (cudaMallocFromPoolAsync(&p, count * sizeof(T), ctx_->pool, ctx_->stream) != cudaSuccess) return nullptr;
     static const bool poison = getenv("SPNGD_POISON_SCRATCH") != nullptr;  // debug: NaN-fill fresh scratch
     if (poison) cudaMemsetAsync(p, 0xff, count * sizeof(T), ctx_->stream);
     ptrs_.push_back(p);

@@ -601,6 +601,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       break;
     }
     case EPI_UPDATE: if constexpr ((kModes >> EPI_UPDATE) & 1) {
+      // No parameter writes after a failed inverse / BN check (precond.cu).
+      if (e.W && status && *reinterpret_cast<volatile int*>(status)) break;
       // Tile of P^T: rows = a-index (M = a), cols = g-index.  W is g x a
       // row-major, so element (i = n0+c, j = m0+r) lives at W[i*a + j]:
       // column chunks of T are contiguous in W.

@@ -9,7 +9,8 @@
 //     chol(S) -> T22 (recurse),  T21 = -T22 U,      finally X = T^T T.
 // Every update is a K-major GEMM on the 3xTF32 tcgen05 engine; triangular
 // operands trim the K range per tile.  Leaves (n <= 128) run one CTA that
-// factors in fp64 registers and forms T by forward elimination.  A
+// factors in fp32 registers and forms T by forward elimination.  Explicit
+// inverses of ill-conditioned matrices get one refinement step (refine.cu).  A
 // non-positive or non-finite pivot raises NotPositiveDefinite (the LLT
 // failure of linalg.cpp:37-40).  X is written upper-tile + mirrored, so the
 // result is exactly symmetric as the reference's 0.5 (X + X^T) makes it.
@@ -18,6 +19,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
+#include <cstring>
 
 #include "ctx.cuh"
 #include "inverse.cuh"
@@ -266,7 +268,10 @@ __global__ void __launch_bounds__(kBaseThreads, 1) base_chol_inv_kernel(const Ba
   __syncthreads();
   leaf_blocks<0>(x, nb, warp, lane, buf, bad);
   LEAF_STAMP(2);
-  if (bad) set_status(status, SPNGD_ERR_NOT_POSITIVE_DEFINITE);
+  if (bad) {
+    set_status(status, SPNGD_ERR_NOT_POSITIVE_DEFINITE);
+    if (t.info && threadIdx.x % 32 == 0) *t.info = SPNGD_ERR_NOT_POSITIVE_DEFINITE;
+  }
   // T = lower triangle of X -> staging (zeros above the diagonal).
 #pragma unroll
   for (int g = 0; g < 4; ++g)
@@ -385,7 +390,10 @@ __global__ void unpack_damp_kernel(const UnpackTask* __restrict__ tasks, int* st
   __shared__ float s[32][33];
   const int64_t span = (t.ld > t.n ? t.ld : t.n) * (t.n + 32);
   const bool bad = span < (int64_t(1) << 31) ? unpack_damp_tiles<int32_t>(t, s) : unpack_damp_tiles<int64_t>(t, s);
-  if (bad) set_status(status, SPNGD_ERR_NOT_POSITIVE_DEFINITE);
+  if (bad) {
+    set_status(status, SPNGD_ERR_NOT_POSITIVE_DEFINITE);
+    if (t.info) *t.info = SPNGD_ERR_NOT_POSITIVE_DEFINITE;
+  }
 }
 
 __global__ void pack_kernel(const PackTask* __restrict__ tasks, int* status) {
@@ -396,10 +404,13 @@ __global__ void pack_kernel(const PackTask* __restrict__ tasks, int* status) {
     for (int64_t j = i + threadIdx.x; j < t.n; j += blockDim.x) {
       const float v = t.dense[i * t.ld + j];
       bad |= !isfinite(v);
-      t.packed[base + (j - i)] = v;
+      if (t.packed) t.packed[base + (j - i)] = v;
     }
   }
-  if (bad) set_status(status, SPNGD_ERR_NOT_POSITIVE_DEFINITE);
+  if (bad) {  // spd_inverse's "inverse has non-finite entries" (linalg.cpp:41-43)
+    set_status(status, SPNGD_ERR_NOT_POSITIVE_DEFINITE);
+    if (t.info) *t.info = SPNGD_ERR_NOT_POSITIVE_DEFINITE;
+  }
 }
 
 // ---------------------------------------------------------------- planning
@@ -467,7 +478,8 @@ void gen_chol(const DenseMatrix& m, int64_t off, int64_t n, Gen& g, std::vector<
   if (n <= kBaseMax) {
     Op o{};
     o.kind = 0;
-    o.base = BaseTask{at(m.ptr, ld, off, off), at(m.tlow, ld, off, off), at(m.tup, ld, off, off), ld, int32_t(n), 0};
+    o.base = BaseTask{at(m.ptr, ld, off, off), at(m.tlow, ld, off, off), at(m.tup, ld, off, off), ld, int32_t(n), 0,
+                      m.info};
     ops.push_back(o);
     return;
   }
@@ -651,35 +663,50 @@ int run_inverse(spngd_ctx* ctx, const InversePlan& plan, const GemmProblem* d_pr
 
 using namespace spngd;
 
-extern "C" int spngd_spd_inverse_batched(spngd_ctx* ctx, int n, const spngd_spd_req* reqs) {
-  if (!ctx || (n > 0 && !reqs)) return fail(SPNGD_ERR_INVALID, "spngd_spd_inverse_batched: null argument");
-  if (n == 0) return SPNGD_OK;
-  DeviceScratch scratch(ctx);
+namespace {
+
+// One matrix of a batched explicit-inverse call.
+struct InvItem {
+  const float* packed;
+  int64_t n;
+  float damp;             // host damping (unused when damp_dev)
+  const float* damp_dev;  // device damping (damp_and_invert's pi-scaled values)
+  float* dense;           // n x ld output (or scratch)
+  int64_t ld;
+  float* packed_out;      // may be null
+  int req;                // request index (info[] slot)
+  int side;               // 0: spd_inverse / A factor, 1: G factor
+};
+
+// unpack + damping, recursive Cholesky inverse, refinement of the
+// ill-conditioned ones, finite check + pack; per-matrix status in info[req]
+// (host array of n_req, may be null).  Synchronous.
+int batched_inverse(spngd_ctx* ctx, DeviceScratch& scratch, std::vector<InvItem>& items, const PiTask* d_pis,
+                    int n_pis, int n_req, int* info, const char* who) {
+  const int nm = int(items.size());
+  int* d_info = scratch.alloc<int>(nm);
+  double* d_fro = scratch.alloc<double>(nm);
+  float* d_damp = scratch.alloc<float>(nm);
+  if (!d_info || !d_fro || !d_damp) return fail(SPNGD_ERR_CUDA, "%s: allocation failed", who);
+  SPNGD_CUDA_TRY(cudaMemsetAsync(d_info, 0, sizeof(int) * nm, ctx->stream));
+  SPNGD_CUDA_TRY(cudaMemsetAsync(d_fro, 0, sizeof(double) * nm, ctx->stream));
   std::vector<DenseMatrix> mats;
   std::vector<UnpackTask> unpack;
+  std::vector<FroTask> fro;
   std::vector<PackTask> pack;
   int64_t max_n = 0;
-  for (int i = 0; i < n; ++i) {
-    const spngd_spd_req& r = reqs[i];
-    if (r.n <= 0) return fail(SPNGD_ERR_SHAPE_MISMATCH, "spd_inverse: empty matrix");
-    if (!r.packed || (!r.dense_out && !r.packed_out)) return fail(SPNGD_ERR_INVALID, "spd_inverse: null pointer");
-    if (r.dense_out && r.ld < r.n) return fail(SPNGD_ERR_SHAPE_MISMATCH, "spd_inverse: ld < n");
-    float* dense = r.dense_out;
-    int64_t ld = r.ld;
-    if (!dense) {
-      ld = round_up(r.n, 32);
-      dense = scratch.alloc<float>(size_t(r.n) * ld);
-      if (!dense) return fail(SPNGD_ERR_CUDA, "spd_inverse: allocation failed");
-    }
-    float* tl = scratch.alloc<float>(size_t(r.n) * ld);
-    float* tu = scratch.alloc<float>(size_t(r.n) * ld);
-    if (!tl || !tu) return fail(SPNGD_ERR_CUDA, "spd_inverse: allocation failed");
-    cudaMemsetAsync(tl, 0, sizeof(float) * r.n * ld, ctx->stream);
-    cudaMemsetAsync(tu, 0, sizeof(float) * r.n * ld, ctx->stream);
-    mats.push_back({dense, tl, tu, ld, r.n});
-    unpack.push_back({r.packed, r.n, r.damping_dev, r.damping, 0, dense, ld});
-    if (r.packed_out) pack.push_back({dense, ld, r.n, r.packed_out});
-    max_n = std::max(max_n, r.n);
+  for (int q = 0; q < nm; ++q) {
+    InvItem& it = items[q];
+    float* tl = scratch.alloc<float>(size_t(it.n) * it.ld);
+    float* tu = scratch.alloc<float>(size_t(it.n) * it.ld);
+    if (!tl || !tu) return fail(SPNGD_ERR_CUDA, "%s: allocation failed", who);
+    SPNGD_CUDA_TRY(cudaMemsetAsync(tl, 0, sizeof(float) * it.n * it.ld, ctx->stream));
+    SPNGD_CUDA_TRY(cudaMemsetAsync(tu, 0, sizeof(float) * it.n * it.ld, ctx->stream));
+    mats.push_back({it.dense, tl, tu, it.ld, it.n, d_info + q});
+    unpack.push_back({it.packed, it.n, it.damp_dev, it.damp, 0, it.dense, it.ld, d_info + q});
+    fro.push_back({it.packed, it.n, it.damp_dev, it.damp, 0, d_fro + q});
+    pack.push_back({it.dense, it.ld, it.n, it.packed_out, d_info + q});
+    max_n = std::max(max_n, it.n);
   }
   InversePlan sizing;
   plan_inverse(mats, nullptr, sizing);
@@ -687,32 +714,99 @@ extern "C" int spngd_spd_inverse_batched(spngd_ctx* ctx, int n, const spngd_spd_
   InversePlan plan;
   plan_inverse(mats, ws, plan);
   auto* d_unpack = scratch.upload(unpack);
-  auto* d_pack = scratch.upload(pack);
+  auto* d_fro_t = scratch.upload(fro);
   auto* d_probs = scratch.upload(plan.probs);
   auto* d_items = scratch.upload(plan.items);
   auto* d_bases = scratch.upload(plan.bases);
-  int rc = launch_unpack(ctx, d_unpack, int(unpack.size()), max_n);
+  int rc = launch_pi(ctx, d_pis, n_pis);
+  if (!rc) rc = launch_unpack(ctx, d_unpack, nm, max_n);
+  if (!rc) rc = launch_fro(ctx, d_fro_t, nm, max_n);
   if (!rc) rc = run_inverse(ctx, plan, d_probs, d_items, d_bases);
-  if (!rc) rc = launch_pack(ctx, d_pack, int(pack.size()), max_n);
   if (rc) return rc;
-  return spngd_ctx_sync(ctx);
+  // refine the matrices whose cond bound ||M + dI||_F / d passes the threshold
+  const double thr = refine_threshold();
+  if (std::isfinite(thr)) {
+    std::vector<double> h_fro(nm);
+    std::vector<int> h_info(nm);
+    std::vector<float> h_damp(nm);
+    for (int q = 0; q < nm; ++q)
+      if (items[q].damp_dev)
+        SPNGD_CUDA_TRY(cudaMemcpyAsync(d_damp + q, items[q].damp_dev, sizeof(float), cudaMemcpyDeviceToDevice,
+                                       ctx->stream));
+    SPNGD_CUDA_TRY(cudaMemcpyAsync(h_fro.data(), d_fro, sizeof(double) * nm, cudaMemcpyDeviceToHost, ctx->stream));
+    SPNGD_CUDA_TRY(cudaMemcpyAsync(h_info.data(), d_info, sizeof(int) * nm, cudaMemcpyDeviceToHost, ctx->stream));
+    SPNGD_CUDA_TRY(cudaMemcpyAsync(h_damp.data(), d_damp, sizeof(float) * nm, cudaMemcpyDeviceToHost, ctx->stream));
+    SPNGD_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    std::vector<RefineJob> jobs;
+    for (int q = 0; q < nm; ++q) {
+      const float d = items[q].damp_dev ? h_damp[q] : items[q].damp;
+      if (h_info[q] || !(d > 0.f)) continue;
+      if (std::sqrt(h_fro[q]) / double(d) > thr) jobs.push_back({items[q].packed, items[q].n, d, items[q].dense, items[q].ld});
+    }
+    rc = refine_inverses(ctx, scratch, jobs);
+    if (rc) return rc;
+  }
+  auto* d_pack = scratch.upload(pack);
+  rc = launch_pack(ctx, d_pack, nm, max_n);
+  if (rc) return rc;
+  std::vector<int> h_info(nm);
+  SPNGD_CUDA_TRY(cudaMemcpyAsync(h_info.data(), d_info, sizeof(int) * nm, cudaMemcpyDeviceToHost, ctx->stream));
+  rc = spngd_ctx_sync(ctx);
+  if (info)
+    for (int r = 0; r < n_req; ++r) info[r] = 0;
+  int first = -1;
+  for (int q = 0; q < nm; ++q) {
+    if (!h_info[q]) continue;
+    if (info && !info[items[q].req]) info[items[q].req] = h_info[q];
+    if (first < 0) first = q;
+  }
+  if (first >= 0) {  // name the failing factor the way layer_tag does (fisher.cpp:48-51)
+    const InvItem& f = items[first];
+    const char* side = f.side ? "G factor" : (std::strcmp(who, "damp_and_invert") == 0 ? "A factor" : "matrix");
+    return fail(h_info[first], "%s: request %d (%s, n=%lld): Cholesky factorization failed -- non-positive pivot or "
+                "non-finite entries", who, f.req, side, (long long)f.n);
+  }
+  return rc;
 }
 
-extern "C" int spngd_damp_and_invert_batched(spngd_ctx* ctx, int n, const spngd_kron_req* reqs, double lambda) {
+}  // namespace
+
+extern "C" int spngd_spd_inverse_batched(spngd_ctx* ctx, int n, const spngd_spd_req* reqs, int* info) {
+  if (!ctx || (n > 0 && !reqs)) return fail(SPNGD_ERR_INVALID, "spngd_spd_inverse_batched: null argument");
+  if (n == 0) return SPNGD_OK;
+  DeviceScratch scratch(ctx);
+  std::vector<InvItem> items;
+  for (int i = 0; i < n; ++i) {
+    const spngd_spd_req& r = reqs[i];
+    if (r.n <= 0) return fail(SPNGD_ERR_SHAPE_MISMATCH, "spd_inverse: request %d: empty matrix", i);
+    if (!r.packed || (!r.dense_out && !r.packed_out)) return fail(SPNGD_ERR_INVALID, "spd_inverse: request %d: null pointer", i);
+    if (r.dense_out && r.ld < r.n) return fail(SPNGD_ERR_SHAPE_MISMATCH, "spd_inverse: request %d: ld < n", i);
+    float* dense = r.dense_out;
+    int64_t ld = r.ld;
+    if (!dense) {
+      ld = round_up(r.n, 32);
+      dense = scratch.alloc<float>(size_t(r.n) * ld);
+      if (!dense) return fail(SPNGD_ERR_CUDA, "spd_inverse: allocation failed");
+    }
+    items.push_back({r.packed, r.n, r.damping, r.damping_dev, dense, ld, r.packed_out, i, 0});
+  }
+  return batched_inverse(ctx, scratch, items, nullptr, 0, n, info, "spd_inverse");
+}
+
+extern "C" int spngd_damp_and_invert_batched(spngd_ctx* ctx, int n, const spngd_kron_req* reqs, double lambda,
+                                             int* info) {
   if (!ctx || (n > 0 && !reqs)) return fail(SPNGD_ERR_INVALID, "spngd_damp_and_invert_batched: null argument");
   if (!(lambda > 0.0)) return fail(SPNGD_ERR_NOT_POSITIVE_DEFINITE, "damp_and_invert: lambda must be > 0");
   if (n == 0) return SPNGD_OK;
   DeviceScratch scratch(ctx);
   float* damps = scratch.alloc<float>(2 * n);
+  if (!damps) return fail(SPNGD_ERR_CUDA, "damp_and_invert: allocation failed");
   std::vector<PiTask> pis;
-  std::vector<DenseMatrix> mats;
-  std::vector<UnpackTask> unpack;
-  std::vector<PackTask> pack;
-  int64_t max_n = 0;
+  std::vector<InvItem> items;
   for (int i = 0; i < n; ++i) {
     const spngd_kron_req& r = reqs[i];
-    if (r.a <= 0 || r.g <= 0) return fail(SPNGD_ERR_SHAPE_MISMATCH, "avg_eigenvalue: empty matrix");
-    if (!r.A_packed || !r.G_packed) return fail(SPNGD_ERR_INVALID, "damp_and_invert: null factor");
+    if (r.a <= 0 || r.g <= 0) return fail(SPNGD_ERR_SHAPE_MISMATCH, "avg_eigenvalue: request %d: empty matrix", i);
+    if (!r.A_packed || !r.G_packed) return fail(SPNGD_ERR_INVALID, "damp_and_invert: request %d: null factor", i);
     pis.push_back({r.A_packed, r.G_packed, r.a, r.g, std::sqrt(lambda), damps + 2 * i, damps + 2 * i + 1, r.pi_out});
     const float* in[2] = {r.A_packed, r.G_packed};
     float* dn[2] = {r.Ainv_dense, r.Ginv_dense};
@@ -722,37 +816,16 @@ extern "C" int spngd_damp_and_invert_batched(spngd_ctx* ctx, int n, const spngd_
     for (int s = 0; s < 2; ++s) {
       float* dense = dn[s];
       int64_t ld = lds[s];
-      if (dense && ld < dims[s]) return fail(SPNGD_ERR_SHAPE_MISMATCH, "damp_and_invert: ld < n");
+      if (dense && ld < dims[s]) return fail(SPNGD_ERR_SHAPE_MISMATCH, "damp_and_invert: request %d: ld < n", i);
       if (!dense) {
         ld = round_up(dims[s], 32);
         dense = scratch.alloc<float>(size_t(dims[s]) * ld);
+        if (!dense) return fail(SPNGD_ERR_CUDA, "damp_and_invert: allocation failed");
       }
-      float* tl = scratch.alloc<float>(size_t(dims[s]) * ld);
-      float* tu = scratch.alloc<float>(size_t(dims[s]) * ld);
-      if (!dense || !tl || !tu) return fail(SPNGD_ERR_CUDA, "damp_and_invert: allocation failed");
-      cudaMemsetAsync(tl, 0, sizeof(float) * dims[s] * ld, ctx->stream);
-      cudaMemsetAsync(tu, 0, sizeof(float) * dims[s] * ld, ctx->stream);
-      mats.push_back({dense, tl, tu, ld, dims[s]});
-      unpack.push_back({in[s], dims[s], damps + 2 * i + s, 0.f, 0, dense, ld});
-      if (pk[s]) pack.push_back({dense, ld, dims[s], pk[s]});
-      max_n = std::max(max_n, dims[s]);
+      items.push_back({in[s], dims[s], 0.f, damps + 2 * i + s, dense, ld, pk[s], i, s});
     }
   }
-  InversePlan sizing;
-  plan_inverse(mats, nullptr, sizing);
-  float* ws = scratch.alloc<float>(std::max<size_t>(sizing.workspace_floats, 1));
-  InversePlan plan;
-  plan_inverse(mats, ws, plan);
   auto* d_pis = scratch.upload(pis);
-  auto* d_unpack = scratch.upload(unpack);
-  auto* d_pack = scratch.upload(pack);
-  auto* d_probs = scratch.upload(plan.probs);
-  auto* d_items = scratch.upload(plan.items);
-  auto* d_bases = scratch.upload(plan.bases);
-  int rc = launch_pi(ctx, d_pis, int(pis.size()));
-  if (!rc) rc = launch_unpack(ctx, d_unpack, int(unpack.size()), max_n);
-  if (!rc) rc = run_inverse(ctx, plan, d_probs, d_items, d_bases);
-  if (!rc) rc = launch_pack(ctx, d_pack, int(pack.size()), max_n);
-  if (rc) return rc;
-  return spngd_ctx_sync(ctx);
+  if (!d_pis) return fail(SPNGD_ERR_CUDA, "damp_and_invert: upload failed");
+  return batched_inverse(ctx, scratch, items, d_pis, int(pis.size()), n, info, "damp_and_invert");
 }

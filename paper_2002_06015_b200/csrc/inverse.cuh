@@ -14,6 +14,7 @@ struct BaseTask {   // n <= 128 diagonal block: L = chol(M), T = L^-1 -> Tlow, T
   int64_t ld;
   int32_t n;
   int32_t pad_;
+  int* info;        // per-matrix status word (NotPositiveDefinite), may be null
 };
 
 struct UnpackTask {  // dense = unpack(packed) + damp * I
@@ -24,13 +25,15 @@ struct UnpackTask {  // dense = unpack(packed) + damp * I
   int32_t pad_;
   float* dense;
   int64_t ld;
+  int* info;        // per-matrix status word (non-finite input), may be null
 };
 
-struct PackTask {
+struct PackTask {    // finite check of the dense result (+ pack when `packed`)
   const float* dense;
   int64_t ld;
   int64_t n;
-  float* packed;
+  float* packed;     // may be null: check only
+  int* info;
 };
 
 struct PiTask {  // damp_and_invert's pi and the two dampings (fisher.cpp:221-226)
@@ -63,6 +66,7 @@ struct DenseMatrix {
   float* tup;     // workspace n x ld, zero below the diagonal: L^-T
   int64_t ld;
   int64_t n;
+  int* info = nullptr;  // per-matrix status word for the leaves
 };
 
 // Builds the plan; temporaries are carved from `workspace` (may be null for a
@@ -72,6 +76,32 @@ struct DenseMatrix {
 void plan_inverse(const std::vector<DenseMatrix>& mats, float* workspace, InversePlan& plan, bool form_inverse = true);
 // X = Tup Tup^T -> m.ptr (the lauum step alone), synchronous.
 int materialize_inverse(spngd_ctx* ctx, const DenseMatrix& m);
+
+// ---- accuracy refinement of explicit inverses (refine.cu) ------------------
+// The fp32 Cholesky inverse has forward error ~3e-9 * cond(M + dI) (measured,
+// DESIGN.md §4).  ||M + dI||_F / d bounds cond from above (lambda_min >= d for
+// PSD M); above kRefineCond one refinement step X1 = X0 + X0 (I - M X0) with
+// the residual formed from exact tf32 splits (M = Mh + Mr, K-concatenated,
+// error ~2^-33 per product) brings the error to ~1e-5.
+struct FroTask {
+  const float* packed;
+  int64_t n;
+  const float* damp_dev;  // overrides damp when non-null
+  float damp;
+  int32_t pad_;
+  double* sumsq;          // out: ||M + dI||_F^2 (accumulated)
+};
+struct RefineJob {
+  const float* packed;    // M (packed), the same input the inverse read
+  int64_t n;
+  float damp;             // the fp32 damping the inverse used
+  float* X;               // dense (n x ld) inverse X0 in, refined symmetric X1 out
+  int64_t ld;
+};
+double refine_threshold();  // kRefineCond or SPNGD_REFINE_COND (<0: never, 0: always)
+int launch_fro(spngd_ctx* ctx, const FroTask* d_tasks, int n, int64_t max_n);
+// Refines every job in place (grouped launches); scratch comes from `scratch`.
+int refine_inverses(spngd_ctx* ctx, DeviceScratch& scratch, const std::vector<RefineJob>& jobs);
 
 int launch_pi(spngd_ctx* ctx, const PiTask* d_tasks, int n);
 int launch_unpack(spngd_ctx* ctx, const UnpackTask* d_tasks, int n, int64_t max_n);

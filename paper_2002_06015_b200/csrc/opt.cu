@@ -183,6 +183,8 @@ struct spngd_opt {
   std::vector<SlotMeanTask> means; SlotMeanTask* d_means = nullptr; int64_t means_max = 0;
   std::vector<PeerCopyTask> pcopy; PeerCopyTask* d_pcopy = nullptr; int64_t pcopy_max = 0;
   double* d_barrier = nullptr;
+  double* d_flag = nullptr;        // world > 1: status agreement before Stage 4 writes
+  int* d_info = nullptr;           // 3 per layer (A, G, F): status of each owned factor's inverse
   cudaStream_t h2d_stream = nullptr;     // spngd_opt_step_host: host inputs, wave by wave
   cudaStream_t d2h_stream = nullptr;     // and the early layers' weights back
   cudaEvent_t d2h_done = nullptr;
@@ -432,6 +434,8 @@ int build(spngd_opt* o, const spngd_layer_desc* descs, int n) {
   // ---- owner-local state and plans
   o->d_damps = o->alloc(2 * size_t(n));
   o->d_norms = reinterpret_cast<double*>(o->alloc(2 * size_t(n)));
+  o->d_info = reinterpret_cast<int*>(o->alloc(3 * size_t(n), true));
+  if (!o->d_damps || !o->d_norms || !o->d_info) return fail(SPNGD_ERR_CUDA, "opt: allocation failed");
   for (int li = 0; li < n; ++li) {
     LayerState& L = o->layers[li];
     if (L.owner != o->rank) continue;
@@ -447,10 +451,11 @@ int build(spngd_opt* o, const spngd_layer_desc* descs, int n) {
         L.tuf = o->alloc(size_t(d2 * L.ldf), true);
         L.yf = o->alloc(size_t(d2), true);
         if (!L.Finv || !L.tlf || !L.tuf || !L.yf || !L.V) return fail(SPNGD_ERR_CUDA, "opt: owner state allocation failed");
-        o->bnf_unpacks.push_back({o->rs_recv + L.off_M, d2, nullptr, float(o->cfg.lambda), 0, L.Finv, L.ldf});
+        o->bnf_unpacks.push_back({o->rs_recv + L.off_M, d2, nullptr, float(o->cfg.lambda), 0, L.Finv, L.ldf,
+                                  o->d_info + 3 * li + 2});
         o->bnf_layer.push_back(li);
         o->bnf_maxn = std::max(o->bnf_maxn, d2);
-        mats.push_back({L.Finv, L.tlf, L.tuf, L.ldf, d2});
+        mats.push_back({L.Finv, L.tlf, L.tuf, L.ldf, d2, o->d_info + 3 * li + 2});
         mat_layer.push_back(li);
         // precondition_bn_full (fisher.cpp:278-296): v = T^T (T u), then the BN update
         spngd_bn_full_update_req r0{}, r1{};
@@ -490,12 +495,12 @@ int build(spngd_opt* o, const spngd_layer_desc* descs, int n) {
     float* dG = dA + 1;
     o->pis.push_back({o->rs_recv + L.off_A, o->rs_recv + L.off_G, a, g, std::sqrt(o->cfg.lambda), dA, dG, nullptr});
     o->pi_layer.push_back(li);
-    o->unpacks.push_back({o->rs_recv + L.off_A, a, dA, 0.f, 0, L.Ainv, L.lda});
-    o->unpacks.push_back({o->rs_recv + L.off_G, g, dG, 0.f, 0, L.Ginv, L.ldg});
+    o->unpacks.push_back({o->rs_recv + L.off_A, a, dA, 0.f, 0, L.Ainv, L.lda, o->d_info + 3 * li});
+    o->unpacks.push_back({o->rs_recv + L.off_G, g, dG, 0.f, 0, L.Ginv, L.ldg, o->d_info + 3 * li + 1});
     o->max_n = std::max({o->max_n, a, g});
-    mats.push_back({L.Ainv, tla, tua, L.lda, a});
+    mats.push_back({L.Ainv, tla, tua, L.lda, a, o->d_info + 3 * li});
     mat_layer.push_back(li);
-    mats.push_back({L.Ginv, tlg, tug, L.ldg, g});
+    mats.push_back({L.Ginv, tlg, tug, L.ldg, g, o->d_info + 3 * li + 1});
     mat_layer.push_back(li);
     L.tla = tla; L.tua = tua; L.tlg = tlg; L.tug = tug;
     ptri.push_back({tla, tua, tlg, tug});
@@ -863,6 +868,10 @@ int spngd_opt_create(spngd_ctx* ctx, const spngd_layer_desc* layers, int n_layer
   o->rank = ctx->rank;
   SPNGD_CUDA_TRY(cudaSetDevice(ctx->device));
   int rc = build(o, layers, n_layers);
+  if (!rc) {
+    o->d_flag = reinterpret_cast<double*>(o->alloc(2, true));
+    if (!o->d_flag) rc = fail(SPNGD_ERR_CUDA, "spngd_opt_create: allocation failed");
+  }
   if (rc) {
     delete o;
     return rc;
@@ -1014,6 +1023,12 @@ int issue_phase(spngd_opt* o, int phase) {
       return SPNGD_OK;
     }
     case 4:  // Stage 4b: precondition + update + rescale, BN solve + update (dist.cpp:604-633).
+      // No parameter is written once any inverse / BN block of any rank failed
+      // (the kernels read the status word): agree on it, then check every
+      // BN determinant before the first update.
+      rc = agree_status(ctx, o->d_flag);
+      if (!rc) rc = launch_bn_det_check(ctx, o->d_bnu, int(o->bnu.size()), o->bnu_maxc, o->cfg.lambda);
+      if (rc) return rc;
       if (o->ov_now && o->pre_split) {  // the early part already ran inside the wave schedule
         const spngd_opt::PrePart& pp = o->pre[1];
         rc = run_precondition(ctx, pp.plan, pp.d_pp, pp.d_pi, pp.d_rescale, pp.d_norms);
@@ -1392,8 +1407,10 @@ int step_impl(spngd_opt* o, int64_t step, double eta, double momentum, bool host
       } else if (ph == 2 && o->world > 1)
         rc = spngd_reduce_scatter_mean(ctx, o->rs_send + int64_t(o->world) * o->seg_stat, o->rs_recv + o->seg_stat,
                                        o->seg_grad);
-      else if (ph == 4)
-        rc = launch_sgd_update(ctx, o->d_sgd, int(o->sgd_tasks.size()), o->d_scal);
+      else if (ph == 4) {
+        rc = agree_status(ctx, o->d_flag);
+        if (!rc) rc = launch_sgd_update(ctx, o->d_sgd, int(o->sgd_tasks.size()), o->d_scal);
+      }
       else if (ph == 5)
         rc = issue_allgather(o);
       if (rc) return rc;
@@ -1799,6 +1816,53 @@ int spngd_opt_phase_ms(spngd_opt* o, float* out6) {
   SPNGD_CUDA_TRY(cudaEventSynchronize(o->ev[6]));
   for (int i = 0; i < 6; ++i) SPNGD_CUDA_TRY(cudaEventElapsedTime(&out6[i], o->ev[i], o->ev[i + 1]));
   return SPNGD_OK;
+}
+
+// spngd_ctx_sync plus the layer tag of a failed step (fisher.cpp:48-51
+// layer_tag): the first owned factor whose inverse failed, or the first BN
+// channel whose damped 2x2 block is singular.
+int spngd_opt_sync(spngd_opt* o) {
+  if (!o) return fail(SPNGD_ERR_INVALID, "spngd_opt_sync: opt is NULL");
+  const int rc = spngd_ctx_sync(o->ctx);
+  if (rc != SPNGD_ERR_NOT_POSITIVE_DEFINITE && rc != SPNGD_ERR_SINGULAR_BLOCK) return rc;
+  const int n = int(o->layers.size());
+  std::vector<int> info(3 * size_t(n));
+  SPNGD_CUDA_TRY(cudaMemcpy(info.data(), o->d_info, sizeof(int) * info.size(), cudaMemcpyDeviceToHost));
+  SPNGD_CUDA_TRY(cudaMemset(o->d_info, 0, sizeof(int) * info.size()));
+  auto tag = [&](int li, char* buf, size_t cap) {
+    const spngd_layer_desc& d = o->layers[li].d;
+    if (d.kind == SPNGD_BN) snprintf(buf, cap, "layer %d (bn(%lld))", li, (long long)d.g);
+    else snprintf(buf, cap, "layer %d (%s a=%lld g=%lld hw=%lld)", li, d.kind == SPNGD_CONV ? "conv" : "fc",
+                  (long long)d.a, (long long)d.g, (long long)d.hw);
+  };
+  char buf[128];
+  static const char* which[3] = {"A factor", "G factor", "full BN block"};
+  for (int li = 0; li < n; ++li)
+    for (int w = 0; w < 3; ++w)
+      if (info[3 * li + w]) {
+        tag(li, buf, sizeof(buf));
+        return fail(info[3 * li + w], "damp_and_invert: %s: %s: Cholesky factorization failed -- non-positive pivot "
+                    "or non-finite entries (no parameter was updated)", buf, which[w]);
+      }
+  if (rc == SPNGD_ERR_SINGULAR_BLOCK) {  // damp_bn (fisher.cpp:230-246): find the channel on the host
+    for (size_t q = 0; q < o->bnu.size(); ++q) {
+      const spngd_bn_update_req& r = o->bnu[q];
+      std::vector<float> m(3 * size_t(r.c));
+      SPNGD_CUDA_TRY(cudaMemcpy(m.data(), r.m3c, sizeof(float) * m.size(), cudaMemcpyDeviceToHost));
+      for (int64_t ch = 0; ch < r.c; ++ch) {
+        const double a = double(m[3 * ch]) + o->cfg.lambda, b = m[3 * ch + 1], d = double(m[3 * ch + 2]) + o->cfg.lambda;
+        if (std::fabs(a * d - b * b) < 1e-30) {
+          int li = -1;
+          for (int k = 0; k < n; ++k)
+            if (o->layers[k].owner == o->rank && o->layers[k].d.kind == SPNGD_BN && o->rs_recv + o->layers[k].off_M == r.m3c) li = k;
+          tag(li < 0 ? 0 : li, buf, sizeof(buf));
+          return fail(rc, "damp_bn: %s: channel %lld: inv2x2 determinant below 1e-30 (no parameter was updated)",
+                      li < 0 ? "BN layer" : buf, (long long)ch);
+        }
+      }
+    }
+  }
+  return rc;
 }
 
 int64_t spngd_opt_launch_count(const spngd_opt* o) { return o ? o->launches : 0; }

@@ -25,7 +25,13 @@ namespace spngd {
 
 namespace {
 
-__global__ void rescale_kernel(const RescaleTask* __restrict__ tasks) {
+// Every parameter-mutating kernel of Stage 4/5 returns without writing when the
+// context status word is set (an inverse, unpack or BN determinant failed
+// earlier in the step): the reference throws in damp_and_invert /
+// precondition_bn before ngd_step, so its parameters stay unchanged
+// (dist.cpp:597-601).  The status stays set until spngd_ctx_sync reports it.
+__global__ void rescale_kernel(const RescaleTask* __restrict__ tasks, const int* __restrict__ status) {
+  if (*status) return;
   const RescaleTask t = tasks[blockIdx.y];
   const double nrm = sqrt(t.norm2[0]);
   const float s = float(t.target / (nrm + 1e-9));  // schemes.cpp:117-118
@@ -53,7 +59,8 @@ __global__ void rescale_kernel(const RescaleTask* __restrict__ tasks) {
   if (t.n_peers) __threadfence_system();
 }
 
-__global__ void peer_copy_kernel(const PeerCopyTask* __restrict__ tasks) {
+__global__ void peer_copy_kernel(const PeerCopyTask* __restrict__ tasks, const int* __restrict__ status) {
+  if (*status) return;
   const PeerCopyTask t = tasks[blockIdx.y];
   const bool vec = t.n % 4 == 0 && (reinterpret_cast<uintptr_t>(t.src) & 15) == 0;
   const int64_t n4 = vec ? t.n / 4 : 0;
@@ -69,6 +76,7 @@ __global__ void peer_copy_kernel(const PeerCopyTask* __restrict__ tasks) {
 
 __global__ void bn_update_kernel(const spngd_bn_update_req* __restrict__ reqs, double lambda, double eta,
                                  double momentum, const float* scal, int* status) {
+  if (*status) return;  // includes a singular block found by bn_det_check_kernel
   if (scal) {
     eta = scal[0];
     momentum = scal[1];
@@ -101,9 +109,32 @@ __global__ void bn_update_kernel(const spngd_bn_update_req* __restrict__ reqs, d
   }
 }
 
+// damp_bn's SingularBlock (fisher.cpp:230-246, linalg.cpp:50-56) for every
+// channel before any parameter is touched, so a singular channel aborts the
+// whole update like the reference's throw.
+__global__ void bn_det_check_kernel(const spngd_bn_update_req* __restrict__ reqs, double lambda, int* status) {
+  const spngd_bn_update_req r = reqs[blockIdx.y];
+  for (int64_t ch = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; ch < r.c; ch += int64_t(gridDim.x) * blockDim.x) {
+    const double a = double(r.m3c[3 * ch]) + lambda, b = double(r.m3c[3 * ch + 1]);
+    const double d = double(r.m3c[3 * ch + 2]) + lambda;
+    if (fabs(a * d - b * b) < 1e-30) set_status(status, SPNGD_ERR_SINGULAR_BLOCK);
+  }
+}
+
+// world > 1: every rank adopts the largest status of any rank before Stage 4
+// mutates parameters (16^code summed over <= 8 ranks decodes exactly).
+__global__ void status_encode_kernel(const int* status, double* flag) {
+  flag[0] = *status ? pow(16.0, double(*status)) : 0.0;
+}
+__global__ void status_decode_kernel(int* status, const double* flag) {
+  if (flag[0] > 0.0 && *status == 0) *status = int(floor(log(flag[0]) / log(16.0) + 1e-9));
+}
+
 // HBM-bound: 16 bytes in / 8 out per element; float4 when every pointer is
 // 16-byte aligned and n % 4 == 0 (true for the owner-major 64-float entries).
-__global__ void sgd_update_kernel(const SgdTask* __restrict__ tasks, const float* __restrict__ scal) {
+__global__ void sgd_update_kernel(const SgdTask* __restrict__ tasks, const float* __restrict__ scal,
+                                  const int* __restrict__ status) {
+  if (*status) return;
   const SgdTask t = tasks[blockIdx.y];
   const double eta = scal[0], mom = scal[1];
   const bool vec = t.n % 4 == 0 && ((reinterpret_cast<uintptr_t>(t.W) | reinterpret_cast<uintptr_t>(t.V) |
@@ -138,7 +169,10 @@ __global__ void sgd_update_kernel(const SgdTask* __restrict__ tasks, const float
 // for packed statistics; 1,2,1 for BN 3c payloads), stale.hpp:23-64.
 __global__ void stat_distance_kernel(const StatJob* __restrict__ jobs) {
   const spngd_stat_req r = jobs[blockIdx.y].r;
-  float* __restrict__ rot = jobs[blockIdx.y].rot;
+  // rot may alias r.x2 (the fused snapshot rotation writes x into x2's slot):
+  // no __restrict__; every element is read by the same thread before that
+  // thread overwrites it, so the rotation is race-free.
+  float* rot = jobs[blockIdx.y].rot;
   double acc[4] = {0, 0, 0, 0};
   if (r.kind == 0) {
     for (int64_t i = blockIdx.x; i < r.n; i += gridDim.x) {
@@ -295,7 +329,7 @@ int run_precondition(spngd_ctx* ctx, const PrecondPlan& plan, GemmProblem* const
   }
   if (!plan.rescale.empty()) {
     dim3 grid(296, unsigned(plan.rescale.size()));
-    rescale_kernel<<<grid, 256, 0, ctx->stream>>>(d_rescale);
+    rescale_kernel<<<grid, 256, 0, ctx->stream>>>(d_rescale, ctx->d_status);
     SPNGD_CUDA_TRY(cudaGetLastError());
     ctx->launches++;
   }
@@ -327,7 +361,7 @@ int launch_slot_mean(spngd_ctx* ctx, const SlotMeanTask* d_tasks, int n, int64_t
 int launch_peer_copy(spngd_ctx* ctx, const PeerCopyTask* d_tasks, int n, int64_t max_n) {
   if (n <= 0) return SPNGD_OK;
   dim3 grid(unsigned(std::min<int64_t>(std::max<int64_t>((max_n / 4 + 255) / 256, 1), 296)), unsigned(n));
-  peer_copy_kernel<<<grid, 256, 0, ctx->stream>>>(d_tasks);
+  peer_copy_kernel<<<grid, 256, 0, ctx->stream>>>(d_tasks, ctx->d_status);
   SPNGD_CUDA_TRY(cudaGetLastError());
   ctx->launches++;
   return SPNGD_OK;
@@ -343,10 +377,31 @@ int launch_bn_update(spngd_ctx* ctx, const spngd_bn_update_req* d_reqs, int n, i
   return SPNGD_OK;
 }
 
+int launch_bn_det_check(spngd_ctx* ctx, const spngd_bn_update_req* d_reqs, int n, int64_t max_c, double lambda) {
+  if (n <= 0) return SPNGD_OK;
+  dim3 grid(unsigned(std::min<int64_t>((max_c + 255) / 256, 64)), unsigned(n));
+  bn_det_check_kernel<<<grid, 256, 0, ctx->stream>>>(d_reqs, lambda, ctx->d_status);
+  SPNGD_CUDA_TRY(cudaGetLastError());
+  ctx->launches++;
+  return SPNGD_OK;
+}
+
+int agree_status(spngd_ctx* ctx, double* d_flag) {
+  if (ctx->world <= 1) return SPNGD_OK;
+  status_encode_kernel<<<1, 1, 0, ctx->stream>>>(ctx->d_status, d_flag);
+  SPNGD_CUDA_TRY(cudaGetLastError());
+  int rc = comm_allreduce_sum_f64(ctx, d_flag, 1);
+  if (rc) return rc;
+  status_decode_kernel<<<1, 1, 0, ctx->stream>>>(ctx->d_status, d_flag);
+  SPNGD_CUDA_TRY(cudaGetLastError());
+  ctx->launches += 2;
+  return SPNGD_OK;
+}
+
 int launch_sgd_update(spngd_ctx* ctx, const SgdTask* d_tasks, int n, const float* scal) {
   if (n <= 0) return SPNGD_OK;
   dim3 grid(296u, unsigned(n));  // 2 x 148 SMs
-  sgd_update_kernel<<<grid, 256, 0, ctx->stream>>>(d_tasks, scal);
+  sgd_update_kernel<<<grid, 256, 0, ctx->stream>>>(d_tasks, scal, ctx->d_status);
   SPNGD_CUDA_TRY(cudaGetLastError());
   ctx->launches++;
   return SPNGD_OK;
@@ -403,7 +458,8 @@ extern "C" int spngd_bn_solve_update_batched(spngd_ctx* ctx, int n, const spngd_
   DeviceScratch scratch(ctx);
   std::vector<spngd_bn_update_req> v(reqs, reqs + n);
   auto* d = scratch.upload(v);
-  int rc = launch_bn_update(ctx, d, n, max_c, lambda, eta, momentum);
+  int rc = launch_bn_det_check(ctx, d, n, max_c, lambda);
+  if (!rc) rc = launch_bn_update(ctx, d, n, max_c, lambda, eta, momentum);
   if (rc) return rc;
   return spngd_ctx_sync(ctx);
 }
@@ -414,7 +470,7 @@ extern "C" int spngd_stat_distance_batched(spngd_ctx* ctx, int n, const spngd_st
   for (int i = 0; i < n; ++i) {
     if (!reqs[i].x || !reqs[i].out4) return fail(SPNGD_ERR_INVALID, "similar: null pointer");
     max_rows = std::max(max_rows, reqs[i].kind == 0 ? reqs[i].n : (3 * reqs[i].n + 255) / 256);
-    cudaMemsetAsync(reqs[i].out4, 0, 4 * sizeof(double), ctx->stream);
+    SPNGD_CUDA_TRY(cudaMemsetAsync(reqs[i].out4, 0, 4 * sizeof(double), ctx->stream));
   }
   if (n == 0) return SPNGD_OK;
   DeviceScratch scratch(ctx);

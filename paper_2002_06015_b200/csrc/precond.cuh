@@ -92,6 +92,10 @@ struct SgdTask {
   int64_t n;
 };
 int launch_sgd_update(spngd_ctx* ctx, const SgdTask* d_tasks, int n, const float* scal);
+// SingularBlock check of every BN channel before any parameter is written.
+int launch_bn_det_check(spngd_ctx* ctx, const spngd_bn_update_req* d_reqs, int n, int64_t max_c, double lambda);
+// world > 1: all ranks adopt the largest status word (d_flag: one device double).
+int agree_status(spngd_ctx* ctx, double* d_flag);
 // One similarity job: the public request plus, on the optimizer path, the
 // snapshot slot the statistic rotates into (x2 <- x1 <- x).  The kernel writes
 // rot[q] = x[q] right after reading x2[q] (rot is x2's slot when it exists), so

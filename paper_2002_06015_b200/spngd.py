@@ -76,6 +76,8 @@ class ParseError(Error):  # errors.hpp: ledger / manifest parsing
     pass
 
 
+# status codes of include/spngd_b200.h (spngd_status)
+SPNGD_OK, SPNGD_ERR_SHAPE_MISMATCH, SPNGD_ERR_NOT_POSITIVE_DEFINITE, SPNGD_ERR_SINGULAR_BLOCK = 0, 1, 2, 3
 _ERRORS = {1: ShapeMismatch, 2: NotPositiveDefinite, 3: SingularBlock, 4: ZeroReference,
            5: EmptyBatch, 6: MissingMcPass, 7: StaleBeyondLimit, 8: RefreshOutOfTurn,
            9: IndivisibleBatch, 10: MissingOwner, 11: EmptyAccumulation, 100: CudaError,
@@ -424,13 +426,15 @@ def spd_inverse(m: SymMatrix, damping: float, dense: bool = False):
     req = N.SpdReq(m.data.data_ptr(), n, damping, None, dn.data_ptr() if dense else None, ld,
                    out.data_ptr())
     arr = (N.SpdReq * 1)(req)
-    check(N.lib().spngd_spd_inverse_batched(context().h, 1, arr))
+    check(N.lib().spngd_spd_inverse_batched(context().h, 1, arr, None))
     res = SymMatrix(n, out)
     return (res, dn[:, :n]) if dense else res
 
 
-def spd_inverse_batched(ms: List[SymMatrix], damping: float) -> List[SymMatrix]:
-    """spd_inverse (linalg.hpp:60) over many matrices in one batched call."""
+def spd_inverse_batched(ms: List[SymMatrix], damping: float, info: list = None) -> List[SymMatrix]:
+    """spd_inverse (linalg.hpp:60) over many matrices in one batched call.
+    `info` (a list) receives the per-request status codes; the raised
+    NotPositiveDefinite names the first failing request."""
     reqs, outs = [], []
     for m in ms:
         if m.dim == 0:
@@ -440,12 +444,17 @@ def spd_inverse_batched(ms: List[SymMatrix], damping: float) -> List[SymMatrix]:
         outs.append(SymMatrix(m.dim, out))
     if reqs:
         arr = (N.SpdReq * len(reqs))(*reqs)
-        check(N.lib().spngd_spd_inverse_batched(context().h, len(reqs), arr))
+        inf = (C.c_int * len(reqs))()
+        rc = N.lib().spngd_spd_inverse_batched(context().h, len(reqs), arr, inf)
+        if info is not None:
+            info[:] = list(inf)
+        check(rc)
     return outs
 
 
-def damp_and_invert_batched(blocks: List[KroneckerBlock], lam: float):
-    """damp_and_invert (fisher.cpp:218-228) for many blocks in one batched call."""
+def damp_and_invert_batched(blocks: List[KroneckerBlock], lam: float, info: list = None):
+    """damp_and_invert (fisher.cpp:218-228) for many blocks in one batched call.
+    `info` (a list) receives the per-block status codes."""
     if not (lam > 0.0):
         raise NotPositiveDefinite("damp_and_invert: lambda must be > 0")
     reqs, keep = [], []
@@ -464,7 +473,11 @@ def damp_and_invert_batched(blocks: List[KroneckerBlock], lam: float):
                               Gd.data_ptr(), ldg, Ap.data_ptr(), Gp.data_ptr(), pi.data_ptr()))
         keep.append((b, Ad, Gd, Ap, Gp, pi))
     arr = (N.KronReq * len(reqs))(*reqs)
-    check(N.lib().spngd_damp_and_invert_batched(context().h, len(reqs), arr, lam))
+    inf = (C.c_int * len(reqs))()
+    rc = N.lib().spngd_damp_and_invert_batched(context().h, len(reqs), arr, lam, inf)
+    if info is not None:
+        info[:] = list(inf)
+    check(rc)
     for b, Ad, Gd, Ap, Gp, pi in keep:
         b.A_inv, b.G_inv = SymMatrix(b.A.dim, Ap), SymMatrix(b.G.dim, Gp)
         b.A_inv_dense, b.G_inv_dense = Ad, Gd

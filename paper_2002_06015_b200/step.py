@@ -160,7 +160,8 @@ class Optimizer:
         self.sync()
 
     def sync(self):
-        check(N.lib().spngd_ctx_sync(self.ctx))
+        # spngd_opt_sync: a failed step names its layer (fisher.cpp:48-51 layer_tag)
+        check(N.lib().spngd_opt_sync(self.h) if getattr(self, "h", None) else N.lib().spngd_ctx_sync(self.ctx))
 
     # ---- synthetic inputs -------------------------
     def synth(self, seed: int = 42):

@@ -1,12 +1,17 @@
 """K-invariance of the NCCL path (tests/test_dist.cpp:363-387 analogue).
 
-torchrun --nproc-per-node 2 scripts/multi_gpu_check.py [--mode default|wgrad|bn_full|one_mc|sgd|host]
+torchrun --nproc-per-node 2 scripts/multi_gpu_check.py [--mode default|wgrad|bn_full|one_mc|sgd|host|p2p...]
+                                                        [--layers toy|r50]
 Every rank runs one step at P = 2 on its own shard; rank 0 then replays the
 same step at P = 1 over the concatenated batch (mean dW) and compares all
 updated weights.  Replicas must be bit-identical across ranks, and the step's
 CommLedger rows must equal the oracle restatement at P (oracle/ledger.py).
 Modes: the optimizer configurations of DESIGN.md §3.6 (wgrad forms dW on each
 rank from its shard; host feeds the rank's inputs through spngd_opt_step_host).
+--layers r50: a ResNet-50 layer sample with the dominant factors (a 4608^2
+A with K < a, a 2304^2 A, a 2048^2 G, conv1, BN, the FC) at 32 images in
+total; rank 0 then also checks every Kronecker layer's updated weights
+against the fp64 oracle (or_kfac_layers) on the concatenated batch.
 Exit 0 on pass.
 """
 import os
@@ -27,6 +32,8 @@ LAYERS = [W.conv(16, 32, 3, 1, 16), W.bn(32), W.conv(32, 64, 3, 2, 16), W.bn(64)
           W.bn(128), W.conv(128, 256, 3, 2, 8), W.bn(256), W.fc(1024, 10),
           W.conv(256, 256, 3, 1, 4), W.conv(512, 512, 3, 1, 4)]  # inverse waves 1 and 0
 B = 8
+R50_LAYERS = [W.conv(3, 64, 7, 2, 224), W.bn(64), W.conv(256, 256, 3, 1, 14), W.bn(256),
+              W.conv(512, 512, 3, 1, 7), W.bn(512), W.conv(512, 2048, 1, 1, 7), W.fc(2048, 1000)]
 
 
 MODES = {"default": {}, "wgrad": {"wgrad": True}, "bn_full": {"bn_mode": 1}, "one_mc": {"fisher_mode": 1},
@@ -37,10 +44,13 @@ MODES = {"default": {}, "wgrad": {"wgrad": True}, "bn_full": {"bn_mode": 1}, "on
 def main():
     mode = sys.argv[sys.argv.index("--mode") + 1] if "--mode" in sys.argv else "default"
     kw = MODES[mode]
-    global B
+    global B, LAYERS
+    r50 = "--layers" in sys.argv and sys.argv[sys.argv.index("--layers") + 1] == "r50"
     if mode.endswith("bn_full"):
         B = 320  # 2c <= 512 < P*B: full-rank F, so fp32 summation order stays below the 1e-4 gate
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    if r50:
+        LAYERS, B = R50_LAYERS, 32 // world
     local = int(os.environ.get("LOCAL_RANK", rank))
     torch.cuda.set_device(local)
     dist.init_process_group("gloo")
@@ -105,6 +115,32 @@ def main():
             worst = max(worst, err)
             print(f"layer {li} {LAYERS[li].kind} owner {owners[li]} rel {err:.2e}")
         ok = ok and worst <= 1e-4
+        if r50 and not kw.get("sgd"):  # the fp64 oracle on the concatenated batch (Stage 2-5, dist.cpp:406-675)
+            import ctypes as C
+            import oracle as O
+            recs, outs, keep = [], [], []
+            for li, l in enumerate(LAYERS):
+                if l.kind == "bn":
+                    continue
+                cat = lambda w: np.ascontiguousarray(np.concatenate([gathered[r][0][li][w] for r in range(world)]),
+                                                     dtype=np.float32)
+                bufs = [cat(ACT), cat(GRAD),
+                        np.mean([gathered[r][0][li][DW] for r in range(world)], axis=0).astype(np.float32),
+                        inputs[li][WB].astype(np.float32), gathered[owners[li]][0][li][V].astype(np.float32)]
+                rec = O.OrLayer()
+                out = np.empty(l.g * l.a)
+                rec.is_conv, rec.a, rec.g, rec.hw, rec.batch = int(l.kind == "conv"), l.a, l.g, l.hw, B * world
+                rec.act, rec.grad, rec.dW, rec.W, rec.V = [b.ctypes.data_as(C.POINTER(C.c_float)) for b in bufs]
+                rec.W_out = out.ctypes.data_as(C.POINTER(C.c_double))
+                recs.append(rec)
+                outs.append((li, out))
+                keep.append(bufs)
+            O.kfac_layers(recs, 2.5e-4, 1.25e-2, 0.993, rescale=True, fast_inverse=True,
+                          threads=min(len(recs), os.cpu_count() or 1))
+            for li, want in outs:
+                err = np.linalg.norm(after[li] - want) / np.linalg.norm(want)
+                print(f"oracle layer {li} ({LAYERS[li].a}x{LAYERS[li].g}) rel {err:.2e}")
+                ok = ok and err <= 1e-4
         print("ledger rows match the oracle at P =", world, ledger_ok, "| NCCL bytes", wire)
         ok = ok and ledger_ok
         ph = opt.phase_ms()

@@ -357,3 +357,59 @@ def test_step_host_equals_device_step(cuda_dev, raw):
             opt.close()
     for a, b in zip(*outs):
         assert np.array_equal(a, b)
+
+
+def _params(opt, layers):
+    return [(opt.download(li, WB).numpy().copy(), opt.download(li, V).numpy().copy()) for li in range(len(layers))]
+
+
+def test_failed_step_names_layer_and_updates_nothing(cuda_dev):
+    """A non-finite capture makes layer 2's A factor fail in damp_and_invert:
+    the step raises NotPositiveDefinite naming layer 2 / its A factor and no
+    parameter of any layer changes -- the reference throws in Stage 4 before
+    ngd_step (dist.cpp:597-601)."""
+    from paper_2002_06015_b200.spngd import NotPositiveDefinite
+    layers = [W.conv(3, 16, 3, 1, 16), W.bn(16), W.conv(16, 32, 3, 2, 16), W.bn(32), W.fc(32 * 64, 10)]
+    opt = Optimizer(layers, 8, lam=LAM)
+    try:
+        opt.set_overlap(False)
+        opt.synth(seed=4)
+        act = opt.download(2, ACT)
+        act[5] = float("nan")
+        opt.upload(2, ACT, act)
+        before = _params(opt, layers)
+        opt.step(1, ETA, MOM)
+        with pytest.raises(NotPositiveDefinite) as e:
+            opt.sync()
+        assert "layer 2" in str(e.value) and "A factor" in str(e.value), str(e.value)
+        after = _params(opt, layers)
+        for li, ((w0, v0), (w1, v1)) in enumerate(zip(before, after)):
+            assert np.array_equal(w0, w1) and np.array_equal(v0, v1), f"layer {li} was updated"
+    finally:
+        opt.close()
+
+
+def test_singular_bn_block_updates_nothing(cuda_dev):
+    """damp_bn's SingularBlock (fisher.cpp:230-246): a BN layer with all-zero
+    per-sample gradients and lambda = 1e-16 has det(F + lambda I) < 1e-30;
+    every channel is checked before any parameter is written."""
+    from paper_2002_06015_b200.spngd import SingularBlock
+    # every Kronecker factor full rank (K = 8 * 64 > a, g), so only the BN block fails
+    layers = [W.conv(3, 16, 3, 1, 8), W.bn(16), W.conv(16, 8, 1, 1, 8)]
+    opt = Optimizer(layers, 8, lam=1e-16)
+    try:
+        opt.set_overlap(False)
+        opt.synth(seed=6)
+        z = torch.zeros(8 * 16)
+        opt.upload(1, BN_GG, z)
+        opt.upload(1, BN_GB, z)
+        before = _params(opt, layers)
+        opt.step(1, ETA, MOM)
+        with pytest.raises(SingularBlock) as e:
+            opt.sync()
+        assert "layer 1" in str(e.value), str(e.value)
+        after = _params(opt, layers)
+        for li, ((w0, v0), (w1, v1)) in enumerate(zip(before, after)):
+            assert np.array_equal(w0, w1) and np.array_equal(v0, v1), f"layer {li} was updated"
+    finally:
+        opt.close()
