@@ -245,6 +245,7 @@ def run_ours(args):
     step_ms = ms.value / args.steps
     phases = opt.phase_ms()  # last step, device events
     launches = opt.launch_count()
+    owners = [opt.owner(li) for li in range(len(layers))]
     barrier()
     if pg:
         import torch
@@ -355,19 +356,27 @@ def run_ours(args):
         # same phase-serial pass (CUDA events on the library stream; each span
         # is the phase's grouped GEMM launches plus its small helpers).
         sp = (serial or {}).get("phases_ms_last_step", phases)
+        if world > 1:  # owner-local phases: this rank's (rank 0's) owned layers' flops
+            fp = fi = 0.0
+            for li, l in enumerate(layers):
+                if l.kind != "bn" and owners[li] == 0:
+                    fi += l.a ** 3 + l.g ** 3
+                    fp += 2 * l.g * l.g * l.a + 2 * l.g * l.a * l.a
         rooflines = {
             "factor_syrk": {k: roofline[k] for k in ("achieved", "peak", "frac", "launch_ms")},
             "precondition": {"achieved": round(fp / (sp["precondition_update"] * 1e-3) / 1e12, 2),
                              "peak": round(peak, 2), "unit": "TFLOP/s",
                              "frac": round(fp / (sp["precondition_update"] * 1e-3) / 1e12 / peak, 4),
                              "span_ms": sp["precondition_update"],
-                             "algorithmic": f"{fp / 1e9:.1f} GF (SURVEY §8d F_pre = sum 2g^2a + 2ga^2)",
+                             "algorithmic": f"{fp / 1e9:.1f} GF (SURVEY §8d F_pre = sum 2g^2a + 2ga^2"
+                                            + (", rank 0's owned layers)" if world > 1 else ")"),
                              "span": "four triangular 3xTF32 GEMM launches (T_A, T_A^T, T_G, T_G^T) with the "
                                      "momentum/velocity/norm epilogue + rescale + BN det check + BN solve/update"},
             "inverse": {"achieved": round(fi / (sp["inverse"] * 1e-3) / 1e12, 2), "peak": round(peak, 2),
                         "unit": "TFLOP/s", "frac": round(fi / (sp["inverse"] * 1e-3) / 1e12 / peak, 4),
                         "span_ms": sp["inverse"],
-                        "algorithmic": f"{fi / 1e9:.1f} GF (SURVEY §8d F_inv = sum a^3 + g^3)",
+                        "algorithmic": f"{fi / 1e9:.1f} GF (SURVEY §8d F_inv = sum a^3 + g^3"
+                                       + (", rank 0's owned layers)" if world > 1 else ")"),
                         "span": "pi + unpack/damping + every recursion round (leaves + grouped 3xTF32 GEMMs) of "
                                 "all 108 factors, size classes on concurrent streams"},
         }

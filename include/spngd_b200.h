@@ -153,6 +153,23 @@ typedef struct spngd_bn_grad_req {
 } spngd_bn_grad_req;
 int spngd_bn_grad_reduce_batched(spngd_ctx* ctx, int n, const spngd_bn_grad_req* reqs);
 
+/* SURVEY §8f row 1, fused: one launch for every BN layer turns dY and x_hat
+ * (M x (c*S)) into the per-sample capture (gg, gb: M x c, may be NULL), the
+ * build_bn_block moments (src/fisher.cpp:147-185) as the interleaved 3c
+ * payload (src/dist.cpp:283-292; out3c may be NULL) and the BN branch of
+ * grad_payload [sum_s gg / M | sum_s gb / M] (src/dist.cpp:364-371; payload,
+ * 2c, may be NULL).  HBM-bound (reads dY and x_hat once); deterministic. */
+typedef struct spngd_bn_backward_req {
+  const float* dy;
+  const float* xhat;
+  int64_t M, c, S;
+  float* gg;
+  float* gb;
+  float* out3c;
+  float* payload;
+} spngd_bn_backward_req;
+int spngd_bn_backward_stats_batched(spngd_ctx* ctx, int n, const spngd_bn_backward_req* reqs);
+
 /* ---- K3/K4: damped SPD inverse ---------------------------------------------
  * Replaces spd_inverse (src/linalg.cpp:29-48): (M + d I)^-1 of a packed
  * symmetric matrix.  `damping_dev` (device float) overrides `damping` when
@@ -485,6 +502,15 @@ int spngd_opt_attach_peers(spngd_opt* opt, const void* handles);
 typedef struct spngd_conv_geom {
   int64_t c_in, h, w, k, stride, pad;
 } spngd_conv_geom;
+/* SURVEY §8f row 1 inside the step: each BN layer takes the backward's dY and
+ * x_hat (buffers 17 / 18, B x (c*S), spatial[l] = S for BN layers, ignored
+ * otherwise) instead of the (g_gamma, g_beta) capture and the BN dW: one
+ * launch per step forms the captures (buffers 5 / 6), the 3c moments
+ * (build_bn_block, unit blocks without stale gating; otherwise the captures
+ * feed the usual moment / 2c x 2c path) and the BN gradient payload
+ * (grad_payload, dist.cpp:364-371) in the buffer-2 slot.  Empirical Fisher
+ * only.  Call before the first step. */
+int spngd_opt_enable_bn_inputs(spngd_opt* opt, const int64_t* spatial);
 int spngd_opt_enable_raw_inputs(spngd_opt* opt, const spngd_conv_geom* geoms);
 /* Batched im2col alone (net.cpp:199-219) for `n` conv inputs, x: batch x
  * c_in x h x w, out: batch x (c_in k k) x (h_out w_out), device pointers. */

@@ -33,6 +33,7 @@
 #include <vector>
 
 #include "bn_full.cuh"
+#include "bn_reduce.cuh"
 #include "ctx.cuh"
 #include "factor.cuh"
 #include "inverse.cuh"
@@ -78,6 +79,9 @@ struct LayerState {
   // recursion scratch / inverse on request, its factors, T u scratch (2c)
   float* u = nullptr;
   float* raw = nullptr;  // raw conv input (enable_raw_inputs); == act for 1x1 stride-1 convs
+  float* dy = nullptr;   // BN backward inputs (enable_bn_inputs): dY and x_hat, B x (c*S)
+  float* xh = nullptr;
+  int64_t bn_S = 0;
   int64_t raw_floats = 0;
   int fa = -1, fg = -1;  // factor-plan problem indices of A and G (wgrad reuses their operands)
   float* Finv = nullptr; int64_t ldf = 0;
@@ -203,6 +207,11 @@ struct spngd_opt {
   std::vector<int> bnf_layer;               // owned BN layers in bnf_unpacks / bnf_upd order
   // raw conv inputs expanded by im2col at the start of each step
   std::vector<spngd_im2col_req> i2c; spngd_im2col_req* d_i2c = nullptr; bool raw_inputs = false;
+  // spngd_opt_enable_bn_inputs: BN layers take dY / x_hat; one fused launch
+  // forms the captures, the 3c moments (unless stale-gated) and the BN payload
+  bool bn_inputs = false;
+  BnxPlan bnx; BnxTask* d_bnx_tasks = nullptr; BnxItem* d_bnx_items = nullptr;
+  double* d_bnx_slots = nullptr; int* d_bnx_cnt = nullptr;
   // cfg.wgrad: grad_payload on the device (dense GEMM over the factor operands + BN column means)
   FactorPlan wplan;                         // OneMC: the true-label grad operands (G reads grad_sampled)
   RepackTask* d_wrepack = nullptr;
@@ -924,6 +933,8 @@ float* spngd_opt_buffer(spngd_opt* o, int layer, int which, int64_t* ld) {
     case 14: return L.gg_s;
     case 15: return L.gb_s;
     case 16: return L.raw;
+    case 17: return L.dy;
+    case 18: return L.xh;
     default: return nullptr;
   }
 }
@@ -945,9 +956,15 @@ int issue_allgather(spngd_opt* o) {
   return rc;
 }
 
-// Raw conv inputs -> the im2col captures the GEMMs read (net.cpp:199-219).
+// Raw conv inputs -> the im2col captures the GEMMs read (net.cpp:199-219);
+// BN dY / x_hat -> captures, moments and payload (net.cpp:467-475,
+// fisher.cpp:147-185, dist.cpp:364-371) in one launch.
 int issue_inputs(spngd_opt* o) {
-  return launch_im2col(o->ctx, o->d_i2c, int(o->i2c.size()));
+  int rc = launch_im2col(o->ctx, o->d_i2c, int(o->i2c.size()));
+  if (!rc && o->bn_inputs)
+    rc = launch_bn_backward(o->ctx, o->d_bnx_tasks, o->d_bnx_items, int64_t(o->bnx.items.size()), o->d_bnx_slots,
+                            o->d_bnx_cnt);
+  return rc;
 }
 
 // cfg.wgrad: this rank's shard-mean gradients from the captures (grad_payload,
@@ -1479,6 +1496,7 @@ int64_t input_floats(const spngd_opt* o, const LayerState& L, int which) {
     case 2: return bn ? 2 * L.d.g : L.d.g * L.d.a;
     case 5: case 6: case 14: case 15: return bn ? B * L.d.g : 0;
     case 16: return L.raw ? L.raw_floats : 0;
+    case 17: case 18: return (bn && L.dy) ? B * L.d.g * L.bn_S : 0;
     default: return 0;
   }
 }
@@ -1499,7 +1517,10 @@ int spngd_opt_step_host(spngd_opt* o, int64_t step, double eta, double momentum,
   cudaStream_t s = ctx->stream;
   struct Copy { float* dst; const void* src; int64_t bytes; int wave; };
   std::vector<Copy> copies;
-  const bool pipelined = o->overlap_on && o->overlap_ok && !o->cfg.wgrad && !o->cfg.sgd && !o->waves.empty();
+  // BN dY / x_hat feed the gradient payload, which the step needs first: with
+  // BN inputs the copies simply precede the step
+  const bool pipelined = o->overlap_on && o->overlap_ok && !o->cfg.wgrad && !o->cfg.sgd && !o->waves.empty() &&
+                         !o->bn_inputs;
   for (int i = 0; i < n; ++i) {
     if (in[i].layer < 0 || in[i].layer >= int(o->layers.size()) || !in[i].host)
       return fail(SPNGD_ERR_INVALID, "spngd_opt_step_host: bad input %d", i);
@@ -1630,6 +1651,52 @@ int64_t spngd_opt_ledger(const spngd_opt* o, spngd_ledger_row* out, int64_t cap)
   return n;
 }
 
+int spngd_opt_enable_bn_inputs(spngd_opt* o, const int64_t* spatial) {
+  if (!o || !spatial) return fail(SPNGD_ERR_INVALID, "spngd_opt_enable_bn_inputs: null argument");
+  if (o->bn_inputs) return fail(SPNGD_ERR_INVALID, "spngd_opt_enable_bn_inputs: already enabled");
+  if (o->graphs_ready || o->graphs_ready_ov || o->timed)
+    return fail(SPNGD_ERR_INVALID, "spngd_opt_enable_bn_inputs: call before the first step");
+  if (o->cfg.fisher_mode != 0)
+    return fail(SPNGD_ERR_INVALID, "spngd_opt_enable_bn_inputs: OneMC needs the sampled-label backward's BN capture");
+  if (o->cfg.sgd) return fail(SPNGD_ERR_INVALID, "spngd_opt_enable_bn_inputs: sgd has no BN statistics");
+  const int64_t B = o->cfg.batch;
+  // moments fused only when every BN statistic is built every step (unit
+  // blocks, no stale gating); otherwise the existing moment / SYRK paths read
+  // the captures this launch writes
+  const bool fuse_moments = o->cfg.bn_mode == 0 && !o->cfg.stale;
+  std::vector<spngd_bn_backward_req> reqs;
+  size_t k = 0;
+  for (size_t li = 0; li < o->layers.size(); ++li) {
+    LayerState& L = o->layers[li];
+    if (L.d.kind != SPNGD_BN) continue;
+    if (spatial[li] <= 0) return fail(SPNGD_ERR_SHAPE_MISMATCH, "spngd_opt_enable_bn_inputs: layer %zu: S <= 0", li);
+    L.bn_S = spatial[li];
+    const size_t n = size_t(B * L.d.g * L.bn_S);
+    L.dy = o->alloc(n);
+    L.xh = o->alloc(n);
+    if (!L.dy || !L.xh) return fail(SPNGD_ERR_CUDA, "opt: BN input allocation failed");
+    float* m3 = nullptr;
+    if (fuse_moments) {  // the bnm entries are in layer order
+      while (k < o->bnm.size() && o->bnm[k].gg != L.gg) ++k;
+      if (k == o->bnm.size()) return fail(SPNGD_ERR_INVALID, "spngd_opt_enable_bn_inputs: no moment slot for layer %zu", li);
+      m3 = o->bnm[k].out3c;
+    }
+    float* pay = spngd_opt_buffer(o, int(li), 2, nullptr);
+    reqs.push_back({L.dy, L.xh, B, L.d.g, L.bn_S, L.gg, L.gb, m3, pay});
+  }
+  int rc = plan_bn_backward(reqs, o->bnx);
+  if (rc) return rc;
+  o->d_bnx_tasks = dev_upload(o->bnx.tasks, o->owned);
+  o->d_bnx_items = dev_upload(o->bnx.items, o->owned);
+  o->d_bnx_slots = reinterpret_cast<double*>(o->alloc(size_t(2 * std::max<int64_t>(o->bnx.slots, 1) * 5)));
+  o->d_bnx_cnt = reinterpret_cast<int*>(o->alloc(size_t(std::max<int64_t>(o->bnx.channels, 1)), true));
+  if (!reqs.empty() && (!o->d_bnx_tasks || !o->d_bnx_items || !o->d_bnx_slots || !o->d_bnx_cnt))
+    return fail(SPNGD_ERR_CUDA, "opt: upload failed");
+  if (fuse_moments) o->bnm.clear();  // the fused launch writes the moments: no separate moment kernel
+  o->bn_inputs = !reqs.empty();
+  return SPNGD_OK;
+}
+
 int spngd_opt_enable_raw_inputs(spngd_opt* o, const spngd_conv_geom* geoms) {
   if (!o || !geoms) return fail(SPNGD_ERR_INVALID, "spngd_opt_enable_raw_inputs: null argument");
   if (o->raw_inputs) return fail(SPNGD_ERR_INVALID, "spngd_opt_enable_raw_inputs: already enabled");
@@ -1705,12 +1772,14 @@ int spngd_opt_attach_peers(spngd_opt* o, const void* handles) {
     for (auto& p : o->fplan.probs) p.C = remap(p.C);
     for (auto& t : o->fplan.reduce) t.packed_out = remap(t.packed_out);
     for (auto& r : o->bnm) r.out3c = remap(r.out3c);
+    for (auto& t : o->bnx.tasks) t.out3c = t.out3c ? remap(t.out3c) : nullptr;
     auto put = [&](void* d, const void* h, size_t bytes) {
       return (bytes && d) ? cudaMemcpy(d, h, bytes, cudaMemcpyHostToDevice) : cudaSuccess;
     };
     SPNGD_CUDA_TRY(put(o->d_fprobs, o->fplan.probs.data(), o->fplan.probs.size() * sizeof(GemmProblem)));
     SPNGD_CUDA_TRY(put(o->d_freduce, o->fplan.reduce.data(), o->fplan.reduce.size() * sizeof(SyrkReduceTask)));
     SPNGD_CUDA_TRY(put(o->d_bnm, o->bnm.data(), o->bnm.size() * sizeof(spngd_bn_moments_req)));
+    SPNGD_CUDA_TRY(put(o->d_bnx_tasks, o->bnx.tasks.data(), o->bnx.tasks.size() * sizeof(BnxTask)));
     for (auto& wv : o->waves) {
       for (auto& t : wv.reduce) t.packed_out = remap(t.packed_out);
       SPNGD_CUDA_TRY(put(wv.d_reduce, wv.reduce.data(), wv.reduce.size() * sizeof(SyrkReduceTask)));

@@ -17,7 +17,7 @@ from .spngd import check
 from .workloads import Layer
 
 (ACT, GRAD, DW, W, V, BN_GG, BN_GB, AINV, GINV, A_PACKED, G_PACKED, BN_M3C, ALL_WEIGHTS,
- GRAD_SAMPLED, BN_GG_SAMPLED, BN_GB_SAMPLED, RAW_ACT) = range(17)
+ GRAD_SAMPLED, BN_GG_SAMPLED, BN_GB_SAMPLED, RAW_ACT, BN_DY, BN_XHAT) = range(19)
 EMPIRICAL, ONE_MC = 0, 1  # FisherMode (fisher.hpp:14)
 BN_UNIT, BN_FULL = 0, 1   # BnMode (fisher.hpp:18)
 PHASES = ["factor_gemm", "factor_reduce_bn", "reduce_scatter", "inverse", "precondition_update", "all_gather"]
@@ -113,6 +113,8 @@ class Optimizer:
             return 2 * l.g if l.kind == "bn" else l.g * l.a
         if which in (BN_GG, BN_GB, BN_GG_SAMPLED, BN_GB_SAMPLED):
             return B * l.g
+        if which in (BN_DY, BN_XHAT):
+            return B * l.g * self.bn_spatial[li]
         if which == A_PACKED:
             return l.a * (l.a + 1) // 2
         if which == G_PACKED:
@@ -172,6 +174,13 @@ class Optimizer:
         gamma = 1, beta = 0.  Captures and dW differ per rank (distinct shards)."""
         L, B, r = N.lib(), self.batch, self.rank
         for li, l in enumerate(self.layers):
+            if l.kind == "bn" and getattr(self, "bn_spatial", None):
+                n = B * l.g * self.bn_spatial[li]
+                dy, _ = self.ptr(li, BN_DY)
+                xh, _ = self.ptr(li, BN_XHAT)
+                check(L.spngd_synth_normal(self.ctx, dy, n, _mix(seed, li, 8, r), float((B * self.bn_spatial[li]) ** -0.5),
+                                           0.0, 0))
+                check(L.spngd_synth_normal(self.ctx, xh, n, _mix(seed, li, 9, r), 1.0, 0.0, 0))
             if l.kind == "bn":
                 gg, _ = self.ptr(li, BN_GG)
                 gb, _ = self.ptr(li, BN_GB)
@@ -240,6 +249,22 @@ class Optimizer:
         buf = C.create_string_buffer(b"".join(allh), 128 * self.world)
         check(N.lib().spngd_opt_attach_peers(self.h, buf))
 
+    def enable_bn_inputs(self, spatial=None):
+        """SURVEY §8f row 1 in the step: every BN layer takes the backward's dY
+        and x_hat (BN_DY / BN_XHAT, B x (c*S)); one launch per step forms the
+        per-sample capture, the moments and the BN gradient payload
+        (spngd_opt_enable_bn_inputs).  `spatial`: S per layer (default: the
+        h_out*w_out of the conv each BN layer follows).  Before the first step."""
+        if spatial is None:
+            spatial, prev = [], 1
+            for l in self.layers:
+                if l.kind == "conv":
+                    prev = l.hw
+                spatial.append(prev if l.kind == "bn" else 0)
+        arr = (C.c_int64 * len(self.layers))(*spatial)
+        check(N.lib().spngd_opt_enable_bn_inputs(self.h, arr))
+        self.bn_spatial = list(spatial)
+
     def enable_raw_inputs(self):
         """The step takes each conv layer's raw input (RAW_ACT, B x c_in x h x w)
         and forms the im2col capture on the device (spngd_opt_enable_raw_inputs,
@@ -256,7 +281,9 @@ class Optimizer:
         inputs when enabled (else the im2col captures), grads, BN pairs, dW."""
         out = []
         for li, l in enumerate(self.layers):
-            if l.kind == "bn":
+            if l.kind == "bn" and getattr(self, "bn_spatial", None):
+                out += [(li, BN_DY), (li, BN_XHAT)]  # the step forms the captures and the BN dW
+            elif l.kind == "bn":
                 out += [(li, BN_GG), (li, BN_GB), (li, DW)]
             else:
                 a = RAW_ACT if (getattr(self, "raw_inputs", False) and l.kind == "conv") else ACT

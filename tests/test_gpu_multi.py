@@ -33,6 +33,9 @@ def _run(world, mode, layers):
            os.path.join(ROOT, "scripts", "multi_gpu_check.py"), "--mode", mode, "--layers", layers]
     p = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=900)
     out = p.stdout + p.stderr
+    if os.path.isdir(os.path.join(ROOT, "gpurun_out")):  # keep the per-layer report of GPU runs
+        with open(os.path.join(ROOT, "gpurun_out", f"multi_{world}_{mode}_{layers}.log"), "w") as f:
+            f.write(p.stdout)
     assert p.returncode == 0 and "PASS" in out, out[-4000:]
     return out
 

@@ -413,3 +413,84 @@ def test_singular_bn_block_updates_nothing(cuda_dev):
             assert np.array_equal(w0, w1) and np.array_equal(v0, v1), f"layer {li} was updated"
     finally:
         opt.close()
+
+
+@pytest.mark.parametrize("overlap", [True, False])
+def test_bn_backward_inputs_in_step(cuda_dev, overlap):
+    """SURVEY §8f row 1 inside the step: BN layers take dY / x_hat; the fused
+    launch forms the per-sample capture (net.cpp:467-475), the moments
+    (fisher.cpp:147-185) and the BN payload (dist.cpp:364-371).  Updated BN
+    parameters vs the oracle chain bn_grad_reduce -> build_bn_block ->
+    precondition_bn -> ngd_step; Kronecker layers unchanged in meaning."""
+    from paper_2002_06015_b200.step import BN_DY, BN_XHAT
+    layers = [W.conv(3, 16, 3, 1, 16), W.bn(16), W.conv(16, 32, 3, 2, 16), W.bn(32), W.conv(32, 32, 1, 1, 8),
+              W.bn(32), W.fc(32 * 64, 10)]
+    batch = 16
+    opt = Optimizer(layers, batch, lam=LAM)
+    try:
+        opt.set_overlap(overlap)
+        opt.enable_bn_inputs()
+        opt.synth(seed=9)
+        before = {}
+        for li, l in enumerate(layers):
+            ws = [BN_DY, BN_XHAT, WB, V] if l.kind == "bn" else [ACT, GRAD, DW, WB, V]
+            before[li] = {w: opt.download(li, w).numpy() for w in ws}
+        opt.step(1, ETA, MOM)
+        opt.sync()
+        for li, l in enumerate(layers):
+            b = before[li]
+            if l.kind != "bn":
+                wo, vo = oracle_layer(l, batch, b)
+                assert rel(opt.download(li, WB).numpy(), wo) <= 1e-4
+                continue
+            c, S = l.g, opt.bn_spatial[li]
+            gg, gb = O.bn_grad_reduce(b[BN_DY], b[BN_XHAT], batch, c, S)
+            # the captures the step formed
+            assert rel(opt.download(li, BN_GG).numpy(), gg.reshape(-1)) <= 1e-5
+            assert rel(opt.download(li, BN_GB).numpy(), gb.reshape(-1)) <= 1e-5
+            m3 = O.build_bn_block(gg, gb, 0, batch)
+            dW = np.concatenate([gg.mean(0), gb.mean(0)])  # grad_payload BN branch
+            assert rel(opt.download(li, DW).numpy(), dW) <= 1e-5
+            pg, pb = O.precondition_bn(m3, dW[:c], dW[c:], LAM)
+            wo, vo = O.ngd_update(b[WB], np.concatenate([pg, pb]), b[V], ETA, MOM)
+            ew, ev = rel(opt.download(li, WB).numpy(), wo), rel(opt.download(li, V).numpy(), vo)
+            assert ew <= 1e-4 and ev <= 1e-4, f"layer {li}: W {ew:.2e} V {ev:.2e}"
+    finally:
+        opt.close()
+
+
+def test_bn_backward_stats_entry_point(cuda_dev):
+    """spngd_bn_backward_stats_batched on the ResNet-50 BN shapes (B = 32):
+    captures, moments and payload vs the oracle on a few layers."""
+    import ctypes as C
+    from paper_2002_06015_b200 import _native as N
+    from paper_2002_06015_b200.spngd import check, context
+    layers = W.resnet50()
+    shapes, prev = [], None
+    for l in layers:
+        if l.kind == "conv":
+            prev = l
+        elif l.kind == "bn":
+            shapes.append((l.g, prev.hw))
+    B = 32
+    g = torch.Generator(device="cuda").manual_seed(1)
+    bufs, reqs = [], []
+    for c, S in shapes:
+        dy = torch.randn(B * c * S, device="cuda", generator=g) / (B * S) ** 0.5
+        xh = torch.randn(B * c * S, device="cuda", generator=g)
+        gg, gb = torch.empty(B * c, device="cuda"), torch.empty(B * c, device="cuda")
+        m3, pay = torch.empty(3 * c, device="cuda"), torch.empty(2 * c, device="cuda")
+        bufs.append((dy, xh, gg, gb, m3, pay))
+        reqs.append(N.BnBackwardReq(dy.data_ptr(), xh.data_ptr(), B, c, S, gg.data_ptr(), gb.data_ptr(), m3.data_ptr(),
+                                    pay.data_ptr()))
+    arr = (N.BnBackwardReq * len(reqs))(*reqs)
+    check(N.lib().spngd_bn_backward_stats_batched(context().h, len(reqs), arr))
+    for k in (0, 1, 10, len(shapes) - 1):
+        (c, S), (dy, xh, gg, gb, m3, pay) = shapes[k], bufs[k]
+        wgg, wgb = O.bn_grad_reduce(dy.cpu().numpy(), xh.cpu().numpy(), B, c, S)
+        assert rel(gg.cpu().numpy(), wgg.reshape(-1)) <= 1e-5
+        assert rel(gb.cpu().numpy(), wgb.reshape(-1)) <= 1e-5
+        # moments / payload of the fp32 captures (what build_bn_block would read)
+        cg, cb = gg.cpu().numpy().reshape(B, c), gb.cpu().numpy().reshape(B, c)
+        assert rel(m3.cpu().numpy(), O.build_bn_block(cg, cb, 0, B)) <= 1e-6
+        assert rel(pay.cpu().numpy(), np.concatenate([cg.astype(np.float64).mean(0), cb.astype(np.float64).mean(0)])) <= 1e-6
