@@ -190,20 +190,6 @@ int plan_factors(const spngd_factor_req* reqs, int n, FactorPlan& plan, float* w
     const int64_t t = (r.dim + kTileM - 1) / kTileM;
     tk.push_back({t * (t + 1) / 2, K});
   }
-  // 2-CTA SYRK (opt-in, SPNGD_PAIR=1; see gemm_pair.cu for its status) when
-  // every operand is TMA-addressable (all ResNet-50 captures are, after the repack).
-  static const bool want_pair = getenv("SPNGD_PAIR") != nullptr;
-  plan.pair = want_pair;
-  for (const auto& p : plan.probs) plan.pair = plan.pair && p.A.mode != OP_ASYNC;
-  if (plan.pair) {
-    tk.clear();
-    for (const auto& p : plan.probs) {
-      const int64_t t = (p.M + kTileM - 1) / kTileM;
-      int64_t ctas = 0;
-      for (int64_t tn = 0; tn < t; ++tn) ctas += 2 * ((tn + 2) / 2);
-      tk.push_back({ctas, p.K});
-    }
-  }
   plan.kchunk = choose_kchunk(tk);
   static const char* kc_env = getenv("SPNGD_KCHUNK");  // experiment override (multiple of 32)
   if (kc_env && atoi(kc_env) >= 32) plan.kchunk = atoi(kc_env) / 32 * 32;
@@ -213,43 +199,21 @@ int plan_factors(const spngd_factor_req* reqs, int n, FactorPlan& plan, float* w
     const bool split = p.K > plan.kchunk;
     p.mode = split ? EPI_PARTIAL : EPI_PACKED;
     const int kc = split ? plan.kchunk : p.K + kTileK;
-    if (plan.pair) {
-      plan_problem_pairs(i, p, kc, plan.items, &plan.reduce, &slot, reqs[i].scale, reqs[i].packed_out);
-      CUtensorMap hm;
-      if (encode_half_map(p.B, padded_k(p.B, p.K) >= p.K ? p.K : p.K, &hm) != SPNGD_OK) plan.pair = false;
-      plan.halfmaps.push_back(hm);
-    } else {
-      plan_problem_tiles(i, p, /*upper_only=*/true, kc, plan.items, &plan.reduce, &slot, reqs[i].scale,
-                         reqs[i].packed_out);
-    }
+    plan_problem_tiles(i, p, /*upper_only=*/true, kc, plan.items, &plan.reduce, &slot, reqs[i].scale,
+                       reqs[i].packed_out);
   }
-  if (!plan.pair && !plan.halfmaps.empty()) return fail(SPNGD_ERR_INVALID, "factor: half-box tensor map failed");
   plan.n_slots = slot;
-  // Longest work first: items are independent, so issue the big K ranges early
-  // (pairs move as units: both CTAs of a cluster read consecutive items).
-  if (plan.pair) {
-    std::vector<std::pair<GemmWorkItem, GemmWorkItem>> pairs;
-    for (size_t q = 0; q + 1 < plan.items.size(); q += 2) pairs.push_back({plan.items[q], plan.items[q + 1]});
-    std::stable_sort(pairs.begin(), pairs.end(), [](const auto& x, const auto& y) {
-      return (x.first.k1 - x.first.k0) > (y.first.k1 - y.first.k0);
-    });
-    plan.items.clear();
-    for (const auto& pr : pairs) {
-      plan.items.push_back(pr.first);
-      plan.items.push_back(pr.second);
-    }
-  } else {
-    std::stable_sort(plan.items.begin(), plan.items.end(), [](const GemmWorkItem& x, const GemmWorkItem& y) {
-      return (x.k1 - x.k0) > (y.k1 - y.k0);
-    });
-  }
+  // Longest work first: items are independent, so issue the big K ranges early.
+  std::stable_sort(plan.items.begin(), plan.items.end(), [](const GemmWorkItem& x, const GemmWorkItem& y) {
+    return (x.k1 - x.k0) > (y.k1 - y.k0);
+  });
   return SPNGD_OK;
 }
 
 int launch_factor_gemm(spngd_ctx* ctx, const FactorPlan& plan, const GemmProblem* d_probs,
                        const CUtensorMap* d_halfmaps, const GemmWorkItem* d_items, int n_items, float* d_partials,
                        cudaStream_t stream) {
-  if (plan.pair) return launch_gemm_pair(d_probs, d_halfmaps, d_items, n_items, d_partials, stream);
+  (void)d_halfmaps;
   return launch_gemm(d_probs, d_items, n_items, d_partials, ctx->d_status, stream,
                      gemm_variant(plan.probs.data(), int(plan.probs.size())));
 }

@@ -22,10 +22,7 @@ struct FactorPlan {
   std::vector<SyrkReduceTask> reduce;
   int n_slots = 0;
   int kchunk = 0;
-  // 2-CTA SYRK (gemm_pair.cu): items come in adjacent cluster pairs and
-  // halfmaps[problem] is the 64-row-box tensor map of the B operand.
-  bool pair = false;
-  std::vector<CUtensorMap> halfmaps;
+  std::vector<CUtensorMap> halfmaps;  // unused (kept for the launch signature)
 };
 
 // `ws` receives the repacked captures (sizing pass when null: only
@@ -35,7 +32,7 @@ int launch_repack(spngd_ctx* ctx, const RepackTask* d_tasks, int n, int64_t max_
 int run_factors(spngd_ctx* ctx, const FactorPlan& plan, const GemmProblem* d_probs, const CUtensorMap* d_halfmaps,
                 const GemmWorkItem* d_items, int n_items, float* d_partials, const SyrkReduceTask* d_reduce,
                 int n_reduce);
-// The factor SYRK launch alone (pair or single-CTA kernel per plan.pair).
+// The factor SYRK launch alone.
 int launch_factor_gemm(spngd_ctx* ctx, const FactorPlan& plan, const GemmProblem* d_probs,
                        const CUtensorMap* d_halfmaps, const GemmWorkItem* d_items, int n_items, float* d_partials,
                        cudaStream_t stream);

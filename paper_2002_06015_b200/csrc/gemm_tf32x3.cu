@@ -35,18 +35,7 @@ namespace spngd {
 namespace {
 
 constexpr int kOperandBytes = kTileM * kTileK * 4;     // 16 KB (128 rows x 128 B)
-// Two smem layouts (template kDeep):
-//  false: 4 stages of (A raw | B raw (= B hi) | B lo), 48 KB each;
-//  true:  6 stages of (A raw, then B lo | B raw), 32 KB each -- the A tile is
-//         dead once split into TMEM, so the B lo plane is written over it and
-//         the ring holds 5 stages in flight instead of 3 (the SYRK waits on
-//         operand delivery: more bytes in flight per SM).
-template <bool kDeep> struct Ring {
-  static constexpr int stages = kDeep ? 6 : 4;
-  static constexpr int stage_bytes = (kDeep ? 2 : 3) * kOperandBytes;
-  static constexpr int a_slots = 4;  // TMEM A hi|lo slots (64 columns each)
-};
-constexpr int kMaxStages = 6;
+constexpr int kStageBytes = 3 * kOperandBytes;         // A raw, B raw (= B hi), B lo
 // Epilogue tile row stride: 132 floats keeps rows 16-byte aligned (float4
 // row access is conflict-free) and makes the (16 columns x 2 row-quads) column
 // access of the transposed/update stores conflict-free too (528 = 16 mod 32).
@@ -55,13 +44,11 @@ constexpr int kTmemCols = 512;  // 2 x 128 accumulator columns + kStages x (A hi
 constexpr uint32_t kTmemA = 256;                       // first A-operand column
 
 struct __align__(64) SmemCtl {
-  uint64_t full[kMaxStages];
-  uint64_t empty[kMaxStages];
+  uint64_t full[kStages];
+  uint64_t empty[kStages];
   uint64_t tmem_full[2];
   uint64_t tmem_empty[2];
-  uint64_t raw[2][kMaxStages];  // TMA raw-tile arrival per operand (A, B)
-  uint64_t a_read[kMaxStages];  // kDeep: the A raw tile has been read (B lo may overwrite it)
-  uint64_t ta_empty[4];         // kDeep: TMEM A slot free (MMAs of the stage that used it done)
+  uint64_t raw[2][kStages];  // TMA raw-tile arrival per operand (A, B)
   uint32_t tmem_base;
   int32_t pad;
   GemmProblem prob;
@@ -180,12 +167,10 @@ __device__ __forceinline__ void issue_stage(const GemmOperand& op, int32_t r0, i
 // variant its problems need: the inverse recursion issues ~100 short launches
 // per matrix that each start with a cold instruction cache, so code size is
 // latency.
-template <uint32_t kModes, bool kAsync, bool kDeep>
+template <uint32_t kModes, bool kAsync>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     gemm_tf32x3_kernel(const GemmProblem* __restrict__ probs, const GemmWorkItem* __restrict__ items,
                        float* __restrict__ partials, int* status, long long* trace) {
-  constexpr int kStages = Ring<kDeep>::stages;
-  constexpr int kStageBytes = Ring<kDeep>::stage_bytes;
   // trace (debug): for CTAs < 4, stages < 64: [cta][stage][4] clock64 stamps
   // {A TMA issued, A raw landed, MMA saw full, drain saw MMA done}.
 #ifdef SPNGD_GEMM_TRACE_BUILD
@@ -207,7 +192,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   // derived pointer keeps the shared address space: LDS/STS, not generic
   // LD/ST (which cost ~10k cycles per epilogue tile and slowed `prob` reads).
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  SmemCtl* ctl = reinterpret_cast<SmemCtl*>(smem + kMaxStages * 32768);  // past the larger ring (6 x 32 = 4 x 48 KB)
+  SmemCtl* ctl = reinterpret_cast<SmemCtl*>(smem + kStages * kStageBytes);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -239,10 +224,6 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       mbar_init(&ctl->tmem_full[b], 1);
       mbar_init(&ctl->tmem_empty[b], 256);
       for (int q = 0; q < kStages; ++q) mbar_init(&ctl->raw[b][q], 1);
-    }
-    if constexpr (kDeep) {
-      for (int q = 0; q < kStages; ++q) mbar_init(&ctl->a_read[q], 128);
-      for (int q = 0; q < 4; ++q) mbar_init(&ctl->ta_empty[q], 1);
     }
     mbar_fence_init();
   }
@@ -300,10 +281,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       if (lane == 0) {
         const uint32_t base = smem_u32(smem + slot * kStageBytes);
         const uint32_t b_hi = diag_shared ? base : base + kOperandBytes;
-        // kDeep: B lo sits over the dead A raw tile (off-diagonal) or in the
-        // unused B raw region (diagonal, where the A raw tile is B hi)
-        const uint32_t b_lo = kDeep ? (diag_shared ? base + kOperandBytes : base) : base + 2 * kOperandBytes;
-        const uint32_t a_hi = tmem + kTmemA + (kDeep ? (it & 3) : slot) * 64, a_lo = a_hi + 32;
+        const uint32_t b_lo = base + 2 * kOperandBytes;
+        const uint32_t a_hi = tmem + kTmemA + slot * 64, a_lo = a_hi + 32;
         const uint32_t dt = tmem + b * 128;
 #pragma unroll
         for (int kk = 0; kk < kTileK / 8; ++kk) {
@@ -314,7 +293,6 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           umma_tf32_ts(dt, a_hi + kk * 8, dbh, idesc, 1u);
         }
         umma_commit(&ctl->empty[slot]);
-        if constexpr (kDeep) umma_commit(&ctl->ta_empty[it & 3]);
         umma_commit(&ctl->tmem_full[b]);
       }
       __syncwarp();
@@ -345,9 +323,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     const int rbase = t >> 3;      // cp.async: 0..15
     const int32_t row0 = (is_b ? item.tn : item.tm) * kTileM;
     const uint32_t raw_off = is_b ? kOperandBytes : 0;
-    // B lo plane: own region (4-stage layout); over the A raw tile (kDeep,
-    // off-diagonal) or in the unused B raw region (kDeep, diagonal)
-    const uint32_t blo_off = kDeep ? (diag_shared ? kOperandBytes : 0) : 2 * kOperandBytes;
+    const uint32_t blo_off = 2 * kOperandBytes;
     // Raw fp32 tiles land three stages ahead -- by TMA (one elected thread,
     // mbarrier complete_tx) when the layout allows, else by per-thread
     // cp.async.  A: each thread takes one row, writes tf32 hi/lo into TMEM
@@ -390,16 +366,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         const float4 v = *reinterpret_cast<const float4*>(stage + raw_off + r * 128 + ((q ^ (r & 7)) << 4));
         x[4 * q] = v.x; x[4 * q + 1] = v.y; x[4 * q + 2] = v.z; x[4 * q + 3] = v.w;
       }
-      if constexpr (kDeep) {
-        // the A raw tile is read: the B group may write its lo plane over it
-        if (!diag_shared) mbar_arrive(&ctl->a_read[slot]);
-        // the MMAs that last read this TMEM A slot (stage it - 4) are done
-        if (it >= 4) mbar_wait(&ctl->ta_empty[it & 3], ((it >> 2) + 1) & 1);
-        tc_fence_after();
-      }
 #pragma unroll
       for (int q = 0; q < 32; ++q) h[q] = __uint_as_float(__float_as_uint(x[q]) & 0xffffe000u);
-      const uint32_t ta = tmem + (uint32_t(warp * 32) << 16) + kTmemA + (kDeep ? (it & 3) : slot) * 64;
+      const uint32_t ta = tmem + (uint32_t(warp * 32) << 16) + kTmemA + slot * 64;
       tmem_st_32x32b_x32(ta, h);
 #pragma unroll
       for (int q = 0; q < 32; ++q) {
@@ -422,7 +391,6 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     auto convert_b = [&](int it) {
       const int slot = it % kStages;
       uint8_t* stage = smem + slot * kStageBytes;
-      if constexpr (kDeep) mbar_wait(&ctl->a_read[slot], (it / kStages) & 1);  // A raw read: overwrite it
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
         const int r = rbase + 16 * j;
@@ -795,67 +763,7 @@ void finalize_operand(GemmOperand& op, int64_t K, bool allow_tma) {
   }
 }
 
-// Same tensor as the operand's own map, 64-row boxes (the B half-tile of the
-// 2-CTA SYRK, gemm_pair.cu).  Valid for OP_TMA2D / OP_TMA3D operands.
-int encode_half_map(const GemmOperand& op, int64_t K, CUtensorMap* out) {
-  auto encode = tma_encode_fn();
-  if (!encode || (op.mode != OP_TMA2D && op.mode != OP_TMA3D)) return SPNGD_ERR_INVALID;
-  cuuint32_t box[3] = {32, 64, 1};
-  cuuint32_t estr[3] = {1, 1, 1};
-  CUresult r;
-  if (op.mode == OP_TMA2D) {
-    cuuint64_t dims[2] = {cuuint64_t(K), cuuint64_t(op.rows)};
-    cuuint64_t strides[1] = {cuuint64_t(op.row_stride) * 4};
-    r = encode(out, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(op.ptr), dims, strides, box, estr,
-               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  } else {
-    cuuint64_t dims[3] = {cuuint64_t(op.seg_len), cuuint64_t(op.rows), cuuint64_t(op.nseg)};
-    cuuint64_t strides[2] = {cuuint64_t(op.row_stride) * 4, cuuint64_t(op.seg_stride) * 4};
-    r = encode(out, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(op.ptr), dims, strides, box, estr,
-               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  }
-  return r == CUDA_SUCCESS ? SPNGD_OK : SPNGD_ERR_INVALID;
-}
-
-// SYRK (upper triangle) tiles as vertical CTA pairs (2p, 2p+1) x tn for the
-// 2-CTA kernel: both items of a pair share tn and the K range; a partner below
-// the diagonal or past the last row tile computes but keeps nothing (slot -1,
-// and the packed epilogue's i <= j mask).
-int plan_problem_pairs(int problem_index, const GemmProblem& p, int kchunk, std::vector<GemmWorkItem>& items,
-                       std::vector<SyrkReduceTask>* reduce, int* next_slot, double reduce_scale, float* packed_out) {
-  const int T = (p.M + kTileM - 1) / kTileM;
-  kchunk = std::max(kTileK, (kchunk / kTileK) * kTileK);
-  const int nchunks = std::max(1, (p.K + kchunk - 1) / kchunk);
-  int used = 0;
-  for (int tn = 0; tn < T; ++tn)
-    for (int tm0 = 0; tm0 <= tn; tm0 += 2) {
-      const bool keep1 = tm0 + 1 <= tn;  // tile (tm0+1, tn) in the upper triangle (and a real row tile)
-      if (nchunks == 1) {
-        items.push_back({problem_index, tm0, tn, 0, p.K, -1});
-        items.push_back({problem_index, tm0 + 1, tn, 0, p.K, -1});
-        continue;
-      }
-      const int s0 = *next_slot;
-      *next_slot += nchunks;
-      const int s1 = keep1 ? *next_slot : -1;
-      if (keep1) *next_slot += nchunks;
-      for (int q = 0; q < nchunks; ++q) {
-        const int k0 = q * kchunk, k1 = std::min(p.K, k0 + kchunk);
-        items.push_back({problem_index, tm0, tn, k0, k1, s0 + q});
-        items.push_back({problem_index, tm0 + 1, tn, k0, k1, keep1 ? s1 + q : -1});
-      }
-      used += nchunks * (keep1 ? 2 : 1);
-      if (reduce) {
-        reduce->push_back({tm0, tn, s0, nchunks, p.M, 0, reduce_scale, packed_out});
-        if (keep1) reduce->push_back({tm0 + 1, tn, s1, nchunks, p.M, 0, reduce_scale, packed_out});
-      }
-    }
-  return used;
-}
-
-size_t gemm_smem_bytes() { return size_t(kMaxStages) * 32768 + sizeof(SmemCtl) + 1024; }
+size_t gemm_smem_bytes() { return size_t(kStages) * kStageBytes + sizeof(SmemCtl) + 1024; }
 
 thread_local int g_gemm_launch_prio = 0;
 
@@ -871,34 +779,18 @@ uint32_t gemm_variant(const GemmProblem* probs, int n) {
 namespace {
 using GemmKernelFn = void (*)(const GemmProblem*, const GemmWorkItem*, float*, int*, long long*);
 
-template <uint32_t kModes, bool kAsync, bool kDeep>
-GemmKernelFn gemm_instance_ring(size_t smem, int* err) {
+template <uint32_t kModes, bool kAsync>
+GemmKernelFn gemm_instance(size_t smem, int* err) {
   static bool attr_set = false;
   if (!attr_set) {
-    if (cudaFuncSetAttribute(gemm_tf32x3_kernel<kModes, kAsync, kDeep>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    if (cudaFuncSetAttribute(gemm_tf32x3_kernel<kModes, kAsync>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              int(smem)) != cudaSuccess) {
       *err = 1;
       return nullptr;
     }
     attr_set = true;
   }
-  return gemm_tf32x3_kernel<kModes, kAsync, kDeep>;
-}
-
-// Ring layout: the 6-stage "B lo over A raw" ring by default; SPNGD_GEMM_RING=4
-// selects the 4-stage (A raw | B raw | B lo) ring (experiments).
-bool deep_ring() {
-  static const bool deep = [] {
-    const char* e = getenv("SPNGD_GEMM_RING");
-    return !(e && atoi(e) == 4);
-  }();
-  return deep;
-}
-
-template <uint32_t kModes, bool kAsync>
-GemmKernelFn gemm_instance(size_t smem, int* err) {
-  return deep_ring() ? gemm_instance_ring<kModes, kAsync, true>(smem, err)
-                     : gemm_instance_ring<kModes, kAsync, false>(smem, err);
+  return gemm_tf32x3_kernel<kModes, kAsync>;
 }
 
 // The variants the planners produce (factor: PARTIAL|PACKED; inverse rounds
@@ -1000,8 +892,9 @@ int plan_problem_tiles(int problem_index, const GemmProblem& p, bool upper_only,
                        double reduce_scale, float* packed_out) {
   const int tiles_m = (p.M + kTileM - 1) / kTileM;
   const int tiles_n = (p.N + kTileN - 1) / kTileN;
+  const bool whole = kchunk >= p.K;  // no split-K (callers pass K + kTileK)
   kchunk = std::max(kTileK, (kchunk / kTileK) * kTileK);
-  const int nchunks = std::max(1, (p.K + kchunk - 1) / kchunk);
+  const int nchunks = whole ? 1 : std::max(1, (p.K + kchunk - 1) / kchunk);
   int used = 0;
   struct SplitTile {
     int tm, tn, slot0;

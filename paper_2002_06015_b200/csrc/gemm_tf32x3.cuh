@@ -123,14 +123,6 @@ int launch_gemm(const GemmProblem* d_probs, const GemmWorkItem* d_items, int n_i
                 int* d_status, cudaStream_t stream, uint32_t variant = 0xFu | kVariantAsync);
 int launch_syrk_reduce(const SyrkReduceTask* d_tasks, int n_tasks, const float* d_partials, cudaStream_t stream);
 
-// 2-CTA SYRK (gemm_pair.cu): items come in cluster pairs (2p, 2p+1) x tn;
-// d_halfmaps[problem] is the B operand's 64-row-box tensor map.
-int encode_half_map(const GemmOperand& op, int64_t K, CUtensorMap* out);
-int plan_problem_pairs(int problem_index, const GemmProblem& p, int kchunk, std::vector<GemmWorkItem>& items,
-                       std::vector<SyrkReduceTask>* reduce, int* next_slot, double reduce_scale, float* packed_out);
-int launch_gemm_pair(const GemmProblem* d_probs, const CUtensorMap* d_halfmaps, const GemmWorkItem* d_items,
-                     int n_items, float* d_partials, cudaStream_t stream);
-
 // Host planning helpers.
 // Upper-triangle (or full) tile list for one problem with K split into chunks
 // of at most `kchunk` (multiple of kTileK).  Appends to items; returns the

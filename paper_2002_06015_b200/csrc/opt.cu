@@ -570,6 +570,9 @@ int build(spngd_opt* o, const spngd_layer_desc* descs, int n) {
       const GemmProblem& pa = o->fplan.probs[L.fa];
       const GemmProblem& pg = one_mc ? o->wplan.probs[k++] : o->fplan.probs[L.fg];
       if (pa.K != pg.K) return fail(SPNGD_ERR_SHAPE_MISMATCH, "wgrad: layer %d operands disagree on K", li);
+      // both operands must walk K in the same order (TMA3D pairs samples per stage)
+      if (pa.A.mode != pg.A.mode || (pa.A.mode == OP_TMA3D && pa.A.cps != pg.A.cps))
+        return fail(SPNGD_ERR_SHAPE_MISMATCH, "wgrad: layer %d operands disagree on the K layout", li);
       GemmProblem p{};
       p.A = pg.A;  // rows: output channels, K: samples x positions (conv: sum_s G_s A_s^T)
       p.B = pa.A;  // rows: c_in k^2 / d_in
