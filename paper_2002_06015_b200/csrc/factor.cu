@@ -194,34 +194,58 @@ int plan_factors(const spngd_factor_req* reqs, int n, FactorPlan& plan, float* w
   static const char* kc_env = getenv("SPNGD_KCHUNK");  // experiment override (multiple of 32)
   if (kc_env && atoi(kc_env) >= 32) plan.kchunk = atoi(kc_env) / 32 * 32;
   int slot = 0;
+  std::vector<GemmWorkItem> pair_items;
+  plan.pair_prob.assign(size_t(n), 0);
   for (int i = 0; i < n; ++i) {
     GemmProblem& p = plan.probs[i];
     const bool split = p.K > plan.kchunk;
     p.mode = split ? EPI_PARTIAL : EPI_PACKED;
     const int kc = split ? plan.kchunk : p.K + kTileK;
-    plan_problem_tiles(i, p, /*upper_only=*/true, kc, plan.items, &plan.reduce, &slot, reqs[i].scale,
-                       reqs[i].packed_out);
+    if (pair_eligible(p)) {  // 256 x 256 tiles on CTA pairs (gemm_pair.cu)
+      plan.pair_prob[size_t(i)] = 1;
+      plan_pair_tiles(i, p, kc, pair_items, &plan.reduce, &slot, reqs[i].scale, reqs[i].packed_out);
+    } else {
+      plan_problem_tiles(i, p, /*upper_only=*/true, kc, plan.items, &plan.reduce, &slot, reqs[i].scale,
+                         reqs[i].packed_out);
+    }
   }
   plan.n_slots = slot;
-  // Longest work first: items are independent, so issue the big K ranges early.
-  std::stable_sort(plan.items.begin(), plan.items.end(), [](const GemmWorkItem& x, const GemmWorkItem& y) {
-    return (x.k1 - x.k0) > (y.k1 - y.k0);
-  });
+  // Longest work first: items are independent, so issue the big K ranges early
+  // (cluster pairs move as units).
+  auto longer = [](const GemmWorkItem& x, const GemmWorkItem& y) { return (x.k1 - x.k0) > (y.k1 - y.k0); };
+  std::stable_sort(plan.items.begin(), plan.items.end(), longer);
+  std::vector<std::pair<GemmWorkItem, GemmWorkItem>> pairs;
+  for (size_t q = 0; q + 1 < pair_items.size(); q += 2) pairs.push_back({pair_items[q], pair_items[q + 1]});
+  std::stable_sort(pairs.begin(), pairs.end(), [&](const auto& x, const auto& y) { return longer(x.first, y.first); });
+  std::vector<GemmWorkItem> all;
+  for (const auto& pr : pairs) {
+    all.push_back(pr.first);
+    all.push_back(pr.second);
+  }
+  plan.n_pair = int(all.size());
+  all.insert(all.end(), plan.items.begin(), plan.items.end());
+  plan.items.swap(all);
   return SPNGD_OK;
 }
 
-int launch_factor_gemm(spngd_ctx* ctx, const FactorPlan& plan, const GemmProblem* d_probs,
-                       const CUtensorMap* d_halfmaps, const GemmWorkItem* d_items, int n_items, float* d_partials,
-                       cudaStream_t stream) {
-  (void)d_halfmaps;
-  return launch_gemm(d_probs, d_items, n_items, d_partials, ctx->d_status, stream,
+int count_pair_items(const FactorPlan& plan, const std::vector<GemmWorkItem>& items) {
+  int k = 0;
+  while (k < int(items.size()) && plan.pair_prob[size_t(items[size_t(k)].problem)]) ++k;
+  return k;
+}
+
+int launch_factor_gemm(spngd_ctx* ctx, const FactorPlan& plan, const GemmProblem* d_probs, int n_pair,
+                       const GemmWorkItem* d_items, int n_items, float* d_partials, cudaStream_t stream) {
+  int rc = launch_syrk_pair(d_probs, d_items, n_pair, d_partials, stream);
+  if (rc || n_items <= n_pair) return rc;
+  return launch_gemm(d_probs, d_items + n_pair, n_items - n_pair, d_partials, ctx->d_status, stream,
                      gemm_variant(plan.probs.data(), int(plan.probs.size())));
 }
 
-int run_factors(spngd_ctx* ctx, const FactorPlan& plan, const GemmProblem* d_probs, const CUtensorMap* d_halfmaps,
+int run_factors(spngd_ctx* ctx, const FactorPlan& plan, const GemmProblem* d_probs, int n_pair,
                 const GemmWorkItem* d_items, int n_items, float* d_partials, const SyrkReduceTask* d_reduce,
                 int n_reduce) {
-  int rc = launch_factor_gemm(ctx, plan, d_probs, d_halfmaps, d_items, n_items, d_partials, ctx->stream);
+  int rc = launch_factor_gemm(ctx, plan, d_probs, n_pair, d_items, n_items, d_partials, ctx->stream);
   if (rc) return rc;
   ctx->launches += n_items > 0;
   rc = launch_syrk_reduce(d_reduce, n_reduce, d_partials, ctx->stream);
@@ -285,10 +309,9 @@ extern "C" int spngd_factor_sym_batched(spngd_ctx* ctx, int n, const spngd_facto
   auto* d_probs = scratch.upload(plan.probs);
   auto* d_items = scratch.upload(plan.items);
   auto* d_reduce = scratch.upload(plan.reduce);
-  auto* d_half = scratch.upload(plan.halfmaps);
   float* d_partials = scratch.alloc<float>(size_t(std::max(plan.n_slots, 1)) * kTileM * kTileN);
   if (!d_probs || !d_items || !d_reduce || !d_partials) return fail(SPNGD_ERR_CUDA, "factor: workspace allocation failed");
-  rc = run_factors(ctx, plan, d_probs, d_half, d_items, int(plan.items.size()), d_partials, d_reduce,
+  rc = run_factors(ctx, plan, d_probs, plan.n_pair, d_items, int(plan.items.size()), d_partials, d_reduce,
                    int(plan.reduce.size()));
   if (rc) return rc;
   SPNGD_CUDA_TRY(cudaStreamSynchronize(ctx->stream));

@@ -22,20 +22,25 @@ struct FactorPlan {
   std::vector<SyrkReduceTask> reduce;
   int n_slots = 0;
   int kchunk = 0;
-  std::vector<CUtensorMap> halfmaps;  // unused (kept for the launch signature)
+  // 2-CTA SYRK: items of pair-eligible problems come first (n_pair of them,
+  // in cluster pairs); every filtered item list keeps that order.
+  std::vector<char> pair_prob;
+  int n_pair = 0;
 };
 
 // `ws` receives the repacked captures (sizing pass when null: only
 // repack_floats is meaningful).
 int plan_factors(const spngd_factor_req* reqs, int n, FactorPlan& plan, float* ws = nullptr);
 int launch_repack(spngd_ctx* ctx, const RepackTask* d_tasks, int n, int64_t max_elems);
-int run_factors(spngd_ctx* ctx, const FactorPlan& plan, const GemmProblem* d_probs, const CUtensorMap* d_halfmaps,
+// Leading items of `items` that belong to the 2-CTA kernel.
+int count_pair_items(const FactorPlan& plan, const std::vector<GemmWorkItem>& items);
+int run_factors(spngd_ctx* ctx, const FactorPlan& plan, const GemmProblem* d_probs, int n_pair,
                 const GemmWorkItem* d_items, int n_items, float* d_partials, const SyrkReduceTask* d_reduce,
                 int n_reduce);
 // The factor SYRK launch alone.
-int launch_factor_gemm(spngd_ctx* ctx, const FactorPlan& plan, const GemmProblem* d_probs,
-                       const CUtensorMap* d_halfmaps, const GemmWorkItem* d_items, int n_items, float* d_partials,
-                       cudaStream_t stream);
+// Items [0, n_pair) run on the 2-CTA kernel, the rest on the single-CTA engine.
+int launch_factor_gemm(spngd_ctx* ctx, const FactorPlan& plan, const GemmProblem* d_probs, int n_pair,
+                       const GemmWorkItem* d_items, int n_items, float* d_partials, cudaStream_t stream);
 int launch_bn_moments(spngd_ctx* ctx, const spngd_bn_moments_req* d_reqs, int n, int64_t max_c);
 
 struct BnGradPayloadTask {  // grad_payload's BN branch (dist.cpp:364-371)

@@ -1,0 +1,435 @@
+// sm_100a 2-CTA (cta_group::2) 3xTF32 SYRK: 256 x 256 output tiles for the
+// large Kronecker factors (K1, mean_outer, fisher.cpp:55-75).
+//
+// Why: the single-CTA engine (gemm_tf32x3.cu) moves 32 KB of operands per
+// 128x128x32 stage and is bound by operand delivery per SM (~14-15 B/cycle of
+// the 42 B/cycle it would need at full MMA rate; neither a deeper ring nor
+// larger TMA boxes helped, profiles/r02_ring).  A CTA pair on one TPC computes
+// a 256x256 tile with one M=256, N=256 tcgen05.mma per product: each CTA loads
+// its 128 A rows and HALF of the B tile (128 rows), the same 32 KB per stage,
+// for twice the MMA work -- half the operand bytes per flop.
+//
+// Layout per CTA and 32-k stage (3 stages, 64 KB each):
+//   A raw (= A hi) | A lo | B raw (= B hi) | B lo        (SS-form MMAs)
+// TMEM: two 256-column fp32 accumulators (each CTA holds its 128 rows x 256),
+// drained into round-to-nearest registers after every stage exactly as in the
+// single-CTA engine, so the RZ accumulation bias stays bounded by one stage.
+// Diagonal super-tiles (A rows == B rows in each CTA) load one tile per stage.
+//
+// Roles (384 threads per CTA, up to 168 registers each): warps 0-3 producers
+// (TMA of the A tile and the B half, both lo planes), warps 4-11 drain (128
+// fp32 accumulators per thread: lane quarter warp % 4, column half
+// (warp - 4) / 4); warp 4 of the leader (cluster rank 0) issues the MMAs.
+// Pair synchronisation: the producers of both CTAs arrive on the leader's
+// `full` barrier (remote mbarrier arrive); the leader's commits are multicast
+// to both CTAs' `empty` and `tmem_full`; drain warps of both CTAs arrive on
+// the leader's `tmem_empty`.  Epilogues (packed triangle / split-K partials)
+// per CTA.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+
+#include "common.cuh"
+#include "gemm_tf32x3.cuh"
+
+namespace spngd {
+
+namespace {
+
+constexpr int kPS = 3;                          // stages
+constexpr int kPOp = kTileM * kTileK * 4;       // 16 KB: one 128 x 32 fp32 plane
+constexpr int kPStage = 4 * kPOp;               // A raw | A lo | B raw | B lo
+constexpr int kPEpi = 2 * kTileN + 4;           // epilogue tile row stride (floats)
+constexpr int kPThreads = 384;
+
+struct __align__(64) PairCtl {
+  uint64_t raw[kPS];         // TMA arrival of this CTA's A tile (+ B half)
+  uint64_t full[kPS];        // leader: 2 arrivals (the producer group of each CTA)
+  uint64_t empty[kPS];       // multicast commit: stage free
+  uint64_t tmem_full[2];     // multicast commit
+  uint64_t tmem_empty[2];    // leader: 16 drain-warp arrivals (8 per CTA)
+  uint32_t tmem_base;
+  int32_t pad;
+  GemmProblem prob;
+  GemmWorkItem item;
+};
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t map_to_rank(uint32_t smem_addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_addr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n.reg .pred p;\nWAITC_%=: mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAITC_%=;\n}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+// Arrive on the leader's copy of `bar` (local when this CTA is the leader).
+__device__ __forceinline__ void arrive_leader(uint64_t* bar, bool leader) {
+  if (leader) {
+    mbar_arrive(bar);
+  } else {
+    const uint32_t remote = map_to_rank(smem_u32(bar), 0);
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
+  }
+}
+__device__ __forceinline__ void tmem_alloc_pair(uint32_t* dst) {
+  asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(dst)), "n"(512)
+               : "memory");
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_dealloc_pair(uint32_t taddr) {
+  asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(taddr), "n"(512) : "memory");
+}
+// D[tmem] (+)= A[smem] * B[smem]^T across the pair (M = 256: 128 rows per CTA).
+__device__ __forceinline__ void umma_pair_ss(uint32_t d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                             uint32_t acc) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc)
+      : "memory");
+}
+__device__ __forceinline__ void commit_pair(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"(uint16_t(3))
+      : "memory");
+}
+__device__ __forceinline__ void expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void load_tile(const GemmOperand& op, const CUtensorMap* map, uint32_t dst, int32_t tq,
+                                          int32_t row0, uint64_t* bar) {
+  if (op.mode == OP_TMA2D) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+            dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(tq * kTileK), "r"(row0), "r"(smem_u32(bar))
+        : "memory");
+  } else {
+    const int32_t seg = tq / op.cps, ch = tq - seg * op.cps;
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(
+            dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(ch * kTileK), "r"(row0), "r"(seg), "r"(smem_u32(bar))
+        : "memory");
+  }
+}
+__device__ __forceinline__ void tmem_ld_x32_nowait(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+}
+
+// Lo plane of a 128 x 32 swizzled fp32 tile: rows rbase + 16 j, 16-byte chunk c.
+__device__ __forceinline__ void lo_plane(const uint8_t* src, uint8_t* dst, int rbase, int c) {
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const int r = rbase + 16 * j;
+    const uint32_t off = r * 128 + ((c ^ (r & 7)) << 4);
+    const float4 x = *reinterpret_cast<const float4*>(src + off);
+    float4 l;
+    l.x = tf32_lo(x.x);
+    l.y = tf32_lo(x.y);
+    l.z = tf32_lo(x.z);
+    l.w = tf32_lo(x.w);
+    *reinterpret_cast<float4*>(dst + off) = l;
+  }
+}
+
+// Work item of CTA r of a pair: tm = 2 I + r (its 128-row tile), tn = 2 J (the
+// first of its two 128-column tiles), slot = first of 2 partial slots (split-K).
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPThreads, 1)
+    syrk_pair_kernel(const GemmProblem* __restrict__ probs, const GemmWorkItem* __restrict__ items,
+                     float* __restrict__ partials) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  PairCtl* ctl = reinterpret_cast<PairCtl*>(smem + kPS * kPStage);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_rank();
+  const bool leader = rank == 0;
+
+  if (threadIdx.x == 0) ctl->item = items[blockIdx.x];
+  __syncthreads();
+  {
+    const int32_t* src = reinterpret_cast<const int32_t*>(probs + ctl->item.problem);
+    int32_t* dst = reinterpret_cast<int32_t*>(&ctl->prob);
+    for (int i = threadIdx.x; i < int(sizeof(GemmProblem) / 4); i += blockDim.x) dst[i] = src[i];
+  }
+  const GemmWorkItem item0 = ctl->item;
+  const bool diag = (item0.tm >> 1) == (item0.tn >> 1);  // A rows == B rows in both CTAs
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kPS; ++s) {
+      mbar_init(&ctl->raw[s], 1);
+      mbar_init(&ctl->full[s], 2);
+      mbar_init(&ctl->empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&ctl->tmem_full[b], 1);
+      mbar_init(&ctl->tmem_empty[b], 16);
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
+  if (warp == 4) tmem_alloc_pair(&ctl->tmem_base);
+  tc_fence_before();
+  cluster_sync_all();  // both CTAs' barriers and the pair's TMEM exist before any remote use
+  tc_fence_after();
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  const uint32_t tmem = ctl->tmem_base;
+  const GemmWorkItem item = ctl->item;
+  const GemmProblem& prob = ctl->prob;
+  const int n_iters = (item.k1 - item.k0 + kTileK - 1) / kTileK;
+  float* T = reinterpret_cast<float*>(smem);
+
+  if (warp >= 4) {
+    // ---------------------------------------- MMA issue (leader warp 4) + drain (4-11)
+    const uint32_t lane_base = uint32_t((warp & 3) * 32) << 16;
+    const uint32_t col_base = ((warp - 4) >> 2) * 128;
+    float acc[128];
+#pragma unroll
+    for (int j = 0; j < 128; ++j) acc[j] = 0.f;
+    auto drain = [&](int j) {
+      const int b = j & 1;
+      mbar_wait(&ctl->tmem_full[b], (j >> 1) & 1);
+      tc_fence_after();
+#pragma unroll
+      for (int h = 0; h < 4; ++h) {
+        uint32_t v[32];
+        tmem_ld_x32_nowait(tmem + lane_base + b * 256 + col_base + 32 * h, v);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+        for (int q = 0; q < 32; ++q) acc[32 * h + q] += __uint_as_float(v[q]);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) arrive_leader(&ctl->tmem_empty[b], leader);
+    };
+    constexpr uint32_t idesc = umma_idesc_tf32(2 * kTileM, 2 * kTileN);  // M = 256 across the pair, N = 256
+    auto issue_mma = [&](int it) {
+      const int s = it % kPS, b = it & 1;
+      mbar_wait_cluster(&ctl->full[s], (it / kPS) & 1);
+      if (it >= 2) mbar_wait_cluster(&ctl->tmem_empty[b], ((it >> 1) + 1) & 1);
+      tc_fence_after();
+      if (lane == 0) {
+        const uint32_t base = smem_u32(smem + s * kPStage);
+        const uint32_t a_hi = base, a_lo = base + kPOp;
+        const uint32_t b_hi = diag ? a_hi : base + 2 * kPOp, b_lo = diag ? a_lo : base + 3 * kPOp;
+        const uint32_t dt = tmem + b * 256;
+#pragma unroll
+        for (int kk = 0; kk < kTileK / 8; ++kk) {
+          const uint32_t koff = kk * 32;  // 8 tf32 = 32 bytes along the swizzled row
+          const uint64_t dah = umma_desc_k_sw128(a_hi + koff), dal = umma_desc_k_sw128(a_lo + koff);
+          const uint64_t dbh = umma_desc_k_sw128(b_hi + koff), dbl = umma_desc_k_sw128(b_lo + koff);
+          umma_pair_ss(dt, dal, dbh, idesc, kk > 0 ? 1u : 0u);
+          umma_pair_ss(dt, dah, dbl, idesc, 1u);
+          umma_pair_ss(dt, dah, dbh, idesc, 1u);
+        }
+        commit_pair(&ctl->empty[s]);
+        commit_pair(&ctl->tmem_full[b]);
+      }
+      __syncwarp();
+    };
+    if (warp == 4 && leader) {
+      for (int it = 0; it < n_iters; ++it) {
+        issue_mma(it);
+        if (it >= 1) drain(it - 1);
+      }
+      if (n_iters >= 1) drain(n_iters - 1);
+    } else {
+      for (int j = 0; j < n_iters; ++j) drain(j);
+    }
+    // every MMA of this CTA's accumulator has completed: the stage ring is free
+    asm volatile("bar.sync 1, 256;" ::: "memory");
+    const int r = (warp & 3) * 32 + lane;
+    float4* trow = reinterpret_cast<float4*>(T + r * kPEpi + col_base);
+#pragma unroll
+    for (int j = 0; j < 32; ++j) trow[j] = make_float4(acc[4 * j], acc[4 * j + 1], acc[4 * j + 2], acc[4 * j + 3]);
+  } else {
+    // ------------------------------------------------------------ producers (warps 0-3)
+    const int t = threadIdx.x;
+    const int c = t & 7, rbase = t >> 3;
+    const CUtensorMap* amap = &probs[item.problem].A.tmap;
+    const CUtensorMap* bmap = &probs[item.problem].B.tmap;
+    // A: this CTA's 128 rows; B: this CTA's half (128 rows) of the 256-row B tile
+    const int32_t arow = item.tm * kTileM, brow = (item.tn + int32_t(rank)) * kTileN;
+    const int32_t tq0 = item.k0 / kTileK;
+    const uint32_t bytes = diag ? kPOp : 2 * kPOp;
+    auto load = [&](int q) {
+      const int ps = q % kPS;
+      const uint32_t st = smem_u32(smem + ps * kPStage);
+      expect_tx(&ctl->raw[ps], bytes);
+      load_tile(prob.A, amap, st, tq0 + q, arow, &ctl->raw[ps]);
+      if (!diag) load_tile(prob.B, bmap, st + 2 * kPOp, tq0 + q, brow, &ctl->raw[ps]);
+    };
+    if (t == 0) {
+      asm volatile("fence.proxy.tensormap::generic.acquire.gpu [%0], 128;" ::"l"(reinterpret_cast<uint64_t>(amap))
+                   : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(amap)) : "memory");
+      if (!diag) {
+        asm volatile("fence.proxy.tensormap::generic.acquire.gpu [%0], 128;" ::"l"(reinterpret_cast<uint64_t>(bmap))
+                     : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(bmap)) : "memory");
+      }
+      for (int q = 0; q < kPS - 1 && q < n_iters; ++q) load(q);
+    }
+    for (int it = 0; it < n_iters; ++it) {
+      const int s = it % kPS;
+      uint8_t* stage = smem + s * kPStage;
+      mbar_wait(&ctl->raw[s], (it / kPS) & 1);
+      lo_plane(stage, stage + kPOp, rbase, c);
+      if (!diag) lo_plane(stage + 2 * kPOp, stage + 3 * kPOp, rbase, c);
+      fence_proxy_async_smem();
+      asm volatile("bar.sync 2, 128;" ::: "memory");
+      if (t == 0) {
+        arrive_leader(&ctl->full[s], leader);
+        const int nx = it + kPS - 1;  // refill the slot the MMAs of stage it-1 released
+        if (nx < n_iters) {
+          mbar_wait(&ctl->empty[nx % kPS], ((nx / kPS) & 1) ^ 1);
+          load(nx);
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync_all();  // the pair's MMAs, commits and remote arrivals are all done
+  if (warp == 4) {
+    tc_fence_after();
+    tmem_dealloc_pair(tmem);
+  }
+
+  // ------------------------------------------------------------ epilogue (this CTA's 128 x 256)
+  const int tid = threadIdx.x;
+  const int64_t n = prob.M;
+  const int64_t m0 = int64_t(item.tm) * kTileM, n0 = int64_t(item.tn) * kTileN;
+  if (prob.mode == EPI_PARTIAL) {
+    if (item.slot < 0) return;
+    // sub-tile q (columns 128 q..) -> slot + q; rows/columns outside the
+    // triangle are written too (the reduction only reads kept tiles)
+    for (int p = tid; p < 8192; p += kPThreads) {  // 8192 float4 chunks
+      const int r = p >> 6, cc = (p & 63) * 4;
+      const int q = cc >> 7;
+      float4* dst = reinterpret_cast<float4*>(partials + (int64_t(item.slot) + q) * kTileM * kTileN);
+      dst[r * 32 + ((cc & 127) >> 2)] = *reinterpret_cast<const float4*>(T + r * kPEpi + cc);
+    }
+  } else {  // EPI_PACKED: alpha * acc -> packed upper triangle
+    float* C = prob.C;
+    const float alpha = prob.alpha;
+    for (int p = tid; p < 8192; p += kPThreads) {
+      const int r = p >> 6, cc = (p & 63) * 4;
+      const int64_t i = m0 + r;
+      if (i >= n) continue;
+      const int64_t rb = packed_offset(n, i, i) - i;
+      const float4 v = *reinterpret_cast<const float4*>(T + r * kPEpi + cc);
+      const float vv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int64_t jj = n0 + cc + q;
+        if (jj < n && i <= jj) C[rb + jj] = alpha * vv[q];
+      }
+    }
+  }
+}
+
+}  // namespace
+
+bool pair_eligible(const GemmProblem& p) {
+  static const bool off = getenv("SPNGD_NO_PAIR") != nullptr;
+  if (off || !(p.flags & FLAG_SAME_AB)) return false;
+  if (p.A.mode != OP_TMA2D && p.A.mode != OP_TMA3D) return false;
+  // 256-row super-tiles: worth it while they cover the triangle with little
+  // waste (n >= 1000: at most ~1.35x the 128-tile MMA work, for half the bytes per flop)
+  return p.M >= 1000;
+}
+
+int plan_pair_tiles(int problem_index, const GemmProblem& p, int kchunk, std::vector<GemmWorkItem>& items,
+                    std::vector<SyrkReduceTask>* reduce, int* next_slot, double reduce_scale, float* packed_out) {
+  const int t128 = (p.M + kTileM - 1) / kTileM;
+  const int ts = (p.M + 2 * kTileM - 1) / (2 * kTileM);
+  const bool whole = kchunk >= p.K;
+  kchunk = std::max(kTileK, (kchunk / kTileK) * kTileK);
+  const int nchunks = whole ? 1 : std::max(1, (p.K + kchunk - 1) / kchunk);
+  struct Pair {
+    int I, J, s0, s1;
+  };
+  std::vector<Pair> pairs;
+  int used = 0;
+  for (int J = 0; J < ts; ++J)
+    for (int I = 0; I <= J; ++I) {
+      Pair pr{I, J, -1, -1};
+      if (nchunks > 1) {
+        for (int r = 0; r < 2; ++r) {
+          const int s0 = *next_slot;
+          *next_slot += 2 * nchunks;
+          used += 2 * nchunks;
+          (r ? pr.s1 : pr.s0) = s0;
+          const int tm = 2 * I + r;
+          for (int q = 0; q < 2; ++q) {
+            const int tn = 2 * J + q;
+            if (tm < t128 && tn < t128 && tm <= tn && reduce)
+              reduce->push_back({tm, tn, s0 + q, nchunks, p.M, 2, reduce_scale, packed_out});
+          }
+        }
+      }
+      pairs.push_back(pr);
+    }
+  // chunk-major so the pairs running together share panels in L2
+  for (int q = 0; q < nchunks; ++q) {
+    const int k0 = q * kchunk, k1 = nchunks == 1 ? p.K : std::min(p.K, k0 + kchunk);
+    for (const Pair& pr : pairs)
+      for (int r = 0; r < 2; ++r)
+        items.push_back({problem_index, 2 * pr.I + r, 2 * pr.J, k0, k1,
+                         nchunks == 1 ? -1 : (r ? pr.s1 : pr.s0) + 2 * q});
+  }
+  return used;
+}
+
+size_t gemm_pair_smem_bytes() { return size_t(kPS) * kPStage + sizeof(PairCtl) + 1024; }
+
+int launch_syrk_pair(const GemmProblem* d_probs, const GemmWorkItem* d_items, int n_items, float* d_partials,
+                     cudaStream_t stream) {
+  if (n_items <= 0) return SPNGD_OK;
+  static bool attr_set = false;
+  const size_t smem = gemm_pair_smem_bytes();
+  if (!attr_set) {
+    SPNGD_CUDA_TRY(cudaFuncSetAttribute(syrk_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    attr_set = true;
+  }
+  static const bool pdl = getenv("SPNGD_NO_PDL") == nullptr;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(unsigned(n_items));
+  cfg.blockDim = dim3(kPThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, syrk_pair_kernel, d_probs, d_items, d_partials);
+  if (e != cudaSuccess) return fail(SPNGD_ERR_CUDA, "syrk_pair launch failed: %s", cudaGetErrorString(e));
+  return SPNGD_OK;
+}
+
+}  // namespace spngd

@@ -705,7 +705,8 @@ __global__ void syrk_reduce_kernel(const SyrkReduceTask* __restrict__ tasks, con
     if (i >= n || j >= n || i > j) continue;
     double s = 0.0;
     const float* p = partials + int64_t(t.slot0) * kTileM * kTileN + idx;
-    for (int q = 0; q < t.nslots; ++q) s += double(p[int64_t(q) * kTileM * kTileN]);
+    const int64_t step = int64_t(t.stride > 1 ? t.stride : 1) * kTileM * kTileN;
+    for (int q = 0; q < t.nslots; ++q) s += double(p[q * step]);
     t.packed_out[packed_offset(n, i, j)] = float(s * t.scale);
   }
 }

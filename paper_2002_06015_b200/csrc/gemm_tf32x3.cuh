@@ -89,7 +89,7 @@ struct SyrkReduceTask {
   int32_t tm, tn;
   int32_t slot0, nslots;
   int32_t n;          // matrix dimension
-  int32_t pad_;
+  int32_t stride;     // slot stride (0 or 1: consecutive; 2: the 2-CTA SYRK's interleaved sub-tiles)
   double scale;
   float* packed_out;
 };
@@ -122,6 +122,15 @@ extern thread_local int g_gemm_launch_prio;
 int launch_gemm(const GemmProblem* d_probs, const GemmWorkItem* d_items, int n_items, float* d_partials,
                 int* d_status, cudaStream_t stream, uint32_t variant = 0xFu | kVariantAsync);
 int launch_syrk_reduce(const SyrkReduceTask* d_tasks, int n_tasks, const float* d_partials, cudaStream_t stream);
+
+// 2-CTA SYRK (gemm_pair.cu): 256 x 256 tiles for the large factors.  Items
+// come in cluster pairs (CTA rank r: tm = 2I + r, tn = 2J, two 128x128
+// sub-tiles, partial slots slot and slot + 1).
+bool pair_eligible(const GemmProblem& p);
+int plan_pair_tiles(int problem_index, const GemmProblem& p, int kchunk, std::vector<GemmWorkItem>& items,
+                    std::vector<SyrkReduceTask>* reduce, int* next_slot, double reduce_scale, float* packed_out);
+int launch_syrk_pair(const GemmProblem* d_probs, const GemmWorkItem* d_items, int n_items, float* d_partials,
+                     cudaStream_t stream);
 
 // Host planning helpers.
 // Upper-triangle (or full) tile list for one problem with K split into chunks

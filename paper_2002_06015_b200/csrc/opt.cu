@@ -118,7 +118,6 @@ struct spngd_opt {
   FactorPlan fplan;
   GemmProblem* d_fprobs = nullptr; GemmWorkItem* d_fitems = nullptr; SyrkReduceTask* d_freduce = nullptr;
   RepackTask* d_repack = nullptr;
-  CUtensorMap* d_fhalf = nullptr;
   float* d_partials = nullptr;
   std::vector<spngd_bn_moments_req> bnm;
   spngd_bn_moments_req* d_bnm = nullptr; int64_t bnm_maxc = 0;
@@ -537,7 +536,6 @@ int build(spngd_opt* o, const spngd_layer_desc* descs, int n) {
   o->d_fprobs = dev_upload(o->fplan.probs, own);
   o->d_fitems = dev_upload(o->fplan.items, own);
   o->d_freduce = dev_upload(o->fplan.reduce, own);
-  o->d_fhalf = dev_upload(o->fplan.halfmaps, own);
   o->d_partials = o->alloc(size_t(std::max(o->fplan.n_slots, 1)) * kTileM * kTileN);
   if (o->cfg.wgrad) {  // grad_payload (dist.cpp:315-391) -> this rank's gradient region
     const bool one_mc = o->cfg.fisher_mode == 1;
@@ -1002,7 +1000,7 @@ int issue_phase(spngd_opt* o, int phase) {
       if (!rc) rc = launch_repack(ctx, o->d_repack, int(o->fplan.repacks.size()), o->fplan.repack_max);
       if (!rc) rc = issue_wgrad(o, false);
       if (rc) return rc;
-      rc = launch_factor_gemm(ctx, o->fplan, o->d_fprobs, o->d_fhalf, o->d_fitems, int(o->fplan.items.size()),
+      rc = launch_factor_gemm(ctx, o->fplan, o->d_fprobs, o->fplan.n_pair, o->d_fitems, int(o->fplan.items.size()),
                               o->d_partials, s);
       ctx->launches++;
       return rc;
@@ -1111,7 +1109,8 @@ int issue_overlap(spngd_opt* o, bool capturing, bool host_in = false) {
       if (rc) return rc;
     }
     if (!wv.items.empty()) {
-      rc = launch_factor_gemm(ctx, o->fplan, o->d_fprobs, o->d_fhalf, wv.d_items, int(wv.items.size()),
+      rc = launch_factor_gemm(ctx, o->fplan, o->d_fprobs, count_pair_items(o->fplan, wv.items), wv.d_items,
+                              int(wv.items.size()),
                               o->d_partials, s);
       if (rc) return rc;
       ctx->launches++;
@@ -1230,7 +1229,8 @@ int stale_partial_phase(spngd_opt* o, int phase) {
         rc = launch_repack(ctx, o->d_repack_dyn, int(rp.size()), o->fplan.repack_max);
       }
       if (!rc && !it.empty()) {
-        rc = launch_factor_gemm(ctx, o->fplan, o->d_fprobs, o->d_fhalf, o->d_fitems_dyn, int(it.size()),
+        rc = launch_factor_gemm(ctx, o->fplan, o->d_fprobs, count_pair_items(o->fplan, it), o->d_fitems_dyn,
+                                int(it.size()),
                                 o->d_partials, s);
         ctx->launches++;
       }
