@@ -160,7 +160,7 @@ __device__ __forceinline__ void lo_plane(const uint8_t* src, uint8_t* dst, int r
 // first of its two 128-column tiles), slot = first of 2 partial slots (split-K).
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPThreads, 1)
     syrk_pair_kernel(const GemmProblem* __restrict__ probs, const GemmWorkItem* __restrict__ items,
-                     float* __restrict__ partials) {
+                     float* __restrict__ partials, int* status) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   PairCtl* ctl = reinterpret_cast<PairCtl*>(smem + kPS * kPStage);
@@ -175,8 +175,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPThreads, 1)
     int32_t* dst = reinterpret_cast<int32_t*>(&ctl->prob);
     for (int i = threadIdx.x; i < int(sizeof(GemmProblem) / 4); i += blockDim.x) dst[i] = src[i];
   }
+  __syncthreads();  // the cooperative descriptor copy is complete before anyone reads it
   const GemmWorkItem item0 = ctl->item;
-  const bool diag = (item0.tm >> 1) == (item0.tn >> 1);  // A rows == B rows in both CTAs
+  // SYRK super-diagonal tile: A rows == B rows in both CTAs, one load per stage
+  const bool diag = (ctl->prob.flags & FLAG_SAME_AB) && (item0.tm >> 1) == (item0.tn >> 1);
   if (threadIdx.x == 0) {
     for (int s = 0; s < kPS; ++s) {
       mbar_init(&ctl->raw[s], 1);
@@ -333,7 +335,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPThreads, 1)
       float4* dst = reinterpret_cast<float4*>(partials + (int64_t(item.slot) + q) * kTileM * kTileN);
       dst[r * 32 + ((cc & 127) >> 2)] = *reinterpret_cast<const float4*>(T + r * kPEpi + cc);
     }
-  } else {  // EPI_PACKED: alpha * acc -> packed upper triangle
+  } else if (prob.mode == EPI_PACKED) {  // alpha * acc -> packed upper triangle
     float* C = prob.C;
     const float alpha = prob.alpha;
     for (int p = tid; p < 8192; p += kPThreads) {
@@ -349,6 +351,88 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPThreads, 1)
         if (jj < n && i <= jj) C[rb + jj] = alpha * vv[q];
       }
     }
+  } else if (prob.mode == EPI_DENSE) {  // C = alpha acc + beta Cin, row-major (no mirror / transposed copy)
+    float* C = prob.C;
+    const float* Cin = prob.Cin;
+    const float alpha = prob.alpha, beta = prob.beta;
+    const int64_t M = prob.M, N = prob.N, ldc = prob.ldc;
+    const bool has_cin = beta != 0.f;
+    const bool vec = ((reinterpret_cast<uintptr_t>(C) | (has_cin ? reinterpret_cast<uintptr_t>(Cin) : 0)) & 15) == 0 &&
+                     (ldc & 3) == 0;
+    for (int p = tid; p < 8192; p += kPThreads) {
+      const int r = p >> 6, cc = (p & 63) * 4;
+      const int64_t i = m0 + r, j = n0 + cc;
+      if (i >= M || j >= N) continue;
+      float4 v = *reinterpret_cast<const float4*>(T + r * kPEpi + cc);
+      float* dst = C + i * ldc + j;
+      if (vec && j + 3 < N) {
+        float4 ci = has_cin ? *reinterpret_cast<const float4*>(Cin + i * ldc + j) : make_float4(0.f, 0.f, 0.f, 0.f);
+        v = make_float4(alpha * v.x + beta * ci.x, alpha * v.y + beta * ci.y, alpha * v.z + beta * ci.z,
+                        alpha * v.w + beta * ci.w);
+        *reinterpret_cast<float4*>(dst) = v;
+      } else {
+        const float vv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          if (j + q < N) dst[q] = alpha * vv[q] + (has_cin ? beta * Cin[i * ldc + j + q] : 0.f);
+      }
+    }
+  } else if (prob.mode == EPI_UPDATE) {
+    // P^T tile (rows: a-index j = m0 + r, columns: g-index i = n0 + c) ->
+    // W' = W - eta P + m V, V' = W' - W (fisher.cpp:332-333) along weight rows
+    // W[i * a + j], plus the ||W'||^2 partials of the rescale.  Nothing is
+    // written after a failed inverse / BN check (status word, precond.cu).
+    if (prob.W && status && *reinterpret_cast<volatile int*>(status)) return;
+    const int64_t a = prob.M, N = prob.N;
+    const float alpha = prob.alpha;
+    const float eta = prob.scal ? prob.scal[0] : prob.eta;
+    const float mom = prob.scal ? prob.scal[1] : prob.momentum;
+    float* W = prob.W;
+    float* V = prob.V;
+    float* Pout = prob.P_out;
+    const bool vec = (a & 3) == 0 && (!W || ((reinterpret_cast<uintptr_t>(W) | reinterpret_cast<uintptr_t>(V)) & 15) == 0) &&
+                     (!Pout || (reinterpret_cast<uintptr_t>(Pout) & 15) == 0);
+    double ss = 0.0;
+    for (int p = tid; p < 8192; p += kPThreads) {
+      // 16 columns x 2 row quads per warp: conflict-free column reads of T
+      const int wk = p >> 5, ln = p & 31;
+      const int c = (wk & 15) * 16 + (ln & 15);
+      const int r = ((wk >> 4) * 2 + (ln >> 4)) * 4;
+      const int64_t j = m0 + r, i = n0 + c;
+      if (i >= N || j >= a) continue;
+      const float t0 = T[r * kPEpi + c], t1 = T[(r + 1) * kPEpi + c], t2 = T[(r + 2) * kPEpi + c],
+                  t3 = T[(r + 3) * kPEpi + c];
+      const float pp[4] = {alpha * t0, alpha * t1, alpha * t2, alpha * t3};
+      const int64_t o = i * a + j;
+      const int nq = (a - j) >= 4 ? 4 : int(a - j);
+      if (vec && nq == 4) {
+        if (Pout) *reinterpret_cast<float4*>(Pout + o) = make_float4(pp[0], pp[1], pp[2], pp[3]);
+        if (W) {
+          const float4 w = *reinterpret_cast<const float4*>(W + o), vl = *reinterpret_cast<const float4*>(V + o);
+          const float4 nw = make_float4(w.x - eta * pp[0] + mom * vl.x, w.y - eta * pp[1] + mom * vl.y,
+                                        w.z - eta * pp[2] + mom * vl.z, w.w - eta * pp[3] + mom * vl.w);
+          *reinterpret_cast<float4*>(W + o) = nw;
+          *reinterpret_cast<float4*>(V + o) = make_float4(nw.x - w.x, nw.y - w.y, nw.z - w.z, nw.w - w.w);
+          ss += double(nw.x) * nw.x + double(nw.y) * nw.y + double(nw.z) * nw.z + double(nw.w) * nw.w;
+        }
+      } else {
+        for (int q = 0; q < nq; ++q) {
+          if (Pout) Pout[o + q] = pp[q];
+          if (W) {
+            const float w = W[o + q];
+            const float nw = w - eta * pp[q] + mom * V[o + q];
+            W[o + q] = nw;
+            V[o + q] = nw - w;
+            ss += double(nw) * nw;
+          }
+        }
+      }
+    }
+    if (prob.norm2) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+      if (lane == 0 && ss != 0.0) atomicAdd(prob.norm2, ss);
+    }
   }
 }
 
@@ -358,9 +442,13 @@ bool pair_eligible(const GemmProblem& p) {
   static const bool off = getenv("SPNGD_NO_PAIR") != nullptr;
   if (off || !(p.flags & FLAG_SAME_AB)) return false;
   if (p.A.mode != OP_TMA2D && p.A.mode != OP_TMA3D) return false;
-  // 256-row super-tiles: worth it while they cover the triangle with little
-  // waste (n >= 1000: at most ~1.35x the 128-tile MMA work, for half the bytes per flop)
-  return p.M >= 1000;
+  // 256-row super-tiles cover the triangle with more (partly empty) MMA work
+  // than 128-row tiles; the pair runs ~1.45x the single-CTA rate on the same
+  // work (ncu: tensor pipe 45.6% vs 38.6%, ResNet-50 B=32), so it wins while
+  // its sub-tile count stays within 1.35x (n = 147, 256, 512, >= 1024; not 64,
+  // 128, 576)
+  const int64_t t = (p.M + kTileM - 1) / kTileM, ts = (p.M + 2 * kTileM - 1) / (2 * kTileM);
+  return double(2 * ts * (ts + 1)) <= 1.35 * double(t * (t + 1) / 2);
 }
 
 int plan_pair_tiles(int problem_index, const GemmProblem& p, int kchunk, std::vector<GemmWorkItem>& items,
@@ -405,10 +493,35 @@ int plan_pair_tiles(int problem_index, const GemmProblem& p, int kchunk, std::ve
   return used;
 }
 
+bool pair_eligible_dense(const GemmProblem& p) {
+  static const bool off = getenv("SPNGD_NO_PAIR") != nullptr;
+  if (off || (p.flags & (FLAG_SYM_MIRROR | FLAG_TRANS)) || (p.mode != EPI_DENSE && p.mode != EPI_UPDATE)) return false;
+  if ((p.A.mode != OP_TMA2D && p.A.mode != OP_TMA3D) || (p.B.mode != OP_TMA2D && p.B.mode != OP_TMA3D)) return false;
+  if (p.M < 256 || p.N < 256) return false;
+  const int64_t tm = (p.M + kTileM - 1) / kTileM, tn = (p.N + kTileN - 1) / kTileN;
+  const int64_t sm = (p.M + 2 * kTileM - 1) / (2 * kTileM), sn = (p.N + 2 * kTileN - 1) / (2 * kTileN);
+  return double(4 * sm * sn) <= 1.2 * double(tm * tn);
+}
+
+int plan_pair_dense(int problem_index, const GemmProblem& p, std::vector<GemmWorkItem>& items) {
+  const int sm = (p.M + 2 * kTileM - 1) / (2 * kTileM), sn = (p.N + 2 * kTileN - 1) / (2 * kTileN);
+  for (int I = 0; I < sm; ++I)
+    for (int J = 0; J < sn; ++J) {
+      int k0 = 0, k1 = p.K;  // triangular operands: the band of the whole 256 x 256 tile
+      if (p.ktri & KTRI_A_LOWER) k1 = std::min(k1, (2 * I + 2) * kTileM);
+      if (p.ktri & KTRI_A_UPPER) k0 = std::max(k0, 2 * I * kTileM);
+      if (p.ktri & KTRI_B_LOWER) k1 = std::min(k1, (2 * J + 2) * kTileN);
+      if (p.ktri & KTRI_B_UPPER) k0 = std::max(k0, 2 * J * kTileN);
+      if (k1 < k0) k1 = k0;
+      for (int r = 0; r < 2; ++r) items.push_back({problem_index, 2 * I + r, 2 * J, k0, k1, -1});
+    }
+  return 0;
+}
+
 size_t gemm_pair_smem_bytes() { return size_t(kPS) * kPStage + sizeof(PairCtl) + 1024; }
 
 int launch_syrk_pair(const GemmProblem* d_probs, const GemmWorkItem* d_items, int n_items, float* d_partials,
-                     cudaStream_t stream) {
+                     cudaStream_t stream, int* d_status) {
   if (n_items <= 0) return SPNGD_OK;
   static bool attr_set = false;
   const size_t smem = gemm_pair_smem_bytes();
@@ -427,7 +540,7 @@ int launch_syrk_pair(const GemmProblem* d_probs, const GemmWorkItem* d_items, in
   attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, syrk_pair_kernel, d_probs, d_items, d_partials);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, syrk_pair_kernel, d_probs, d_items, d_partials, d_status);
   if (e != cudaSuccess) return fail(SPNGD_ERR_CUDA, "syrk_pair launch failed: %s", cudaGetErrorString(e));
   return SPNGD_OK;
 }

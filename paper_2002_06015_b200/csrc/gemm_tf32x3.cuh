@@ -129,8 +129,12 @@ int launch_syrk_reduce(const SyrkReduceTask* d_tasks, int n_tasks, const float* 
 bool pair_eligible(const GemmProblem& p);
 int plan_pair_tiles(int problem_index, const GemmProblem& p, int kchunk, std::vector<GemmWorkItem>& items,
                     std::vector<SyrkReduceTask>* reduce, int* next_slot, double reduce_scale, float* packed_out);
+// Dense problems (EPI_DENSE without mirror/transposed copy, EPI_UPDATE) on
+// the pair kernel: 256 x 256 tiles, K band per tile for triangular operands.
+bool pair_eligible_dense(const GemmProblem& p);
+int plan_pair_dense(int problem_index, const GemmProblem& p, std::vector<GemmWorkItem>& items);
 int launch_syrk_pair(const GemmProblem* d_probs, const GemmWorkItem* d_items, int n_items, float* d_partials,
-                     cudaStream_t stream);
+                     cudaStream_t stream, int* d_status = nullptr);
 
 // Host planning helpers.
 // Upper-triangle (or full) tile list for one problem with K split into chunks

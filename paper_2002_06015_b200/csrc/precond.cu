@@ -238,6 +238,7 @@ int plan_precondition(const spngd_precond_req* reqs, int n, double eta, double m
                       double* norms, PrecondPlan& plan, const float* scal, const PrecondTri* tri) {
   plan = PrecondPlan();
   plan.stages = tri ? 4 : 2;
+  std::vector<std::vector<GemmWorkItem>> pair_items[4];  // per stage, per problem: cluster-pair items
   size_t off = 0;
   auto take = [&](int64_t floats) {
     float* p = tmp ? tmp + off : nullptr;
@@ -305,7 +306,12 @@ int plan_precondition(const spngd_precond_req* reqs, int n, double eta, double m
     for (int q = 0; q < plan.stages; ++q) {
       plan.probs[q].push_back(st[q]);
       int slot = 0;
-      plan_problem_tiles(idx, st[q], false, st[q].K + kTileK, plan.items[q], nullptr, &slot, 1.0, nullptr);
+      if (pair_eligible_dense(st[q])) {  // 256 x 256 tiles on CTA pairs (gemm_pair.cu)
+        pair_items[q].push_back({});
+        plan_pair_dense(idx, st[q], pair_items[q].back());
+      } else {
+        plan_problem_tiles(idx, st[q], false, st[q].K + kTileK, plan.items[q], nullptr, &slot, 1.0, nullptr);
+      }
     }
     if (r.W && r.rescale)
       plan.rescale.push_back({r.W, r.V, r.g * r.a, norms ? norms + i : nullptr, std::sqrt(2.0 * double(r.g))});
@@ -313,7 +319,21 @@ int plan_precondition(const spngd_precond_req* reqs, int n, double eta, double m
   plan.tmp_floats = off;
   plan.n_norms = n;
   auto longest = [](const GemmWorkItem& x, const GemmWorkItem& y) { return (x.k1 - x.k0) > (y.k1 - y.k0); };
-  for (int q = 0; q < plan.stages; ++q) std::stable_sort(plan.items[q].begin(), plan.items[q].end(), longest);
+  for (int q = 0; q < plan.stages; ++q) {
+    std::stable_sort(plan.items[q].begin(), plan.items[q].end(), longest);
+    std::vector<std::pair<GemmWorkItem, GemmWorkItem>> pairs;  // longest first, pairs as units
+    for (const auto& v : pair_items[q])
+      for (size_t k = 0; k + 1 < v.size(); k += 2) pairs.push_back({v[k], v[k + 1]});
+    std::stable_sort(pairs.begin(), pairs.end(), [&](const auto& x, const auto& y) { return longest(x.first, y.first); });
+    std::vector<GemmWorkItem> all;
+    for (const auto& pr : pairs) {
+      all.push_back(pr.first);
+      all.push_back(pr.second);
+    }
+    plan.n_pair[q] = int(all.size());
+    all.insert(all.end(), plan.items[q].begin(), plan.items[q].end());
+    plan.items[q].swap(all);
+  }
   return SPNGD_OK;
 }
 
@@ -322,10 +342,14 @@ int run_precondition(spngd_ctx* ctx, const PrecondPlan& plan, GemmProblem* const
   if (d_norms && plan.n_norms > 0)
     SPNGD_CUDA_TRY(cudaMemsetAsync(d_norms, 0, sizeof(double) * plan.n_norms, ctx->stream));
   for (int q = 0; q < plan.stages; ++q) {
-    int rc = launch_gemm(d_probs[q], d_items[q], int(plan.items[q].size()), nullptr, ctx->d_status, ctx->stream,
-                         gemm_variant(plan.probs[q].data(), int(plan.probs[q].size())));
+    const int np = plan.n_pair[q], n = int(plan.items[q].size());
+    int rc = launch_syrk_pair(d_probs[q], d_items[q], np, nullptr, ctx->stream, ctx->d_status);
+    ctx->launches += np > 0;
+    if (!rc && n > np)
+      rc = launch_gemm(d_probs[q], d_items[q] + np, n - np, nullptr, ctx->d_status, ctx->stream,
+                       gemm_variant(plan.probs[q].data(), int(plan.probs[q].size())));
     if (rc) return rc;
-    ctx->launches++;
+    ctx->launches += n > np;
   }
   if (!plan.rescale.empty()) {
     dim3 grid(296, unsigned(plan.rescale.size()));

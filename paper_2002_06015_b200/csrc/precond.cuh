@@ -52,7 +52,8 @@ struct PrecondPlan {
   // plan_precondition).
   int stages = 2;
   std::vector<GemmProblem> probs[4];
-  std::vector<GemmWorkItem> items[4];
+  std::vector<GemmWorkItem> items[4];   // per stage: the 2-CTA pair items first (n_pair)
+  int n_pair[4] = {0, 0, 0, 0};
   std::vector<RescaleTask> rescale;
   size_t tmp_floats = 0;    // intermediate products
   int n_norms = 0;
