@@ -190,6 +190,45 @@ __device__ __forceinline__ float tf32_lo(float x) {
   return __uint_as_float(l);
 }
 
+// Implicit im2col gather (net.cpp:199-219) of one 32-k stage of a 128-row tile
+// into a 128B-swizzled K-major fp32 plane: warp `wg` of a 4-warp group takes
+// rows wg, wg + 4, ..., lane = k offset, one 4-byte cp.async per element with
+// zero fill for padding / rows or k beyond the operand.  Row (ch, ky, kx) is
+// stepped incrementally (4 rows per step), so the loop has no divisions.
+template <typename Geo>
+__device__ __forceinline__ void im2col_stage(const float* x, const Geo& g, int32_t rows, int32_t row0, int32_t kbase,
+                                             int32_t kend, uint32_t plane, int wg, int lane) {
+  const int32_t kk = kbase + lane;
+  const int32_t s = kk / g.seg_pad, p = kk - s * g.seg_pad;
+  const bool kval = kk < kend && p < g.hw;
+  const int32_t oy = p / g.wo, ox = p - oy * g.wo;
+  const int32_t iy0 = oy * g.stride - g.pad, ix0 = ox * g.stride - g.pad;
+  const int64_t plane_elems = int64_t(g.h) * g.w;
+  const float* xs = x + int64_t(s) * g.c * plane_elems;
+  const int32_t kk2 = g.k * g.k;
+  int32_t r = row0 + wg;
+  int32_t ch = r / kk2, rem = r - ch * kk2;
+  int32_t ky = rem / g.k, kx = rem - ky * g.k;
+#pragma unroll 4
+  for (int j = 0; j < 32; ++j, r += 4) {
+    const int rl = wg + 4 * j;
+    const int32_t iy = iy0 + ky, ix = ix0 + kx;
+    const bool ok = kval && r < rows && uint32_t(iy) < uint32_t(g.h) && uint32_t(ix) < uint32_t(g.w);
+    const float* src = ok ? xs + ch * plane_elems + int64_t(iy) * g.w + ix : x;
+    const uint32_t dst = plane + rl * 128 + ((((lane >> 2) ^ (rl & 7)) << 4) | ((lane & 3) << 2));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(dst), "l"(src), "r"(ok ? 4u : 0u) : "memory");
+    // next row = r + 4: (ch, ky, kx) += 4 in row-major (ky, kx) order
+    kx += 4;
+    while (kx >= g.k) {
+      kx -= g.k;
+      if (++ky == g.k) {
+        ky = 0;
+        ++ch;
+      }
+    }
+  }
+}
+
 __device__ __forceinline__ int64_t packed_offset(int64_t n, int64_t i, int64_t j) {
   // linalg.hpp:48-51, requires i <= j
   return i * n - i * (i - 1) / 2 + (j - i);

@@ -140,6 +140,20 @@ __device__ __forceinline__ void tmem_ld_x32_nowait(uint32_t taddr, uint32_t (&r)
       : "r"(taddr));
 }
 
+#ifdef SPNGD_GEMM_TRACE_BUILD
+// make TRACE=1 + SPNGD_GEMM_TRACE=1: clock64 stamps of the first pair's stages
+// {TMA issued, landed, full arrived (producers), MMA issued (leader), drained}
+__device__ long long g_pair_trace[2][64][5];
+#define PAIR_STAMP(cond, cta, it, k) \
+  do {                               \
+    if ((cond) && blockIdx.x < 2 && (it) < 64) g_pair_trace[cta][it][k] = clock64(); \
+  } while (0)
+#else
+#define PAIR_STAMP(cond, cta, it, k) \
+  do {                               \
+  } while (0)
+#endif
+
 // Lo plane of a 128 x 32 swizzled fp32 tile: rows rbase + 16 j, 16-byte chunk c.
 __device__ __forceinline__ void lo_plane(const uint8_t* src, uint8_t* dst, int rbase, int c) {
 #pragma unroll
@@ -215,6 +229,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPThreads, 1)
       const int b = j & 1;
       mbar_wait(&ctl->tmem_full[b], (j >> 1) & 1);
       tc_fence_after();
+      PAIR_STAMP(warp == 4 && lane == 0, rank, j, 4);
 #pragma unroll
       for (int h = 0; h < 4; ++h) {
         uint32_t v[32];
@@ -233,6 +248,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPThreads, 1)
       mbar_wait_cluster(&ctl->full[s], (it / kPS) & 1);
       if (it >= 2) mbar_wait_cluster(&ctl->tmem_empty[b], ((it >> 1) + 1) & 1);
       tc_fence_after();
+      PAIR_STAMP(lane == 0, 0, it, 3);
       if (lane == 0) {
         const uint32_t base = smem_u32(smem + s * kPStage);
         const uint32_t a_hi = base, a_lo = base + kPOp;
@@ -277,14 +293,29 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPThreads, 1)
     const int32_t arow = item.tm * kTileM, brow = (item.tn + int32_t(rank)) * kTileN;
     const int32_t tq0 = item.k0 / kTileK;
     const uint32_t bytes = diag ? kPOp : 2 * kPOp;
+    // implicit im2col operands (raw conv inputs) are gathered by all 128
+    // producer threads with cp.async (one commit group per stage)
+    const bool gather = prob.A.mode == OP_IM2COL;
     auto load = [&](int q) {
       const int ps = q % kPS;
+      PAIR_STAMP(t == 0, rank, q, 0);
       const uint32_t st = smem_u32(smem + ps * kPStage);
+      if (gather) {
+        const int32_t kb = item.k0 + q * kTileK;
+        im2col_stage(prob.A.ptr, prob.A.geo, prob.A.rows, arow, kb, item.k1, st, warp, lane);
+        if (!diag) im2col_stage(prob.B.ptr, prob.B.geo, prob.B.rows, brow, kb, item.k1, st + 2 * kPOp, warp, lane);
+        return;
+      }
       expect_tx(&ctl->raw[ps], bytes);
       load_tile(prob.A, amap, st, tq0 + q, arow, &ctl->raw[ps]);
       if (!diag) load_tile(prob.B, bmap, st + 2 * kPOp, tq0 + q, brow, &ctl->raw[ps]);
     };
-    if (t == 0) {
+    if (gather) {
+      for (int q = 0; q < kPS - 1; ++q) {
+        if (q < n_iters) load(q);
+        asm volatile("cp.async.commit_group;" ::: "memory");
+      }
+    } else if (t == 0) {
       asm volatile("fence.proxy.tensormap::generic.acquire.gpu [%0], 128;" ::"l"(reinterpret_cast<uint64_t>(amap))
                    : "memory");
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(amap)) : "memory");
@@ -298,18 +329,31 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPThreads, 1)
     for (int it = 0; it < n_iters; ++it) {
       const int s = it % kPS;
       uint8_t* stage = smem + s * kPStage;
-      mbar_wait(&ctl->raw[s], (it / kPS) & 1);
+      if (gather) {
+        asm volatile("cp.async.wait_group %0;" ::"n"(kPS - 2) : "memory");
+        asm volatile("bar.sync 2, 128;" ::: "memory");  // rows span other threads' copies
+      } else {
+        mbar_wait(&ctl->raw[s], (it / kPS) & 1);
+      }
+      PAIR_STAMP(t == 0, rank, it, 1);
       lo_plane(stage, stage + kPOp, rbase, c);
       if (!diag) lo_plane(stage + 2 * kPOp, stage + 3 * kPOp, rbase, c);
       fence_proxy_async_smem();
       asm volatile("bar.sync 2, 128;" ::: "memory");
       if (t == 0) {
+        PAIR_STAMP(true, rank, it, 2);
         arrive_leader(&ctl->full[s], leader);
-        const int nx = it + kPS - 1;  // refill the slot the MMAs of stage it-1 released
+      }
+      const int nx = it + kPS - 1;  // refill the slot the MMAs of stage it-1 released
+      if (gather) {
         if (nx < n_iters) {
           mbar_wait(&ctl->empty[nx % kPS], ((nx / kPS) & 1) ^ 1);
           load(nx);
         }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+      } else if (t == 0 && nx < n_iters) {
+        mbar_wait(&ctl->empty[nx % kPS], ((nx / kPS) & 1) ^ 1);
+        load(nx);
       }
     }
   }
@@ -542,6 +586,21 @@ int launch_syrk_pair(const GemmProblem* d_probs, const GemmWorkItem* d_items, in
   cfg.numAttrs = 1;
   cudaError_t e = cudaLaunchKernelEx(&cfg, syrk_pair_kernel, d_probs, d_items, d_partials, d_status);
   if (e != cudaSuccess) return fail(SPNGD_ERR_CUDA, "syrk_pair launch failed: %s", cudaGetErrorString(e));
+#ifdef SPNGD_GEMM_TRACE_BUILD
+  static int printed = 0;
+  if (getenv("SPNGD_GEMM_TRACE") && printed++ < 3) {
+    long long h[2][64][5];
+    cudaStreamSynchronize(stream);
+    cudaMemcpyFromSymbol(h, g_pair_trace, sizeof(h));
+    printf("pair launch %d (%d CTAs): CTA r: stage issue landed full | mma_issue drained (cycles rel. to CTA 0's first issue)\n",
+           printed - 1, n_items);
+    const long long t0 = h[0][0][0];
+    for (int q = 0; q < 24; ++q)
+      printf("  %2d  r0 %7lld %7lld %7lld | r1 %7lld %7lld %7lld | mma %7lld  drained r0 %7lld r1 %7lld\n", q,
+             h[0][q][0] - t0, h[0][q][1] - t0, h[0][q][2] - t0, h[1][q][0] - t0, h[1][q][1] - t0, h[1][q][2] - t0,
+             h[0][q][3] - t0, h[0][q][4] - t0, h[1][q][4] - t0);
+  }
+#endif
   return SPNGD_OK;
 }
 

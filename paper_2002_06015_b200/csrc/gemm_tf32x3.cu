@@ -331,7 +331,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     // tensor core truncates fp32 to tf32), each thread derives the lo plane
     // for its 8 16-byte chunks.
     const int32_t r0 = row0 + rbase;
-    const bool tma = !kAsync || op.mode != OP_ASYNC;
+    const bool tma = !kAsync || (op.mode == OP_TMA2D || op.mode == OP_TMA3D);
+    const bool im2col = kAsync && op.mode == OP_IM2COL;
     const CUtensorMap* tmap = is_b ? &probs[item.problem].B.tmap : &probs[item.problem].A.tmap;
     uint64_t* raw = ctl->raw[is_b ? 1 : 0];
     KCursor cur{};
@@ -352,7 +353,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         }
         ++tq;
       } else if constexpr (kAsync) {
-        issue_stage(op, r0, rbase, c, cur, item.k1, plane);
+        if (im2col) im2col_stage(op.ptr, op.geo, op.rows, row0, cur.k - 4 * c, item.k1, plane, warp & 3, lane);
+        else issue_stage(op, r0, rbase, c, cur, item.k1, plane);
         cursor_advance(op, cur, kTileK);
       }
     };
@@ -433,7 +435,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           TRACE_STAMP(tr && !is_b && t == 0 && it < 64, tr[it * 4 + 1]);
         } else if constexpr (kAsync) {
           cp_async_wait<kStages - 2>();
-          if (!is_b) asm volatile("bar.sync 2, 128;" ::: "memory");  // rows span other threads' copies
+          // rows span other threads' copies (A always, B when gathered by rows)
+          if (!is_b) asm volatile("bar.sync 2, 128;" ::: "memory");
+          else if (im2col) asm volatile("bar.sync 3, 128;" ::: "memory");
         }
         if (is_b) convert_b(it);
         else convert_a(it);
@@ -729,6 +733,19 @@ PFN_cuTensorMapEncodeTiled_v12000 tma_encode_fn() {
 }
 }  // namespace
 
+void make_im2col_operand(GemmOperand& op, const float* x, int c, int h, int w, int k, int stride, int pad) {
+  Im2colGeo g{};
+  g.c = c; g.h = h; g.w = w; g.k = k; g.stride = stride; g.pad = pad;
+  g.wo = (w + 2 * pad - k) / stride + 1;
+  const int ho = (h + 2 * pad - k) / stride + 1;
+  g.hw = ho * g.wo;
+  g.seg_pad = op.mode == OP_TMA3D ? op.cps * 32 : g.hw;  // the k order the operand had
+  op.geo = g;
+  op.ptr = x;
+  op.mode = OP_IM2COL;
+  op.vec = 0;
+}
+
 void finalize_operand(GemmOperand& op, int64_t K, bool allow_tma) {
   const uintptr_t addr = reinterpret_cast<uintptr_t>(op.ptr);
   op.vec = (addr % 16 == 0) && (op.seg_len % 4 == 0) && (op.row_stride % 4 == 0) && (op.seg_stride % 4 == 0);
@@ -772,7 +789,9 @@ uint32_t gemm_variant(const GemmProblem* probs, int n) {
   uint32_t v = 0;
   for (int i = 0; i < n; ++i) {
     v |= 1u << probs[i].mode;
-    if (probs[i].A.mode == OP_ASYNC || probs[i].B.mode == OP_ASYNC) v |= kVariantAsync;
+    if (probs[i].A.mode == OP_ASYNC || probs[i].B.mode == OP_ASYNC || probs[i].A.mode == OP_IM2COL ||
+        probs[i].B.mode == OP_IM2COL)
+      v |= kVariantAsync;
   }
   return v;
 }

@@ -20,6 +20,16 @@ enum OperandMode : int32_t {
   OP_ASYNC = 0,   // cp.async (LDGSTS) from any layout (fallback)
   OP_TMA2D = 1,   // TMA 2D box {32 k, 128 rows} of a K-contiguous matrix
   OP_TMA3D = 2,   // TMA 3D box {32 p, 128 rows, 1 segment}; K = nseg * cps * 32 (zero-padded chunks)
+  OP_IM2COL = 3,  // implicit im2col of a raw conv input: row (ch, ky, kx),
+                  // k = s * seg_pad + p (p < hw valid), gathered by cp.async with zero fill
+};
+
+// Geometry of an OP_IM2COL operand (the raw input x is B x c x h x w, row-major).
+struct Im2colGeo {
+  int32_t c, h, w, k, stride, pad;
+  int32_t wo, hw;      // output width, h_out * w_out
+  int32_t seg_pad;     // k-axis period per sample: the partner operand's layout (cps*32 or hw)
+  int32_t pad_;
 };
 
 struct alignas(64) GemmOperand {
@@ -33,7 +43,13 @@ struct alignas(64) GemmOperand {
   int32_t vec;        // float4 loads legal (OP_ASYNC)
   int32_t mode;       // OperandMode
   int32_t cps;        // 32-wide chunks per segment (OP_TMA3D)
+  Im2colGeo geo;      // OP_IM2COL
 };
+
+// Turns `op` (the factor operand of a conv capture: TMA3D with cps chunks per
+// sample, or K-contiguous after a repack) into an implicit-im2col operand over
+// the raw input x with the same k order, so K, tiles and partner operands stay valid.
+void make_im2col_operand(GemmOperand& op, const float* x, int c, int h, int w, int k, int stride, int pad);
 
 enum GemmEpi : int32_t {
   EPI_PARTIAL = 0,  // raw fp32 tile -> partials[slot] (split-K)

@@ -32,9 +32,9 @@ constexpr int kBaseMax = 128;
 constexpr int kLeafWarps = 8;           // warp w owns rows 4 w + t + 32 g (t, g = 0..3)
 constexpr int kBaseThreads = 32 * kLeafWarps;
 constexpr int kLd = kBaseMax + 1;       // padded smem row (floats)
-// staging [128][129] | published rows R [2][4][64] float2 | -L columns [2][128] float4
-constexpr size_t kBaseSmem = size_t(kBaseMax) * kLd * sizeof(float) + 2 * 4 * 64 * sizeof(float2) +
-                             2 * kBaseMax * sizeof(float4);
+// staging [128][129] | published rows R [3][4][64] float2 | -L columns [3][128] float4
+constexpr size_t kBaseSmem = size_t(kBaseMax) * kLd * sizeof(float) + 3 * 4 * 64 * sizeof(float2) +
+                             3 * kBaseMax * sizeof(float4);
 
 __device__ __forceinline__ float pivot_rsqrt(float p, bool& bad) {
   if (!(p > 0.f) || !isfinite(p)) {
@@ -74,8 +74,8 @@ __device__ long long g_leaf_trace[8];
 #endif
 
 struct LeafBufs {
-  float2* R;   // [2][4][64]: published rows by column pair
-  float4* L;   // [2][128]:  (-L_i,4b .. -L_i,4b+3) by row i
+  float2* R;   // [3][4][64]: published rows by column pair
+  float4* L;   // [3][128]:  (-L_i,4b .. -L_i,4b+3) by row i
 };
 
 // Apply block b (column pair group P = b >> 4, pairs 2b, 2b+1 in lanes lk0,
@@ -185,8 +185,11 @@ __device__ __forceinline__ void leaf_blocks(float2 (&x)[4][4][2], int nb, int wa
   for (int wp = 0; wp < kLeafWarps; ++wp) {
     const int b = kLeafWarps * G + wp;
     if (b >= nb) return;
-    const float2* Rb = buf.R + (b & 1) * 256;
-    const float4* Lb = buf.L + (b & 1) * kBaseMax;
+    // published rows rotate over three buffers: the producer of block b + 1
+    // arrives as soon as it has published and may still be applying block b
+    // while the producer of b + 2 writes the next buffer
+    const float2* Rb = buf.R + (b % 3) * 256;
+    const float4* Lb = buf.L + (b % 3) * kBaseMax;
     float2 r[4][2];
 #pragma unroll
     for (int t = 0; t < 4; ++t)
@@ -195,8 +198,8 @@ __device__ __forceinline__ void leaf_blocks(float2 (&x)[4][4][2], int nb, int wa
     const float m = ((lane >> 1) == (b & 15)) ? 0.f : 1.f;  // zero the block's own columns first
     const int b1 = b + 1;
     const bool producer = b1 < nb && warp == (b1 & (kLeafWarps - 1));
-    float2* Rn = buf.R + (b1 & 1) * 256;
-    float4* Ln = buf.L + (b1 & 1) * kBaseMax;
+    float2* Rn = buf.R + (b1 % 3) * 256;
+    float4* Ln = buf.L + (b1 % 3) * kBaseMax;
     if (producer) {
       if (wp < kLeafWarps - 1) {
         leaf_apply<G, P>(x, r, Lb, 4 * warp + 32 * G, m);
@@ -205,11 +208,13 @@ __device__ __forceinline__ void leaf_blocks(float2 (&x)[4][4][2], int nb, int wa
         leaf_apply<G + 1, P>(x, r, Lb, 4 * warp + 32 * (G + 1), m);
         leaf_publish<G + 1>(x, b1, lane, Rn, Ln, bad);
       }
+      // block b1 is published: release the other warps before finishing this
+      // warp's remaining rows (the critical path is publish -> barrier -> publish)
+      asm volatile("bar.arrive %0, %1;" ::"r"(1 + (b1 & 1)), "r"(kBaseThreads) : "memory");
     }
     if ((warp > wp) && !(producer && wp < kLeafWarps - 1)) leaf_apply<G, P>(x, r, Lb, 4 * warp + 32 * G, m);
     if constexpr (G < 3) leaf_apply_rest<G + 1, P>(x, r, Lb, 4 * warp, m, !(producer && wp == kLeafWarps - 1));
-    if (producer) asm volatile("bar.arrive %0, %1;" ::"r"(1 + (b1 & 1)), "r"(kBaseThreads) : "memory");
-    else asm volatile("bar.sync %0, %1;" ::"r"(1 + (b1 & 1)), "r"(kBaseThreads) : "memory");
+    if (!producer) asm volatile("bar.sync %0, %1;" ::"r"(1 + (b1 & 1)), "r"(kBaseThreads) : "memory");
   }
   if constexpr (G < 3) leaf_blocks<G + 1>(x, nb, warp, lane, buf, bad);
 }
@@ -220,7 +225,7 @@ __global__ void __launch_bounds__(kBaseThreads, 1) base_chol_inv_kernel(const Ba
   float* S = reinterpret_cast<float*>(base_smem);  // [128][129] staging (M in, T out)
   LeafBufs buf;
   buf.R = reinterpret_cast<float2*>(S + kBaseMax * kLd);
-  buf.L = reinterpret_cast<float4*>(buf.R + 2 * 4 * 64);
+  buf.L = reinterpret_cast<float4*>(buf.R + 3 * 4 * 64);
   const BaseTask t = tasks[blockIdx.x];
   const int n = t.n;
   // PDL: the task table is static; the matrix comes from the previous kernel.

@@ -1706,6 +1706,10 @@ int spngd_opt_enable_raw_inputs(spngd_opt* o, const spngd_conv_geom* geoms) {
   if (o->graphs_ready || o->graphs_ready_ov || o->timed)
     return fail(SPNGD_ERR_INVALID, "spngd_opt_enable_raw_inputs: call before the first step");
   const int64_t B = o->cfg.batch;
+  // Implicit im2col: the A-factor SYRK (and the wgrad GEMM)
+  // gather the (ch, ky, kx) x (s, oy, ox) operand straight from the raw input;
+  // the capture is never materialized and its buffer is released.
+  bool changed = false;
   for (size_t li = 0; li < o->layers.size(); ++li) {
     LayerState& L = o->layers[li];
     if (L.d.kind != SPNGD_CONV) continue;
@@ -1720,12 +1724,42 @@ int spngd_opt_enable_raw_inputs(spngd_opt* o, const spngd_conv_geom* geoms) {
     L.raw_floats = B * g.c_in * g.h * g.w;
     L.raw = o->alloc(size_t(L.raw_floats));
     if (!L.raw) return fail(SPNGD_ERR_CUDA, "opt: raw input allocation failed");
-    o->i2c.push_back({L.raw, L.act, B, g});
-    if (o->overlap_ok) o->waves[wave_of(L.d)].i2c.push_back(o->i2c.back());
+    if (L.fa < 0) return fail(SPNGD_ERR_INVALID, "opt: conv layer %zu has no factor problem", li);
+    float* act = L.act;
+    GemmProblem& p = o->fplan.probs[size_t(L.fa)];
+    const float* old_op = p.A.ptr;  // the capture, or its K-contiguous repack
+    make_im2col_operand(p.A, L.raw, int(g.c_in), int(g.h), int(g.w), int(g.k), int(g.stride), int(g.pad));
+    p.B = p.A;
+    // the capture's repack (hw % 4 != 0) has nothing left to do
+    for (auto& t : o->fplan.repacks)
+      if (t.src == act) t.n = 0;
+    for (auto& wv : o->waves)
+      for (auto& t : wv.repacks)
+        if (t.src == act) t.n = 0;
+    for (auto& wp : o->wprobs)  // wgrad reads the same operand
+      if (wp.B.ptr == old_op) wp.B = p.A;
+    for (size_t q = 0; q < o->owned.size(); ++q)
+      if (o->owned[q] == act) {
+        cudaFree(act);
+        o->owned.erase(o->owned.begin() + long(q));
+        break;
+      }
+    L.act = nullptr;
+    changed = true;
   }
-  for (auto& wv : o->waves) wv.d_i2c = dev_upload(wv.i2c, o->owned);
-  o->d_i2c = dev_upload(o->i2c, o->owned);
-  if (!o->i2c.empty() && !o->d_i2c) return fail(SPNGD_ERR_CUDA, "opt: upload failed");
+  if (changed) {
+    auto put = [&](void* d, const void* h, size_t bytes) {
+      return (bytes && d) ? cudaMemcpy(d, h, bytes, cudaMemcpyHostToDevice) : cudaSuccess;
+    };
+    SPNGD_CUDA_TRY(put(o->d_fprobs, o->fplan.probs.data(), o->fplan.probs.size() * sizeof(GemmProblem)));
+    SPNGD_CUDA_TRY(put(o->d_repack, o->fplan.repacks.data(), o->fplan.repacks.size() * sizeof(RepackTask)));
+    for (auto& wv : o->waves)
+      SPNGD_CUDA_TRY(put(wv.d_repacks, wv.repacks.data(), wv.repacks.size() * sizeof(RepackTask)));
+    if (!o->wprobs.empty()) {
+      SPNGD_CUDA_TRY(put(o->d_wprobs, o->wprobs.data(), o->wprobs.size() * sizeof(GemmProblem)));
+      o->wvariant = gemm_variant(o->wprobs.data(), int(o->wprobs.size()));
+    }
+  }
   o->raw_inputs = true;
   return SPNGD_OK;
 }
