@@ -309,7 +309,28 @@ def run_ours(args):
         e2e_raw = {"value": round(v, 3), "unit": UNIT, "h2d_bytes_per_step": h2d_r, "d2h_bytes_per_step": ob_r,
                    "inputs": "raw conv layer inputs (B x c_in x h x w) expanded on the device by im2col "
                              "(spngd_opt_enable_raw_inputs); 1x1 stride-1 inputs are the captures themselves"}
+
+        def device_ms(o, step0, n=5):
+            ev4 = (C.c_void_p * 2)()
+            check(L.spngd_event_time(o.ctx, ev4, 0, C.byref(ms)))
+            for s in range(n):
+                o.step(step0 + s)
+            check(L.spngd_event_time(o.ctx, ev4, 1, C.byref(ms)))
+            return ms.value / n
+
+        e2e_raw["device_ms_explicit_im2col"] = round(device_ms(opt_r, args.warmup + args.e2e_steps + 1), 3)
         opt_r.close()
+        # the same step with implicit im2col (no capture; the
+        # GEMMs gather from the raw inputs), device time with resident inputs
+        opt_i = Optimizer(layers, batch, lam=args.lam, device=local, world=world, rank=rank, nccl_id=new_nccl_id())
+        opt_i.enable_raw_inputs(implicit=True)
+        if p2p:
+            opt_i.attach_peers(pg)
+        opt_i.synth(seed=42)
+        for s in range(args.warmup):
+            opt_i.step(s + 1)
+        e2e_raw["device_ms_implicit_im2col"] = round(device_ms(opt_i, args.warmup + 1), 3)
+        opt_i.close()
 
     # ---- phase-serial pass (single GPU): the factor SYRK launch alone, for
     # the roofline (in the overlapped schedule it shares the GPU with the

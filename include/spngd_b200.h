@@ -512,6 +512,10 @@ typedef struct spngd_conv_geom {
  * only.  Call before the first step. */
 int spngd_opt_enable_bn_inputs(spngd_opt* opt, const int64_t* spatial);
 int spngd_opt_enable_raw_inputs(spngd_opt* opt, const spngd_conv_geom* geoms);
+/* implicit = 1: no capture is formed -- the A-factor SYRK and the wgrad GEMM
+ * gather the im2col operand from the raw input (cp.async,
+ * LSU-bound, so slower than expanding first); implicit = 0 is the call above. */
+int spngd_opt_enable_raw_inputs_ex(spngd_opt* opt, const spngd_conv_geom* geoms, int implicit);
 /* Batched im2col alone (net.cpp:199-219) for `n` conv inputs, x: batch x
  * c_in x h x w, out: batch x (c_in k k) x (h_out w_out), device pointers. */
 typedef struct spngd_im2col_req {

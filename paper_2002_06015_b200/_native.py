@@ -124,7 +124,7 @@ EXPORTS = [
     "spngd_nccl_unique_id", "spngd_ctx_init_comm", "spngd_reduce_scatter_mean", "spngd_all_gather",
     "spngd_plan_layout", "spngd_opt_create", "spngd_opt_destroy", "spngd_opt_buffer", "spngd_opt_owner", "spngd_opt_step",
     "spngd_opt_phase_ms", "spngd_opt_launch_count", "spngd_opt_stale_info", "spngd_opt_set_overlap", "spngd_opt_sync",
-    "spngd_opt_enable_bn_inputs", "spngd_bn_backward_stats_batched",
+    "spngd_opt_enable_bn_inputs", "spngd_bn_backward_stats_batched", "spngd_opt_enable_raw_inputs_ex",
 ]
 
 
@@ -199,6 +199,7 @@ def _declare(L):
         "spngd_opt_set_overlap": (C.c_int, [P, C.c_int]),
         "spngd_opt_sync": (C.c_int, [P]),
         "spngd_opt_enable_bn_inputs": (C.c_int, [P, C.POINTER(C.c_int64)]),
+        "spngd_opt_enable_raw_inputs_ex": (C.c_int, [P, C.POINTER(ConvGeom), C.c_int]),
         "spngd_bn_backward_stats_batched": (C.c_int, [P, C.c_int, C.POINTER(BnBackwardReq)]),
         "spngd_opt_launch_count": (_i64, [P]),
         "spngd_opt_stale_info": (C.c_int, [P, C.c_int, C.c_int, C.POINTER(_i64), C.POINTER(_i64), C.POINTER(_i64),

@@ -16,10 +16,12 @@
 // single-CTA engine, so the RZ accumulation bias stays bounded by one stage.
 // Diagonal super-tiles (A rows == B rows in each CTA) load one tile per stage.
 //
-// Roles (384 threads per CTA, up to 168 registers each): warps 0-3 producers
-// (TMA of the A tile and the B half, both lo planes), warps 4-11 drain (128
-// fp32 accumulators per thread: lane quarter warp % 4, column half
-// (warp - 4) / 4); warp 4 of the leader (cluster rank 0) issues the MMAs.
+// Roles (512 threads per CTA, registers rebalanced with setmaxnreg): warps
+// 0-3 producers (TMA of the A tile and the B half, both lo planes), warp 4 of
+// the leader (cluster rank 0) issues the MMAs and does nothing else (a warp
+// that also drains blocks on the tensor core's issue queue and delays the
+// drains the next MMAs wait for), warps 8-15 drain (184 registers: 128 fp32
+// accumulators per thread, lane quarter warp % 4, column half (warp - 8) / 4).
 // Pair synchronisation: the producers of both CTAs arrive on the leader's
 // `full` barrier (remote mbarrier arrive); the leader's commits are multicast
 // to both CTAs' `empty` and `tmem_full`; drain warps of both CTAs arrive on
@@ -41,7 +43,7 @@ constexpr int kPS = 3;                          // stages
 constexpr int kPOp = kTileM * kTileK * 4;       // 16 KB: one 128 x 32 fp32 plane
 constexpr int kPStage = 4 * kPOp;               // A raw | A lo | B raw | B lo
 constexpr int kPEpi = 2 * kTileN + 4;           // epilogue tile row stride (floats)
-constexpr int kPThreads = 384;
+constexpr int kPThreads = 512;
 
 struct __align__(64) PairCtl {
   uint64_t raw[kPS];         // TMA arrival of this CTA's A tile (+ B half)
@@ -218,18 +220,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPThreads, 1)
   const int n_iters = (item.k1 - item.k0 + kTileK - 1) / kTileK;
   float* T = reinterpret_cast<float*>(smem);
 
-  if (warp >= 4) {
-    // ---------------------------------------- MMA issue (leader warp 4) + drain (4-11)
+  if (warp >= 8) {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 184;" ::: "memory");
+    // ---------------------------------------- drain (warps 8-15)
     const uint32_t lane_base = uint32_t((warp & 3) * 32) << 16;
-    const uint32_t col_base = ((warp - 4) >> 2) * 128;
+    const uint32_t col_base = ((warp - 8) >> 2) * 128;
     float acc[128];
 #pragma unroll
     for (int j = 0; j < 128; ++j) acc[j] = 0.f;
-    auto drain = [&](int j) {
+    for (int j = 0; j < n_iters; ++j) {
       const int b = j & 1;
       mbar_wait(&ctl->tmem_full[b], (j >> 1) & 1);
       tc_fence_after();
-      PAIR_STAMP(warp == 4 && lane == 0, rank, j, 4);
+      PAIR_STAMP(warp == 8 && lane == 0, rank, j, 4);
 #pragma unroll
       for (int h = 0; h < 4; ++h) {
         uint32_t v[32];
@@ -241,41 +244,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPThreads, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) arrive_leader(&ctl->tmem_empty[b], leader);
-    };
-    constexpr uint32_t idesc = umma_idesc_tf32(2 * kTileM, 2 * kTileN);  // M = 256 across the pair, N = 256
-    auto issue_mma = [&](int it) {
-      const int s = it % kPS, b = it & 1;
-      mbar_wait_cluster(&ctl->full[s], (it / kPS) & 1);
-      if (it >= 2) mbar_wait_cluster(&ctl->tmem_empty[b], ((it >> 1) + 1) & 1);
-      tc_fence_after();
-      PAIR_STAMP(lane == 0, 0, it, 3);
-      if (lane == 0) {
-        const uint32_t base = smem_u32(smem + s * kPStage);
-        const uint32_t a_hi = base, a_lo = base + kPOp;
-        const uint32_t b_hi = diag ? a_hi : base + 2 * kPOp, b_lo = diag ? a_lo : base + 3 * kPOp;
-        const uint32_t dt = tmem + b * 256;
-#pragma unroll
-        for (int kk = 0; kk < kTileK / 8; ++kk) {
-          const uint32_t koff = kk * 32;  // 8 tf32 = 32 bytes along the swizzled row
-          const uint64_t dah = umma_desc_k_sw128(a_hi + koff), dal = umma_desc_k_sw128(a_lo + koff);
-          const uint64_t dbh = umma_desc_k_sw128(b_hi + koff), dbl = umma_desc_k_sw128(b_lo + koff);
-          umma_pair_ss(dt, dal, dbh, idesc, kk > 0 ? 1u : 0u);
-          umma_pair_ss(dt, dah, dbl, idesc, 1u);
-          umma_pair_ss(dt, dah, dbh, idesc, 1u);
-        }
-        commit_pair(&ctl->empty[s]);
-        commit_pair(&ctl->tmem_full[b]);
-      }
-      __syncwarp();
-    };
-    if (warp == 4 && leader) {
-      for (int it = 0; it < n_iters; ++it) {
-        issue_mma(it);
-        if (it >= 1) drain(it - 1);
-      }
-      if (n_iters >= 1) drain(n_iters - 1);
-    } else {
-      for (int j = 0; j < n_iters; ++j) drain(j);
     }
     // every MMA of this CTA's accumulator has completed: the stage ring is free
     asm volatile("bar.sync 1, 256;" ::: "memory");
@@ -283,7 +251,41 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPThreads, 1)
     float4* trow = reinterpret_cast<float4*>(T + r * kPEpi + col_base);
 #pragma unroll
     for (int j = 0; j < 32; ++j) trow[j] = make_float4(acc[4 * j], acc[4 * j + 1], acc[4 * j + 2], acc[4 * j + 3]);
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 128;" ::: "memory");  // uniform again for the epilogue
+  } else if (warp >= 4) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 56;" ::: "memory");
+    // ---------------------------------------- MMA issue (leader warp 4 only)
+    if (warp == 4 && leader) {
+      constexpr uint32_t idesc = umma_idesc_tf32(2 * kTileM, 2 * kTileN);  // M = 256 across the pair, N = 256
+      for (int it = 0; it < n_iters; ++it) {
+        const int s = it % kPS, b = it & 1;
+        mbar_wait_cluster(&ctl->full[s], (it / kPS) & 1);
+        if (it >= 2) mbar_wait_cluster(&ctl->tmem_empty[b], ((it >> 1) + 1) & 1);
+        tc_fence_after();
+        PAIR_STAMP(lane == 0, 0, it, 3);
+        if (lane == 0) {
+          const uint32_t base = smem_u32(smem + s * kPStage);
+          const uint32_t a_hi = base, a_lo = base + kPOp;
+          const uint32_t b_hi = diag ? a_hi : base + 2 * kPOp, b_lo = diag ? a_lo : base + 3 * kPOp;
+          const uint32_t dt = tmem + b * 256;
+#pragma unroll
+          for (int kk = 0; kk < kTileK / 8; ++kk) {
+            const uint32_t koff = kk * 32;  // 8 tf32 = 32 bytes along the swizzled row
+            const uint64_t dah = umma_desc_k_sw128(a_hi + koff), dal = umma_desc_k_sw128(a_lo + koff);
+            const uint64_t dbh = umma_desc_k_sw128(b_hi + koff), dbl = umma_desc_k_sw128(b_lo + koff);
+            umma_pair_ss(dt, dal, dbh, idesc, kk > 0 ? 1u : 0u);
+            umma_pair_ss(dt, dah, dbl, idesc, 1u);
+            umma_pair_ss(dt, dah, dbh, idesc, 1u);
+          }
+          commit_pair(&ctl->empty[s]);
+          commit_pair(&ctl->tmem_full[b]);
+        }
+        __syncwarp();
+      }
+    }
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 128;" ::: "memory");
   } else {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 80;" ::: "memory");
     // ------------------------------------------------------------ producers (warps 0-3)
     const int t = threadIdx.x;
     const int c = t & 7, rbase = t >> 3;
@@ -356,6 +358,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPThreads, 1)
         load(nx);
       }
     }
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 128;" ::: "memory");
   }
   tc_fence_before();
   __syncthreads();

@@ -1701,14 +1701,21 @@ int spngd_opt_enable_bn_inputs(spngd_opt* o, const int64_t* spatial) {
 }
 
 int spngd_opt_enable_raw_inputs(spngd_opt* o, const spngd_conv_geom* geoms) {
+  return spngd_opt_enable_raw_inputs_ex(o, geoms, 0);
+}
+
+int spngd_opt_enable_raw_inputs_ex(spngd_opt* o, const spngd_conv_geom* geoms, int implicit) {
   if (!o || !geoms) return fail(SPNGD_ERR_INVALID, "spngd_opt_enable_raw_inputs: null argument");
   if (o->raw_inputs) return fail(SPNGD_ERR_INVALID, "spngd_opt_enable_raw_inputs: already enabled");
   if (o->graphs_ready || o->graphs_ready_ov || o->timed)
     return fail(SPNGD_ERR_INVALID, "spngd_opt_enable_raw_inputs: call before the first step");
   const int64_t B = o->cfg.batch;
-  // Implicit im2col: the A-factor SYRK (and the wgrad GEMM)
-  // gather the (ch, ky, kx) x (s, oy, ox) operand straight from the raw input;
-  // the capture is never materialized and its buffer is released.
+  // implicit = 0: im2col_kernel expands the raw input into the capture before
+  // the SYRK (TMA-fed).  implicit = 1: the A-factor SYRK
+  // (and the wgrad GEMM) gather the (ch, ky, kx) x (s, oy, ox) operand straight
+  // from the raw input; the capture is never materialized and its buffer is
+  // released.  The gather is LSU-bound (one 4-byte cp.async per element), so
+  // the explicit expansion is the default.
   bool changed = false;
   for (size_t li = 0; li < o->layers.size(); ++li) {
     LayerState& L = o->layers[li];
@@ -1724,6 +1731,11 @@ int spngd_opt_enable_raw_inputs(spngd_opt* o, const spngd_conv_geom* geoms) {
     L.raw_floats = B * g.c_in * g.h * g.w;
     L.raw = o->alloc(size_t(L.raw_floats));
     if (!L.raw) return fail(SPNGD_ERR_CUDA, "opt: raw input allocation failed");
+    if (!implicit) {
+      o->i2c.push_back({L.raw, L.act, B, g});
+      if (o->overlap_ok) o->waves[wave_of(L.d)].i2c.push_back(o->i2c.back());
+      continue;
+    }
     if (L.fa < 0) return fail(SPNGD_ERR_INVALID, "opt: conv layer %zu has no factor problem", li);
     float* act = L.act;
     GemmProblem& p = o->fplan.probs[size_t(L.fa)];
@@ -1759,6 +1771,11 @@ int spngd_opt_enable_raw_inputs(spngd_opt* o, const spngd_conv_geom* geoms) {
       SPNGD_CUDA_TRY(put(o->d_wprobs, o->wprobs.data(), o->wprobs.size() * sizeof(GemmProblem)));
       o->wvariant = gemm_variant(o->wprobs.data(), int(o->wprobs.size()));
     }
+  }
+  if (!o->i2c.empty()) {
+    for (auto& wv : o->waves) wv.d_i2c = dev_upload(wv.i2c, o->owned);
+    o->d_i2c = dev_upload(o->i2c, o->owned);
+    if (!o->d_i2c) return fail(SPNGD_ERR_CUDA, "opt: upload failed");
   }
   o->raw_inputs = true;
   return SPNGD_OK;

@@ -265,15 +265,17 @@ class Optimizer:
         check(N.lib().spngd_opt_enable_bn_inputs(self.h, arr))
         self.bn_spatial = list(spatial)
 
-    def enable_raw_inputs(self):
+    def enable_raw_inputs(self, implicit: bool = False):
         """The step takes each conv layer's raw input (RAW_ACT, B x c_in x h x w)
-        and forms the im2col capture on the device (spngd_opt_enable_raw_inputs,
-        net.cpp:199-219).  Call before the first step."""
+        and forms the im2col capture on the device (net.cpp:199-219), or with
+        implicit=True never forms it: the factor / wgrad GEMMs gather the
+        operand from the raw input (spngd_opt_enable_raw_inputs_ex).  Call
+        before the first step."""
         g = (N.ConvGeom * len(self.layers))()
         for i, l in enumerate(self.layers):
             if l.kind == "conv":
                 g[i] = N.ConvGeom(l.c_in, l.h_in, l.w_in, l.k, l.stride, l.pad)
-        check(N.lib().spngd_opt_enable_raw_inputs(self.h, g))
+        check(N.lib().spngd_opt_enable_raw_inputs_ex(self.h, g, int(implicit)))
         self.raw_inputs = True
 
     def input_buffers(self):

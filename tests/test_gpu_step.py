@@ -278,21 +278,23 @@ def test_wgrad_in_step(cuda_dev, fisher_mode):
         opt.close()
 
 
-@pytest.mark.parametrize("wgrad", [False, True])
-def test_raw_inputs_step(cuda_dev, wgrad):
-    """spngd_opt_enable_raw_inputs: the step takes each conv
-    layer's raw input and the A-factor SYRK (and the in-step wgrad GEMM) gather
-    the im2col operand straight from it (net.cpp:199-219: padding, stride 2,
-    7x7, 1x1 stride 2; 1x1 stride 1 aliases the capture) -- the capture is
-    never materialized.  A factor, gradient payload and the updated weights
-    vs the oracle on the oracle's im2col of the same raw tensor."""
+@pytest.mark.parametrize("implicit,wgrad", [(False, False), (True, False), (True, True)])
+def test_raw_inputs_step(cuda_dev, implicit, wgrad):
+    """spngd_opt_enable_raw_inputs(_ex): the step takes each
+    conv layer's raw input (net.cpp:199-219: padding, stride 2, 7x7, 1x1
+    stride 2; 1x1 stride 1 aliases the capture) and either expands it on the
+    device (the capture must equal the oracle's im2col bit for bit) or, with
+    implicit=True, the A-factor SYRK (and the in-step wgrad GEMM) gather the
+    im2col operand straight from it and no capture exists.  A factor,
+    gradient payload and the updated weights vs the oracle on the oracle's
+    im2col of the same raw tensor."""
     from paper_2002_06015_b200.step import A_PACKED, RAW_ACT
     layers = [W.conv(3, 8, 7, 2, 20), W.bn(8, 100), W.conv(8, 16, 3, 1, 10), W.conv(16, 32, 1, 1, 10),
               W.conv(32, 16, 1, 2, 10), W.fc(16 * 25, 10), W.conv(128, 64, 3, 1, 8)]  # a = 1152: 2-CTA SYRK
     B = 6
     opt = Optimizer(layers, B, lam=LAM, wgrad=wgrad)
     try:
-        opt.enable_raw_inputs()
+        opt.enable_raw_inputs(implicit=implicit)
         opt.synth(seed=31)
         raws = {li: opt.download(li, RAW_ACT).numpy() for li, l in enumerate(layers) if l.kind == "conv"}
         before = {li: {w: opt.download(li, w).numpy() for w in (GRAD, DW, WB, V)} for li in raws}
@@ -302,6 +304,9 @@ def test_raw_inputs_step(cuda_dev, wgrad):
             l = layers[li]
             cap = np.concatenate([O.im2col(x.reshape(B, l.c_in * l.h_in * l.w_in)[s], l.c_in, l.h_in, l.w_in, l.k,
                                            l.stride, l.pad) for s in range(B)])
+            if not implicit:
+                got = opt.download(li, ACT).numpy().reshape(B * l.a, l.hw)
+                assert np.array_equal(got, cap.astype(np.float32)), li
             A = O.factor_A(cap, True, l.a, l.hw, 0, B)
             assert rel(opt.download(li, A_PACKED).numpy(), A) <= 1e-5, li
             b = dict(before[li])
@@ -315,10 +320,11 @@ def test_raw_inputs_step(cuda_dev, wgrad):
             wo, vo = oracle_layer(l, B, b)
             assert rel(opt.download(li, WB).numpy(), wo) <= 1e-4, li
             assert rel(opt.download(li, V).numpy(), vo) <= 1e-4, li
-        # 1x1 stride-1 convs alias the capture; every other conv's capture is gone
+        # 1x1 stride-1 convs alias the capture; with implicit im2col every other
+        # conv's capture is gone
         assert opt.ptr(3, RAW_ACT)[0] == opt.ptr(3, ACT)[0]
         for li in (0, 2, 4, 6):
-            assert opt.ptr(li, ACT)[0] is None, li
+            assert (opt.ptr(li, ACT)[0] is None) == implicit, li
     finally:
         opt.close()
 
