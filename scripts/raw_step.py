@@ -1,4 +1,6 @@
-"""Two ResNet-50 B=32 steps with raw conv inputs (device im2col), for ncu."""
+"""One phase-serial ResNet-50 B=32 step with raw conv inputs, for ncu:
+--implicit gathers the im2col operand inside the GEMMs (no capture),
+otherwise im2col_kernel expands it first."""
 import os
 import sys
 
@@ -7,10 +9,10 @@ from paper_2002_06015_b200 import workloads as W  # noqa: E402
 from paper_2002_06015_b200.step import Optimizer  # noqa: E402
 
 opt = Optimizer(W.resnet50(), 32)
-opt.enable_raw_inputs()
+opt.set_overlap(False)
+opt.enable_raw_inputs(implicit="--implicit" in sys.argv)
 opt.synth(42)
-for s in (1, 2):
-    opt.step(s)
+opt.step(1)
 opt.sync()
+print(opt.phase_ms())
 opt.close()
-print("ok")
