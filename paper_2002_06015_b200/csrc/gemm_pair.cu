@@ -398,11 +398,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPThreads, 1)
         if (jj < n && i <= jj) C[rb + jj] = alpha * vv[q];
       }
     }
-  } else if (prob.mode == EPI_DENSE) {  // C = alpha acc + beta Cin, row-major (no mirror / transposed copy)
+  } else if (prob.mode == EPI_DENSE) {
+    // C = alpha acc + beta Cin row-major; FLAG_SYM_MIRROR writes i <= j and
+    // mirrors to (j, i); FLAG_TRANS also writes CT[j][i] (the inverse recursion)
     float* C = prob.C;
     const float* Cin = prob.Cin;
     const float alpha = prob.alpha, beta = prob.beta;
     const int64_t M = prob.M, N = prob.N, ldc = prob.ldc;
+    const bool mirror = (prob.flags & FLAG_SYM_MIRROR) != 0, trans = (prob.flags & FLAG_TRANS) != 0;
     const bool has_cin = beta != 0.f;
     const bool vec = ((reinterpret_cast<uintptr_t>(C) | (has_cin ? reinterpret_cast<uintptr_t>(Cin) : 0)) & 15) == 0 &&
                      (ldc & 3) == 0;
@@ -410,18 +413,56 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPThreads, 1)
       const int r = p >> 6, cc = (p & 63) * 4;
       const int64_t i = m0 + r, j = n0 + cc;
       if (i >= M || j >= N) continue;
-      float4 v = *reinterpret_cast<const float4*>(T + r * kPEpi + cc);
+      float4* tp = reinterpret_cast<float4*>(T + r * kPEpi + cc);
+      float4 v = *tp;
+      float4 ci = make_float4(0.f, 0.f, 0.f, 0.f);  // Cin first: C and Cin may alias
+      if (has_cin) {
+        if (vec && j + 3 < N) {
+          ci = *reinterpret_cast<const float4*>(Cin + i * ldc + j);
+        } else {
+          const float* src = Cin + i * ldc + j;
+          ci.x = src[0];
+          if (j + 1 < N) ci.y = src[1];
+          if (j + 2 < N) ci.z = src[2];
+          if (j + 3 < N) ci.w = src[3];
+        }
+      }
+      v = make_float4(alpha * v.x + beta * ci.x, alpha * v.y + beta * ci.y, alpha * v.z + beta * ci.z,
+                      alpha * v.w + beta * ci.w);
+      *tp = v;
       float* dst = C + i * ldc + j;
-      if (vec && j + 3 < N) {
-        float4 ci = has_cin ? *reinterpret_cast<const float4*>(Cin + i * ldc + j) : make_float4(0.f, 0.f, 0.f, 0.f);
-        v = make_float4(alpha * v.x + beta * ci.x, alpha * v.y + beta * ci.y, alpha * v.z + beta * ci.z,
-                        alpha * v.w + beta * ci.w);
+      if (vec && j + 3 < N && (!mirror || i <= j)) {
         *reinterpret_cast<float4*>(dst) = v;
       } else {
         const float vv[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
         for (int q = 0; q < 4; ++q)
-          if (j + q < N) dst[q] = alpha * vv[q] + (has_cin ? beta * Cin[i * ldc + j + q] : 0.f);
+          if (j + q < N && (!mirror || i <= j + q)) dst[q] = vv[q];
+      }
+    }
+    if (mirror || trans) {
+      __syncthreads();
+      float* dstT = mirror ? C : prob.CT;
+      const int64_t ldt = mirror ? ldc : prob.ldct;
+      const bool vt = (reinterpret_cast<uintptr_t>(dstT) & 15) == 0 && (ldt & 3) == 0;
+      for (int p = tid; p < 8192; p += kPThreads) {
+        // 16 columns x 2 row quads per warp: conflict-free column reads of T
+        const int wk = p >> 5, ln = p & 31;
+        const int c = (wk & 15) * 16 + (ln & 15);
+        const int r = ((wk >> 4) * 2 + (ln >> 4)) * 4;
+        const int64_t i = m0 + r, j = n0 + c;  // writes dstT[j][i .. i+3]
+        if (j >= N || i >= M) continue;
+        const float4 v = make_float4(T[r * kPEpi + c], T[(r + 1) * kPEpi + c], T[(r + 2) * kPEpi + c],
+                                     T[(r + 3) * kPEpi + c]);
+        float* dst = dstT + j * ldt + i;
+        if (vt && i + 3 < M && (!mirror || i + 3 < j)) {
+          *reinterpret_cast<float4*>(dst) = v;
+        } else {
+          const float vv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            if (i + q < M && (!mirror || i + q < j)) dst[q] = vv[q];
+        }
       }
     }
   } else if (prob.mode == EPI_UPDATE) {
@@ -540,20 +581,22 @@ int plan_pair_tiles(int problem_index, const GemmProblem& p, int kchunk, std::ve
   return used;
 }
 
-bool pair_eligible_dense(const GemmProblem& p) {
+bool pair_eligible_dense(const GemmProblem& p, bool upper_only) {
   static const bool off = getenv("SPNGD_NO_PAIR") != nullptr;
-  if (off || (p.flags & (FLAG_SYM_MIRROR | FLAG_TRANS)) || (p.mode != EPI_DENSE && p.mode != EPI_UPDATE)) return false;
+  if (off || (p.mode != EPI_DENSE && p.mode != EPI_UPDATE)) return false;
   if ((p.A.mode != OP_TMA2D && p.A.mode != OP_TMA3D) || (p.B.mode != OP_TMA2D && p.B.mode != OP_TMA3D)) return false;
   if (p.M < 256 || p.N < 256) return false;
   const int64_t tm = (p.M + kTileM - 1) / kTileM, tn = (p.N + kTileN - 1) / kTileN;
   const int64_t sm = (p.M + 2 * kTileM - 1) / (2 * kTileM), sn = (p.N + 2 * kTileN - 1) / (2 * kTileN);
-  return double(4 * sm * sn) <= 1.2 * double(tm * tn);
+  if (upper_only)  // square, upper super-tiles (symmetric results)
+    return double(2 * sm * (sm + 1)) <= 1.35 * double(tm * (tm + 1) / 2);
+  return double(4 * sm * sn) <= 1.25 * double(tm * tn);
 }
 
-int plan_pair_dense(int problem_index, const GemmProblem& p, std::vector<GemmWorkItem>& items) {
+int plan_pair_dense(int problem_index, const GemmProblem& p, std::vector<GemmWorkItem>& items, bool upper_only) {
   const int sm = (p.M + 2 * kTileM - 1) / (2 * kTileM), sn = (p.N + 2 * kTileN - 1) / (2 * kTileN);
   for (int I = 0; I < sm; ++I)
-    for (int J = 0; J < sn; ++J) {
+    for (int J = upper_only ? I : 0; J < sn; ++J) {
       int k0 = 0, k1 = p.K;  // triangular operands: the band of the whole 256 x 256 tile
       if (p.ktri & KTRI_A_LOWER) k1 = std::min(k1, (2 * I + 2) * kTileM);
       if (p.ktri & KTRI_A_UPPER) k0 = std::max(k0, 2 * I * kTileM);
@@ -563,6 +606,12 @@ int plan_pair_dense(int problem_index, const GemmProblem& p, std::vector<GemmWor
       for (int r = 0; r < 2; ++r) items.push_back({problem_index, 2 * I + r, 2 * J, k0, k1, -1});
     }
   return 0;
+}
+
+bool pair_group_wins(int64_t pair_ctas, int64_t single_ctas, int64_t rest_ctas) {
+  if (pair_ctas <= 0) return false;
+  auto waves = [](int64_t c) { return double((c + kNumSMs - 1) / kNumSMs); };
+  return 1.45 * waves(pair_ctas) + waves(rest_ctas) < waves(single_ctas + rest_ctas);
 }
 
 size_t gemm_pair_smem_bytes() { return size_t(kPS) * kPStage + sizeof(PairCtl) + 1024; }

@@ -145,10 +145,24 @@ int launch_syrk_reduce(const SyrkReduceTask* d_tasks, int n_tasks, const float* 
 bool pair_eligible(const GemmProblem& p);
 int plan_pair_tiles(int problem_index, const GemmProblem& p, int kchunk, std::vector<GemmWorkItem>& items,
                     std::vector<SyrkReduceTask>* reduce, int* next_slot, double reduce_scale, float* packed_out);
-// Dense problems (EPI_DENSE without mirror/transposed copy, EPI_UPDATE) on
-// the pair kernel: 256 x 256 tiles, K band per tile for triangular operands.
-bool pair_eligible_dense(const GemmProblem& p);
-int plan_pair_dense(int problem_index, const GemmProblem& p, std::vector<GemmWorkItem>& items);
+// Dense problems (EPI_DENSE incl. mirror / transposed copy, EPI_UPDATE) on the
+// pair kernel: 256 x 256 tiles (upper super-tiles for symmetric results), K
+// band per tile for triangular operands.
+bool pair_eligible_dense(const GemmProblem& p, bool upper_only = false);
+// One launch group's choice between the kernels by wave-quantized time: a pair
+// CTA (128 x 256 outputs) costs ~1.45 single-kernel 128 x 128 CTAs (SYRK
+// efficiency 0.62 vs 0.43 of the roofline); `rest` (ineligible problems) runs
+// as a second launch in pair mode.  Small rounds keep the single kernel
+// (config-5 sweep: n = 512/1024 were 9% slower on pairs, n = 4608 5% faster).
+bool pair_group_wins(int64_t pair_ctas, int64_t single_ctas, int64_t rest_ctas);
+// SPNGD_NO_PAIR_INV: keep the inverse recursion / refinement GEMMs on the
+// 128-row kernel (A/B experiments).
+inline bool no_pair_inv() {
+  static const bool off = getenv("SPNGD_NO_PAIR_INV") != nullptr;
+  return off;
+}
+int plan_pair_dense(int problem_index, const GemmProblem& p, std::vector<GemmWorkItem>& items,
+                    bool upper_only = false);
 int launch_syrk_pair(const GemmProblem* d_probs, const GemmWorkItem* d_items, int n_items, float* d_partials,
                      cudaStream_t stream, int* d_status = nullptr);
 

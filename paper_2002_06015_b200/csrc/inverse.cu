@@ -535,26 +535,40 @@ void plan_inverse(const std::vector<DenseMatrix>& mats, float* workspace, Invers
     max_ops = std::max(max_ops, per[m].size());
   }
   plan.workspace_floats = g.used;
-  // Round r runs op r of every matrix: one base launch + one grouped GEMM.
+  // Round r runs op r of every matrix: one base launch + the grouped GEMMs,
+  // the 2-CTA 256 x 256 kernel's items first (pair_cnt), then the 128 x 256 ones.
   for (size_t r = 0; r < max_ops; ++r) {
-    InverseRound rd{int(plan.items.size()), 0, int(plan.bases.size()), 0};
+    InverseRound rd{int(plan.items.size()), 0, int(plan.bases.size()), 0, 0};
+    // eligible problems planned both ways, the rest single; the round goes to
+    // the pair kernel only when that is faster at wave granularity
+    std::vector<GemmWorkItem> pair, single_elig, single;
     for (size_t m = 0; m < mats.size(); ++m) {
       if (r >= per[m].size()) continue;
       const Op& o = per[m][r];
       if (o.kind == 0) {
         plan.bases.push_back(o.base);
-      } else {
+        continue;
+      }
+      for (int h = 0; h < (o.has2 ? 2 : 1); ++h) {
+        const GemmProblem& p = h ? o.prob2 : o.prob;
+        const bool upper = h ? o.upper2 : o.upper;
         const int pi = int(plan.probs.size());
-        plan.probs.push_back(o.prob);
+        plan.probs.push_back(p);
         int slot = 0;
-        plan_problem_tiles(pi, o.prob, o.upper, o.prob.K + kTileK, plan.items, nullptr, &slot, 1.0, nullptr);
-        if (o.has2) {
-          const int pj = int(plan.probs.size());
-          plan.probs.push_back(o.prob2);
-          plan_problem_tiles(pj, o.prob2, o.upper2, o.prob2.K + kTileK, plan.items, nullptr, &slot, 1.0, nullptr);
+        if (!no_pair_inv() && pair_eligible_dense(p, upper)) {
+          plan_pair_dense(pi, p, pair, upper);
+          plan_problem_tiles(pi, p, upper, p.K + kTileK, single_elig, nullptr, &slot, 1.0, nullptr);
+        } else {
+          plan_problem_tiles(pi, p, upper, p.K + kTileK, single, nullptr, &slot, 1.0, nullptr);
         }
       }
     }
+    if (pair_group_wins(int64_t(pair.size()), int64_t(single_elig.size()), int64_t(single.size())))
+      plan.items.insert(plan.items.end(), pair.begin(), pair.end());
+    else
+      single.insert(single.begin(), single_elig.begin(), single_elig.end());
+    rd.pair_cnt = int(plan.items.size()) - rd.item_off;
+    plan.items.insert(plan.items.end(), single.begin(), single.end());
     rd.item_cnt = int(plan.items.size()) - rd.item_off;
     rd.base_cnt = int(plan.bases.size()) - rd.base_off;
     plan.rounds.push_back(rd);
@@ -654,8 +668,14 @@ int run_inverse(spngd_ctx* ctx, const InversePlan& plan, const GemmProblem* d_pr
   for (const InverseRound& r : plan.rounds) {
     rc = launch_base(ctx, d_bases + r.base_off, r.base_cnt);
     if (rc) break;
-    if (r.item_cnt > 0) {
-      rc = launch_gemm(d_probs, d_items + r.item_off, r.item_cnt, nullptr, ctx->d_status, ctx->stream, variant);
+    if (r.pair_cnt > 0) {
+      rc = launch_syrk_pair(d_probs, d_items + r.item_off, r.pair_cnt, nullptr, ctx->stream, ctx->d_status);
+      if (rc) break;
+      ctx->launches++;
+    }
+    if (r.item_cnt > r.pair_cnt) {
+      rc = launch_gemm(d_probs, d_items + r.item_off + r.pair_cnt, r.item_cnt - r.pair_cnt, nullptr, ctx->d_status,
+                       ctx->stream, variant);
       if (rc) break;
       ctx->launches++;
     }

@@ -47,8 +47,9 @@ struct PiTask {  // damp_and_invert's pi and the two dampings (fisher.cpp:221-22
 };
 
 struct InverseRound {
-  int item_off, item_cnt;
+  int item_off, item_cnt;  // items [item_off, item_off + pair_cnt) run on the 2-CTA kernel
   int base_off, base_cnt;
+  int pair_cnt;
 };
 
 // Schedule of the Schur-complement recursion for a batch of dense matrices.

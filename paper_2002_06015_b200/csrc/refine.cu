@@ -183,6 +183,46 @@ int launch_fro(spngd_ctx* ctx, const FroTask* d_tasks, int n, int64_t max_n) {
   return SPNGD_OK;
 }
 
+namespace {
+
+// One grouped GEMM over `probs`: the 2-CTA 256 x 256 kernel for the problems it
+// covers without waste, the 128 x 256 kernel for the rest.
+int launch_dense_group(spngd_ctx* ctx, DeviceScratch& scratch, const std::vector<GemmProblem>& probs) {
+  std::vector<GemmWorkItem> pair, single_elig, single;
+  for (size_t q = 0; q < probs.size(); ++q) {
+    int slot = 0;
+    if (!no_pair_inv() && pair_eligible_dense(probs[q])) {
+      plan_pair_dense(int(q), probs[q], pair);
+      plan_problem_tiles(int(q), probs[q], false, probs[q].K + kTileK, single_elig, nullptr, &slot, 1.0, nullptr);
+    } else {
+      plan_problem_tiles(int(q), probs[q], false, probs[q].K + kTileK, single, nullptr, &slot, 1.0, nullptr);
+    }
+  }
+  if (!pair_group_wins(int64_t(pair.size()), int64_t(single_elig.size()), int64_t(single.size()))) {
+    pair.clear();
+    single.insert(single.begin(), single_elig.begin(), single_elig.end());
+  }
+  auto* d_probs = scratch.upload(probs);
+  auto* d_pair = pair.empty() ? nullptr : scratch.upload(pair);
+  auto* d_single = single.empty() ? nullptr : scratch.upload(single);
+  if (!d_probs || (!pair.empty() && !d_pair) || (!single.empty() && !d_single))
+    return fail(SPNGD_ERR_CUDA, "refine: descriptor upload failed");
+  int rc = SPNGD_OK;
+  if (!pair.empty()) {
+    if ((rc = launch_syrk_pair(d_probs, d_pair, int(pair.size()), nullptr, ctx->stream, ctx->d_status))) return rc;
+    ctx->launches++;
+  }
+  if (!single.empty()) {
+    rc = launch_gemm(d_probs, d_single, int(single.size()), nullptr, ctx->d_status, ctx->stream,
+                     gemm_variant(probs.data(), int(probs.size())));
+    if (rc) return rc;
+    ctx->launches++;
+  }
+  return SPNGD_OK;
+}
+
+}  // namespace
+
 int refine_inverses(spngd_ctx* ctx, DeviceScratch& scratch, const std::vector<RefineJob>& jobs) {
   if (jobs.empty()) return SPNGD_OK;
   std::vector<UnpackTask> unpack;
@@ -211,21 +251,10 @@ int refine_inverses(spngd_ctx* ctx, DeviceScratch& scratch, const std::vector<Re
     max_n = std::max(max_n, n);
     max_elems = std::max(max_elems, n * ld);
   }
-  std::vector<GemmWorkItem> it1, it2;
-  for (size_t q = 0; q < jobs.size(); ++q) {
-    int slot = 0;
-    plan_problem_tiles(int(q), p1[q], false, p1[q].K + kTileK, it1, nullptr, &slot, 1.0, nullptr);
-    plan_problem_tiles(int(q), p2[q], false, p2[q].K + kTileK, it2, nullptr, &slot, 1.0, nullptr);
-  }
   auto* d_unpack = scratch.upload(unpack);
   auto* d_split = scratch.upload(split);
   auto* d_sym = scratch.upload(sym);
-  auto* d_p1 = scratch.upload(p1);
-  auto* d_p2 = scratch.upload(p2);
-  auto* d_i1 = scratch.upload(it1);
-  auto* d_i2 = scratch.upload(it2);
-  if (!d_unpack || !d_split || !d_sym || !d_p1 || !d_p2 || !d_i1 || !d_i2)
-    return fail(SPNGD_ERR_CUDA, "refine: descriptor upload failed");
+  if (!d_unpack || !d_split || !d_sym) return fail(SPNGD_ERR_CUDA, "refine: descriptor upload failed");
   int rc = launch_unpack(ctx, d_unpack, int(unpack.size()), max_n);
   if (rc) return rc;
   {
@@ -235,12 +264,8 @@ int refine_inverses(spngd_ctx* ctx, DeviceScratch& scratch, const std::vector<Re
     SPNGD_CUDA_TRY(cudaGetLastError());
     ctx->launches++;
   }
-  rc = launch_gemm(d_p1, d_i1, int(it1.size()), nullptr, ctx->d_status, ctx->stream, gemm_variant(p1.data(), int(p1.size())));
-  if (rc) return rc;
-  ctx->launches++;
-  rc = launch_gemm(d_p2, d_i2, int(it2.size()), nullptr, ctx->d_status, ctx->stream, gemm_variant(p2.data(), int(p2.size())));
-  if (rc) return rc;
-  ctx->launches++;
+  if ((rc = launch_dense_group(ctx, scratch, p1))) return rc;
+  if ((rc = launch_dense_group(ctx, scratch, p2))) return rc;
   {
     const int64_t tn = (max_n + 31) / 32;
     dim3 grid(unsigned(std::min<int64_t>(tn * tn, 1024)), unsigned(sym.size()));
