@@ -700,18 +700,44 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 #endif
 }
 
-__global__ void syrk_reduce_kernel(const SyrkReduceTask* __restrict__ tasks, const float* __restrict__ partials) {
+// Split-K reduction: block (task, y) sums rows 16y .. 16y+15 of one tile's
+// partial slots in fp64, float4 loads with four slots in flight per thread
+// (the one-block-per-tile loop over slots was latency-bound: ~1 ms for the
+// last wave's factors inside the step).
+constexpr int kReduceRows = 16;
+__global__ void __launch_bounds__(256) syrk_reduce_kernel(const SyrkReduceTask* __restrict__ tasks,
+                                                          const float* __restrict__ partials) {
   const SyrkReduceTask t = tasks[blockIdx.x];
   const int64_t n = t.n;
-  for (int idx = threadIdx.x; idx < kTileM * kTileN; idx += blockDim.x) {
-    const int r = idx >> 7, c = idx & 127;
+  const int r0 = blockIdx.y * kReduceRows;
+  const int64_t i_first = int64_t(t.tm) * kTileM + r0, j_last = int64_t(t.tn) * kTileN + kTileN - 1;
+  if (i_first >= n || i_first > j_last) return;
+  const int64_t step4 = int64_t(t.stride > 1 ? t.stride : 1) * (kTileM * kTileN / 4);
+  for (int v = threadIdx.x; v < kReduceRows * (kTileN / 4); v += blockDim.x) {
+    const int r = r0 + (v >> 5), c = (v & 31) * 4;
     const int64_t i = int64_t(t.tm) * kTileM + r, j = int64_t(t.tn) * kTileN + c;
-    if (i >= n || j >= n || i > j) continue;
-    double s = 0.0;
-    const float* p = partials + int64_t(t.slot0) * kTileM * kTileN + idx;
-    const int64_t step = int64_t(t.stride > 1 ? t.stride : 1) * kTileM * kTileN;
-    for (int q = 0; q < t.nslots; ++q) s += double(p[q * step]);
-    t.packed_out[packed_offset(n, i, j)] = float(s * t.scale);
+    if (i >= n || j >= n || j + 3 < i) continue;
+    const float4* p = reinterpret_cast<const float4*>(partials + int64_t(t.slot0) * kTileM * kTileN + r * kTileN + c);
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+    int q = 0;
+    for (; q + 4 <= t.nslots; q += 4) {
+      float4 x[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) x[u] = __ldcs(p + (q + u) * step4);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        s0 += double(x[u].x); s1 += double(x[u].y); s2 += double(x[u].z); s3 += double(x[u].w);
+      }
+    }
+    for (; q < t.nslots; ++q) {
+      const float4 x = __ldcs(p + q * step4);
+      s0 += double(x.x); s1 += double(x.y); s2 += double(x.z); s3 += double(x.w);
+    }
+    const double sv[4] = {s0, s1, s2, s3};
+    float* out = t.packed_out + packed_offset(n, i, j);  // row i is contiguous from (i, i)
+#pragma unroll
+    for (int e = 0; e < 4; ++e)
+      if (j + e < n && j + e >= i) out[e] = float(sv[e] * t.scale);
   }
 }
 
@@ -902,7 +928,7 @@ int launch_gemm(const GemmProblem* d_probs, const GemmWorkItem* d_items, int n_i
 
 int launch_syrk_reduce(const SyrkReduceTask* d_tasks, int n_tasks, const float* d_partials, cudaStream_t stream) {
   if (n_tasks <= 0) return SPNGD_OK;
-  syrk_reduce_kernel<<<n_tasks, 256, 0, stream>>>(d_tasks, d_partials);
+  syrk_reduce_kernel<<<dim3(unsigned(n_tasks), kTileM / kReduceRows), 256, 0, stream>>>(d_tasks, d_partials);
   SPNGD_CUDA_TRY(cudaGetLastError());
   return SPNGD_OK;
 }

@@ -273,7 +273,7 @@ __global__ void __launch_bounds__(kBaseThreads, 1) base_chol_inv_kernel(const Ba
   __syncthreads();
   leaf_blocks<0>(x, nb, warp, lane, buf, bad);
   LEAF_STAMP(2);
-  if (bad) {
+  if (bad || t.inject) {
     set_status(status, SPNGD_ERR_NOT_POSITIVE_DEFINITE);
     if (t.info && threadIdx.x % 32 == 0) *t.info = SPNGD_ERR_NOT_POSITIVE_DEFINITE;
   }
@@ -534,6 +534,17 @@ void plan_inverse(const std::vector<DenseMatrix>& mats, float* workspace, Invers
     gen_ops(mats[m], g, per[m], form_inverse);
     max_ops = std::max(max_ops, per[m].size());
   }
+  // Failure-path test hook: the last leaf of every n == SPNGD_TEST_FAIL_N
+  // matrix reports a non-positive pivot (the failure found at the very end of
+  // its recursion, after earlier classes' parameters could have been written).
+  const long long fail_n = getenv("SPNGD_TEST_FAIL_N") ? atoll(getenv("SPNGD_TEST_FAIL_N")) : -1;
+  for (size_t m = 0; m < mats.size(); ++m)
+    if (mats[m].n == fail_n)
+      for (size_t r = per[m].size(); r-- > 0;)
+        if (per[m][r].kind == 0) {
+          per[m][r].base.inject = 1;
+          break;
+        }
   plan.workspace_floats = g.used;
   // Round r runs op r of every matrix: one base launch + the grouped GEMMs,
   // the 2-CTA 256 x 256 kernel's items first (pair_cnt), then the 128 x 256 ones.

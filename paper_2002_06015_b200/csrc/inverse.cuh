@@ -13,7 +13,7 @@ struct BaseTask {   // n <= 128 diagonal block: L = chol(M), T = L^-1 -> Tlow, T
   float* tup;
   int64_t ld;
   int32_t n;
-  int32_t pad_;
+  int32_t inject;   // test hook (SPNGD_TEST_FAIL_N): report a non-positive pivot
   int* info;        // per-matrix status word (NotPositiveDefinite), may be null
 };
 

@@ -231,22 +231,34 @@ struct spngd_opt {
   // Wave schedule: the precondition of layers whose inverses finish before the
   // last inverse wave runs on its own stream beside that wave's recursion
   // (which leaves most SMs idle); phase 4 then covers the rest.
+  // The early layers are grouped by the inverse class that finishes last for
+  // them (the longest recursion among their factors' classes), one part per
+  // group on its own stream, so e.g. the 2048-class layers do not wait for
+  // the 4608 chain.
   struct PrePart {
     PrecondPlan plan;
     GemmProblem* d_pp[4] = {};
     GemmWorkItem* d_pi[4] = {};
     RescaleTask* d_rescale = nullptr;
     double* d_norms = nullptr;
+    std::vector<int> wait;         // inverse classes (indices into inv) this part reads
+    cudaStream_t stream = nullptr;
+    cudaEvent_t done = nullptr;
   };
-  PrePart pre[2];
+  std::vector<PrePart> pre_early;
+  PrePart pre_late;
+  std::vector<SnapTask> snap; SnapTask* d_snap = nullptr; int64_t snap_max = 0;
+  cudaStream_t snap_stream = nullptr;
+  cudaEvent_t snap_fork = nullptr, snap_done = nullptr;
   bool pre_split = false;
   int pre_cut = 0;                 // layers of waves < pre_cut are early
-  cudaStream_t pre_stream = nullptr;
-  cudaEvent_t pre_done = nullptr;
   bool ov_now = false;             // the running step uses the wave schedule
   std::vector<spngd_bn_update_req> bnu; spngd_bn_update_req* d_bnu = nullptr; int64_t bnu_maxc = 0;
   float* d_damps = nullptr;
   cudaEvent_t ev[7] = {};
+  // SPNGD_STEP_TRACE (ungraphed steps): labelled events of the wave schedule,
+  // printed against ev[0] by spngd_opt_phase_ms (critical-path diagnosis)
+  std::vector<std::pair<std::string, cudaEvent_t>> trace;
   int64_t launches = 0;
   bool timed = false;
   // ---- stale gating
@@ -287,8 +299,13 @@ struct spngd_opt {
       if (p) cudaIpcCloseMemHandle(p);
     for (float* p : peer_inbox)
       if (p) cudaIpcCloseMemHandle(p);
-    if (pre_done) cudaEventDestroy(pre_done);
-    if (pre_stream) cudaStreamDestroy(pre_stream);
+    if (snap_fork) cudaEventDestroy(snap_fork);
+    if (snap_done) cudaEventDestroy(snap_done);
+    if (snap_stream) cudaStreamDestroy(snap_stream);
+    for (auto& pp : pre_early) {
+      if (pp.done) cudaEventDestroy(pp.done);
+      if (pp.stream) cudaStreamDestroy(pp.stream);
+    }
     if (d2h_done) cudaEventDestroy(d2h_done);
     if (d2h_stream) cudaStreamDestroy(d2h_stream);
     if (h2d_start) cudaEventDestroy(h2d_start);
@@ -675,33 +692,74 @@ int build(spngd_opt* o, const spngd_layer_desc* descs, int n) {
     int last = 0;
     for (const auto& c : o->inv) last = std::max(last, c.wave);
     o->pre_cut = last;
-    std::vector<spngd_precond_req> part[2];
-    std::vector<PrecondTri> ptr[2];
+    std::vector<std::vector<int>> layer_classes(o->layers.size());
+    for (size_t ci = 0; ci < o->inv.size(); ++ci)
+      for (int li : o->inv[ci].mat_layer) layer_classes[size_t(li)].push_back(int(ci));
+    // part key: the layer's class with the longest recursion (-1: late part)
+    std::vector<int> keys;
+    std::vector<int> key_of(preqs.size(), -1);
     for (size_t i = 0; i < preqs.size(); ++i) {
-      const int k = wave_of(o->layers[preq_layer[i]].d) < last ? 0 : 1;
-      part[k].push_back(preqs[i]);
-      ptr[k].push_back(ptri[i]);
+      const int li = preq_layer[i];
+      if (wave_of(o->layers[li].d) >= last || layer_classes[size_t(li)].empty()) continue;
+      int best = -1;
+      for (int ci : layer_classes[size_t(li)])
+        if (best < 0 || o->inv[size_t(ci)].plan.rounds.size() > o->inv[size_t(best)].plan.rounds.size()) best = ci;
+      key_of[i] = best;
+      if (std::find(keys.begin(), keys.end(), best) == keys.end()) keys.push_back(best);
     }
-    if (!part[0].empty() && !part[1].empty()) {
-      for (int k = 0; k < 2; ++k) {
-        spngd_opt::PrePart& pp = o->pre[k];
+    const size_t n_late = size_t(std::count(key_of.begin(), key_of.end(), -1));
+    if (!keys.empty() && n_late > 0) {
+      auto build = [&](spngd_opt::PrePart& pp, int key) -> int {
+        std::vector<spngd_precond_req> part;
+        std::vector<PrecondTri> tri;
+        for (size_t i = 0; i < preqs.size(); ++i) {
+          if (key_of[i] != key) continue;
+          part.push_back(preqs[i]);
+          tri.push_back(ptri[i]);
+          for (int ci : layer_classes[size_t(preq_layer[i])])
+            if (std::find(pp.wait.begin(), pp.wait.end(), ci) == pp.wait.end()) pp.wait.push_back(ci);
+        }
         PrecondPlan sz;
-        if ((rc = plan_precondition(part[k].data(), int(part[k].size()), 0.0, 0.0, nullptr, nullptr, sz, nullptr,
-                                    ptr[k].data())))
-          return rc;
+        int rc2 = plan_precondition(part.data(), int(part.size()), 0.0, 0.0, nullptr, nullptr, sz, nullptr, tri.data());
+        if (rc2) return rc2;
         float* tmp = o->alloc(sz.tmp_floats);
-        pp.d_norms = reinterpret_cast<double*>(o->alloc(2 * part[k].size() + 2));
-        if ((rc = plan_precondition(part[k].data(), int(part[k].size()), 0.0, 0.0, tmp, pp.d_norms, pp.plan, o->d_scal,
-                                    ptr[k].data())))
-          return rc;
+        pp.d_norms = reinterpret_cast<double*>(o->alloc(2 * part.size() + 2));
+        if ((rc2 = plan_precondition(part.data(), int(part.size()), 0.0, 0.0, tmp, pp.d_norms, pp.plan, o->d_scal,
+                                     tri.data())))
+          return rc2;
         for (int q = 0; q < pp.plan.stages; ++q) {
           pp.d_pp[q] = dev_upload(pp.plan.probs[q], own);
           pp.d_pi[q] = dev_upload(pp.plan.items[q], own);
         }
         pp.d_rescale = dev_upload(pp.plan.rescale, own);
+        return SPNGD_OK;
+      };
+      o->pre_early.resize(keys.size());
+      for (size_t k = 0; k < keys.size(); ++k) {
+        spngd_opt::PrePart& pp = o->pre_early[k];
+        if ((rc = build(pp, keys[k]))) return rc;
+        SPNGD_CUDA_TRY(cudaStreamCreateWithFlags(&pp.stream, cudaStreamNonBlocking));
+        SPNGD_CUDA_TRY(cudaEventCreateWithFlags(&pp.done, cudaEventDisableTiming));
       }
-      SPNGD_CUDA_TRY(cudaStreamCreateWithFlags(&o->pre_stream, cudaStreamNonBlocking));
-      SPNGD_CUDA_TRY(cudaEventCreateWithFlags(&o->pre_done, cudaEventDisableTiming));
+      if ((rc = build(o->pre_late, -1))) return rc;
+      o->pre_late.wait.clear();
+      // failure atomicity: the replica and the early layers' velocities
+      const int64_t nag = int64_t(o->world) * o->seg_ag;
+      o->snap.push_back({o->ag, o->alloc(size_t(nag)), nag});
+      for (size_t i = 0; i < preqs.size(); ++i) {
+        if (key_of[i] < 0) continue;
+        const LayerState& L = o->layers[size_t(preq_layer[i])];
+        const int64_t cnt = L.d.g * L.d.a;
+        o->snap.push_back({L.V, o->alloc(size_t(cnt)), cnt});
+      }
+      for (const auto& t : o->snap) {
+        if (!t.save) return fail(SPNGD_ERR_CUDA, "opt: snapshot allocation failed");
+        o->snap_max = std::max(o->snap_max, t.n);
+      }
+      o->d_snap = dev_upload(o->snap, own);
+      SPNGD_CUDA_TRY(cudaStreamCreateWithFlags(&o->snap_stream, cudaStreamNonBlocking));
+      SPNGD_CUDA_TRY(cudaEventCreateWithFlags(&o->snap_fork, cudaEventDisableTiming));
+      SPNGD_CUDA_TRY(cudaEventCreateWithFlags(&o->snap_done, cudaEventDisableTiming));
       o->pre_split = true;
     }
   }
@@ -1046,9 +1104,11 @@ int issue_phase(spngd_opt* o, int phase) {
       // BN determinant before the first update.
       rc = agree_status(ctx, o->d_flag);
       if (!rc) rc = launch_bn_det_check(ctx, o->d_bnu, int(o->bnu.size()), o->bnu_maxc, o->cfg.lambda);
+      if (!rc && o->ov_now && o->pre_split)  // undo the early parts of a failed step
+        rc = launch_snapshot(ctx, o->d_snap, int(o->snap.size()), o->snap_max, true);
       if (rc) return rc;
-      if (o->ov_now && o->pre_split) {  // the early part already ran inside the wave schedule
-        const spngd_opt::PrePart& pp = o->pre[1];
+      if (o->ov_now && o->pre_split) {  // the early parts already ran inside the wave schedule
+        const spngd_opt::PrePart& pp = o->pre_late;
         rc = run_precondition(ctx, pp.plan, pp.d_pp, pp.d_pi, pp.d_rescale, pp.d_norms);
       } else {
         rc = run_precondition(ctx, o->pplan, o->d_pp, o->d_pi, o->d_rescale, o->d_norms);
@@ -1082,6 +1142,14 @@ int issue_overlap(spngd_opt* o, bool capturing, bool host_in = false) {
   auto mark = [&](cudaEvent_t e) {
     return capturing ? cudaEventRecordWithFlags(e, s, cudaEventRecordExternal) : cudaEventRecord(e, s);
   };
+  static const bool tracing = getenv("SPNGD_STEP_TRACE") != nullptr;
+  auto tmark = [&](cudaStream_t st, std::string label) {
+    if (!tracing || capturing) return;
+    cudaEvent_t e;
+    if (cudaEventCreate(&e) != cudaSuccess) return;
+    cudaEventRecord(e, st);
+    o->trace.emplace_back(std::move(label), e);
+  };
   int rc = SPNGD_OK;
   if (!host_in) {  // host-input steps expand / repack wave by wave as the captures land
     rc = issue_inputs(o);
@@ -1097,6 +1165,21 @@ int issue_overlap(spngd_opt* o, bool capturing, bool host_in = false) {
                                    o->seg_grad);
     ctx->stream = s;
     if (rc) return rc;
+  }
+  if (o->pre_split) {
+    // Save what the early parts overwrite before the step is known good: one
+    // short full-machine burst ahead of wave 0 (a small long-running grid or
+    // copy-engine copies held SMs / HBM against the inverse chains and cost
+    // 0.8-0.9 ms per step).  World > 1: peers store into this replica only
+    // after a later wave barrier on prep.
+    SPNGD_CUDA_TRY(cudaEventRecord(o->snap_fork, s));
+    SPNGD_CUDA_TRY(cudaStreamWaitEvent(o->snap_stream, o->snap_fork, 0));
+    ctx->stream = o->snap_stream;
+    rc = launch_snapshot(ctx, o->d_snap, int(o->snap.size()), o->snap_max, false);
+    ctx->stream = s;
+    if (rc) return rc;
+    SPNGD_CUDA_TRY(cudaEventRecord(o->snap_done, o->snap_stream));
+    if (prep != s) SPNGD_CUDA_TRY(cudaStreamWaitEvent(prep, o->snap_done, 0));
   }
   const int nw = int(o->waves.size());
   for (int w = 0; w < nw; ++w) {
@@ -1115,6 +1198,7 @@ int issue_overlap(spngd_opt* o, bool capturing, bool host_in = false) {
       if (rc) return rc;
       ctx->launches++;
     }
+    tmark(s, "wave " + std::to_string(w) + " syrk end");
     if (last) SPNGD_CUDA_TRY(mark(o->ev[1]));
     // The wave's split-K reduction and (last wave) BN moments run on the
     // high-priority prep stream: on the main stream they queued behind the
@@ -1143,6 +1227,7 @@ int issue_overlap(spngd_opt* o, bool capturing, bool host_in = false) {
     ctx->stream = s;
     if (rc) return rc;
     SPNGD_CUDA_TRY(cudaEventRecord(wv.fork, prep));
+    tmark(prep, "wave " + std::to_string(w) + " reduce+pi+unpack end");
     for (auto& c : o->inv) {
       if (c.wave != w) continue;
       SPNGD_CUDA_TRY(cudaStreamWaitEvent(c.stream, wv.fork, 0));
@@ -1153,22 +1238,28 @@ int issue_overlap(spngd_opt* o, bool capturing, bool host_in = false) {
       ctx->stream = s;
       if (rc) return rc;
       SPNGD_CUDA_TRY(cudaEventRecord(c.done, c.stream));
+      tmark(c.stream, "wave " + std::to_string(w) + " inverse class n=" +
+                          std::to_string(c.mats.empty() ? 0 : c.mats[0].n) + " x" + std::to_string(c.mats.size()) +
+                          " end (" + std::to_string(c.plan.rounds.size()) + " rounds)");
     }
   }
   if (prep != s) {
     SPNGD_CUDA_TRY(cudaEventRecord(o->comm_done, prep));
     SPNGD_CUDA_TRY(cudaStreamWaitEvent(s, o->comm_done, 0));
   }
-  if (o->pre_split) {  // early precondition beside the last wave's recursion
-    for (auto& c : o->inv)
-      if (c.wave < o->pre_cut) SPNGD_CUDA_TRY(cudaStreamWaitEvent(o->pre_stream, c.done, 0));
-    ctx->stream = o->pre_stream;
-    const spngd_opt::PrePart& pp = o->pre[0];
-    rc = run_precondition(ctx, pp.plan, pp.d_pp, pp.d_pi, pp.d_rescale, pp.d_norms);
-    ctx->stream = s;
-    if (rc) return rc;
-    SPNGD_CUDA_TRY(cudaEventRecord(o->pre_done, o->pre_stream));
-    SPNGD_CUDA_TRY(cudaStreamWaitEvent(s, o->pre_done, 0));
+  if (o->pre_split) {  // early precondition parts, each as soon as its inverse classes are done
+    for (size_t k = 0; k < o->pre_early.size(); ++k) {
+      const spngd_opt::PrePart& pp = o->pre_early[k];
+      for (int ci : pp.wait) SPNGD_CUDA_TRY(cudaStreamWaitEvent(pp.stream, o->inv[size_t(ci)].done, 0));
+      SPNGD_CUDA_TRY(cudaStreamWaitEvent(pp.stream, o->snap_done, 0));
+      ctx->stream = pp.stream;
+      rc = run_precondition(ctx, pp.plan, pp.d_pp, pp.d_pi, pp.d_rescale, pp.d_norms);
+      ctx->stream = s;
+      if (rc) return rc;
+      SPNGD_CUDA_TRY(cudaEventRecord(pp.done, pp.stream));
+      tmark(pp.stream, "early precondition part " + std::to_string(k) + " end");
+      SPNGD_CUDA_TRY(cudaStreamWaitEvent(s, pp.done, 0));
+    }
   }
   SPNGD_CUDA_TRY(mark(o->ev[3]));
   for (auto& c : o->inv) SPNGD_CUDA_TRY(cudaStreamWaitEvent(s, c.done, 0));
@@ -1441,6 +1532,11 @@ int step_impl(spngd_opt* o, int64_t step, double eta, double momentum, bool host
     return SPNGD_OK;
   }
   o->ov_now = ov;
+  if (!o->trace.empty()) {  // keep the last step's trace only
+    SPNGD_CUDA_TRY(cudaStreamSynchronize(s));
+    for (auto& t : o->trace) cudaEventDestroy(t.second);
+    o->trace.clear();
+  }
   bool& ready = ov ? o->graphs_ready_ov : o->graphs_ready;
   const bool capture = o->use_graph && !ready && full && !host_in;
   const int64_t l0 = ctx->launches;
@@ -1575,7 +1671,7 @@ int spngd_opt_step_host(spngd_opt* o, int64_t step, double eta, double momentum,
       SPNGD_CUDA_TRY(cudaStreamCreateWithFlags(&o->d2h_stream, cudaStreamNonBlocking));
       SPNGD_CUDA_TRY(cudaEventCreateWithFlags(&o->d2h_done, cudaEventDisableTiming));
     }
-    SPNGD_CUDA_TRY(cudaStreamWaitEvent(o->d2h_stream, o->pre_done, 0));
+    for (const auto& pp : o->pre_early) SPNGD_CUDA_TRY(cudaStreamWaitEvent(o->d2h_stream, pp.done, 0));
     for (const LayerState& L : o->layers) {
       const int64_t cnt = L.d.kind == SPNGD_BN ? 2 * L.d.g : L.d.g * L.d.a;
       const bool early = L.d.kind != SPNGD_BN && wave_of(L.d) < o->pre_cut;
@@ -1871,7 +1967,11 @@ int spngd_opt_attach_peers(spngd_opt* o, const void* handles) {
     if (!o->pplan.rescale.empty())
       SPNGD_CUDA_TRY(cudaMemcpy(o->d_rescale, o->pplan.rescale.data(), o->pplan.rescale.size() * sizeof(RescaleTask),
                                 cudaMemcpyHostToDevice));
-    for (auto& pp : o->pre) {
+    std::vector<spngd_opt::PrePart*> parts;
+    for (auto& pp : o->pre_early) parts.push_back(&pp);
+    parts.push_back(&o->pre_late);
+    for (auto* ppp : parts) {
+      spngd_opt::PrePart& pp = *ppp;
       for (auto& t : pp.plan.rescale) t.n_peers = peers_of(t.W, t.peers);
       if (!pp.plan.rescale.empty())
         SPNGD_CUDA_TRY(cudaMemcpy(pp.d_rescale, pp.plan.rescale.data(), pp.plan.rescale.size() * sizeof(RescaleTask),
@@ -1938,6 +2038,18 @@ int spngd_opt_phase_ms(spngd_opt* o, float* out6) {
   if (!o->timed) return fail(SPNGD_ERR_INVALID, "spngd_opt_phase_ms: no step yet");
   SPNGD_CUDA_TRY(cudaEventSynchronize(o->ev[6]));
   for (int i = 0; i < 6; ++i) SPNGD_CUDA_TRY(cudaEventElapsedTime(&out6[i], o->ev[i], o->ev[i + 1]));
+  if (!o->trace.empty()) {
+    for (auto& t : o->trace) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, o->ev[0], t.second);
+      fprintf(stderr, "[step trace] %8.3f ms  %s\n", ms, t.first.c_str());
+      cudaEventDestroy(t.second);
+    }
+    float total = 0.f;
+    cudaEventElapsedTime(&total, o->ev[0], o->ev[6]);
+    fprintf(stderr, "[step trace] %8.3f ms  step end\n", total);
+    o->trace.clear();
+  }
   return SPNGD_OK;
 }
 

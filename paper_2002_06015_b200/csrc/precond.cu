@@ -74,6 +74,19 @@ __global__ void peer_copy_kernel(const PeerCopyTask* __restrict__ tasks, const i
   __threadfence_system();
 }
 
+__global__ void snapshot_kernel(const SnapTask* __restrict__ tasks, bool restore, const int* __restrict__ status) {
+  if (restore && *status == 0) return;
+  const SnapTask t = tasks[blockIdx.y];
+  const float* src = restore ? t.save : t.live;
+  float* dst = restore ? t.live : t.save;
+  const bool vec = t.n % 4 == 0 && ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15) == 0;
+  const int64_t n4 = vec ? t.n / 4 : 0;
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; q < n4; q += stride)
+    reinterpret_cast<float4*>(dst)[q] = reinterpret_cast<const float4*>(src)[q];
+  for (int64_t i = 4 * n4 + int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < t.n; i += stride) dst[i] = src[i];
+}
+
 __global__ void bn_update_kernel(const spngd_bn_update_req* __restrict__ reqs, double lambda, double eta,
                                  double momentum, const float* scal, int* status) {
   if (*status) return;  // includes a singular block found by bn_det_check_kernel
@@ -386,6 +399,15 @@ int launch_peer_copy(spngd_ctx* ctx, const PeerCopyTask* d_tasks, int n, int64_t
   if (n <= 0) return SPNGD_OK;
   dim3 grid(unsigned(std::min<int64_t>(std::max<int64_t>((max_n / 4 + 255) / 256, 1), 296)), unsigned(n));
   peer_copy_kernel<<<grid, 256, 0, ctx->stream>>>(d_tasks, ctx->d_status);
+  SPNGD_CUDA_TRY(cudaGetLastError());
+  ctx->launches++;
+  return SPNGD_OK;
+}
+
+int launch_snapshot(spngd_ctx* ctx, const SnapTask* d_tasks, int n, int64_t max_n, bool restore) {
+  if (n <= 0) return SPNGD_OK;
+  dim3 grid(unsigned(std::min<int64_t>(std::max<int64_t>((max_n / 4 + 255) / 256, 1), 2 * kNumSMs)), unsigned(n));
+  snapshot_kernel<<<grid, 256, 0, ctx->stream>>>(d_tasks, restore, ctx->d_status);
   SPNGD_CUDA_TRY(cudaGetLastError());
   ctx->launches++;
   return SPNGD_OK;

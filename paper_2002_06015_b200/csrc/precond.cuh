@@ -33,6 +33,17 @@ struct PeerCopyTask {
 };
 int launch_peer_copy(spngd_ctx* ctx, const PeerCopyTask* d_tasks, int n, int64_t max_n);
 
+// Parameters the wave schedule updates before every inverse is known good
+// (early precondition parts): saved at step start, restored in phase 4 when
+// the step failed, so a failed step changes no parameter (dist.cpp:597-601).
+struct SnapTask {
+  float* live;
+  float* save;
+  int64_t n;
+};
+// restore = false: save <- live; restore = true: live <- save iff *d_status.
+int launch_snapshot(spngd_ctx* ctx, const SnapTask* d_tasks, int n, int64_t max_n, bool restore);
+
 // Owner side of the fused reduce-scatter: out = mean over the `world` source
 // slots (slot q at in + q * slot_stride), summed in ascending rank order
 // like reduce_scatter_v (dist.cpp:204-213).

@@ -1,0 +1,12 @@
+#!/bin/bash
+# early precondition split by the inverse class each layer waits for: step tests, bench, trace
+set -u
+O=gpurun_out
+mkdir -p $O
+timeout 900 python -m pytest tests/test_gpu_step.py tests/test_gpu_large.py -q -x > $O/r2v_tests.log 2>&1; echo "exit $?" >> $O/r2v_tests.log
+for v in 1 2; do
+  timeout 300 python bench.py --steps 20 --no-cpu-baseline --e2e-steps 0 --no-raw-e2e > $O/r2v_bench_$v.json 2>/dev/null
+  SPNGD_KCHUNK=4096 timeout 300 python bench.py --steps 20 --no-cpu-baseline --e2e-steps 0 --no-raw-e2e > $O/r2v_bench_kc4096_$v.json 2>/dev/null
+done
+CUDA_DEVICE_MAX_CONNECTIONS=32 SPNGD_NO_GRAPH=1 SPNGD_STEP_TRACE=1 timeout 300 python bench.py --steps 3 --warmup 3 --no-cpu-baseline --e2e-steps 0 --no-raw-e2e > /dev/null 2> $O/r2v_trace.err
+timeout 600 python bench.py --steps 10 --no-cpu-baseline > $O/r2v_bench_e2e.json 2>/dev/null

@@ -428,6 +428,45 @@ def test_singular_bn_block_updates_nothing(cuda_dev):
         opt.close()
 
 
+def test_failed_step_under_wave_schedule_updates_nothing(cuda_dev, monkeypatch):
+    """Failure atomicity with the wave schedule on: the early precondition
+    part (the FC layer, wave 1) writes W and V while the last wave's SYRK and
+    recursion still run; the conv layer's A factor (n = 576, last wave) then
+    reports a non-positive pivot at its final leaf (SPNGD_TEST_FAIL_N hook).
+    The step must raise naming layer 0 and leave every parameter as it was:
+    phase 4 restores the snapshot taken at step start (dist.cpp:597-601)."""
+    from paper_2002_06015_b200.spngd import NotPositiveDefinite
+    monkeypatch.setenv("SPNGD_TEST_FAIL_N", "576")
+    # conv: a = 576 (last wave), K = 32 * 112^2 -> a long last-wave SYRK; fc: a = 1600 (wave 1, early part)
+    layers = [W.conv(64, 64, 3, 1, 112), W.fc(1600, 8)]
+    opt = Optimizer(layers, 32, lam=LAM)
+    try:
+        opt.synth(seed=9)
+        before = _params(opt, layers)
+        opt.step(1, ETA, MOM)
+        with pytest.raises(NotPositiveDefinite) as e:
+            opt.sync()
+        assert "layer 0" in str(e.value) and "A factor" in str(e.value), str(e.value)
+        after = _params(opt, layers)
+        for li, ((w0, v0), (w1, v1)) in enumerate(zip(before, after)):
+            assert np.array_equal(w0, w1) and np.array_equal(v0, v1), f"layer {li} was updated"
+    finally:
+        opt.close()
+    # without the hook the same optimizer updates both layers (the early part did run)
+    monkeypatch.delenv("SPNGD_TEST_FAIL_N")
+    opt = Optimizer(layers, 32, lam=LAM)
+    try:
+        opt.synth(seed=9)
+        before = _params(opt, layers)
+        opt.step(1, ETA, MOM)
+        opt.sync()
+        after = _params(opt, layers)
+        for li, ((w0, _), (w1, _)) in enumerate(zip(before, after)):
+            assert not np.array_equal(w0, w1), f"layer {li} was not updated"
+    finally:
+        opt.close()
+
+
 @pytest.mark.parametrize("overlap", [True, False])
 def test_bn_backward_inputs_in_step(cuda_dev, overlap):
     """SURVEY §8f row 1 inside the step: BN layers take dY / x_hat; the fused
