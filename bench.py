@@ -450,10 +450,14 @@ def overlap_labels(phases, world):
     them: in that schedule the inverse recursion runs beside the factor SYRKs,
     so the phase-serial names (factor_gemm, ..., inverse) do not apply."""
     v = list(phases.values())
-    names = ["factor_syrk_waves (earlier waves' inverses overlapped)", "last_wave_reduce_and_bn_moments",
-             ("comm_join_and_" if world > 1 else "") + "early_precondition (layers of the earlier waves)",
-             "inverse_tail (last wave's recursion)", "precondition_update_late_and_bn",
-             "all_gather" if world > 1 else "all_gather (none at P=1)"]
+    if world > 1:
+        names = ["factor_syrk_waves (earlier waves' inverses overlapped)", "last_wave_reduce_and_bn_moments",
+                 "comm_join_and_early_precondition (layers of the earlier waves)",
+                 "inverse_tail (last wave's recursion)", "precondition_update_late_and_bn", "all_gather"]
+    else:  # one GPU: every precondition part runs inside the schedule, per inverse class
+        names = ["factor_syrk_waves (earlier waves' inverses overlapped)", "last_wave_reduce_and_bn_moments",
+                 "inverse_tail_and_precondition (parts as their inverse classes finish)",
+                 "join", "status_restore_and_bn_update", "all_gather (none at P=1)"]
     return {n: round(x, 3) for n, x in zip(names, v)}
 
 

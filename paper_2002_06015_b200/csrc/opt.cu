@@ -246,7 +246,8 @@ struct spngd_opt {
     cudaEvent_t done = nullptr;
   };
   std::vector<PrePart> pre_early;
-  PrePart pre_late;
+  PrePart pre_late;                // world 1: also inside the wave schedule (stream/done below)
+  bool late_in_overlap = false;
   std::vector<SnapTask> snap; SnapTask* d_snap = nullptr; int64_t snap_max = 0;
   cudaStream_t snap_stream = nullptr;
   cudaEvent_t snap_fork = nullptr, snap_done = nullptr;
@@ -299,6 +300,8 @@ struct spngd_opt {
       if (p) cudaIpcCloseMemHandle(p);
     for (float* p : peer_inbox)
       if (p) cudaIpcCloseMemHandle(p);
+    if (pre_late.done) cudaEventDestroy(pre_late.done);
+    if (pre_late.stream) cudaStreamDestroy(pre_late.stream);
     if (snap_fork) cudaEventDestroy(snap_fork);
     if (snap_done) cudaEventDestroy(snap_done);
     if (snap_stream) cudaStreamDestroy(snap_stream);
@@ -742,7 +745,16 @@ int build(spngd_opt* o, const spngd_layer_desc* descs, int n) {
         SPNGD_CUDA_TRY(cudaEventCreateWithFlags(&pp.done, cudaEventDisableTiming));
       }
       if ((rc = build(o->pre_late, -1))) return rc;
+      // One GPU: the late part runs inside the schedule too, as soon as every
+      // inverse (the step's status) and the BN determinant check are done
+      // (world > 1 agrees on the status with a collective in phase 4 first).
       o->pre_late.wait.clear();
+      for (size_t ci = 0; ci < o->inv.size(); ++ci) o->pre_late.wait.push_back(int(ci));
+      o->late_in_overlap = o->world == 1;
+      if (o->late_in_overlap) {
+        SPNGD_CUDA_TRY(cudaStreamCreateWithFlags(&o->pre_late.stream, cudaStreamNonBlocking));
+        SPNGD_CUDA_TRY(cudaEventCreateWithFlags(&o->pre_late.done, cudaEventDisableTiming));
+      }
       // failure atomicity: the replica and the early layers' velocities
       const int64_t nag = int64_t(o->world) * o->seg_ag;
       o->snap.push_back({o->ag, o->alloc(size_t(nag)), nag});
@@ -1103,13 +1115,14 @@ int issue_phase(spngd_opt* o, int phase) {
       // (the kernels read the status word): agree on it, then check every
       // BN determinant before the first update.
       rc = agree_status(ctx, o->d_flag);
-      if (!rc) rc = launch_bn_det_check(ctx, o->d_bnu, int(o->bnu.size()), o->bnu_maxc, o->cfg.lambda);
+      if (!rc && !(o->ov_now && o->pre_split && o->late_in_overlap))
+        rc = launch_bn_det_check(ctx, o->d_bnu, int(o->bnu.size()), o->bnu_maxc, o->cfg.lambda);
       if (!rc && o->ov_now && o->pre_split)  // undo the early parts of a failed step
         rc = launch_snapshot(ctx, o->d_snap, int(o->snap.size()), o->snap_max, true);
       if (rc) return rc;
       if (o->ov_now && o->pre_split) {  // the early parts already ran inside the wave schedule
         const spngd_opt::PrePart& pp = o->pre_late;
-        rc = run_precondition(ctx, pp.plan, pp.d_pp, pp.d_pi, pp.d_rescale, pp.d_norms);
+        if (!o->late_in_overlap) rc = run_precondition(ctx, pp.plan, pp.d_pp, pp.d_pi, pp.d_rescale, pp.d_norms);
       } else {
         rc = run_precondition(ctx, o->pplan, o->d_pp, o->d_pi, o->d_rescale, o->d_norms);
       }
@@ -1258,6 +1271,20 @@ int issue_overlap(spngd_opt* o, bool capturing, bool host_in = false) {
       if (rc) return rc;
       SPNGD_CUDA_TRY(cudaEventRecord(pp.done, pp.stream));
       tmark(pp.stream, "early precondition part " + std::to_string(k) + " end");
+      SPNGD_CUDA_TRY(cudaStreamWaitEvent(s, pp.done, 0));
+    }
+    if (o->late_in_overlap) {  // every inverse + the last wave's BN moments (its fork on prep) done
+      spngd_opt::PrePart& pp = o->pre_late;
+      for (int ci : pp.wait) SPNGD_CUDA_TRY(cudaStreamWaitEvent(pp.stream, o->inv[size_t(ci)].done, 0));
+      SPNGD_CUDA_TRY(cudaStreamWaitEvent(pp.stream, o->waves.back().fork, 0));
+      SPNGD_CUDA_TRY(cudaStreamWaitEvent(pp.stream, o->snap_done, 0));
+      ctx->stream = pp.stream;
+      rc = launch_bn_det_check(ctx, o->d_bnu, int(o->bnu.size()), o->bnu_maxc, o->cfg.lambda);
+      if (!rc) rc = run_precondition(ctx, pp.plan, pp.d_pp, pp.d_pi, pp.d_rescale, pp.d_norms);
+      ctx->stream = s;
+      if (rc) return rc;
+      SPNGD_CUDA_TRY(cudaEventRecord(pp.done, pp.stream));
+      tmark(pp.stream, "late precondition end");
       SPNGD_CUDA_TRY(cudaStreamWaitEvent(s, pp.done, 0));
     }
   }
