@@ -59,6 +59,8 @@ class LayerData:
 
         def take(count):
             nonlocal off
+            if count > n:  # larger than the pool (ResNet-18 CIFAR at batch 128): repeat it
+                return np.resize(pool, count)
             if off + count > n:
                 off = 0
             v = pool[off:off + count]

@@ -574,6 +574,7 @@ void plan_inverse(const std::vector<DenseMatrix>& mats, float* workspace, Invers
         }
       }
     }
+    plan.item_bound += std::max(pair.size(), single_elig.size()) + single.size();
     if (pair_group_wins(int64_t(pair.size()), int64_t(single_elig.size()), int64_t(single.size())))
       plan.items.insert(plan.items.end(), pair.begin(), pair.end());
     else

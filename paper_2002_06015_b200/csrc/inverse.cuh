@@ -59,6 +59,9 @@ struct InversePlan {
   std::vector<BaseTask> bases;
   std::vector<InverseRound> rounds;
   size_t workspace_floats = 0;
+  // Upper bound of items.size() for any subset of the matrices (each round's
+  // 2-CTA / single-CTA choice can differ for a subset): sizes re-plan buffers.
+  size_t item_bound = 0;
 };
 
 struct DenseMatrix {

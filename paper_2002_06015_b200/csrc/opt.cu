@@ -651,7 +651,9 @@ int build(spngd_opt* o, const spngd_layer_desc* descs, int n) {
       c.d_bases = dev_upload(c.plan.bases, own);
       if (o->cfg.stale) {  // room for a re-planned subset (never larger than the full class plan)
         c.d_probs_dyn = dev_upload(c.plan.probs, own);
-        c.d_items_dyn = dev_upload(c.plan.items, own);
+        c.d_items_dyn = reinterpret_cast<GemmWorkItem*>(
+            o->alloc((c.plan.item_bound * sizeof(GemmWorkItem) + sizeof(float) - 1) / sizeof(float)));
+        if (!c.d_items_dyn) return fail(SPNGD_ERR_CUDA, "opt: allocation failed");
         c.d_bases_dyn = dev_upload(c.plan.bases, own);
       }
       SPNGD_CUDA_TRY(cudaStreamCreateWithPriority(&c.stream, cudaStreamNonBlocking,
@@ -1417,6 +1419,9 @@ int stale_partial_phase(spngd_opt* o, int phase) {
           if (touched[c.mat_layer[m]]) sub.push_back(c.mats[m]);
         if (sub.empty()) continue;
         plan_inverse(sub, c.ws, c.dyn, false);
+        if (c.dyn.items.size() > c.plan.item_bound || c.dyn.probs.size() > c.plan.probs.size() ||
+            c.dyn.bases.size() > c.plan.bases.size())
+          return fail(SPNGD_ERR_INVALID, "stale re-plan exceeds the class plan's buffers");
         if ((rc = upload_async(ctx, c.d_probs_dyn, c.dyn.probs))) return rc;
         if ((rc = upload_async(ctx, c.d_items_dyn, c.dyn.items))) return rc;
         if ((rc = upload_async(ctx, c.d_bases_dyn, c.dyn.bases))) return rc;
