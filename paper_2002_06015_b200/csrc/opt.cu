@@ -1412,7 +1412,7 @@ int stale_partial_phase(spngd_opt* o, int phase) {
         if (!rc) rc = launch_unpack(ctx, o->d_unpacks_dyn, int(ups.size()), o->max_n);
         if (rc) return rc;
       }
-      SPNGD_CUDA_TRY(cudaEventRecord(o->inv_fork, s));
+      std::vector<cudaEvent_t> joins;
       for (auto& c : o->inv) {
         std::vector<DenseMatrix> sub;
         for (size_t m = 0; m < c.mats.size(); ++m)
@@ -1425,14 +1425,18 @@ int stale_partial_phase(spngd_opt* o, int phase) {
         if ((rc = upload_async(ctx, c.d_probs_dyn, c.dyn.probs))) return rc;
         if ((rc = upload_async(ctx, c.d_items_dyn, c.dyn.items))) return rc;
         if ((rc = upload_async(ctx, c.d_bases_dyn, c.dyn.bases))) return rc;
+        // the class stream forks after this class's descriptor uploads (on s)
+        SPNGD_CUDA_TRY(cudaEventRecord(o->inv_fork, s));
         SPNGD_CUDA_TRY(cudaStreamWaitEvent(c.stream, o->inv_fork, 0));
         ctx->stream = c.stream;
         rc = run_inverse(ctx, c.dyn, c.d_probs_dyn, c.d_items_dyn, c.d_bases_dyn);
         ctx->stream = s;
         if (rc) return rc;
         SPNGD_CUDA_TRY(cudaEventRecord(c.done, c.stream));
-        SPNGD_CUDA_TRY(cudaStreamWaitEvent(s, c.done, 0));
+        joins.push_back(c.done);
       }
+      // join after every class is issued: the classes' recursions run concurrently
+      for (cudaEvent_t e : joins) SPNGD_CUDA_TRY(cudaStreamWaitEvent(s, e, 0));
       return SPNGD_OK;
     }
   }
