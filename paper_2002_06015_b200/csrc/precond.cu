@@ -252,6 +252,7 @@ int plan_precondition(const spngd_precond_req* reqs, int n, double eta, double m
   plan = PrecondPlan();
   plan.stages = tri ? 4 : 2;
   std::vector<std::vector<GemmWorkItem>> pair_items[4];  // per stage, per problem: cluster-pair items
+  std::vector<GemmWorkItem> elig_single[4];  // the same problems as 128 x 128 tiles
   size_t off = 0;
   auto take = [&](int64_t floats) {
     float* p = tmp ? tmp + off : nullptr;
@@ -319,9 +320,10 @@ int plan_precondition(const spngd_precond_req* reqs, int n, double eta, double m
     for (int q = 0; q < plan.stages; ++q) {
       plan.probs[q].push_back(st[q]);
       int slot = 0;
-      if (pair_eligible_dense(st[q])) {  // 256 x 256 tiles on CTA pairs (gemm_pair.cu)
+      if (pair_eligible_dense(st[q])) {  // 256 x 256 tiles on CTA pairs (gemm_pair.cu), or not (below)
         pair_items[q].push_back({});
         plan_pair_dense(idx, st[q], pair_items[q].back());
+        plan_problem_tiles(idx, st[q], false, st[q].K + kTileK, elig_single[q], nullptr, &slot, 1.0, nullptr);
       } else {
         plan_problem_tiles(idx, st[q], false, st[q].K + kTileK, plan.items[q], nullptr, &slot, 1.0, nullptr);
       }
@@ -333,6 +335,16 @@ int plan_precondition(const spngd_precond_req* reqs, int n, double eta, double m
   plan.n_norms = n;
   auto longest = [](const GemmWorkItem& x, const GemmWorkItem& y) { return (x.k1 - x.k0) > (y.k1 - y.k0); };
   for (int q = 0; q < plan.stages; ++q) {
+    // the stage takes the 2-CTA kernel only when that is faster at wave
+    // granularity (a stage with ~one wave of 128 x 128 tiles finishes sooner
+    // on it: the 4608-wide layers' stages were 1.4x longer on pairs)
+    size_t npair = 0;
+    for (const auto& v : pair_items[q]) npair += v.size();
+    static const bool always = getenv("SPNGD_PRE_PAIR_ALWAYS") != nullptr;  // A/B experiments
+    if (!always && !pair_group_wins(int64_t(npair), int64_t(elig_single[q].size()), int64_t(plan.items[q].size()))) {
+      pair_items[q].clear();
+      plan.items[q].insert(plan.items[q].end(), elig_single[q].begin(), elig_single[q].end());
+    }
     std::stable_sort(plan.items[q].begin(), plan.items[q].end(), longest);
     std::vector<std::pair<GemmWorkItem, GemmWorkItem>> pairs;  // longest first, pairs as units
     for (const auto& v : pair_items[q])
