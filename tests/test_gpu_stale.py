@@ -166,3 +166,71 @@ def test_stale_constant_inputs_equal_plain_step(cuda_dev):
             opt.close()
     for a, b in zip(*ws):
         assert np.array_equal(a, b)
+
+
+def test_stale_partial_refresh_replans_large_classes(cuda_dev):
+    """Partial refreshes whose due subset changes from step to step, in a size
+    class large enough for 2-CTA recursion rounds (three 4608-wide FC layers):
+    each re-planned recursion covers only the due members, and its plan may
+    choose 2-CTA / single-CTA rounds differently from the full class plan (the
+    re-plan buffers are sized for either).  Each layer's captures jump at its
+    own step, so the due subsets differ; held statistics and the inverses
+    formed from them match the fp64 oracle (dist.cpp:588-601 re-invert both).
+    (The descriptor-upload ordering bug a drifting ResNet-50 stream exposed is
+    covered by scripts/stale_bench.py --drift, profiles/r02_configs/.)"""
+    layers = [W.fc(4608, 16) for _ in range(3)]
+    bq = 8
+    jumps = [3, 4, 6]
+    lam = 0.1  # rank-8 factors: keeps cond(A + dI) ~1e3 so the fp32 inverse meets 1e-4 without refinement
+
+    def caps(step):
+        out = []
+        for li, l in enumerate(layers):
+            r = np.random.default_rng(1000 * li + 1 + (step >= jumps[li]))
+            act = np.maximum(r.standard_normal((bq, l.a)), 0).astype(np.float32)
+            grad = r.standard_normal((bq, l.g)).astype(np.float32)
+            out.append((act, grad))
+        return out
+
+    opt = Optimizer(layers, bq, lam=lam, stale=True, stale_alpha=ALPHA)
+    try:
+        trackers = {(li, k): PyTracker() for li in range(len(layers)) for k in ("A", "G")}
+        held, subsets = {}, set()
+        for step in range(1, 10):
+            cs = caps(step)
+            for li, (act, grad) in enumerate(cs):
+                opt.upload(li, ACT, torch.from_numpy(act.reshape(-1)))
+                opt.upload(li, GRAD, torch.from_numpy(grad.reshape(-1)))
+            due = {}
+            for (li, k), tr in trackers.items():
+                due[(li, k)] = step == tr.t_x
+                if due[(li, k)]:
+                    act, grad = cs[li]
+                    l = layers[li]
+                    x = (O.factor_A(act.astype(np.float64), False, l.a, 1, 0, bq) if k == "A"
+                         else O.factor_G(grad.astype(np.float64), False, l.g, 1, 0, bq))
+                    tr.refresh(x, packed_weights(l.a if k == "A" else l.g), step)
+                    held[(li, k)] = x
+            touched = tuple(li for li in range(len(layers)) if due[(li, "A")] or due[(li, "G")])
+            if 0 < len(touched) < len(layers):
+                subsets.add(touched)
+            opt.step(step, 1.25e-2, 0.993)
+            opt.sync()
+            for (li, k) in trackers:
+                assert opt.stale_info(li, k)["refreshed"] == due[(li, k)], (step, li, k)
+        assert len(subsets) >= 2, subsets
+        for li, l in enumerate(layers):
+            # damp_and_invert (fisher.cpp:218-228) with the blocked fp64 inverse of the oracle
+            ea = np.trace(O.unpack(held[(li, "A")], l.a)) / l.a
+            eg = np.trace(O.unpack(held[(li, "G")], l.g)) / l.g
+            pi = np.sqrt(ea / eg) if min(ea, eg) >= 1e-12 else 1.0
+            ai = O.spd_inverse(held[(li, "A")], l.a, pi * np.sqrt(lam), fast=True)
+            gi = O.spd_inverse(held[(li, "G")], l.g, np.sqrt(lam) / pi, fast=True)
+            got_a = opt.download(li, AINV).numpy().astype(np.float64)
+            want_a = O.unpack(ai, l.a)
+            assert np.linalg.norm(got_a - want_a) <= 1e-4 * np.linalg.norm(want_a), li
+            got_g = opt.download(li, GINV).numpy().astype(np.float64)
+            want_g = O.unpack(gi, l.g)
+            assert np.linalg.norm(got_g - want_g) <= 1e-4 * np.linalg.norm(want_g), li
+    finally:
+        opt.close()
