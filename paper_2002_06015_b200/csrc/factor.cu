@@ -201,16 +201,24 @@ int plan_factors(const spngd_factor_req* reqs, int n, FactorPlan& plan, float* w
     tk.push_back({t * (t + 1) / 2, K});
   }
   plan.kchunk = choose_kchunk(tk);
+  // The single-CTA problems (n = 64, 128, 576) form their own launch after the
+  // 2-CTA one: chunk them for ~4 waves of their own (with the shared chunk the
+  // ResNet-50 launch had 193 CTAs, 1.3 waves, ~1.85 ms at 0.23 of the roofline).
+  std::vector<std::pair<int64_t, int64_t>> tk_single;
+  for (int i = 0; i < n; ++i)
+    if (!pair_eligible(plan.probs[i])) tk_single.push_back(tk[size_t(i)]);
+  int kchunk_single = tk_single.empty() ? plan.kchunk : std::min(plan.kchunk, choose_kchunk(tk_single, 4));
   static const char* kc_env = getenv("SPNGD_KCHUNK");  // experiment override (multiple of 32)
-  if (kc_env && atoi(kc_env) >= 32) plan.kchunk = atoi(kc_env) / 32 * 32;
+  if (kc_env && atoi(kc_env) >= 32) plan.kchunk = kchunk_single = atoi(kc_env) / 32 * 32;
   int slot = 0;
   std::vector<GemmWorkItem> pair_items;
   plan.pair_prob.assign(size_t(n), 0);
   for (int i = 0; i < n; ++i) {
     GemmProblem& p = plan.probs[i];
-    const bool split = p.K > plan.kchunk;
+    const int chunk = pair_eligible(p) ? plan.kchunk : kchunk_single;
+    const bool split = p.K > chunk;
     p.mode = split ? EPI_PARTIAL : EPI_PACKED;
-    const int kc = split ? plan.kchunk : p.K + kTileK;
+    const int kc = split ? chunk : p.K + kTileK;
     if (pair_eligible(p)) {  // 256 x 256 tiles on CTA pairs (gemm_pair.cu)
       plan.pair_prob[size_t(i)] = 1;
       plan_pair_tiles(i, p, kc, pair_items, &plan.reduce, &slot, reqs[i].scale, reqs[i].packed_out);
