@@ -170,7 +170,22 @@ struct spngd_opt {
     std::vector<spngd_im2col_req> i2c;
     spngd_im2col_req* d_i2c = nullptr;
     cudaEvent_t in_ready = nullptr;
+    // Host-input steps, last wave: its SYRK split by layer groups that launch
+    // as their captures land (the last wave holds most of the capture bytes,
+    // so one launch after its last byte left ~3 ms of SYRK after the PCIe
+    // stream ended).  Used when the wave has no repack / im2col.
+    struct Sub {
+      std::vector<GemmWorkItem> items;
+      GemmWorkItem* d_items = nullptr;
+      cudaEvent_t ready = nullptr;
+    };
+    std::vector<Sub> subs;
+    bool subs_usable() const {
+      static const bool off = getenv("SPNGD_NO_SUBWAVES") != nullptr;  // A/B experiments
+      return !off && !subs.empty() && repacks.empty() && i2c.empty();
+    }
   };
+  std::vector<int> sub_of_layer;         // last wave's layer -> sub index (-1: none)
   std::vector<Wave> waves;
   cudaStream_t comm_stream = nullptr;    // world > 1: NCCL + owner-side prep of the waves
   cudaEvent_t comm_fork = nullptr, comm_done = nullptr;
@@ -318,6 +333,8 @@ struct spngd_opt {
       if (w.in_ready) cudaEventDestroy(w.in_ready);
       if (w.fork) cudaEventDestroy(w.fork);
       if (w.ready) cudaEventDestroy(w.ready);
+      for (auto& sb : w.subs)
+        if (sb.ready) cudaEventDestroy(sb.ready);
     }
     if (comm_fork) cudaEventDestroy(comm_fork);
     if (comm_done) cudaEventDestroy(comm_done);
@@ -826,6 +843,34 @@ int build(spngd_opt* o, const spngd_layer_desc* descs, int n) {
       wv.repacks.push_back(t);
       wv.repack_max = std::max(wv.repack_max, t.n * t.dim * t.hw);
     }
+    {  // host-input sub-waves of the last wave: 8 layer groups of equal SYRK work, in layer order
+       // (e2e A/B: 1 / 2 / 4 / 8 groups 87.3 / 85.2 / 84.3 / 83.5 ms)
+      spngd_opt::Wave& wv = o->waves.back();
+      o->sub_of_layer.assign(o->layers.size(), -1);
+      std::vector<double> work(o->layers.size(), 0.0);
+      double total = 0;
+      for (const auto& it : wv.items) {
+        const int li = o->stats[o->prob_stat[it.problem]].layer;
+        work[size_t(li)] += double(it.k1 - it.k0);
+        total += double(it.k1 - it.k0);
+      }
+      static const int kSubs = getenv("SPNGD_SUBWAVES") ? std::max(1, atoi(getenv("SPNGD_SUBWAVES"))) : 8;
+      double acc = 0;
+      for (size_t li = 0; li < o->layers.size() && total > 0; ++li) {
+        if (work[li] <= 0) continue;
+        o->sub_of_layer[li] = std::min(kSubs - 1, int(acc / total * kSubs));
+        acc += work[li];
+      }
+      if (total > 0) {
+        wv.subs.resize(kSubs);
+        for (const auto& it : wv.items)  // wave order kept: pair items first in every sub
+          wv.subs[size_t(o->sub_of_layer[size_t(o->stats[o->prob_stat[it.problem]].layer)])].items.push_back(it);
+        for (auto& sb : wv.subs) {
+          sb.d_items = dev_upload(sb.items, own);
+          SPNGD_CUDA_TRY(cudaEventCreateWithFlags(&sb.ready, cudaEventDisableTiming));
+        }
+      }
+    }
     for (auto& wv : o->waves) {
       wv.d_repacks = dev_upload(wv.repacks, own);
       SPNGD_CUDA_TRY(cudaEventCreateWithFlags(&wv.in_ready, cudaEventDisableTiming));
@@ -1200,13 +1245,24 @@ int issue_overlap(spngd_opt* o, bool capturing, bool host_in = false) {
   for (int w = 0; w < nw; ++w) {
     spngd_opt::Wave& wv = o->waves[w];
     const bool last = w == nw - 1;
-    if (host_in) {
+    const bool by_sub = host_in && last && wv.subs_usable();
+    if (by_sub) {  // each layer group's SYRK as soon as its captures have landed
+      for (auto& sb : wv.subs) {
+        SPNGD_CUDA_TRY(cudaStreamWaitEvent(s, sb.ready, 0));
+        if (sb.items.empty()) continue;
+        rc = launch_factor_gemm(ctx, o->fplan, o->d_fprobs, count_pair_items(o->fplan, sb.items), sb.d_items,
+                                int(sb.items.size()), o->d_partials, s);
+        if (rc) return rc;
+        ctx->launches++;
+      }
+      SPNGD_CUDA_TRY(cudaStreamWaitEvent(s, wv.in_ready, 0));  // the wave's BN inputs
+    } else if (host_in) {
       SPNGD_CUDA_TRY(cudaStreamWaitEvent(s, wv.in_ready, 0));
       rc = launch_im2col(ctx, wv.d_i2c, int(wv.i2c.size()));
       if (!rc) rc = launch_repack(ctx, wv.d_repacks, int(wv.repacks.size()), wv.repack_max);
       if (rc) return rc;
     }
-    if (!wv.items.empty()) {
+    if (!by_sub && !wv.items.empty()) {
       rc = launch_factor_gemm(ctx, o->fplan, o->d_fprobs, count_pair_items(o->fplan, wv.items), wv.d_items,
                               int(wv.items.size()),
                               o->d_partials, s);
@@ -1650,7 +1706,7 @@ int spngd_opt_step_host(spngd_opt* o, int64_t step, double eta, double momentum,
   if (!o || (n > 0 && !in)) return fail(SPNGD_ERR_INVALID, "spngd_opt_step_host: null argument");
   spngd_ctx* ctx = o->ctx;
   cudaStream_t s = ctx->stream;
-  struct Copy { float* dst; const void* src; int64_t bytes; int wave; };
+  struct Copy { float* dst; const void* src; int64_t bytes; int wave; int sub; };
   std::vector<Copy> copies;
   // BN dY / x_hat feed the gradient payload, which the step needs first: with
   // BN inputs the copies simply precede the step
@@ -1667,9 +1723,16 @@ int spngd_opt_step_host(spngd_opt* o, int64_t step, double eta, double momentum,
     // dW first (the gradient reduce-scatter and every update need it), then
     // the captures in wave order (wave_of, largest factors first)
     const int wave = in[i].which == 2 ? -1 : (pipelined ? wave_of(L.d) : 0);
-    copies.push_back({dst, in[i].host, cnt * int64_t(sizeof(float)), wave});
+    // last wave: by sub-wave (layer group), inputs of no group (BN) last
+    int sub = 0;
+    if (pipelined && wave == int(o->waves.size()) - 1 && o->waves.back().subs_usable()) {
+      const int g = o->sub_of_layer[size_t(in[i].layer)];
+      sub = g >= 0 ? g : int(o->waves.back().subs.size());
+    }
+    copies.push_back({dst, in[i].host, cnt * int64_t(sizeof(float)), wave, sub});
   }
-  std::stable_sort(copies.begin(), copies.end(), [](const Copy& x, const Copy& y) { return x.wave < y.wave; });
+  std::stable_sort(copies.begin(), copies.end(),
+                   [](const Copy& x, const Copy& y) { return x.wave != y.wave ? x.wave < y.wave : x.sub < y.sub; });
   if (!pipelined) {  // same inputs, copied before the step on its stream
     for (const Copy& c : copies) SPNGD_CUDA_TRY(cudaMemcpyAsync(c.dst, c.src, c.bytes, cudaMemcpyHostToDevice, s));
     int rc = step_impl(o, step, eta, momentum, false);
@@ -1689,10 +1752,15 @@ int spngd_opt_step_host(spngd_opt* o, int64_t step, double eta, double momentum,
                                      o->h2d_stream));
     SPNGD_CUDA_TRY(cudaEventRecord(o->grads_ready, o->h2d_stream));
     for (int w = 0; w < int(o->waves.size()); ++w) {
-      for (; i < copies.size() && copies[i].wave == w; ++i)
-        SPNGD_CUDA_TRY(cudaMemcpyAsync(copies[i].dst, copies[i].src, copies[i].bytes, cudaMemcpyHostToDevice,
-                                       o->h2d_stream));
-      SPNGD_CUDA_TRY(cudaEventRecord(o->waves[w].in_ready, o->h2d_stream));
+      spngd_opt::Wave& wv = o->waves[w];
+      const bool by_sub = w == int(o->waves.size()) - 1 && wv.subs_usable();
+      for (int k = 0; k <= (by_sub ? int(wv.subs.size()) : 0); ++k) {
+        for (; i < copies.size() && copies[i].wave == w && (!by_sub || copies[i].sub == k); ++i)
+          SPNGD_CUDA_TRY(cudaMemcpyAsync(copies[i].dst, copies[i].src, copies[i].bytes, cudaMemcpyHostToDevice,
+                                         o->h2d_stream));
+        if (by_sub && k < int(wv.subs.size())) SPNGD_CUDA_TRY(cudaEventRecord(wv.subs[size_t(k)].ready, o->h2d_stream));
+      }
+      SPNGD_CUDA_TRY(cudaEventRecord(wv.in_ready, o->h2d_stream));
     }
     SPNGD_CUDA_TRY(cudaStreamWaitEvent(s, o->grads_ready, 0));
     int rc = step_impl(o, step, eta, momentum, true);
