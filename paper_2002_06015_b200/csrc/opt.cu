@@ -843,8 +843,9 @@ int build(spngd_opt* o, const spngd_layer_desc* descs, int n) {
       wv.repacks.push_back(t);
       wv.repack_max = std::max(wv.repack_max, t.n * t.dim * t.hw);
     }
-    {  // host-input sub-waves of the last wave: 8 layer groups of equal SYRK work, in layer order
-       // (e2e A/B: 1 / 2 / 4 / 8 groups 87.3 / 85.2 / 84.3 / 83.5 ms)
+    // Host-input sub-waves of the last wave: 8 layer groups of equal SYRK work,
+    // in layer order (e2e A/B: 1 / 2 / 4 / 8 groups 87.3 / 85.2 / 84.3 / 83.5 ms).
+    {
       spngd_opt::Wave& wv = o->waves.back();
       o->sub_of_layer.assign(o->layers.size(), -1);
       std::vector<double> work(o->layers.size(), 0.0);
