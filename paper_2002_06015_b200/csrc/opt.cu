@@ -1766,6 +1766,13 @@ int spngd_opt_step_host(spngd_opt* o, int64_t step, double eta, double momentum,
     SPNGD_CUDA_TRY(cudaStreamWaitEvent(s, o->grads_ready, 0));
     int rc = step_impl(o, step, eta, momentum, true);
     if (rc) return rc;
+    if (getenv("SPNGD_STEP_TRACE")) {  // the trace's ev[0] is the step start on s
+      cudaEvent_t e;
+      if (cudaEventCreate(&e) == cudaSuccess) {
+        cudaEventRecord(e, o->h2d_stream);
+        o->trace.emplace_back("host inputs: last H2D copy landed", e);
+      }
+    }
   }
   if (!host_weights_out) return SPNGD_OK;
   if (pipelined && o->world == 1 && o->pre_split) {
