@@ -769,11 +769,12 @@ int build(spngd_opt* o, const spngd_layer_desc* descs, int n) {
       // (world > 1 agrees on the status with a collective in phase 4 first).
       o->pre_late.wait.clear();
       for (size_t ci = 0; ci < o->inv.size(); ++ci) o->pre_late.wait.push_back(int(ci));
+      // world > 1: its stages before the update (temporaries only) still run
+      // inside the schedule; the update stage and the rescale follow the
+      // status agreement in phase 4
       o->late_in_overlap = o->world == 1;
-      if (o->late_in_overlap) {
-        SPNGD_CUDA_TRY(cudaStreamCreateWithFlags(&o->pre_late.stream, cudaStreamNonBlocking));
-        SPNGD_CUDA_TRY(cudaEventCreateWithFlags(&o->pre_late.done, cudaEventDisableTiming));
-      }
+      SPNGD_CUDA_TRY(cudaStreamCreateWithFlags(&o->pre_late.stream, cudaStreamNonBlocking));
+      SPNGD_CUDA_TRY(cudaEventCreateWithFlags(&o->pre_late.done, cudaEventDisableTiming));
       // failure atomicity: the replica and the early layers' velocities
       const int64_t nag = int64_t(o->world) * o->seg_ag;
       o->snap.push_back({o->ag, o->alloc(size_t(nag)), nag});
@@ -1170,7 +1171,9 @@ int issue_phase(spngd_opt* o, int phase) {
       if (rc) return rc;
       if (o->ov_now && o->pre_split) {  // the early parts already ran inside the wave schedule
         const spngd_opt::PrePart& pp = o->pre_late;
-        if (!o->late_in_overlap) rc = run_precondition(ctx, pp.plan, pp.d_pp, pp.d_pi, pp.d_rescale, pp.d_norms);
+        if (!o->late_in_overlap)  // the stages before the update ran in the schedule
+          rc = run_precondition_stages(ctx, pp.plan, pp.d_pp, pp.d_pi, pp.d_rescale, pp.d_norms,
+                                       pp.plan.stages > 1 ? pp.plan.stages - 1 : 0, pp.plan.stages, true);
       } else {
         rc = run_precondition(ctx, o->pplan, o->d_pp, o->d_pi, o->d_rescale, o->d_norms);
       }
@@ -1344,6 +1347,18 @@ int issue_overlap(spngd_opt* o, bool capturing, bool host_in = false) {
       if (rc) return rc;
       SPNGD_CUDA_TRY(cudaEventRecord(pp.done, pp.stream));
       tmark(pp.stream, "late precondition end");
+      SPNGD_CUDA_TRY(cudaStreamWaitEvent(s, pp.done, 0));
+    } else if (o->pre_late.plan.stages > 1) {  // world > 1: the late part's stages before its update
+      spngd_opt::PrePart& pp = o->pre_late;
+      for (int ci : pp.wait) SPNGD_CUDA_TRY(cudaStreamWaitEvent(pp.stream, o->inv[size_t(ci)].done, 0));
+      SPNGD_CUDA_TRY(cudaStreamWaitEvent(pp.stream, o->waves.back().fork, 0));
+      ctx->stream = pp.stream;
+      rc = run_precondition_stages(ctx, pp.plan, pp.d_pp, pp.d_pi, pp.d_rescale, pp.d_norms, 0, pp.plan.stages - 1,
+                                   false);
+      ctx->stream = s;
+      if (rc) return rc;
+      SPNGD_CUDA_TRY(cudaEventRecord(pp.done, pp.stream));
+      tmark(pp.stream, "late precondition stages before the update end");
       SPNGD_CUDA_TRY(cudaStreamWaitEvent(s, pp.done, 0));
     }
   }

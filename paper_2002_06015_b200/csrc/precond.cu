@@ -364,9 +364,15 @@ int plan_precondition(const spngd_precond_req* reqs, int n, double eta, double m
 
 int run_precondition(spngd_ctx* ctx, const PrecondPlan& plan, GemmProblem* const* d_probs,
                      GemmWorkItem* const* d_items, const RescaleTask* d_rescale, double* d_norms) {
-  if (d_norms && plan.n_norms > 0)
+  return run_precondition_stages(ctx, plan, d_probs, d_items, d_rescale, d_norms, 0, plan.stages, true);
+}
+
+int run_precondition_stages(spngd_ctx* ctx, const PrecondPlan& plan, GemmProblem* const* d_probs,
+                            GemmWorkItem* const* d_items, const RescaleTask* d_rescale, double* d_norms, int q0, int q1,
+                            bool finish) {
+  if (finish && d_norms && plan.n_norms > 0)
     SPNGD_CUDA_TRY(cudaMemsetAsync(d_norms, 0, sizeof(double) * plan.n_norms, ctx->stream));
-  for (int q = 0; q < plan.stages; ++q) {
+  for (int q = q0; q < q1; ++q) {
     const int np = plan.n_pair[q], n = int(plan.items[q].size());
     int rc = launch_syrk_pair(d_probs[q], d_items[q], np, nullptr, ctx->stream, ctx->d_status);
     ctx->launches += np > 0;
@@ -376,7 +382,7 @@ int run_precondition(spngd_ctx* ctx, const PrecondPlan& plan, GemmProblem* const
     if (rc) return rc;
     ctx->launches += n > np;
   }
-  if (!plan.rescale.empty()) {
+  if (finish && !plan.rescale.empty()) {
     dim3 grid(296, unsigned(plan.rescale.size()));
     rescale_kernel<<<grid, 256, 0, ctx->stream>>>(d_rescale, ctx->d_status);
     SPNGD_CUDA_TRY(cudaGetLastError());

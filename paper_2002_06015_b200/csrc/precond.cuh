@@ -89,6 +89,11 @@ int plan_precondition(const spngd_precond_req* reqs, int n, double eta, double m
                       const PrecondTri* tri = nullptr);
 int run_precondition(spngd_ctx* ctx, const PrecondPlan& plan, GemmProblem* const* d_probs,
                      GemmWorkItem* const* d_items, const RescaleTask* d_rescale, double* d_norms);
+// Stages [q0, q1) only; `finish` also zeroes the norms first and runs the
+// rescale pass after (the stages before the last write only temporaries).
+int run_precondition_stages(spngd_ctx* ctx, const PrecondPlan& plan, GemmProblem* const* d_probs,
+                            GemmWorkItem* const* d_items, const RescaleTask* d_rescale, double* d_norms, int q0, int q1,
+                            bool finish);
 
 struct BnUpdateTask {
   spngd_bn_update_req r;
