@@ -177,12 +177,16 @@ struct spngd_opt {
     struct Sub {
       std::vector<GemmWorkItem> items;
       GemmWorkItem* d_items = nullptr;
+      std::vector<spngd_im2col_req> i2c;  // raw-input mode: this group's device im2col
+      spngd_im2col_req* d_i2c = nullptr;
       cudaEvent_t ready = nullptr;
     };
     std::vector<Sub> subs;
     bool subs_usable() const {
       static const bool off = getenv("SPNGD_NO_SUBWAVES") != nullptr;  // A/B experiments
-      return !off && !subs.empty() && repacks.empty() && i2c.empty();
+      size_t n_i2c = 0;
+      for (const auto& sb : subs) n_i2c += sb.i2c.size();
+      return !off && !subs.empty() && repacks.empty() && n_i2c == i2c.size();
     }
   };
   std::vector<int> sub_of_layer;         // last wave's layer -> sub index (-1: none)
@@ -1253,6 +1257,8 @@ int issue_overlap(spngd_opt* o, bool capturing, bool host_in = false) {
     if (by_sub) {  // each layer group's SYRK as soon as its captures have landed
       for (auto& sb : wv.subs) {
         SPNGD_CUDA_TRY(cudaStreamWaitEvent(s, sb.ready, 0));
+        rc = launch_im2col(ctx, sb.d_i2c, int(sb.i2c.size()));
+        if (rc) return rc;
         if (sb.items.empty()) continue;
         rc = launch_factor_gemm(ctx, o->fplan, o->d_fprobs, count_pair_items(o->fplan, sb.items), sb.d_items,
                                 int(sb.items.size()), o->d_partials, s);
@@ -1956,7 +1962,12 @@ int spngd_opt_enable_raw_inputs_ex(spngd_opt* o, const spngd_conv_geom* geoms, i
     if (!L.raw) return fail(SPNGD_ERR_CUDA, "opt: raw input allocation failed");
     if (!implicit) {
       o->i2c.push_back({L.raw, L.act, B, g});
-      if (o->overlap_ok) o->waves[wave_of(L.d)].i2c.push_back(o->i2c.back());
+      if (o->overlap_ok) {
+        spngd_opt::Wave& wv = o->waves[wave_of(L.d)];
+        wv.i2c.push_back(o->i2c.back());
+        const int sub = &wv == &o->waves.back() ? o->sub_of_layer[li] : -1;
+        if (sub >= 0 && size_t(sub) < wv.subs.size()) wv.subs[size_t(sub)].i2c.push_back(o->i2c.back());
+      }
       continue;
     }
     if (L.fa < 0) return fail(SPNGD_ERR_INVALID, "opt: conv layer %zu has no factor problem", li);
@@ -1996,7 +2007,10 @@ int spngd_opt_enable_raw_inputs_ex(spngd_opt* o, const spngd_conv_geom* geoms, i
     }
   }
   if (!o->i2c.empty()) {
-    for (auto& wv : o->waves) wv.d_i2c = dev_upload(wv.i2c, o->owned);
+    for (auto& wv : o->waves) {
+      wv.d_i2c = dev_upload(wv.i2c, o->owned);
+      for (auto& sb : wv.subs) sb.d_i2c = dev_upload(sb.i2c, o->owned);
+    }
     o->d_i2c = dev_upload(o->i2c, o->owned);
     if (!o->d_i2c) return fail(SPNGD_ERR_CUDA, "opt: upload failed");
   }
