@@ -54,6 +54,9 @@ typedef struct spngd_ctx spngd_ctx;
 
 /* Last error message of the calling thread (empty string if none). */
 const char* spngd_last_error(void);
+/* Last error message of a call made on this context (or on an optimizer
+ * created from it), from any thread; empty string if none. */
+const char* spngd_ctx_last_error(const spngd_ctx* ctx);
 const char* spngd_version(void);
 
 /* One context per GPU and host thread; owns workspace and the stream.

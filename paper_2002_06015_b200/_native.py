@@ -113,7 +113,7 @@ STATUS_NAMES = {
 }
 
 EXPORTS = [
-    "spngd_last_error", "spngd_version", "spngd_ctx_create", "spngd_ctx_destroy", "spngd_ctx_sync",
+    "spngd_last_error", "spngd_ctx_last_error", "spngd_version", "spngd_ctx_create", "spngd_ctx_destroy", "spngd_ctx_sync",
     "spngd_ctx_stream", "spngd_copy", "spngd_host_alloc", "spngd_host_free", "spngd_event_time",
     "spngd_factor_sym_batched", "spngd_bn_moments_batched", "spngd_bn_grad_reduce_batched",
     "spngd_bn_full_moments_batched", "spngd_bn_full_solve_update_batched",
@@ -151,6 +151,7 @@ def _declare(L):
     P = C.c_void_p
     sig = {
         "spngd_last_error": (C.c_char_p, []),
+        "spngd_ctx_last_error": (C.c_char_p, [C.c_void_p]),
         "spngd_version": (C.c_char_p, []),
         "spngd_ctx_create": (C.c_int, [C.c_int, P, C.POINTER(P)]),
         "spngd_ctx_destroy": (None, [P]),

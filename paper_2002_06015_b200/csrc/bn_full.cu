@@ -92,6 +92,7 @@ int launch_bn_full_update(spngd_ctx* ctx, const spngd_bn_full_update_req* d_reqs
 using namespace spngd;
 
 extern "C" int spngd_bn_full_moments_batched(spngd_ctx* ctx, int n, const spngd_bn_full_req* reqs) {
+  SPNGD_CTX_SCOPE(ctx);
   if (!ctx || (n > 0 && !reqs)) return fail(SPNGD_ERR_INVALID, "spngd_bn_full_moments_batched: null argument");
   if (n == 0) return SPNGD_OK;
   DeviceScratch scratch(ctx);
@@ -119,6 +120,7 @@ extern "C" int spngd_bn_full_moments_batched(spngd_ctx* ctx, int n, const spngd_
 
 extern "C" int spngd_bn_full_solve_update_batched(spngd_ctx* ctx, int n, const spngd_bn_full_update_req* reqs,
                                                   double eta, double momentum) {
+  SPNGD_CTX_SCOPE(ctx);
   if (!ctx || (n > 0 && !reqs)) return fail(SPNGD_ERR_INVALID, "spngd_bn_full_solve_update_batched: null argument");
   if (n == 0) return SPNGD_OK;
   int64_t max_dim = 0;

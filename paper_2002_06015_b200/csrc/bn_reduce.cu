@@ -231,6 +231,7 @@ int launch_bn_backward(spngd_ctx* ctx, const BnxTask* d_tasks, const BnxItem* d_
 using namespace spngd;
 
 extern "C" int spngd_bn_backward_stats_batched(spngd_ctx* ctx, int n, const spngd_bn_backward_req* reqs) {
+  SPNGD_CTX_SCOPE(ctx);
   if (!ctx || (n > 0 && !reqs)) return fail(SPNGD_ERR_INVALID, "spngd_bn_backward_stats_batched: null argument");
   if (n == 0) return SPNGD_OK;
   BnxPlan plan;
@@ -249,6 +250,7 @@ extern "C" int spngd_bn_backward_stats_batched(spngd_ctx* ctx, int n, const spng
 }
 
 extern "C" int spngd_bn_grad_reduce_batched(spngd_ctx* ctx, int n, const spngd_bn_grad_req* reqs) {
+  SPNGD_CTX_SCOPE(ctx);
   if (!ctx || (n > 0 && !reqs)) return fail(SPNGD_ERR_INVALID, "spngd_bn_grad_reduce_batched: null argument");
   std::vector<BnGradTask> tasks;
   int64_t segs = 0;

@@ -66,6 +66,7 @@ int spngd_nccl_unique_id(void* out128) {
 }
 
 int spngd_ctx_init_comm(spngd_ctx* ctx, int world, int rank, const void* id128) {
+  SPNGD_CTX_SCOPE(ctx);
   if (!ctx || !id128 || world < 1 || rank < 0 || rank >= world)
     return fail(SPNGD_ERR_INVALID, "spngd_ctx_init_comm: bad argument");
   ctx->world = world;
@@ -81,6 +82,7 @@ int spngd_ctx_init_comm(spngd_ctx* ctx, int world, int rank, const void* id128) 
 }
 
 int spngd_reduce_scatter_mean(spngd_ctx* ctx, const float* send, float* recv, int64_t count) {
+  SPNGD_CTX_SCOPE(ctx);
   if (!ctx) return fail(SPNGD_ERR_INVALID, "reduce_scatter: ctx is NULL");
   if (ctx->world == 1) {
     if (send != recv && count > 0)
@@ -94,6 +96,7 @@ int spngd_reduce_scatter_mean(spngd_ctx* ctx, const float* send, float* recv, in
 }
 
 int spngd_all_gather(spngd_ctx* ctx, const float* send, float* recv, int64_t count) {
+  SPNGD_CTX_SCOPE(ctx);
   if (!ctx) return fail(SPNGD_ERR_INVALID, "all_gather: ctx is NULL");
   if (ctx->world == 1) {
     if (send != recv && count > 0)

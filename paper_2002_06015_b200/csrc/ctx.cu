@@ -14,11 +14,14 @@ thread_local char g_last_error[1024] = "";
 
 namespace spngd {
 
+thread_local spngd_ctx* g_cur_ctx = nullptr;
+
 int fail(int code, const char* fmt, ...) {
   va_list ap;
   va_start(ap, fmt);
   vsnprintf(g_last_error, sizeof(g_last_error), fmt, ap);
   va_end(ap);
+  if (g_cur_ctx) snprintf(g_cur_ctx->last_error, sizeof(g_cur_ctx->last_error), "%s", g_last_error);
   return code;
 }
 
@@ -41,6 +44,7 @@ int choose_kchunk(const std::vector<std::pair<int64_t, int64_t>>& tiles_and_k, i
 extern "C" {
 
 const char* spngd_last_error(void) { return g_last_error; }
+const char* spngd_ctx_last_error(const spngd_ctx* ctx) { return ctx ? ctx->last_error : ""; }
 const char* spngd_version(void) { return "spngd_b200 0.1 (sm_100a, tcgen05 3xTF32)"; }
 
 int spngd_ctx_create(int device, void* stream, spngd_ctx** out) {
@@ -100,6 +104,7 @@ void spngd_ctx_destroy(spngd_ctx* ctx) {
 }
 
 int spngd_copy(spngd_ctx* ctx, void* dst, const void* src, size_t bytes) {
+  SPNGD_CTX_SCOPE(ctx);
   if (!ctx) return spngd::fail(SPNGD_ERR_INVALID, "spngd_copy: ctx is NULL");
   SPNGD_CUDA_TRY(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, ctx->stream));
   return SPNGD_OK;
@@ -113,6 +118,7 @@ int spngd_host_alloc(void** out, size_t bytes) {
 void spngd_host_free(void* p) { cudaFreeHost(p); }
 
 int spngd_event_time(spngd_ctx* ctx, void** ev_pair, int record_second, float* ms) {
+  SPNGD_CTX_SCOPE(ctx);
   // Harness helper: ev_pair[0] created+recorded on first call, ev_pair[1] on second.
   if (!ctx || !ev_pair) return spngd::fail(SPNGD_ERR_INVALID, "spngd_event_time: bad argument");
   cudaEvent_t* e = reinterpret_cast<cudaEvent_t*>(ev_pair);
@@ -131,6 +137,7 @@ int spngd_event_time(spngd_ctx* ctx, void** ev_pair, int record_second, float* m
 void* spngd_ctx_stream(spngd_ctx* ctx) { return ctx ? static_cast<void*>(ctx->stream) : nullptr; }
 
 int spngd_ctx_sync(spngd_ctx* ctx) {
+  SPNGD_CTX_SCOPE(ctx);
   if (!ctx) return spngd::fail(SPNGD_ERR_INVALID, "spngd_ctx_sync: ctx is NULL");
   SPNGD_CUDA_TRY(cudaMemcpyAsync(ctx->h_status, ctx->d_status, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
   SPNGD_CUDA_TRY(cudaMemsetAsync(ctx->d_status, 0, sizeof(int), ctx->stream));

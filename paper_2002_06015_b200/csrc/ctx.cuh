@@ -23,9 +23,20 @@ struct spngd_ctx {
   int64_t launches = 0;         // kernels launched through this context
   int launch_prio = 0;          // != 0: cudaLaunchAttributePriority of the recursion kernels
   cudaMemPool_t pool = nullptr; // private stream-ordered pool of DeviceScratch (kept cached)
+  char last_error[1024] = "";   // spngd_ctx_last_error: the last failure of a call on this context
 };
 
 namespace spngd {
+
+// The context of the ABI call running on this thread: fail() also records the
+// message there (spngd_ctx_last_error).
+extern thread_local spngd_ctx* g_cur_ctx;
+struct CtxScope {
+  spngd_ctx* prev;
+  explicit CtxScope(spngd_ctx* c) : prev(g_cur_ctx) { g_cur_ctx = c ? c : prev; }
+  ~CtxScope() { g_cur_ctx = prev; }
+};
+#define SPNGD_CTX_SCOPE(c) ::spngd::CtxScope spngd_ctx_scope_(c)
 
 // Stream-ordered scratch buffer from the context's private pool, released at scope exit.
 class DeviceScratch {

@@ -311,6 +311,7 @@ int launch_bn_moments(spngd_ctx* ctx, const spngd_bn_moments_req* d_reqs, int n,
 }  // namespace spngd
 
 extern "C" int spngd_factor_sym_batched(spngd_ctx* ctx, int n, const spngd_factor_req* reqs) {
+  SPNGD_CTX_SCOPE(ctx);
   using namespace spngd;
   if (!ctx || (n > 0 && !reqs)) return fail(SPNGD_ERR_INVALID, "spngd_factor_sym_batched: null argument");
   if (n == 0) return SPNGD_OK;
@@ -337,6 +338,7 @@ extern "C" int spngd_factor_sym_batched(spngd_ctx* ctx, int n, const spngd_facto
 }
 
 extern "C" int spngd_bn_moments_batched(spngd_ctx* ctx, int n, const spngd_bn_moments_req* reqs) {
+  SPNGD_CTX_SCOPE(ctx);
   using namespace spngd;
   if (!ctx || (n > 0 && !reqs)) return fail(SPNGD_ERR_INVALID, "spngd_bn_moments_batched: null argument");
   int64_t max_c = 0;
@@ -358,6 +360,7 @@ extern "C" int spngd_bn_moments_batched(spngd_ctx* ctx, int n, const spngd_bn_mo
 using namespace spngd;
 
 extern "C" int spngd_im2col_batched(spngd_ctx* ctx, int n, const spngd_im2col_req* reqs) {
+  SPNGD_CTX_SCOPE(ctx);
   if (!ctx || (n > 0 && !reqs)) return fail(SPNGD_ERR_INVALID, "spngd_im2col_batched: null argument");
   if (n == 0) return SPNGD_OK;
   for (int i = 0; i < n; ++i) {

@@ -809,6 +809,7 @@ int batched_inverse(spngd_ctx* ctx, DeviceScratch& scratch, std::vector<InvItem>
 }  // namespace
 
 extern "C" int spngd_spd_inverse_batched(spngd_ctx* ctx, int n, const spngd_spd_req* reqs, int* info) {
+  SPNGD_CTX_SCOPE(ctx);
   if (!ctx || (n > 0 && !reqs)) return fail(SPNGD_ERR_INVALID, "spngd_spd_inverse_batched: null argument");
   if (n == 0) return SPNGD_OK;
   DeviceScratch scratch(ctx);
@@ -832,6 +833,7 @@ extern "C" int spngd_spd_inverse_batched(spngd_ctx* ctx, int n, const spngd_spd_
 
 extern "C" int spngd_damp_and_invert_batched(spngd_ctx* ctx, int n, const spngd_kron_req* reqs, double lambda,
                                              int* info) {
+  SPNGD_CTX_SCOPE(ctx);
   if (!ctx || (n > 0 && !reqs)) return fail(SPNGD_ERR_INVALID, "spngd_damp_and_invert_batched: null argument");
   if (!(lambda > 0.0)) return fail(SPNGD_ERR_NOT_POSITIVE_DEFINITE, "damp_and_invert: lambda must be > 0");
   if (n == 0) return SPNGD_OK;

@@ -978,6 +978,7 @@ int spngd_plan_layout_ex(const spngd_layer_desc* descs, int n, int W, int flags,
 
 int spngd_opt_create(spngd_ctx* ctx, const spngd_layer_desc* layers, int n_layers, const spngd_opt_config* cfg,
                      spngd_opt** out) {
+  SPNGD_CTX_SCOPE(ctx);
   if (!ctx || !layers || n_layers <= 0 || !cfg || !out) return fail(SPNGD_ERR_INVALID, "spngd_opt_create: bad argument");
   if (!(cfg->lambda > 0.0)) return fail(SPNGD_ERR_NOT_POSITIVE_DEFINITE, "OptimizerConfig: lambda must be > 0");
   if (cfg->batch < 1) return fail(SPNGD_ERR_EMPTY_BATCH, "spngd_opt_create: empty per-rank batch");
@@ -1719,12 +1720,14 @@ int64_t input_floats(const spngd_opt* o, const LayerState& L, int which) {
 extern "C" {
 
 int spngd_opt_step(spngd_opt* o, int64_t step, double eta, double momentum) {
+  SPNGD_CTX_SCOPE(o ? o->ctx : nullptr);
   if (!o) return fail(SPNGD_ERR_INVALID, "spngd_opt_step: opt is NULL");
   return step_impl(o, step, eta, momentum, false);
 }
 
 int spngd_opt_step_host(spngd_opt* o, int64_t step, double eta, double momentum, const spngd_host_input* in, int n,
                         float* host_weights_out) {
+  SPNGD_CTX_SCOPE(o ? o->ctx : nullptr);
   if (!o || (n > 0 && !in)) return fail(SPNGD_ERR_INVALID, "spngd_opt_step_host: null argument");
   spngd_ctx* ctx = o->ctx;
   cudaStream_t s = ctx->stream;
@@ -1884,6 +1887,7 @@ int64_t spngd_opt_ledger(const spngd_opt* o, spngd_ledger_row* out, int64_t cap)
 }
 
 int spngd_opt_enable_bn_inputs(spngd_opt* o, const int64_t* spatial) {
+  SPNGD_CTX_SCOPE(o ? o->ctx : nullptr);
   if (!o || !spatial) return fail(SPNGD_ERR_INVALID, "spngd_opt_enable_bn_inputs: null argument");
   if (o->bn_inputs) return fail(SPNGD_ERR_INVALID, "spngd_opt_enable_bn_inputs: already enabled");
   if (o->graphs_ready || o->graphs_ready_ov || o->timed)
@@ -1930,10 +1934,12 @@ int spngd_opt_enable_bn_inputs(spngd_opt* o, const int64_t* spatial) {
 }
 
 int spngd_opt_enable_raw_inputs(spngd_opt* o, const spngd_conv_geom* geoms) {
+  SPNGD_CTX_SCOPE(o ? o->ctx : nullptr);
   return spngd_opt_enable_raw_inputs_ex(o, geoms, 0);
 }
 
 int spngd_opt_enable_raw_inputs_ex(spngd_opt* o, const spngd_conv_geom* geoms, int implicit) {
+  SPNGD_CTX_SCOPE(o ? o->ctx : nullptr);
   if (!o || !geoms) return fail(SPNGD_ERR_INVALID, "spngd_opt_enable_raw_inputs: null argument");
   if (o->raw_inputs) return fail(SPNGD_ERR_INVALID, "spngd_opt_enable_raw_inputs: already enabled");
   if (o->graphs_ready || o->graphs_ready_ov || o->timed)
@@ -2019,6 +2025,7 @@ int spngd_opt_enable_raw_inputs_ex(spngd_opt* o, const spngd_conv_geom* geoms, i
 }
 
 int spngd_opt_ipc_handle(spngd_opt* o, void* out128) {
+  SPNGD_CTX_SCOPE(o ? o->ctx : nullptr);
   if (!o || !out128) return fail(SPNGD_ERR_INVALID, "spngd_opt_ipc_handle: null argument");
   static_assert(sizeof(cudaIpcMemHandle_t) == 64, "cudaIpcMemHandle_t is 64 bytes");
   cudaIpcMemHandle_t h[2];
@@ -2034,6 +2041,7 @@ int spngd_opt_ipc_handle(spngd_opt* o, void* out128) {
 }
 
 int spngd_opt_attach_peers(spngd_opt* o, const void* handles) {
+  SPNGD_CTX_SCOPE(o ? o->ctx : nullptr);
   if (!o || !handles) return fail(SPNGD_ERR_INVALID, "spngd_opt_attach_peers: null argument");
   if (o->world < 2 || o->world > kMaxPeers + 1) return fail(SPNGD_ERR_INVALID, "spngd_opt_attach_peers: world must be 2..8");
   if (o->p2p) return fail(SPNGD_ERR_INVALID, "spngd_opt_attach_peers: already attached");
@@ -2137,6 +2145,7 @@ int spngd_opt_attach_peers(spngd_opt* o, const void* handles) {
 }
 
 int spngd_opt_ledger_clear(spngd_opt* o) {
+  SPNGD_CTX_SCOPE(o ? o->ctx : nullptr);
   if (!o) return fail(SPNGD_ERR_INVALID, "spngd_opt_ledger_clear: opt is NULL");
   o->ledger.clear();
   return SPNGD_OK;
@@ -2152,6 +2161,7 @@ int spngd_opt_wire_bytes(const spngd_opt* o, int64_t* stat_bytes, int64_t* grad_
 
 int spngd_opt_stale_info(spngd_opt* o, int layer, int which, int64_t* t_x, int64_t* delta, int64_t* refresh_count,
                          int* due_last) {
+  SPNGD_CTX_SCOPE(o ? o->ctx : nullptr);
   if (!o || !o->cfg.stale) return fail(SPNGD_ERR_INVALID, "spngd_opt_stale_info: stale gating is off");
   int rc = stale_apply_pending(o);
   if (rc) return rc;
@@ -2167,6 +2177,7 @@ int spngd_opt_stale_info(spngd_opt* o, int layer, int which, int64_t* t_x, int64
 }
 
 int spngd_opt_set_overlap(spngd_opt* o, int on) {
+  SPNGD_CTX_SCOPE(o ? o->ctx : nullptr);
   if (!o) return fail(SPNGD_ERR_INVALID, "spngd_opt_set_overlap: opt is NULL");
   if (on && !o->overlap_ok)
     return fail(SPNGD_ERR_INVALID, "spngd_opt_set_overlap: the wave schedule needs stale gating off");
@@ -2175,6 +2186,7 @@ int spngd_opt_set_overlap(spngd_opt* o, int on) {
 }
 
 int spngd_opt_phase_ms(spngd_opt* o, float* out6) {
+  SPNGD_CTX_SCOPE(o ? o->ctx : nullptr);
   if (!o || !out6) return fail(SPNGD_ERR_INVALID, "spngd_opt_phase_ms: bad argument");
   if (!o->timed) return fail(SPNGD_ERR_INVALID, "spngd_opt_phase_ms: no step yet");
   SPNGD_CUDA_TRY(cudaEventSynchronize(o->ev[6]));
@@ -2198,6 +2210,7 @@ int spngd_opt_phase_ms(spngd_opt* o, float* out6) {
 // layer_tag): the first owned factor whose inverse failed, or the first BN
 // channel whose damped 2x2 block is singular.
 int spngd_opt_sync(spngd_opt* o) {
+  SPNGD_CTX_SCOPE(o ? o->ctx : nullptr);
   if (!o) return fail(SPNGD_ERR_INVALID, "spngd_opt_sync: opt is NULL");
   const int rc = spngd_ctx_sync(o->ctx);
   if (rc != SPNGD_ERR_NOT_POSITIVE_DEFINITE && rc != SPNGD_ERR_SINGULAR_BLOCK) return rc;

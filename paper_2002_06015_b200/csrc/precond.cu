@@ -486,6 +486,7 @@ using namespace spngd;
 
 extern "C" int spngd_precondition_update_batched(spngd_ctx* ctx, int n, const spngd_precond_req* reqs, double eta,
                                                  double momentum) {
+  SPNGD_CTX_SCOPE(ctx);
   if (!ctx || (n > 0 && !reqs)) return fail(SPNGD_ERR_INVALID, "spngd_precondition_update_batched: null argument");
   if (n == 0) return SPNGD_OK;
   PrecondPlan sizing;
@@ -510,6 +511,7 @@ extern "C" int spngd_precondition_update_batched(spngd_ctx* ctx, int n, const sp
 
 extern "C" int spngd_bn_solve_update_batched(spngd_ctx* ctx, int n, const spngd_bn_update_req* reqs, double lambda,
                                              double eta, double momentum) {
+  SPNGD_CTX_SCOPE(ctx);
   if (!ctx || (n > 0 && !reqs)) return fail(SPNGD_ERR_INVALID, "spngd_bn_solve_update_batched: null argument");
   int64_t max_c = 0;
   for (int i = 0; i < n; ++i) {
@@ -529,6 +531,7 @@ extern "C" int spngd_bn_solve_update_batched(spngd_ctx* ctx, int n, const spngd_
 }
 
 extern "C" int spngd_stat_distance_batched(spngd_ctx* ctx, int n, const spngd_stat_req* reqs) {
+  SPNGD_CTX_SCOPE(ctx);
   if (!ctx || (n > 0 && !reqs)) return fail(SPNGD_ERR_INVALID, "spngd_stat_distance_batched: null argument");
   int64_t max_rows = 0;
   for (int i = 0; i < n; ++i) {

@@ -77,6 +77,7 @@ unsigned grid_for(int64_t n) {
 extern "C" {
 
 int spngd_synth_normal(spngd_ctx* ctx, float* out, int64_t n, uint64_t key, float scale, float shift, int relu) {
+  SPNGD_CTX_SCOPE(ctx);
   if (!ctx || !out) return spngd::fail(SPNGD_ERR_INVALID, "synth: null");
   normal_kernel<<<grid_for(n), 256, 0, ctx->stream>>>(out, n, key, scale, shift, relu);
   SPNGD_CUDA_TRY(cudaGetLastError());
@@ -85,6 +86,7 @@ int spngd_synth_normal(spngd_ctx* ctx, float* out, int64_t n, uint64_t key, floa
 
 int spngd_synth_conv_capture(spngd_ctx* ctx, float* out, int64_t batch, int64_t c, int64_t h, int64_t w, int64_t k,
                              int64_t stride, int64_t pad, uint64_t key, int relu, float scale, float shift) {
+  SPNGD_CTX_SCOPE(ctx);
   if (!ctx || !out) return spngd::fail(SPNGD_ERR_INVALID, "synth: null");
   const int64_t ho = (h + 2 * pad - k) / stride + 1, wo = (w + 2 * pad - k) / stride + 1;
   const int64_t total = batch * c * k * k * ho * wo;
@@ -95,6 +97,7 @@ int spngd_synth_conv_capture(spngd_ctx* ctx, float* out, int64_t batch, int64_t 
 }
 
 int spngd_synth_bn_pairs(spngd_ctx* ctx, float* gg, float* gb, int64_t n, uint64_t key) {
+  SPNGD_CTX_SCOPE(ctx);
   if (!ctx || !gg || !gb) return spngd::fail(SPNGD_ERR_INVALID, "synth: null");
   bn_pairs_kernel<<<grid_for(n), 256, 0, ctx->stream>>>(gg, gb, n, key);
   SPNGD_CUDA_TRY(cudaGetLastError());

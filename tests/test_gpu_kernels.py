@@ -69,6 +69,22 @@ def test_factor_subrange_and_errors(cuda_dev):
         P.factor_sym(x, a, hw, 1, 2, 2, 1.0)
 
 
+def test_ctx_last_error_is_per_context(cuda_dev):
+    """spngd_last_error(ctx) -- a failure on one context
+    is readable from that context (and not from another) after the call."""
+    from paper_2002_06015_b200.spngd import Context
+    L = P._native.lib()
+    ctx = P.context()
+    other = Context(0)
+    x, a, hw = conv_capture(6, 2, 4, 4, 3, 1, 1, 99)
+    with pytest.raises(P.EmptyBatch):
+        P.factor_sym(x, a, hw, 1, 2, 2, 1.0)
+    msg = L.spngd_ctx_last_error(ctx.h).decode()
+    assert "empty sample range" in msg, msg
+    assert msg == L.spngd_last_error().decode()
+    assert L.spngd_ctx_last_error(other.h).decode() == ""
+
+
 def test_conv_factor_G_scaling(cuda_dev):
     batch, g, hw = 5, 64, 196
     gr = torch.randn(batch * g * hw, device="cuda") / np.sqrt(batch * hw)
