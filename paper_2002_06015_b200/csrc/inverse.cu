@@ -350,40 +350,66 @@ __global__ void pi_kernel(const PiTask* __restrict__ tasks) {
 
 // dense = unpack(packed) + d I, by 32x32 tiles of the upper triangle so both
 // the packed reads and the mirrored (transposed) dense writes are coalesced.
-// 32-bit index math whenever the dense square fits (every ResNet-50 factor):
-// the 64-bit products made the kernel issue-bound at ~2.2 TB/s (ncu,
-// profiles/r01_kernel_captures.json).
+// Blocks walk the upper tiles only (triangular index), two tiles per pass so
+// eight loads per thread are in flight (one tile per pass over all tn^2
+// tiles, half of them skipped, was latency-bound at 2.4 TB/s).  32-bit index
+// math whenever the dense square fits (every ResNet-50 factor).
 template <typename I>
-__device__ __forceinline__ bool unpack_damp_tiles(const UnpackTask& t, float (*s)[33]) {
+__device__ __forceinline__ void upper_tile(I u, I tn, I& ti, I& tj) {
+  // row-major over the upper triangle: row r starts at r*tn - r(r-1)/2
+  const double b = 2.0 * double(tn) + 1.0;
+  I r = I((b - sqrt(b * b - 8.0 * double(u))) * 0.5);
+  if (r < 0) r = 0;
+  while (r > 0 && r * tn - r * (r - 1) / 2 > u) --r;
+  while ((r + 1) * tn - (r + 1) * r / 2 <= u) ++r;
+  ti = r;
+  tj = r + (u - (r * tn - r * (r - 1) / 2));
+}
+
+template <typename I>
+__device__ __forceinline__ bool unpack_damp_tiles(const UnpackTask& t, float (*s)[32][33]) {
   const float d = t.damp_dev ? t.damp_dev[0] : t.damp;
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
   const I n = I(t.n), ld = I(t.ld);
-  const I tn = (n + 31) / 32;
+  const I tn = (n + 31) / 32, nt = tn * (tn + 1) / 2;
   bool bad = false;
-  for (I tt = blockIdx.x; tt < tn * tn; tt += gridDim.x) {
-    const I ti = tt / tn, tj = tt - ti * tn;
-    if (ti > tj) continue;
-    __syncthreads();
+  for (I u0 = I(blockIdx.x) * 2; u0 < nt; u0 += I(gridDim.x) * 2) {
+    I ti[2], tj[2];
+    float v[2][4];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const I i = ti * 32 + ty + 8 * q, j = tj * 32 + tx;
-      float v = 0.f;
-      if (i < n && j < n && j >= i) {
-        v = t.packed[i * n - i * (i - 1) / 2 + (j - i)];
-        bad |= !isfinite(v);
-        if (i == j) v += d;
+    for (int h = 0; h < 2; ++h) {
+      const I u = u0 + h < nt ? u0 + h : u0;
+      upper_tile<I>(u, tn, ti[h], tj[h]);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const I i = ti[h] * 32 + ty + 8 * q, j = tj[h] * 32 + tx;
+        float x = 0.f;
+        if (i < n && j < n && j >= i) {
+          x = t.packed[i * n - i * (i - 1) / 2 + (j - i)];
+          bad |= !isfinite(x);
+          if (i == j) x += d;
+        }
+        v[h][q] = x;
       }
-      s[ty + 8 * q][tx] = v;
     }
     __syncthreads();
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int li = ty + 8 * q;
-      const I i = ti * 32 + li, j = tj * 32 + tx;
-      if (i < n && j < n) t.dense[i * ld + j] = (j >= i) ? s[li][tx] : s[tx][li];
-      if (ti != tj) {
-        const I r = tj * 32 + li, c = ti * 32 + tx;  // transposed tile
-        if (r < n && c < n) t.dense[r * ld + c] = s[tx][li];
+    for (int h = 0; h < 2; ++h)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) s[h][ty + 8 * q][tx] = v[h][q];
+    __syncthreads();
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      if (u0 + h >= nt) break;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int li = ty + 8 * q;
+        const I i = ti[h] * 32 + li, j = tj[h] * 32 + tx;
+        if (i < n && j < n) t.dense[i * ld + j] = (j >= i) ? s[h][li][tx] : s[h][tx][li];
+        if (ti[h] != tj[h]) {
+          const I r = tj[h] * 32 + li, c = ti[h] * 32 + tx;  // transposed tile
+          if (r < n && c < n) t.dense[r * ld + c] = s[h][tx][li];
+        }
       }
     }
   }
@@ -392,7 +418,7 @@ __device__ __forceinline__ bool unpack_damp_tiles(const UnpackTask& t, float (*s
 
 __global__ void unpack_damp_kernel(const UnpackTask* __restrict__ tasks, int* status) {
   const UnpackTask t = tasks[blockIdx.y];
-  __shared__ float s[32][33];
+  __shared__ float s[2][32][33];
   const int64_t span = (t.ld > t.n ? t.ld : t.n) * (t.n + 32);
   const bool bad = span < (int64_t(1) << 31) ? unpack_damp_tiles<int32_t>(t, s) : unpack_damp_tiles<int64_t>(t, s);
   if (bad) {
@@ -598,7 +624,7 @@ int launch_pi(spngd_ctx* ctx, const PiTask* d_tasks, int n) {
 int launch_unpack(spngd_ctx* ctx, const UnpackTask* d_tasks, int n, int64_t max_n) {
   if (n <= 0) return SPNGD_OK;
   const int64_t tn = (max_n + 31) / 32;
-  dim3 grid(unsigned(std::min<int64_t>(tn * tn, 1024)), unsigned(n));
+  dim3 grid(unsigned(std::min<int64_t>((tn * (tn + 1) / 2 + 1) / 2, 1024)), unsigned(n));
   unpack_damp_kernel<<<grid, 256, 0, ctx->stream>>>(d_tasks, ctx->d_status);
   SPNGD_CUDA_TRY(cudaGetLastError());
   ctx->launches++;
