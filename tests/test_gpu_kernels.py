@@ -251,6 +251,7 @@ def test_bn_full_block_matches_oracle(cuda_dev, m, c, lam):
     """BnMode::Full (SURVEY §8f row 4): build_bn_full (fisher.cpp:187-216),
     damp_bn_full (:248-253), precondition_bn_full (:278-296) and the BN update
     of ngd_step (:346-359) against the fp64 oracle."""
+    torch.manual_seed(1000 * m + c)  # fixed inputs: the c = 1 case compares a 1-element beta
     gg = torch.randn(m, c, device="cuda")
     gb = 0.6 * gg + 0.8 * torch.randn(m, c, device="cuda")
     cap = P.CaptureBuffer(m, [P.LayerCapture(bn_ggamma_true=gg, bn_gbeta_true=gb)])
