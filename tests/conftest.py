@@ -18,3 +18,19 @@ def cuda_dev():
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     return torch.device("cuda:0")
+
+
+@pytest.fixture(autouse=True)
+def _deterministic_inputs(request):
+    """Every test draws its random inputs from a seed fixed by its node id, so a
+    parity case near its tolerance cannot pass or fail by the draw."""
+    import zlib
+
+    import numpy as np
+    seed = zlib.crc32(request.node.nodeid.encode())
+    np.random.seed(seed)
+    try:
+        import torch
+        torch.manual_seed(seed)
+    except ImportError:
+        pass
