@@ -115,14 +115,32 @@ __global__ void bn_grad_payload_kernel(const BnGradPayloadTask* __restrict__ tas
 }
 
 // X'[i][s*hw + p] = X[(s*dim + i)*hw + p]: coalesced reads, runs of hw writes.
+// Four consecutive source elements per thread: one float4 load (the source
+// base is 16-byte aligned), one division for the group, four scalar stores.
 template <typename I>
 __device__ __forceinline__ void repack_range(const RepackTask& t) {
   const I hw = I(t.hw), dim = I(t.dim), n = I(t.n);
   const I total = n * dim * hw;
-  for (I e = I(blockIdx.x) * blockDim.x + threadIdx.x; e < total; e += I(gridDim.x) * blockDim.x) {
+  const bool vec = (reinterpret_cast<uintptr_t>(t.src) & 15) == 0;
+  const I step = I(gridDim.x) * blockDim.x;
+  if (vec) {
+    const I total4 = total / 4;
+    for (I q = I(blockIdx.x) * blockDim.x + threadIdx.x; q < total4; q += step) {
+      const float4 v = __ldg(reinterpret_cast<const float4*>(t.src) + q);
+      const float vv[4] = {v.x, v.y, v.z, v.w};
+      I e = 4 * q, row = e / hw, p = e - row * hw;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const I s_ = row / dim, i = row - s_ * dim;
+        t.dst[int64_t(i) * (n * hw) + s_ * hw + p] = vv[u];
+        if (++p == hw) { p = 0; ++row; }
+      }
+    }
+  }
+  for (I e = (vec ? total / 4 * 4 : 0) + I(blockIdx.x) * blockDim.x + threadIdx.x; e < total; e += step) {
     const I row = e / hw, p = e - row * hw;
-    const I s = row / dim, i = row - s * dim;
-    t.dst[int64_t(i) * (n * hw) + s * hw + p] = __ldg(t.src + e);
+    const I s_ = row / dim, i = row - s_ * dim;
+    t.dst[int64_t(i) * (n * hw) + s_ * hw + p] = __ldg(t.src + e);
   }
 }
 
